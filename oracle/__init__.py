@@ -1,0 +1,264 @@
+"""CPU oracle for the BF16-split FP32 GEMM of arXiv 1904.06376 -- TEST INFRASTRUCTURE.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s ``cpu_baseline``
+/ ``--impl reference`` leg may import this package.  The product package
+(``paper_1904_06376_b200``) never imports it and shares no code with it.
+
+The arithmetic lives in ``bf16x_oracle.c`` (plain C99, one IEEE FP32 operation
+per source operation, no FTZ); this module is argument marshalling plus the
+plain-numpy error metrics and the iterative-refinement loop (§III), each
+citing the passage it follows.  Pins: ``tests/test_oracle_*.py``; see DESIGN.md
+"Oracle pins" for the list (the LU-IR convergence statistics are *parity
+unpinned*: the paper's table is for single-BF16/FP16 LU).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_HERE, "liboracle.so")
+_lib = None
+
+_f32p = np.ctypeslib.ndpointer(dtype=np.float32, flags="F_CONTIGUOUS")
+_vp = ctypes.c_void_p
+
+
+def build(force: bool = False) -> str:
+    """Compile liboracle.so (plain gcc, see Makefile flags)."""
+    src = os.path.join(_HERE, "bf16x_oracle.c")
+    if force or not os.path.exists(_LIB_PATH) or os.path.getmtime(_LIB_PATH) < os.path.getmtime(src):
+        subprocess.check_call(["make", "-C", os.path.dirname(_HERE), "oracle"])
+    return _LIB_PATH
+
+
+def lib() -> ctypes.CDLL:
+    global _lib
+    if _lib is None:
+        build()
+        L = ctypes.CDLL(_LIB_PATH)
+        L.orc_bf16_round.argtypes = [ctypes.c_float]
+        L.orc_bf16_round.restype = ctypes.c_uint16
+        L.orc_bf16_widen.argtypes = [ctypes.c_uint16]
+        L.orc_bf16_widen.restype = ctypes.c_float
+        L.orc_split.argtypes = [ctypes.c_int64, _vp, _vp, _vp, _vp]
+        L.orc_split_patterns.argtypes = [ctypes.c_uint64, ctypes.c_int64, _vp, _vp, _vp]
+        L.orc_partials.argtypes = [ctypes.c_int] * 3 + [_vp, ctypes.c_int, _vp, ctypes.c_int, _vp, ctypes.c_int, _vp]
+        L.orc_gemm_split_cols.argtypes = ([ctypes.c_int] * 3 + [ctypes.c_float, _vp, ctypes.c_int, _vp, ctypes.c_int,
+                                          ctypes.c_float, _vp, ctypes.c_int, ctypes.c_int, _vp, ctypes.c_int, _vp])
+        L.orc_gemm_split.argtypes = ([ctypes.c_int] * 3 + [ctypes.c_float, _vp, ctypes.c_int, _vp, ctypes.c_int,
+                                     ctypes.c_float, _vp, ctypes.c_int, ctypes.c_int])
+        L.orc_sgemm_fma_cols.argtypes = ([ctypes.c_int] * 3 + [ctypes.c_float, _vp, ctypes.c_int, _vp, ctypes.c_int,
+                                         ctypes.c_float, _vp, ctypes.c_int, _vp, ctypes.c_int, _vp])
+        L.orc_dgemm_cols.argtypes = [ctypes.c_int] * 3 + [_vp, ctypes.c_int, _vp, ctypes.c_int, _vp, ctypes.c_int, _vp]
+        L.orc_getrf_split.argtypes = [ctypes.c_int, _vp, ctypes.c_int, _vp, ctypes.c_int, ctypes.c_int]
+        L.orc_lu_solve_f64.argtypes = [ctypes.c_int, _vp, ctypes.c_int, _vp, _vp]
+        L.orc_residual_f64.argtypes = [ctypes.c_int, _vp, ctypes.c_int, _vp, _vp, _vp]
+        L.orc_num_threads.restype = ctypes.c_int
+        _lib = L
+    return _lib
+
+
+def _ptr(a: np.ndarray) -> int:
+    return a.ctypes.data
+
+
+def _colmajor_f32(x) -> np.ndarray:
+    x = np.asarray(x, dtype=np.float32)
+    if x.ndim == 1:
+        x = x.reshape(-1, 1)
+    return np.asfortranarray(x)
+
+
+def num_threads() -> int:
+    return int(lib().orc_num_threads())
+
+
+# --------------------------------------------------------------------------
+# O-1 / O-2: conversion and split (§II-A)
+# --------------------------------------------------------------------------
+def bf16_round(x: float) -> int:
+    """(B16) operator on one FP32 value -> 16-bit pattern (R1/R3/R4)."""
+    return int(lib().orc_bf16_round(ctypes.c_float(float(np.float32(x)))))
+
+
+def bf16_widen(b: int) -> float:
+    """(F32) widening of a 16-bit pattern (exact)."""
+    return float(lib().orc_bf16_widen(ctypes.c_uint16(b)))
+
+
+def split(x) -> tuple[np.ndarray, np.ndarray, np.ndarray]:
+    """3-way split of FP32 values.  Returns three uint16 arrays of x's shape."""
+    x = np.ascontiguousarray(np.asarray(x, dtype=np.float32))
+    flat = x.reshape(-1)
+    out = [np.empty(flat.shape, dtype=np.uint16) for _ in range(3)]
+    lib().orc_split(flat.size, _ptr(flat), _ptr(out[0]), _ptr(out[1]), _ptr(out[2]))
+    return tuple(o.reshape(x.shape) for o in out)
+
+
+def split_patterns(first: int, count: int):
+    """Split every FP32 bit pattern in [first, first+count)."""
+    out = [np.empty(count, dtype=np.uint16) for _ in range(3)]
+    lib().orc_split_patterns(first, count, _ptr(out[0]), _ptr(out[1]), _ptr(out[2]))
+    return tuple(out)
+
+
+def widen(p: np.ndarray) -> np.ndarray:
+    """Exact BF16 pattern -> FP32 values (bits << 16); plain numpy bit view."""
+    return (np.asarray(p, dtype=np.uint16).astype(np.uint32) << 16).view(np.float32)
+
+
+# --------------------------------------------------------------------------
+# O-3..O-6: partial products, combine, scale, FP32/FP64 references
+# --------------------------------------------------------------------------
+def partials(A, B, cols=None) -> np.ndarray:
+    """All nine Z^(i,j) for C = A*B; returns array [3,3,m,ncols]."""
+    A = _colmajor_f32(A)
+    B = _colmajor_f32(B)
+    m, k = A.shape
+    k2, n = B.shape
+    assert k == k2
+    cols_arr = np.arange(n, dtype=np.int32) if cols is None else np.ascontiguousarray(cols, dtype=np.int32)
+    nc = cols_arr.size
+    Z = np.zeros((9, nc, m), dtype=np.float32)
+    lib().orc_partials(m, n, k, _ptr(A), max(1, m), _ptr(B), max(1, k), _ptr(cols_arr), nc, _ptr(Z))
+    return Z.reshape(3, 3, nc, m).transpose(0, 1, 3, 2)
+
+
+def gemm(A, B, C=None, alpha=1.0, beta=0.0, variant=6, cols=None) -> np.ndarray:
+    """Split GEMM C_out = alpha*A*B + beta*C (BLAS scaling R19).
+
+    variant in {1, 3, 6, 8, 9}.  Returns the m x len(cols) FP32 result."""
+    A = _colmajor_f32(A)
+    B = _colmajor_f32(B)
+    m, k = A.shape
+    k2, n = B.shape
+    assert k == k2
+    cols_arr = np.arange(n, dtype=np.int32) if cols is None else np.ascontiguousarray(cols, dtype=np.int32)
+    nc = cols_arr.size
+    out = np.zeros((m, nc), dtype=np.float32, order="F")
+    if C is None:
+        Cin = np.zeros((1, 1), dtype=np.float32, order="F")
+        ldc = max(1, m)
+        if beta != 0.0:
+            raise ValueError("beta != 0 needs C")
+    else:
+        Cin = _colmajor_f32(C)
+        ldc = max(1, m)
+    rc = lib().orc_gemm_split_cols(m, n, k, float(alpha), _ptr(A), max(1, m), _ptr(B), max(1, k), float(beta),
+                                   _ptr(Cin), ldc, int(variant), _ptr(cols_arr), nc, _ptr(out))
+    if rc != 0:
+        raise ValueError(f"oracle gemm returned {rc}")
+    return out
+
+
+def sgemm_fma(A, B, C=None, alpha=1.0, beta=0.0, cols=None) -> np.ndarray:
+    """FP32 FMA reference GEMM (§II-C)."""
+    A = _colmajor_f32(A)
+    B = _colmajor_f32(B)
+    m, k = A.shape
+    _, n = B.shape
+    cols_arr = np.arange(n, dtype=np.int32) if cols is None else np.ascontiguousarray(cols, dtype=np.int32)
+    nc = cols_arr.size
+    out = np.zeros((m, nc), dtype=np.float32, order="F")
+    Cin = np.zeros((1, 1), dtype=np.float32, order="F") if C is None else _colmajor_f32(C)
+    lib().orc_sgemm_fma_cols(m, n, k, float(alpha), _ptr(A), max(1, m), _ptr(B), max(1, k), float(beta),
+                             _ptr(Cin), max(1, m), _ptr(cols_arr), nc, _ptr(out))
+    return out
+
+
+def dgemm(A, B, cols=None) -> np.ndarray:
+    """FP64 reference product of FP32 data ("DGEMM"), sequential FP64 sums."""
+    A = _colmajor_f32(A)
+    B = _colmajor_f32(B)
+    m, k = A.shape
+    _, n = B.shape
+    cols_arr = np.arange(n, dtype=np.int32) if cols is None else np.ascontiguousarray(cols, dtype=np.int32)
+    nc = cols_arr.size
+    out = np.zeros((m, nc), dtype=np.float64, order="F")
+    lib().orc_dgemm_cols(m, n, k, _ptr(A), max(1, m), _ptr(B), max(1, k), _ptr(cols_arr), nc, _ptr(out))
+    return out
+
+
+# --------------------------------------------------------------------------
+# Metrics (north star; Fig. 2 caption)
+# --------------------------------------------------------------------------
+def normwise_error(C, C64, A, B) -> float:
+    """North-star metric ||C - C64||_F / (||A||_F ||B||_F), in FP64."""
+    C = np.asarray(C, dtype=np.float64)
+    C64 = np.asarray(C64, dtype=np.float64)
+    den = np.linalg.norm(np.asarray(A, dtype=np.float64)) * np.linalg.norm(np.asarray(B, dtype=np.float64))
+    return float(np.linalg.norm(C - C64) / den) if den > 0 else float(np.linalg.norm(C - C64))
+
+
+def relative_frobenius_error(C, C64) -> float:
+    """The paper's ||C - DGEMM||_F / ||DGEMM||_F (Fig. 2 caption)."""
+    C64 = np.asarray(C64, dtype=np.float64)
+    return float(np.linalg.norm(np.asarray(C, dtype=np.float64) - C64) / np.linalg.norm(C64))
+
+
+# --------------------------------------------------------------------------
+# O-7: LU + iterative refinement (§III)
+# --------------------------------------------------------------------------
+def getrf(A, variant=3, nb=64):
+    """Blocked LU, FP32 panel, split-GEMM trailing update.  Returns (LU, ipiv, info)."""
+    LU = np.array(A, dtype=np.float32, order="F", copy=True)
+    n = LU.shape[0]
+    ipiv = np.zeros(n, dtype=np.int32)
+    info = lib().orc_getrf_split(n, _ptr(LU), max(1, n), _ptr(ipiv), int(nb), int(variant))
+    return LU, ipiv, int(info)
+
+
+def lu_solve_f64(LU, ipiv, b) -> np.ndarray:
+    """FP64 forward/back substitution with the FP32 factors."""
+    n = LU.shape[0]
+    x = np.array(b, dtype=np.float64, copy=True)
+    lib().orc_lu_solve_f64(n, _ptr(LU), max(1, n), _ptr(ipiv), _ptr(x))
+    return x
+
+
+def residual_f64(A, b, x) -> np.ndarray:
+    A = _colmajor_f32(A)
+    n = A.shape[0]
+    b = np.ascontiguousarray(b, dtype=np.float64)
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    r = np.empty(n, dtype=np.float64)
+    lib().orc_residual_f64(n, _ptr(A), max(1, n), _ptr(b), _ptr(x), _ptr(r))
+    return r
+
+
+def gesv_ir(A, b, variant=3, nb=64, max_iter=30):
+    """LU + iterative refinement: factor in low precision; loop { r = b - A x
+    in FP64; solve A d = r with the factors in FP64; x += d }.
+
+    Stopping rule (reading R14): converged when
+    ||r||_inf <= sqrt(n) * ||x||_inf * ||A||_inf * 2^-53 (LAPACK dsgesv's rule);
+    stagnation = residual not halved over 3 consecutive iterations.
+    Returns dict(x, converged, iterations, info, history)."""
+    A = _colmajor_f32(A)
+    n = A.shape[0]
+    LU, ipiv, info = getrf(A, variant=variant, nb=nb)
+    if info != 0:
+        return dict(x=np.zeros(n), converged=False, iterations=0, info=info, history=[])
+    anrm = float(np.max(np.sum(np.abs(A.astype(np.float64)), axis=1)))
+    eps = 2.0 ** -53
+    x = lu_solve_f64(LU, ipiv, b)
+    hist = []
+    converged = False
+    it = 0
+    for it in range(0, max_iter + 1):
+        r = residual_f64(A, b, x)
+        rn = float(np.max(np.abs(r)))
+        hist.append(rn)
+        if rn <= np.sqrt(n) * float(np.max(np.abs(x))) * anrm * eps:
+            converged = True
+            break
+        if it == max_iter:
+            break
+        if len(hist) >= 4 and hist[-1] > 0.5 * hist[-4]:
+            break
+        x = x + lu_solve_f64(LU, ipiv, r)
+    return dict(x=x, converged=converged, iterations=it, info=0, history=hist)
