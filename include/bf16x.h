@@ -1,0 +1,162 @@
+/*
+ * bf16x.h -- C ABI of libbf16x.so: FP32 GEMM emulated with BF16 splits on B200 (sm_100a).
+ *
+ * Method: Henry, Tang, Heinecke, "Leveraging the bfloat16 Artificial Intelligence
+ * Datatype For Higher-Precision Computations", arXiv 1904.06376 (cited P:<line> of
+ * /root/reference/PAPER.md).  Readings of the paper are numbered R<n> in DESIGN.md.
+ *
+ * Conventions for every entry point
+ *  - Storage is column-major (BLAS): element (i,j) of X is X[i + j*ldx].
+ *  - Matrix/vector pointers are CUDA DEVICE pointers unless the name ends in _host.
+ *  - Work is enqueued on `stream` (or the library stream set by bf16x_set_stream for
+ *    entry points without a stream argument); the call returns before the work is
+ *    done, cuBLAS-style.  Buffers must stay valid until the stream reaches the work.
+ *    bf16x_gemm_host and bf16x_gesv_ir are synchronous.
+ *  - The caller owns every buffer it passes.  The library owns a cached device
+ *    workspace (pieces of A and B), released by bf16x_release().
+ *  - Return value: BF16X_SUCCESS (0), a positive BF16X_* status, or -i when argument
+ *    i (1-based) is invalid (LAPACK xerbla convention).  NaN/Inf inputs are never
+ *    rejected; they propagate (reading R4).
+ *  - There is no CPU fallback: on a device that is not sm_100 every compute entry
+ *    point returns BF16X_ERR_ARCH.
+ *  - C must not alias A or B.
+ */
+#ifndef BF16X_H
+#define BF16X_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st *bf16x_stream_t; /* == cudaStream_t; NULL = legacy default stream */
+
+enum {
+    BF16X_SUCCESS = 0,
+    BF16X_ERR_CUDA = 1,      /* CUDA runtime / launch error (see bf16x_status_string) */
+    BF16X_ERR_ALLOC = 2,     /* device or host allocation failed */
+    BF16X_ERR_ARCH = 3,      /* current device is not sm_100 */
+    BF16X_ERR_SINGULAR = 4,  /* exact zero pivot in bf16x_gesv_ir (report->info = column) */
+    BF16X_NOT_CONVERGED = 5  /* iterative refinement stopped without meeting its test */
+};
+
+/* gemm_ex flags: FP32 promoted-accumulator carry between k-chunks (multi-GPU overlap). */
+#define BF16X_ACC_IN  1u  /* the promoted accumulator starts from acc_carry instead of 0 */
+#define BF16X_ACC_OUT 2u  /* store the raw accumulator to acc_carry; skip alpha/beta/C  */
+
+/* ------------------------------------------------------------------------------------
+ * bf16x_split -- the 3-way decomposition of P:180-184 (section II-A):
+ *     b0 = (B16) x,   b1 = (B16)((F32)(x - b0)),   b2 = (B16)((F32)(x - b0 - b1))
+ * with (B16) = round-to-nearest-even, finite overflow saturating to +-0x7F7F, NaN ->
+ * 0x7FC0 (R1, R3, R4); residuals are single FP32 subtractions left to right (R5);
+ * subnormals are kept (R6).  Non-finite x gives (bf16(x), +0, +0).
+ *   rows, cols : matrix shape (>= 0)
+ *   X, ldx     : FP32 source, ldx >= max(1, rows)
+ *   P0, P1, P2 : BF16 bit-pattern outputs (uint16), same shape as X with leading
+ *                dimension ldp >= max(1, rows).  P1 and P2 may be NULL (fewer pieces:
+ *                P0 only = 1 piece, P0+P1 = the pair used by bf16x3);
+ *                P2 != NULL requires P1 != NULL.
+ * Errors: -1 rows<0, -2 cols<0, -4 ldx, -5 P0 NULL, -7 P2 without P1, -8 ldp.
+ * ---------------------------------------------------------------------------------- */
+int bf16x_split(int64_t rows, int64_t cols, const float *X, int64_t ldx,
+                uint16_t *P0, uint16_t *P1, uint16_t *P2, int64_t ldp, bf16x_stream_t stream);
+
+/* Same decomposition, written transposed: piece element (i,j) lands at P[j + i*ldp]
+ * (ldp >= max(1, cols)).  This is the K-major layout the GEMM consumes for A.
+ * Errors as bf16x_split, with -8 for ldp < max(1, cols). */
+int bf16x_split_t(int64_t rows, int64_t cols, const float *X, int64_t ldx,
+                  uint16_t *P0, uint16_t *P1, uint16_t *P2, int64_t ldp, bf16x_stream_t stream);
+
+/* ------------------------------------------------------------------------------------
+ * bf16x_gemm -- C = alpha*A*B + beta*C (BLAS sgemm, transa = transb = 'N') with the
+ * FP32 product emulated by BF16 x BF16 -> FP32 tensor-core products (section IV-A):
+ *   variant 3: pieces 0-1, products {00,01,10}            ("pair of BF16s")
+ *   variant 6: pieces 0-2, products {00,01,10,02,11,20}   (Z_2)
+ *   variant 9: all nine products                          (R9)
+ *   variant 1: b0 only, one product (debug / plain-BF16 peak)
+ * Products are accumulated smallest bin first into an FP32 tensor-memory
+ * partial that is added, with FP32 round-to-nearest, into a promoted accumulator every
+ * BK = 32 values of k.  alpha/beta follow BLAS (R19):
+ * beta == 0 never reads C; alpha == 0 or k == 0 returns beta*C.
+ *   A: m x k, lda >= max(1,m);  B: k x n, ldb >= max(1,k);  C: m x n, ldc >= max(1,m).
+ * Runs on the library stream (bf16x_set_stream).  Errors: -1 m, -2 n, -3 k, -6 lda,
+ * -8 ldb, -11 ldc, -12 variant; BF16X_ERR_ALLOC if the workspace cannot grow.
+ * ---------------------------------------------------------------------------------- */
+int bf16x_gemm(int m, int n, int k, float alpha, const float *A, int lda,
+               const float *B, int ldb, float beta, float *C, int ldc, int variant);
+
+/* Bytes of caller workspace bf16x_gemm_ex needs: 2 * p * (m + n) * round_up(k, 8). */
+size_t bf16x_gemm_workspace_size(int m, int n, int k, int variant);
+
+/* Extended GEMM: explicit stream, caller workspace (NULL = library cache), optional
+ * pre-split pieces, optional accumulator carry.
+ *   A_pieces : NULL, or the base of p K-major piece planes of A as written by
+ *              bf16x_split_t: element (i,l) of piece q at A_pieces[q*a_plane + l + i*ldap],
+ *              ldap >= k, ldap % 8 == 0, a_plane % 8 == 0, 16-byte aligned base;
+ *              then A may be NULL.
+ *   B_pieces : NULL, or the base of p piece planes of B as written by bf16x_split:
+ *              element (l,j) of piece q at B_pieces[q*b_plane + l + j*ldbp], ldbp >= k,
+ *              ldbp % 8 == 0, b_plane % 8 == 0; then B may be NULL.
+ *   acc_carry: m x n FP32 (ld = ldc) used by BF16X_ACC_IN / BF16X_ACC_OUT.
+ * Errors: as bf16x_gemm, plus -13 flags, -14 A_pieces layout, -16 B_pieces layout,
+ * -19 acc_carry NULL with ACC flags, -21 ws_bytes too small. */
+int bf16x_gemm_ex(int m, int n, int k, float alpha, const float *A, int lda,
+                  const float *B, int ldb, float beta, float *C, int ldc, int variant,
+                  unsigned flags, const uint16_t *A_pieces, int64_t ldap, int64_t a_plane,
+                  const uint16_t *B_pieces, int64_t ldbp, int64_t b_plane, float *acc_carry,
+                  void *workspace, size_t ws_bytes, bf16x_stream_t stream);
+
+/* Host-buffer GEMM (synchronous): copies A, B (and C when beta != 0) from host memory
+ * into cached device buffers, runs bf16x_gemm_ex, copies C back.  Same arguments and
+ * errors as bf16x_gemm with HOST pointers.  Pinned host memory gives full PCIe speed. */
+int bf16x_gemm_host(int m, int n, int k, float alpha, const float *A_host, int lda,
+                    const float *B_host, int ldb, float beta, float *C_host, int ldc, int variant);
+
+/* ------------------------------------------------------------------------------------
+ * bf16x_gesv_ir -- solve A x = b by LU with partial pivoting whose cubic work (the
+ * trailing updates A22 -= L21*U12) runs in bf16x_gemm(variant), followed by FP64
+ * iterative refinement (section III: "compute the residual in higher precision,
+ * r = A*x - b, and use the results from the lower precision solver to solve the updated
+ * system Ay = r ... and then update x with x + y").  Panel factorisation and U12 solves
+ * are FP32; residuals and triangular solves are FP64 (the factors widened exactly).
+ * Stopping rule (R14): ||r||_inf <= sqrt(n)*||x||_inf*||A||_inf*2^-53 (LAPACK dsgesv);
+ * stagnation = residual not halved over 3 iterations.  Synchronous.
+ *   n         : order (>= 0);  A: n x n FP32 device, lda >= max(1,n), NOT modified
+ *   b, x      : FP64 device vectors of length n (x is output)
+ *   variant   : 3, 6 or 9;  nb: panel width (<= 0: 256)
+ *   max_iter  : refinement iterations (<= 0: 30)
+ *   residual_history : HOST, nullable, max_iter+1 doubles (||r||_inf per iteration)
+ *   report    : HOST, required; always filled.
+ * Returns BF16X_SUCCESS, BF16X_ERR_SINGULAR (report->info = 1-based column),
+ * BF16X_NOT_CONVERGED (x = last iterate), or an error. */
+typedef struct {
+    int converged;           /* 1 if the stopping test was met */
+    int iterations;          /* refinement corrections applied */
+    int info;                /* 0, or the 1-based column of an exact zero pivot */
+    double final_residual;   /* ||b - A x||_inf at exit */
+    double backward_error;   /* ||r||_inf / (||A||_inf ||x||_inf) at exit */
+    double tol;              /* threshold the test compared ||r||_inf against */
+    double factor_ms;        /* device time of the LU factorisation */
+    double refine_ms;        /* device time of the refinement loop */
+} bf16x_ir_report;
+
+int bf16x_gesv_ir(int n, const float *A, int lda, const double *b, double *x, int variant,
+                  int nb, int max_iter, double *residual_history, bf16x_ir_report *report);
+
+/* ------------------------------------------------------------------------------------
+ * Library state.
+ * ---------------------------------------------------------------------------------- */
+int bf16x_set_stream(bf16x_stream_t stream);   /* stream used by bf16x_gemm / _host */
+bf16x_stream_t bf16x_get_stream(void);
+void bf16x_release(void);                      /* free cached device/host workspace */
+const char *bf16x_status_string(int status);   /* static string; includes the last CUDA error */
+int bf16x_device_check(void);                  /* BF16X_SUCCESS iff the current device is sm_100 */
+/* Number of library kernels launched by this process so far (all entry points). */
+uint64_t bf16x_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BF16X_H */

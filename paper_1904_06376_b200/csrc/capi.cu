@@ -1,0 +1,290 @@
+// capi.cu -- the C ABI of libbf16x.so (include/bf16x.h): argument checks, library stream,
+// cached workspace, quick returns, and the split -> GEMM sequence of bf16x_gemm.
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace bf16x {
+
+static thread_local char g_err[256] = "";
+static cudaStream_t g_stream = nullptr;
+static std::atomic<uint64_t> g_launches{0};
+static std::mutex g_ws_mu;
+static void *g_ws = nullptr;
+static size_t g_ws_bytes = 0;
+
+void set_cuda_error(cudaError_t e, const char *where) {
+    snprintf(g_err, sizeof(g_err), "%s: %s", where, cudaGetErrorString(e));
+}
+int check_launch(const char *where) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        set_cuda_error(e, where);
+        return BF16X_ERR_CUDA;
+    }
+    return BF16X_SUCCESS;
+}
+void count_launch(uint64_t n) { g_launches += n; }
+cudaStream_t current_stream() { return g_stream; }
+
+int arch_ok() {
+    static int cached = -1;
+    if (cached < 0) {
+        int dev = 0, major = 0, minor = 0;
+        if (cudaGetDevice(&dev) != cudaSuccess ||
+            cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev) != cudaSuccess ||
+            cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev) != cudaSuccess) {
+            cudaGetLastError();
+            snprintf(g_err, sizeof(g_err), "no CUDA device");
+            return BF16X_ERR_ARCH;  // not cached: a device may appear later
+        }
+        cached = (major == 10 && minor == 0) ? BF16X_SUCCESS : BF16X_ERR_ARCH;
+        if (cached) snprintf(g_err, sizeof(g_err), "device is sm_%d%d, library is built for sm_100a", major, minor);
+    }
+    return cached;
+}
+
+static int64_t round_up8(int64_t v) { return (v + 7) / 8 * 8; }
+
+// cached library workspace (grown on demand, never shrunk until bf16x_release)
+static void *workspace(size_t bytes, int *rc) {
+    std::lock_guard<std::mutex> g(g_ws_mu);
+    *rc = BF16X_SUCCESS;
+    if (bytes <= g_ws_bytes) return g_ws;
+    if (g_ws) {
+        cudaDeviceSynchronize();
+        cudaFree(g_ws);
+        g_ws = nullptr;
+        g_ws_bytes = 0;
+    }
+    if (cudaMalloc(&g_ws, bytes) != cudaSuccess) {
+        cudaGetLastError();
+        snprintf(g_err, sizeof(g_err), "workspace: cannot allocate %zu bytes", bytes);
+        g_ws = nullptr;
+        *rc = BF16X_ERR_ALLOC;
+        return nullptr;
+    }
+    g_ws_bytes = bytes;
+    return g_ws;
+}
+
+static int gemm_args(int m, int n, int k, int lda, int ldb, int ldc, int variant) {
+    if (m < 0) return -1;
+    if (n < 0) return -2;
+    if (k < 0) return -3;
+    if (lda < (m > 1 ? m : 1)) return -6;
+    if (ldb < (k > 1 ? k : 1)) return -8;
+    if (ldc < (m > 1 ? m : 1)) return -11;
+    if (variant != 1 && variant != 3 && variant != 6 && variant != 9) return -12;
+    return 0;
+}
+
+int gemm_core(int m, int n, int k, float alpha, const float *A, int lda, const float *B, int ldb, float beta,
+              float *C, int ldc, int variant, unsigned flags, const uint16_t *Ap, int64_t ldap, int64_t a_plane,
+              const uint16_t *Bp, int64_t ldbp, int64_t b_plane, float *acc, void *ws, size_t ws_bytes,
+              cudaStream_t st, int cta_group) {
+    int rc = arch_ok();
+    if (rc) return rc;
+    if (m == 0 || n == 0) return BF16X_SUCCESS;
+    if ((alpha == 0.f || k == 0) && !(flags & (BF16X_ACC_IN | BF16X_ACC_OUT)))
+        return launch_scale(m, n, beta, C, ldc, st);
+    const int p = pieces_of(variant);
+    const int64_t kp = round_up8(k);
+    const size_t need = 2ull * p * ((Ap ? 0 : (size_t)m) + (Bp ? 0 : (size_t)n)) * (size_t)kp;
+    uint8_t *w = nullptr;
+    if (need) {
+        if (ws) {
+            if (ws_bytes < need) return -21;
+            w = (uint8_t *)ws;
+        } else {
+            w = (uint8_t *)workspace(need, &rc);
+            if (rc) return rc;
+        }
+    }
+    if (!Ap) {
+        uint16_t *a = (uint16_t *)w;
+        a_plane = (int64_t)m * kp;
+        ldap = kp;
+        rc = launch_split(m, k, A, lda, a, p > 1 ? a + a_plane : nullptr, p > 2 ? a + 2 * a_plane : nullptr, ldap,
+                          true, st);
+        if (rc) return rc;
+        Ap = a;
+        w += 2ull * p * (size_t)a_plane;
+    }
+    if (!Bp) {
+        uint16_t *b = (uint16_t *)w;
+        b_plane = (int64_t)n * kp;
+        ldbp = kp;
+        rc = launch_split(k, n, B, ldb, b, p > 1 ? b + b_plane : nullptr, p > 2 ? b + 2 * b_plane : nullptr, ldbp,
+                          false, st);
+        if (rc) return rc;
+        Bp = b;
+    }
+    GemmPlan pl;
+    pl.m = m; pl.n = n; pl.k = k;
+    pl.alpha = alpha; pl.beta = beta;
+    pl.C = C; pl.ldc = ldc;
+    pl.variant = variant; pl.flags = flags;
+    pl.Ap = Ap; pl.ldap = ldap; pl.a_plane = a_plane;
+    pl.Bp = Bp; pl.ldbp = ldbp; pl.b_plane = b_plane;
+    pl.acc = acc;
+    pl.cta_group = cta_group;
+    pl.max_ctas = 0;
+    return launch_gemm_pieces(pl, st);
+}
+
+}  // namespace bf16x
+
+using namespace bf16x;
+
+extern "C" {
+
+int bf16x_gemm(int m, int n, int k, float alpha, const float *A, int lda, const float *B, int ldb, float beta,
+               float *C, int ldc, int variant) {
+    int a = gemm_args(m, n, k, lda, ldb, ldc, variant);
+    if (a) return a;
+    return gemm_core(m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, variant, 0u, nullptr, 0, 0, nullptr, 0, 0,
+                     nullptr, nullptr, 0, g_stream, 0);
+}
+
+size_t bf16x_gemm_workspace_size(int m, int n, int k, int variant) {
+    if (m < 0 || n < 0 || k < 0) return 0;
+    int v = (variant == 1 || variant == 3 || variant == 6 || variant == 9) ? variant : 9;
+    return 2ull * (size_t)pieces_of(v) * ((size_t)m + (size_t)n) * (size_t)round_up8(k);
+}
+
+int bf16x_gemm_ex(int m, int n, int k, float alpha, const float *A, int lda, const float *B, int ldb, float beta,
+                  float *C, int ldc, int variant, unsigned flags, const uint16_t *A_pieces, int64_t ldap,
+                  int64_t a_plane, const uint16_t *B_pieces, int64_t ldbp, int64_t b_plane, float *acc_carry,
+                  void *workspace_ptr, size_t ws_bytes, bf16x_stream_t stream) {
+    int a = gemm_args(m, n, k, A_pieces ? (m > 1 ? m : 1) : lda, B_pieces ? (k > 1 ? k : 1) : ldb, ldc, variant);
+    if (a) return a;
+    if (flags & ~(BF16X_ACC_IN | BF16X_ACC_OUT)) return -13;
+    if (A_pieces && (ldap < k || ldap % 8 || a_plane % 8 || a_plane < ldap * (int64_t)m ||
+                     (reinterpret_cast<uintptr_t>(A_pieces) & 15u)))
+        return -14;
+    if (B_pieces && (ldbp < k || ldbp % 8 || b_plane % 8 || b_plane < ldbp * (int64_t)n ||
+                     (reinterpret_cast<uintptr_t>(B_pieces) & 15u)))
+        return -16;
+    if ((flags & (BF16X_ACC_IN | BF16X_ACC_OUT)) && !acc_carry) return -19;
+    return gemm_core(m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, variant, flags, A_pieces, ldap, a_plane,
+                     B_pieces, ldbp, b_plane, acc_carry, workspace_ptr, ws_bytes, (cudaStream_t)stream, 0);
+}
+
+// testing hook (not in the public header): force cta_group 1 or 2
+int bf16x_gemm_cg(int m, int n, int k, float alpha, const float *A, int lda, const float *B, int ldb, float beta,
+                  float *C, int ldc, int variant, int cta_group, bf16x_stream_t stream) {
+    int a = gemm_args(m, n, k, lda, ldb, ldc, variant);
+    if (a) return a;
+    return gemm_core(m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, variant, 0u, nullptr, 0, 0, nullptr, 0, 0,
+                     nullptr, nullptr, 0, (cudaStream_t)stream, cta_group);
+}
+
+static std::mutex g_host_mu;
+static float *g_hA = nullptr, *g_hB = nullptr, *g_hC = nullptr;
+static size_t g_hA_n = 0, g_hB_n = 0, g_hC_n = 0;
+
+static int ensure(float **p, size_t *cap, size_t n) {
+    if (n <= *cap) return BF16X_SUCCESS;
+    if (*p) cudaFree(*p);
+    *p = nullptr;
+    *cap = 0;
+    if (cudaMalloc((void **)p, n * sizeof(float)) != cudaSuccess) {
+        cudaGetLastError();
+        return BF16X_ERR_ALLOC;
+    }
+    *cap = n;
+    return BF16X_SUCCESS;
+}
+
+int bf16x_gemm_host(int m, int n, int k, float alpha, const float *A_host, int lda, const float *B_host, int ldb,
+                    float beta, float *C_host, int ldc, int variant) {
+    int a = gemm_args(m, n, k, lda, ldb, ldc, variant);
+    if (a) return a;
+    int rc = arch_ok();
+    if (rc) return rc;
+    if (m == 0 || n == 0) return BF16X_SUCCESS;
+    std::lock_guard<std::mutex> g(g_host_mu);
+    cudaStream_t st = g_stream;
+    if ((rc = ensure(&g_hA, &g_hA_n, (size_t)m * (k > 0 ? k : 1))) ||
+        (rc = ensure(&g_hB, &g_hB_n, (size_t)(k > 0 ? k : 1) * n)) || (rc = ensure(&g_hC, &g_hC_n, (size_t)m * n)))
+        return rc;
+    cudaError_t e = cudaSuccess;
+    if (k > 0) {
+        e = cudaMemcpy2DAsync(g_hA, (size_t)m * 4, A_host, (size_t)lda * 4, (size_t)m * 4, k, cudaMemcpyHostToDevice,
+                              st);
+        if (e == cudaSuccess)
+            e = cudaMemcpy2DAsync(g_hB, (size_t)k * 4, B_host, (size_t)ldb * 4, (size_t)k * 4, n,
+                                  cudaMemcpyHostToDevice, st);
+    }
+    if (e == cudaSuccess && beta != 0.f)
+        e = cudaMemcpy2DAsync(g_hC, (size_t)m * 4, C_host, (size_t)ldc * 4, (size_t)m * 4, n, cudaMemcpyHostToDevice,
+                              st);
+    if (e != cudaSuccess) {
+        set_cuda_error(e, "gemm_host h2d");
+        return BF16X_ERR_CUDA;
+    }
+    rc = gemm_core(m, n, k, alpha, g_hA, m, g_hB, k > 0 ? k : 1, beta, g_hC, m, variant, 0u, nullptr, 0, 0, nullptr,
+                   0, 0, nullptr, nullptr, 0, st, 0);
+    if (rc) return rc;
+    e = cudaMemcpy2DAsync(C_host, (size_t)ldc * 4, g_hC, (size_t)m * 4, (size_t)m * 4, n, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) {
+        set_cuda_error(e, "gemm_host d2h");
+        return BF16X_ERR_CUDA;
+    }
+    return BF16X_SUCCESS;
+}
+
+int bf16x_set_stream(bf16x_stream_t stream) {
+    g_stream = (cudaStream_t)stream;
+    return BF16X_SUCCESS;
+}
+bf16x_stream_t bf16x_get_stream(void) { return (bf16x_stream_t)g_stream; }
+
+void bf16x_release(void) {
+    std::lock_guard<std::mutex> g(g_ws_mu);
+    cudaDeviceSynchronize();
+    if (g_ws) cudaFree(g_ws);
+    g_ws = nullptr;
+    g_ws_bytes = 0;
+    std::lock_guard<std::mutex> h(g_host_mu);
+    if (g_hA) cudaFree(g_hA);
+    if (g_hB) cudaFree(g_hB);
+    if (g_hC) cudaFree(g_hC);
+    g_hA = g_hB = g_hC = nullptr;
+    g_hA_n = g_hB_n = g_hC_n = 0;
+}
+
+const char *bf16x_status_string(int status) {
+    static thread_local char buf[320];
+    const char *s = "unknown status";
+    switch (status) {
+    case BF16X_SUCCESS: s = "success"; break;
+    case BF16X_ERR_CUDA: s = "CUDA error"; break;
+    case BF16X_ERR_ALLOC: s = "allocation failed"; break;
+    case BF16X_ERR_ARCH: s = "device is not sm_100 (no CPU fallback)"; break;
+    case BF16X_ERR_SINGULAR: s = "exactly singular matrix"; break;
+    case BF16X_NOT_CONVERGED: s = "iterative refinement did not converge"; break;
+    default:
+        if (status < 0) s = "invalid argument";
+    }
+    if (status < 0)
+        snprintf(buf, sizeof(buf), "%s %d", s, -status);
+    else
+        snprintf(buf, sizeof(buf), "%s%s%s", s, g_err[0] ? ": " : "", g_err);
+    return buf;
+}
+
+int bf16x_device_check(void) { return arch_ok(); }
+
+uint64_t bf16x_launch_count(void) { return g_launches.load(); }
+
+// testing/bench hook (not in the public header)
+int bf16x_default_cta_group(void) { return default_cta_group(); }
+
+}  // extern "C"

@@ -1,0 +1,408 @@
+// gemm.cu -- K2: the multi-product BF16-split GEMM on tcgen05 tensor cores (sm_100a).
+//
+// Method: the FP32 product A*B is the sum of BF16 x BF16 partial products
+// Z^(i,j) = A_i * B_j accumulated in FP32 (section II-D), grouped into bins of
+// equal i+j and added smallest bin first ("the terms should be added in
+// the reverse order, so that the smallest terms come first").  Variants: 3 products
+// {00,01,10}, 6 products = Z_2, 9 products (R9).
+//
+// B200 mapping:
+//   * persistent grid, one CTA per SM (cta_group::1, 128 x 256 tile) or one CTA pair per
+//     two SMs (cta_group::2, 256 x 256 tile, B halves split across the pair);
+//   * warp 0: TMA producer.  One 3D TMA box per operand per stage brings BK = 32 values of
+//     k for all p pieces: smem [piece][rows][32 bf16] with the 64-byte swizzle;
+//   * warp 1: MMA issuer (one thread).  Per stage (= one promotion interval of 32 k) it
+//     issues the variant's products band by band, smallest bin first, both K=16 halves
+//     of a band before the next band, into one TMEM accumulator whose first MMA
+//     overwrites it (enable-input-d = 0);
+//   * warps 4..11: promotion + epilogue.  After each interval they read the 128 x 256 FP32
+//     partial from TMEM (tcgen05.ld) and add it with FP32 round-to-nearest into a
+//     register accumulator G (the B200 form of the paper's FP32-accumulated bins); TMEM
+//     is double buffered so the tensor core fills one buffer while the other drains.
+//     After the last interval: C = fmaf(alpha, G, beta*C) (beta == 0: C is not read).
+#include <algorithm>
+#include <mutex>
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace bf16x {
+
+constexpr int kBM = 128;              // accumulator lanes (rows) per CTA
+constexpr int kBN = 256;              // MMA N = accumulator columns
+constexpr int kBK = 32;               // k per stage = promotion interval
+constexpr int kUK = 16;               // k per tcgen05.mma kind::f16
+constexpr int kRowBytes = kBK * 2;    // 64 B rows -> SWIZZLE_64B
+constexpr int kSwizzleAtom = 8 * kRowBytes;  // 8 rows x 64 B: stride between row groups (SBO)
+constexpr int kNumEpiWarps = 8;       // 2 per TMEM lane quadrant, 128 columns each
+constexpr int kThreads = (4 + kNumEpiWarps) * 32;
+constexpr int kTmemCols = 2 * kBN;    // double-buffered accumulator = all 512 columns
+constexpr int kGroupM = 8;            // tile raster: 8 m-tiles per group for L2 reuse
+constexpr int kDefaultCtaGroup = 1;   // measured faster than the 2-CTA variant
+
+__host__ __device__ constexpr int variant_pieces(int v) { return v == 1 ? 1 : (v == 3 ? 2 : 3); }
+
+template <int CG, int V>
+struct Cfg {
+    static constexpr int P = variant_pieces(V);
+    static constexpr int TILE_M = kBM * CG;
+    static constexpr int BN_LOCAL = kBN / CG;
+    static constexpr int A_PIECE = kBM * kRowBytes;
+    static constexpr int B_PIECE = BN_LOCAL * kRowBytes;
+    static constexpr int A_STAGE = P * A_PIECE;
+    static constexpr int B_STAGE = P * B_PIECE;
+    static constexpr int STAGE = A_STAGE + B_STAGE;
+    static constexpr int STAGES_RAW = (200 * 1024) / STAGE;
+    static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
+    static constexpr int BAR_BYTES = 256;
+    static constexpr int SMEM = STAGES * STAGE + BAR_BYTES + 1024;
+    static_assert(STAGES >= 2, "need at least two pipeline stages");
+};
+
+struct KParams {
+    int m, n, k;
+    float alpha, beta;
+    float *C;
+    int ldc;
+    unsigned flags;
+    float *acc;
+    int tiles_m, tiles_n, nkb;
+};
+
+__device__ __forceinline__ void tile_coords(int tile, int tiles_m, int tiles_n, int &tm, int &tn) {
+    const int per_group = kGroupM * tiles_n;
+    const int group = tile / per_group;
+    const int first_m = group * kGroupM;
+    const int gm = min(kGroupM, tiles_m - first_m);
+    const int r = tile - group * per_group;
+    tm = first_m + r % gm;
+    tn = r / gm;
+}
+
+// Issue one interval's MMAs, smallest bin first.  For each band both K=16
+// halves of the 32-wide stage are issued before moving to the next (larger) band.
+template <int CG, int V>
+__device__ __forceinline__ void issue_interval(uint32_t d_tmem, uint32_t a_base, uint32_t b_base, uint32_t idesc) {
+    using Cf = Cfg<CG, V>;
+    bool first = true;
+    auto mma = [&](int i, int j, int kk) {
+        const uint64_t ad = smem_desc_kmajor(a_base + i * Cf::A_PIECE + kk * (kUK * 2), kSwizzleAtom, 4);
+        const uint64_t bd = smem_desc_kmajor(b_base + j * Cf::B_PIECE + kk * (kUK * 2), kSwizzleAtom, 4);
+        umma_bf16<CG>(d_tmem, ad, bd, idesc, first ? 0u : 1u);
+        first = false;
+    };
+    if constexpr (V == 9) {
+#pragma unroll
+        for (int kk = 0; kk < kBK / kUK; ++kk) mma(2, 2, kk);                       // bin 4: 2^-32
+#pragma unroll
+        for (int kk = 0; kk < kBK / kUK; ++kk) { mma(1, 2, kk); mma(2, 1, kk); }    // bin 3: 2^-24
+    }
+    if constexpr (V >= 6) {
+#pragma unroll
+        for (int kk = 0; kk < kBK / kUK; ++kk) { mma(0, 2, kk); mma(1, 1, kk); mma(2, 0, kk); }  // bin 2
+    }
+    if constexpr (V >= 3) {
+#pragma unroll
+        for (int kk = 0; kk < kBK / kUK; ++kk) { mma(0, 1, kk); mma(1, 0, kk); }    // bin 1: 2^-8
+    }
+#pragma unroll
+    for (int kk = 0; kk < kBK / kUK; ++kk) mma(0, 0, kk);                           // bin 0
+}
+
+template <int CG, int V>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_split_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                      const KParams p) {
+    using Cf = Cfg<CG, V>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t *sA = smem;
+    uint8_t *sB = smem + Cf::STAGES * Cf::A_STAGE;
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem + Cf::STAGES * Cf::STAGE);
+    uint64_t *empty = full + Cf::STAGES;
+    uint64_t *acc_full = empty + Cf::STAGES;
+    uint64_t *acc_empty = acc_full + 2;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(acc_empty + 2);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = (CG == 2) ? cluster_ctarank() : 0u;
+
+    if (warp == 0 && lane == 0) {
+        prefetch_tmap(&tmA);
+        prefetch_tmap(&tmB);
+    }
+    if (warp == 1 && lane == 0) {
+        for (int s = 0; s < Cf::STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&acc_full[b], 1);
+            mbar_init(&acc_empty[b], kNumEpiWarps * CG);
+        }
+        fence_barrier_init();
+    }
+    if (warp == 2) tmem_alloc<CG>(tmem_slot, kTmemCols);
+    tc_fence_before();
+    if constexpr (CG == 2) cluster_sync(); else __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    const int num_tiles = p.tiles_m * p.tiles_n;
+    const int cid = blockIdx.x / CG, ncl = gridDim.x / CG;
+
+    if (warp == 0) {
+        // ------------------------------ TMA producer ------------------------------
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int tile = cid; tile < num_tiles; tile += ncl) {
+                int tm, tn;
+                tile_coords(tile, p.tiles_m, p.tiles_n, tm, tn);
+                const int a_row = tm * Cf::TILE_M + (int)rank * kBM;
+                const int b_row = tn * kBN + (int)rank * Cf::BN_LOCAL;
+                for (int kb = 0; kb < p.nkb; ++kb) {
+                    mbar_wait(&empty[stage], phase ^ 1u);
+                    uint8_t *a_dst = sA + stage * Cf::A_STAGE;
+                    uint8_t *b_dst = sB + stage * Cf::B_STAGE;
+                    if constexpr (CG == 1) {
+                        mbar_arrive_expect_tx(&full[stage], Cf::STAGE);
+                        tma_load_3d(a_dst, &tmA, &full[stage], kb * kBK, a_row, 0);
+                        tma_load_3d(b_dst, &tmB, &full[stage], kb * kBK, b_row, 0);
+                    } else {
+                        if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * Cf::STAGE);
+                        tma_load_3d_2sm(a_dst, &tmA, &full[stage], kb * kBK, a_row, 0);
+                        tma_load_3d_2sm(b_dst, &tmB, &full[stage], kb * kBK, b_row, 0);
+                    }
+                    if (++stage == Cf::STAGES) { stage = 0; phase ^= 1u; }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ------------------------------ MMA issuer --------------------------------
+        if (rank == 0 && lane == 0) {
+            const uint32_t idesc = idesc_bf16_f32(kBM * CG, kBN);
+            int stage = 0;
+            uint32_t phase = 0, acc_it = 0;
+            for (int tile = cid; tile < num_tiles; tile += ncl) {
+                for (int kb = 0; kb < p.nkb; ++kb, ++acc_it) {
+                    const uint32_t buf = acc_it & 1u, apar = (acc_it >> 1) & 1u;
+                    mbar_wait(&acc_empty[buf], apar ^ 1u);
+                    mbar_wait(&full[stage], phase);
+                    tc_fence_after();
+                    issue_interval<CG, V>(tmem_base + buf * kBN, smem_u32(sA + stage * Cf::A_STAGE),
+                                          smem_u32(sB + stage * Cf::B_STAGE), idesc);
+                    umma_commit<CG>(&empty[stage]);
+                    umma_commit<CG>(&acc_full[buf]);
+                    if (++stage == Cf::STAGES) { stage = 0; phase ^= 1u; }
+                }
+            }
+        }
+    } else if (warp >= 4) {
+        // ------------------------- promotion + epilogue ---------------------------
+        const int ew = warp - 4;
+        const int quad = warp & 3;                // TMEM lane quadrant this warp may access
+        const int half = ew >> 2;                 // which 128 of the 256 accumulator columns
+        const uint32_t lane_addr = (uint32_t)(quad * 32) << 16;
+        uint32_t acc_it = 0;
+        for (int tile = cid; tile < num_tiles; tile += ncl) {
+            int tm, tn;
+            tile_coords(tile, p.tiles_m, p.tiles_n, tm, tn);
+            const int row = tm * Cf::TILE_M + (int)rank * kBM + quad * 32 + lane;
+            const int col0 = tn * kBN + half * 128;
+            float G[128];
+            if (p.flags & BF16X_ACC_IN) {
+#pragma unroll
+                for (int j = 0; j < 128; ++j)
+                    G[j] = (row < p.m && col0 + j < p.n) ? p.acc[(int64_t)(col0 + j) * p.ldc + row] : 0.f;
+            } else {
+#pragma unroll
+                for (int j = 0; j < 128; ++j) G[j] = 0.f;
+            }
+            for (int kb = 0; kb < p.nkb; ++kb, ++acc_it) {
+                const uint32_t buf = acc_it & 1u, apar = (acc_it >> 1) & 1u;
+                mbar_wait(&acc_full[buf], apar);
+                tc_fence_after();
+                const uint32_t taddr = tmem_base + lane_addr + buf * kBN + half * 128;
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    float v[32];
+                    tmem_ld32(taddr + c * 32, v);
+                    tmem_ld_wait();
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) G[c * 32 + j] = __fadd_rn(G[c * 32 + j], v[j]);
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) {
+                    if (CG == 1 || rank == 0) mbar_arrive(&acc_empty[buf]);
+                    else mbar_arrive_cluster(&acc_empty[buf], 0);
+                }
+            }
+            if (row < p.m) {
+                if (p.flags & BF16X_ACC_OUT) {
+#pragma unroll
+                    for (int j = 0; j < 128; ++j)
+                        if (col0 + j < p.n) p.acc[(int64_t)(col0 + j) * p.ldc + row] = G[j];
+                } else if (p.beta == 0.f) {
+#pragma unroll
+                    for (int j = 0; j < 128; ++j)
+                        if (col0 + j < p.n) __stcs(&p.C[(int64_t)(col0 + j) * p.ldc + row], fmaf(p.alpha, G[j], 0.f));
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 128; ++j)
+                        if (col0 + j < p.n) {
+                            float *c = &p.C[(int64_t)(col0 + j) * p.ldc + row];
+                            *c = fmaf(p.alpha, G[j], p.beta * *c);
+                        }
+                }
+            }
+        }
+    }
+
+    tc_fence_before();
+    if constexpr (CG == 2) cluster_sync(); else __syncthreads();
+    if (warp == 2) {
+        tc_fence_after();
+        tmem_dealloc<CG>(tmem_base, kTmemCols);
+    }
+}
+
+// ------------------------------------------------------------------------------------
+// host side
+// ------------------------------------------------------------------------------------
+typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                  const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+    static EncodeTiledFn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void *f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiledFn>(f);
+    });
+    return fn;
+}
+
+// 3D map over p K-major piece planes: dims (k, rows, p), box (BK, box_rows, p).
+static int make_piece_map(CUtensorMap *map, const uint16_t *base, int k, int rows, int64_t ld, int64_t plane,
+                          int p, int box_rows) {
+    EncodeTiledFn enc = encode_fn();
+    if (!enc) return BF16X_ERR_CUDA;
+    cuuint64_t dims[3] = {(cuuint64_t)k, (cuuint64_t)rows, (cuuint64_t)p};
+    cuuint64_t strides[2] = {(cuuint64_t)ld * 2, (cuuint64_t)plane * 2};
+    cuuint32_t box[3] = {(cuuint32_t)kBK, (cuuint32_t)box_rows, (cuuint32_t)p};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<uint16_t *>(base), dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? BF16X_SUCCESS : BF16X_ERR_CUDA;
+}
+
+int num_sms() {
+    static int n = 0;
+    if (!n) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        if (n <= 0) n = 148;
+    }
+    return n;
+}
+
+int pieces_of(int variant) { return variant_pieces(variant); }
+int default_cta_group() { return kDefaultCtaGroup; }
+
+template <int CG, int V>
+static int launch_t(const GemmPlan &pl, cudaStream_t st) {
+    using Cf = Cfg<CG, V>;
+    CUtensorMap tmA, tmB;
+    int rc = make_piece_map(&tmA, pl.Ap, pl.k, pl.m, pl.ldap, pl.a_plane, Cf::P, kBM);
+    if (rc) return rc;
+    rc = make_piece_map(&tmB, pl.Bp, pl.k, pl.n, pl.ldbp, pl.b_plane, Cf::P, Cf::BN_LOCAL);
+    if (rc) return rc;
+    KParams kp;
+    kp.m = pl.m; kp.n = pl.n; kp.k = pl.k;
+    kp.alpha = pl.alpha; kp.beta = pl.beta;
+    kp.C = pl.C; kp.ldc = pl.ldc; kp.flags = pl.flags; kp.acc = pl.acc;
+    kp.tiles_m = (pl.m + Cf::TILE_M - 1) / Cf::TILE_M;
+    kp.tiles_n = (pl.n + kBN - 1) / kBN;
+    kp.nkb = (pl.k + kBK - 1) / kBK;
+    const int tiles = kp.tiles_m * kp.tiles_n;
+    int units = num_sms() / CG;
+    if (pl.max_ctas > 0) units = std::max(1, pl.max_ctas / CG);
+    const int grid = std::min(tiles, units) * CG;
+
+    static bool attr_set = false;  // per template instance
+    if (!attr_set) {
+        if (cudaFuncSetAttribute(gemm_split_kernel<CG, V>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cf::SMEM) !=
+            cudaSuccess)
+            return check_launch("gemm attr");
+        attr_set = true;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = Cf::SMEM;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CG;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, gemm_split_kernel<CG, V>, tmA, tmB, kp);
+    if (e != cudaSuccess) {
+        set_cuda_error(e, "gemm launch");
+        return BF16X_ERR_CUDA;
+    }
+    count_launch();
+    return check_launch("gemm");
+}
+
+int launch_gemm_pieces(const GemmPlan &pl, cudaStream_t st) {
+    int cg = pl.cta_group;
+    if (cg == 0) cg = kDefaultCtaGroup;
+    if (cg == 1) {
+        switch (pl.variant) {
+        case 1: return launch_t<1, 1>(pl, st);
+        case 3: return launch_t<1, 3>(pl, st);
+        case 6: return launch_t<1, 6>(pl, st);
+        case 9: return launch_t<1, 9>(pl, st);
+        }
+    } else {
+        switch (pl.variant) {
+        case 1: return launch_t<2, 1>(pl, st);
+        case 3: return launch_t<2, 3>(pl, st);
+        case 6: return launch_t<2, 6>(pl, st);
+        case 9: return launch_t<2, 9>(pl, st);
+        }
+    }
+    return -12;
+}
+
+// C <- beta*C (quick return of BLAS sgemm when alpha == 0 or k == 0; beta == 0 -> 0).
+__global__ void scale_kernel(int m, int n, float beta, float *C, int ldc) {
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < (int64_t)m * n;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = t % m, j = t / m;
+        float *c = C + j * ldc + i;
+        *c = (beta == 0.f) ? 0.f : beta * *c;
+    }
+}
+
+int launch_scale(int m, int n, float beta, float *C, int ldc, cudaStream_t st) {
+    if (m == 0 || n == 0) return BF16X_SUCCESS;
+    const int64_t total = (int64_t)m * n;
+    const int blocks = (int)std::min<int64_t>((total + 255) / 256, (int64_t)num_sms() * 16);
+    scale_kernel<<<blocks, 256, 0, st>>>(m, n, beta, C, ldc);
+    count_launch();
+    return check_launch("scale");
+}
+
+}  // namespace bf16x

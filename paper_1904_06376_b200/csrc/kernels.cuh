@@ -1,0 +1,33 @@
+// kernels.cuh -- internal (non-ABI) launch entry points shared by the .cu files.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace bf16x {
+
+int launch_split(int64_t rows, int64_t cols, const float *X, int64_t ldx, uint16_t *P0, uint16_t *P1,
+                 uint16_t *P2, int64_t ldp, bool transpose, cudaStream_t st);
+
+struct GemmPlan {
+    int m, n, k;
+    float alpha, beta;
+    float *C;
+    int ldc;
+    int variant;
+    unsigned flags;
+    const uint16_t *Ap;  // K-major A pieces: plane q at Ap + q*a_plane, element (i,l) at i*ldap + l
+    int64_t ldap, a_plane;
+    const uint16_t *Bp;  // K-major B pieces: plane q at Bp + q*b_plane, element (j,l) at j*ldbp + l
+    int64_t ldbp, b_plane;
+    float *acc;          // carry (ld = ldc) or nullptr
+    int cta_group;       // 1 or 2 (0 = choose)
+    int max_ctas;        // 0 = all SMs
+};
+
+int launch_gemm_pieces(const GemmPlan &p, cudaStream_t st);
+int launch_scale(int m, int n, float beta, float *C, int ldc, cudaStream_t st);
+int pieces_of(int variant);
+int num_sms();
+int default_cta_group();
+
+}  // namespace bf16x

@@ -1,0 +1,70 @@
+"""The C ABI boundary: libbf16x.so loads, exports every entry point include/bf16x.h declares,
+validates arguments LAPACK-style on the host, and (without a GPU) refuses to compute instead of
+falling back to the CPU."""
+import ctypes
+import re
+
+import pytest
+
+import paper_1904_06376_b200 as bx
+
+
+def _declared_functions():
+    src = open(bx.HEADER_PATH).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    names = re.findall(r"\b(bf16x_[a-z0-9_]+)\s*\(", src)
+    return sorted(set(names))
+
+
+def test_library_exports_every_declared_symbol():
+    L = bx.lib()
+    names = _declared_functions()
+    assert {"bf16x_split", "bf16x_split_t", "bf16x_gemm", "bf16x_gemm_ex", "bf16x_gemm_host",
+            "bf16x_gesv_ir", "bf16x_gemm_workspace_size"} <= set(names)
+    for name in names:
+        assert hasattr(L, name), name
+
+
+def test_gemm_argument_errors():
+    L = bx.lib()
+    f = L.bf16x_gemm
+    assert f(-1, 4, 4, 1.0, None, 4, None, 4, 0.0, None, 4, 6) == -1
+    assert f(4, -1, 4, 1.0, None, 4, None, 4, 0.0, None, 4, 6) == -2
+    assert f(4, 4, -1, 1.0, None, 4, None, 4, 0.0, None, 4, 6) == -3
+    assert f(4, 4, 4, 1.0, None, 3, None, 4, 0.0, None, 4, 6) == -6
+    assert f(4, 4, 4, 1.0, None, 4, None, 3, 0.0, None, 4, 6) == -8
+    assert f(4, 4, 4, 1.0, None, 4, None, 4, 0.0, None, 3, 6) == -11
+    assert f(4, 4, 4, 1.0, None, 4, None, 4, 0.0, None, 4, 7) == -12
+    ex = L.bf16x_gemm_ex
+    assert ex(4, 4, 4, 1.0, None, 4, None, 4, 0.0, None, 4, 6, 8, None, 0, 0, None, 0, 0, None, None, 0, None) == -13
+    assert ex(4, 4, 4, 1.0, None, 4, None, 4, 0.0, None, 4, 6, 0, 16, 3, 32, None, 0, 0, None, None, 0, None) == -14
+    assert ex(4, 4, 4, 1.0, None, 4, None, 4, 0.0, None, 4, 6, 0, None, 0, 0, 16, 8, 4, None, None, 0, None) == -16
+    assert ex(4, 4, 4, 1.0, None, 4, None, 4, 0.0, None, 4, 6, 1, None, 0, 0, None, 0, 0, None, None, 0, None) == -19
+
+
+def test_split_argument_errors():
+    L = bx.lib()
+    s = L.bf16x_split
+    assert s(-1, 2, None, 1, 16, None, None, 1, None) == -1
+    assert s(2, -1, None, 2, 16, None, None, 2, None) == -2
+    assert s(4, 2, None, 3, 16, None, None, 4, None) == -4
+    assert s(4, 2, None, 4, None, None, None, 4, None) == -5
+    assert s(4, 2, None, 4, 16, None, 32, 4, None) == -7
+    assert s(4, 2, None, 4, 16, None, None, 3, None) == -8
+    assert L.bf16x_split_t(4, 6, None, 4, 16, None, None, 5, None) == -8
+
+
+def test_workspace_size_formula():
+    # 2 bytes * p pieces * (m + n) rows * round_up(k, 8)
+    assert bx.workspace_size(100, 50, 33, 6) == 2 * 3 * 150 * 40
+    assert bx.workspace_size(100, 50, 33, 3) == 2 * 2 * 150 * 40
+
+
+def test_no_cpu_fallback_without_gpu():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    L = bx.lib()
+    rc = L.bf16x_gemm(4, 4, 4, 1.0, None, 4, None, 4, 0.0, None, 4, 6)
+    assert rc == bx.ERR_ARCH
+    assert b"sm_100" in L.bf16x_status_string(rc)
