@@ -90,27 +90,33 @@ class ClockSampler:
                 "reasons": [v for k, v in self.REASONS.items() if self.reasons & k], "samples": len(self.samples)}
 
 
-def _ncu_traffic(kernel_tag: str, workload: str):
+def _ncu_traffic(kernel_tag: str, workload: str, kernel: str):
     """dram__bytes_read.sum + dram__bytes_write.sum per launch from the committed ncu --set full
-    summary (profiles/ncu_summary.json), if it was captured on this workload."""
+    summary (profiles/ncu_summary.json), if it was captured on this workload and kernel."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
             s = json.load(f)
         ent = s.get(kernel_tag)
-        if ent and ent.get("workload") == workload:
+        if ent and ent.get("workload") == workload and ent.get("kernel") == kernel:
             return float(ent["dram_bytes_per_launch"])
     except Exception:
         pass
     return None
 
 
-def cpu_baseline(m, n, k, variant, ncols, seed_a=1, seed_b=2):
-    """The oracle as it stands on the host cores, on `ncols` sampled output columns of the
-    same workload (all m rows, full k): effective TFLOPS = 2*m*k*ncols / t."""
+def cpu_baseline(m, n, k, variant, ncols, seed_a=1, seed_b=2, target_s=15.0):
+    """The oracle as it stands on the host cores, on a bounded sample of output columns of the
+    same workload (all m rows, full k): effective TFLOPS = 2*m*k*ncols / t.  ncols <= 0 sizes the
+    sample to about `target_s` seconds from a 64-column probe."""
     import oracle
     import synthetic
     A = synthetic.uniform(m, k, seed=seed_a)
     B = synthetic.uniform(k, n, seed=seed_b)
+    if ncols <= 0:
+        probe = np.linspace(0, n - 1, 64).astype(np.int32)
+        t0 = time.perf_counter()
+        oracle.gemm(A, B, variant=variant, cols=probe)
+        ncols = int(min(n, max(64, 64 * target_s / (time.perf_counter() - t0))))
     cols = np.linspace(0, n - 1, ncols).astype(np.int32)
     t0 = time.perf_counter()
     oracle.gemm(A, B, variant=variant, cols=cols)
@@ -249,7 +255,8 @@ def run_ours(args):
     mma_flops = v * 2.0 * m * n_loc * k           # algorithmic BF16 MMA flops per GEMM launch
     achieved = mma_flops / (gemm_ms * 1e-3) / 1e12
     workload = cfg["label"].format(v=v)
-    traffic = _ncu_traffic(f"gemm_split_kernel_v{v}", workload)
+    kname = f"gemm_split_kernel<{bx.default_cta_group()},{v}>"
+    traffic = _ncu_traffic(f"gemm_split_kernel_v{v}", workload, kname)
     split_bytes = (4 + 2 * p) * (m * k + k * n_loc)
 
     # e2e: the public host-buffer entry point (H2D of A and B from pinned memory, GEMM, D2H of C)
@@ -288,7 +295,7 @@ def run_ours(args):
         "pct_of_scaled_roofline": 100.0 * value / world / (peak_burst / v),
         "split_ms": split_ms, "gemm_ms": gemm_ms,
         "split_gbs": split_bytes / (split_ms * 1e-3) / 1e9,
-        "roofline": {"bound": "tensor", "kernel": f"gemm_split_kernel<{bx.default_cta_group()},{v}>", "achieved": achieved,
+        "roofline": {"bound": "tensor", "kernel": kname, "achieved": achieved,
                      "peak": peak_burst, "unit": "TFLOP/s", "frac": achieved / peak_burst, "traffic": traffic,
                      "peak_source": f"{peak_src} bf16 burst (MEASURED_PEAKS.json bf16_tflops)",
                      "achieved_def": f"{v} products x 2mnk BF16 MMA flops per launch / mean CUDA-event launch time",
@@ -318,7 +325,7 @@ def main():
     ap.add_argument("--variant", type=int, default=6, choices=[1, 3, 6, 9])
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--e2e-steps", type=int, default=10)
-    ap.add_argument("--cpu-cols", type=int, default=768, help="oracle sample (columns) for cpu_baseline")
+    ap.add_argument("--cpu-cols", type=int, default=0, help="oracle sample (columns) for cpu_baseline; 0 = about 15 s")
     ap.add_argument("--ref-cols", type=int, default=32, help="oracle sample (columns) per --impl reference step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

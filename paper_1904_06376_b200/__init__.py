@@ -134,6 +134,8 @@ def split(x, pieces: int = 3, stream=None):
     import torch
     if x.dtype != torch.float32 or not x.is_cuda:
         raise TypeError("split expects a float32 CUDA tensor")
+    if x.numel() == 0:
+        return tuple(torch.empty(x.shape, dtype=torch.uint16, device=x.device) for _ in range(pieces))
     if x.dim() == 1:
         x2 = x.reshape(-1, 1)
     else:
@@ -191,7 +193,10 @@ def gemm(A, B, C=None, alpha: float = 1.0, beta: float = 0.0, variant: int = 6, 
     if C is None:
         if beta != 0.0:
             raise ValueError("beta != 0 needs C")
-        C = torch.empty_strided((m, n), (1, max(1, m)), dtype=torch.float32, device=A.device)
+        if _colmajor(A) and _colmajor(B):
+            C = torch.empty_strided((m, n), (1, max(1, m)), dtype=torch.float32, device=A.device)
+        else:
+            C = torch.empty((m, n), dtype=torch.float32, device=A.device)
     st = _stream(stream)
     a, b, c = _colmajor(A), _colmajor(B), _colmajor(C)
     if a and b and c:

@@ -16,6 +16,7 @@ static std::atomic<uint64_t> g_launches{0};
 static std::mutex g_ws_mu;
 static void *g_ws = nullptr;
 static size_t g_ws_bytes = 0;
+static int g_force_cg = 0, g_force_bn = 0, g_force_spi = 0;  // tuning overrides (bf16x_tune; not in the public ABI)
 
 void set_cuda_error(cudaError_t e, const char *where) {
     snprintf(g_err, sizeof(g_err), "%s: %s", where, cudaGetErrorString(e));
@@ -132,8 +133,10 @@ int gemm_core(int m, int n, int k, float alpha, const float *A, int lda, const f
     pl.Ap = Ap; pl.ldap = ldap; pl.a_plane = a_plane;
     pl.Bp = Bp; pl.ldbp = ldbp; pl.b_plane = b_plane;
     pl.acc = acc;
-    pl.cta_group = cta_group;
+    pl.cta_group = cta_group ? cta_group : g_force_cg;
     pl.max_ctas = 0;
+    pl.tile_n = g_force_bn;
+    pl.stages_per_interval = g_force_spi;
     return launch_gemm_pieces(pl, st);
 }
 
@@ -284,7 +287,12 @@ int bf16x_device_check(void) { return arch_ok(); }
 
 uint64_t bf16x_launch_count(void) { return g_launches.load(); }
 
-// testing/bench hook (not in the public header)
+// testing/bench hooks (not in the public header)
 int bf16x_default_cta_group(void) { return default_cta_group(); }
+void bf16x_tune(int cta_group, int tile_n, int stages_per_interval) {
+    g_force_cg = cta_group;
+    g_force_bn = tile_n;
+    g_force_spi = stages_per_interval;
+}
 
 }  // extern "C"

@@ -29,34 +29,37 @@
 namespace bf16x {
 
 constexpr int kBM = 128;              // accumulator lanes (rows) per CTA
-constexpr int kBN = 256;              // MMA N = accumulator columns
 constexpr int kBK = 32;               // k per stage = promotion interval
 constexpr int kUK = 16;               // k per tcgen05.mma kind::f16
 constexpr int kRowBytes = kBK * 2;    // 64 B rows -> SWIZZLE_64B
 constexpr int kSwizzleAtom = 8 * kRowBytes;  // 8 rows x 64 B: stride between row groups (SBO)
-constexpr int kNumEpiWarps = 8;       // 2 per TMEM lane quadrant, 128 columns each
+constexpr int kNumEpiWarps = 8;       // 2 per TMEM lane quadrant, BN/2 columns each
 constexpr int kThreads = (4 + kNumEpiWarps) * 32;
-constexpr int kTmemCols = 2 * kBN;    // double-buffered accumulator = all 512 columns
+constexpr int kTmemCols = 512;        // two accumulator buffers at column 0 and 256
+constexpr int kTmemBufStride = 256;
 constexpr int kGroupM = 8;            // tile raster: 8 m-tiles per group for L2 reuse
-constexpr int kDefaultCtaGroup = 1;   // measured faster than the 2-CTA variant
+constexpr int kDefaultCtaGroup = 2;   // 2-CTA pairs, 64-k promotion interval
+constexpr int kSmemBudget = 224 * 1024;
 
 __host__ __device__ constexpr int variant_pieces(int v) { return v == 1 ? 1 : (v == 3 ? 2 : 3); }
 
-template <int CG, int V>
+template <int CG, int V, int BN>
 struct Cfg {
     static constexpr int P = variant_pieces(V);
     static constexpr int TILE_M = kBM * CG;
-    static constexpr int BN_LOCAL = kBN / CG;
+    static constexpr int BN_LOCAL = BN / CG;          // B rows (output columns) loaded per CTA
+    static constexpr int EPI_COLS = BN / 2;           // accumulator columns per epilogue warp
     static constexpr int A_PIECE = kBM * kRowBytes;
     static constexpr int B_PIECE = BN_LOCAL * kRowBytes;
     static constexpr int A_STAGE = P * A_PIECE;
     static constexpr int B_STAGE = P * B_PIECE;
     static constexpr int STAGE = A_STAGE + B_STAGE;
-    static constexpr int STAGES_RAW = (200 * 1024) / STAGE;
-    static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
     static constexpr int BAR_BYTES = 256;
+    static constexpr int STAGES_RAW = (kSmemBudget - BAR_BYTES - 1024) / STAGE;
+    static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
     static constexpr int SMEM = STAGES * STAGE + BAR_BYTES + 1024;
     static_assert(STAGES >= 2, "need at least two pipeline stages");
+    static_assert(BN % (16 * CG) == 0 && BN <= 256 && EPI_COLS % 32 == 0, "invalid tile N");
 };
 
 struct KParams {
@@ -79,41 +82,46 @@ __device__ __forceinline__ void tile_coords(int tile, int tiles_m, int tiles_n, 
     tn = r / gm;
 }
 
-// Issue one interval's MMAs, smallest bin first.  For each band both K=16
-// halves of the 32-wide stage are issued before moving to the next (larger) band.
-template <int CG, int V>
-__device__ __forceinline__ void issue_interval(uint32_t d_tmem, uint32_t a_base, uint32_t b_base, uint32_t idesc) {
-    using Cf = Cfg<CG, V>;
+// Issue one promotion interval's MMAs, smallest bin first: every band is
+// issued over all K=16 halves of the interval's ns stages (ns <= S) before the next,
+// larger band.  The interval's first MMA overwrites the TMEM accumulator.
+template <int CG, int V, int BN, int S>
+__device__ __forceinline__ void issue_interval(uint32_t d_tmem, const uint32_t (&a_base)[S],
+                                               const uint32_t (&b_base)[S], int ns, uint32_t idesc) {
+    using Cf = Cfg<CG, V, BN>;
+    constexpr int H = S * (kBK / kUK);     // K=16 halves per interval (max)
+    const int nh = ns * (kBK / kUK);
     bool first = true;
-    auto mma = [&](int i, int j, int kk) {
-        const uint64_t ad = smem_desc_kmajor(a_base + i * Cf::A_PIECE + kk * (kUK * 2), kSwizzleAtom, 4);
-        const uint64_t bd = smem_desc_kmajor(b_base + j * Cf::B_PIECE + kk * (kUK * 2), kSwizzleAtom, 4);
+    auto mma = [&](int i, int j, int h) {
+        const int st = h / (kBK / kUK), kk = h % (kBK / kUK);
+        const uint64_t ad = smem_desc_kmajor(a_base[st] + i * Cf::A_PIECE + kk * (kUK * 2), kSwizzleAtom, 4);
+        const uint64_t bd = smem_desc_kmajor(b_base[st] + j * Cf::B_PIECE + kk * (kUK * 2), kSwizzleAtom, 4);
         umma_bf16<CG>(d_tmem, ad, bd, idesc, first ? 0u : 1u);
         first = false;
     };
     if constexpr (V == 9) {
 #pragma unroll
-        for (int kk = 0; kk < kBK / kUK; ++kk) mma(2, 2, kk);                       // bin 4: 2^-32
+        for (int h = 0; h < H; ++h) if (h < nh) mma(2, 2, h);                              // bin 4: 2^-32
 #pragma unroll
-        for (int kk = 0; kk < kBK / kUK; ++kk) { mma(1, 2, kk); mma(2, 1, kk); }    // bin 3: 2^-24
+        for (int h = 0; h < H; ++h) if (h < nh) { mma(1, 2, h); mma(2, 1, h); }           // bin 3: 2^-24
     }
     if constexpr (V >= 6) {
 #pragma unroll
-        for (int kk = 0; kk < kBK / kUK; ++kk) { mma(0, 2, kk); mma(1, 1, kk); mma(2, 0, kk); }  // bin 2
+        for (int h = 0; h < H; ++h) if (h < nh) { mma(0, 2, h); mma(1, 1, h); mma(2, 0, h); }  // bin 2: 2^-16
     }
     if constexpr (V >= 3) {
 #pragma unroll
-        for (int kk = 0; kk < kBK / kUK; ++kk) { mma(0, 1, kk); mma(1, 0, kk); }    // bin 1: 2^-8
+        for (int h = 0; h < H; ++h) if (h < nh) { mma(0, 1, h); mma(1, 0, h); }           // bin 1: 2^-8
     }
 #pragma unroll
-    for (int kk = 0; kk < kBK / kUK; ++kk) mma(0, 0, kk);                           // bin 0
+    for (int h = 0; h < H; ++h) if (h < nh) mma(0, 0, h);                                  // bin 0
 }
 
-template <int CG, int V>
+template <int CG, int V, int BN, int S>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_split_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                       const KParams p) {
-    using Cf = Cfg<CG, V>;
+    using Cf = Cfg<CG, V, BN>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t *sA = smem;
@@ -151,86 +159,104 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int num_tiles = p.tiles_m * p.tiles_n;
     const int cid = blockIdx.x / CG, ncl = gridDim.x / CG;
 
-    if (warp == 0) {
-        // ------------------------------ TMA producer ------------------------------
-        if (lane == 0) {
-            int stage = 0;
-            uint32_t phase = 0;
-            for (int tile = cid; tile < num_tiles; tile += ncl) {
-                int tm, tn;
-                tile_coords(tile, p.tiles_m, p.tiles_n, tm, tn);
-                const int a_row = tm * Cf::TILE_M + (int)rank * kBM;
-                const int b_row = tn * kBN + (int)rank * Cf::BN_LOCAL;
-                for (int kb = 0; kb < p.nkb; ++kb) {
-                    mbar_wait(&empty[stage], phase ^ 1u);
-                    uint8_t *a_dst = sA + stage * Cf::A_STAGE;
-                    uint8_t *b_dst = sB + stage * Cf::B_STAGE;
-                    if constexpr (CG == 1) {
-                        mbar_arrive_expect_tx(&full[stage], Cf::STAGE);
-                        tma_load_3d(a_dst, &tmA, &full[stage], kb * kBK, a_row, 0);
-                        tma_load_3d(b_dst, &tmB, &full[stage], kb * kBK, b_row, 0);
-                    } else {
-                        if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * Cf::STAGE);
-                        tma_load_3d_2sm(a_dst, &tmA, &full[stage], kb * kBK, a_row, 0);
-                        tma_load_3d_2sm(b_dst, &tmB, &full[stage], kb * kBK, b_row, 0);
+    if (warp < 4) {
+        if (warp == 0) {
+            // ------------------------------ TMA producer ------------------------------
+            if (lane == 0) {
+                int stage = 0;
+                uint32_t phase = 0;
+                for (int tile = cid; tile < num_tiles; tile += ncl) {
+                    int tm, tn;
+                    tile_coords(tile, p.tiles_m, p.tiles_n, tm, tn);
+                    const int a_row = tm * Cf::TILE_M + (int)rank * kBM;
+                    const int b_row = tn * BN + (int)rank * Cf::BN_LOCAL;
+                    for (int kb = 0; kb < p.nkb; ++kb) {
+                        mbar_wait(&empty[stage], phase ^ 1u);
+                        uint8_t *a_dst = sA + stage * Cf::A_STAGE;
+                        uint8_t *b_dst = sB + stage * Cf::B_STAGE;
+                        if constexpr (CG == 1) {
+                            mbar_arrive_expect_tx(&full[stage], Cf::STAGE);
+                            tma_load_3d(a_dst, &tmA, &full[stage], kb * kBK, a_row, 0);
+                            tma_load_3d(b_dst, &tmB, &full[stage], kb * kBK, b_row, 0);
+                        } else {
+                            if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * Cf::STAGE);
+                            tma_load_3d_2sm(a_dst, &tmA, &full[stage], kb * kBK, a_row, 0);
+                            tma_load_3d_2sm(b_dst, &tmB, &full[stage], kb * kBK, b_row, 0);
+                        }
+                        if (++stage == Cf::STAGES) { stage = 0; phase ^= 1u; }
                     }
-                    if (++stage == Cf::STAGES) { stage = 0; phase ^= 1u; }
+                }
+            }
+        } else if (warp == 1) {
+            // ------------------------------ MMA issuer --------------------------------
+            if (rank == 0 && lane == 0) {
+                const uint32_t idesc = idesc_bf16_f32(kBM * CG, BN);
+                int stage = 0;
+                uint32_t phase = 0, acc_it = 0;
+                for (int tile = cid; tile < num_tiles; tile += ncl) {
+                    for (int kb = 0; kb < p.nkb; kb += S, ++acc_it) {
+                        const int ns = min(S, p.nkb - kb);
+                        const uint32_t buf = acc_it & 1u, apar = (acc_it >> 1) & 1u;
+                        mbar_wait(&acc_empty[buf], apar ^ 1u);
+                        uint32_t a_base[S], b_base[S];
+                        int stages[S];
+#pragma unroll
+                        for (int q = 0; q < S; ++q) {
+                            stages[q] = stage;
+                            if (q < ns) {
+                                mbar_wait(&full[stage], phase);
+                                a_base[q] = smem_u32(sA + stage * Cf::A_STAGE);
+                                b_base[q] = smem_u32(sB + stage * Cf::B_STAGE);
+                                if (++stage == Cf::STAGES) { stage = 0; phase ^= 1u; }
+                            } else {
+                                a_base[q] = a_base[0];
+                                b_base[q] = b_base[0];
+                            }
+                        }
+                        tc_fence_after();
+                        issue_interval<CG, V, BN, S>(tmem_base + buf * kTmemBufStride, a_base, b_base, ns, idesc);
+#pragma unroll
+                        for (int q = 0; q < S; ++q)
+                            if (q < ns) umma_commit<CG>(&empty[stages[q]]);
+                        umma_commit<CG>(&acc_full[buf]);
+                    }
                 }
             }
         }
-    } else if (warp == 1) {
-        // ------------------------------ MMA issuer --------------------------------
-        if (rank == 0 && lane == 0) {
-            const uint32_t idesc = idesc_bf16_f32(kBM * CG, kBN);
-            int stage = 0;
-            uint32_t phase = 0, acc_it = 0;
-            for (int tile = cid; tile < num_tiles; tile += ncl) {
-                for (int kb = 0; kb < p.nkb; ++kb, ++acc_it) {
-                    const uint32_t buf = acc_it & 1u, apar = (acc_it >> 1) & 1u;
-                    mbar_wait(&acc_empty[buf], apar ^ 1u);
-                    mbar_wait(&full[stage], phase);
-                    tc_fence_after();
-                    issue_interval<CG, V>(tmem_base + buf * kBN, smem_u32(sA + stage * Cf::A_STAGE),
-                                          smem_u32(sB + stage * Cf::B_STAGE), idesc);
-                    umma_commit<CG>(&empty[stage]);
-                    umma_commit<CG>(&acc_full[buf]);
-                    if (++stage == Cf::STAGES) { stage = 0; phase ^= 1u; }
-                }
-            }
-        }
-    } else if (warp >= 4) {
+    } else {
         // ------------------------- promotion + epilogue ---------------------------
+        constexpr int EC = Cf::EPI_COLS;
         const int ew = warp - 4;
         const int quad = warp & 3;                // TMEM lane quadrant this warp may access
-        const int half = ew >> 2;                 // which 128 of the 256 accumulator columns
-        const uint32_t lane_addr = (uint32_t)(quad * 32) << 16;
+        const int half = ew >> 2;                 // which half of the accumulator columns
+        const uint32_t tm_lane = tmem_base + ((uint32_t)(quad * 32) << 16) + half * EC;
         uint32_t acc_it = 0;
         for (int tile = cid; tile < num_tiles; tile += ncl) {
             int tm, tn;
             tile_coords(tile, p.tiles_m, p.tiles_n, tm, tn);
             const int row = tm * Cf::TILE_M + (int)rank * kBM + quad * 32 + lane;
-            const int col0 = tn * kBN + half * 128;
-            float G[128];
+            const int col0 = tn * BN + half * EC;
+            float G[EC];
             if (p.flags & BF16X_ACC_IN) {
 #pragma unroll
-                for (int j = 0; j < 128; ++j)
+                for (int j = 0; j < EC; ++j)
                     G[j] = (row < p.m && col0 + j < p.n) ? p.acc[(int64_t)(col0 + j) * p.ldc + row] : 0.f;
             } else {
 #pragma unroll
-                for (int j = 0; j < 128; ++j) G[j] = 0.f;
+                for (int j = 0; j < EC; ++j) G[j] = 0.f;
             }
-            for (int kb = 0; kb < p.nkb; ++kb, ++acc_it) {
+            for (int kb = 0; kb < p.nkb; kb += S, ++acc_it) {
                 const uint32_t buf = acc_it & 1u, apar = (acc_it >> 1) & 1u;
                 mbar_wait(&acc_full[buf], apar);
                 tc_fence_after();
-                const uint32_t taddr = tmem_base + lane_addr + buf * kBN + half * 128;
+                const uint32_t taddr = tm_lane + buf * kTmemBufStride;
 #pragma unroll
-                for (int c = 0; c < 4; ++c) {
-                    float v[32];
-                    tmem_ld32(taddr + c * 32, v);
+                for (int c = 0; c < EC / 16; ++c) {
+                    float v[16];
+                    tmem_ld16(taddr + c * 16, v);
                     tmem_ld_wait();
 #pragma unroll
-                    for (int j = 0; j < 32; ++j) G[c * 32 + j] = __fadd_rn(G[c * 32 + j], v[j]);
+                    for (int j = 0; j < 16; ++j) G[c * 16 + j] = __fadd_rn(G[c * 16 + j], v[j]);
                 }
                 tc_fence_before();
                 __syncwarp();
@@ -240,19 +266,20 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
             }
             if (row < p.m) {
+                float *crow = p.C + row;
                 if (p.flags & BF16X_ACC_OUT) {
 #pragma unroll
-                    for (int j = 0; j < 128; ++j)
+                    for (int j = 0; j < EC; ++j)
                         if (col0 + j < p.n) p.acc[(int64_t)(col0 + j) * p.ldc + row] = G[j];
                 } else if (p.beta == 0.f) {
 #pragma unroll
-                    for (int j = 0; j < 128; ++j)
-                        if (col0 + j < p.n) __stcs(&p.C[(int64_t)(col0 + j) * p.ldc + row], fmaf(p.alpha, G[j], 0.f));
+                    for (int j = 0; j < EC; ++j)
+                        if (col0 + j < p.n) __stcs(crow + (int64_t)(col0 + j) * p.ldc, fmaf(p.alpha, G[j], 0.f));
                 } else {
 #pragma unroll
-                    for (int j = 0; j < 128; ++j)
+                    for (int j = 0; j < EC; ++j)
                         if (col0 + j < p.n) {
-                            float *c = &p.C[(int64_t)(col0 + j) * p.ldc + row];
+                            float *c = crow + (int64_t)(col0 + j) * p.ldc;
                             *c = fmaf(p.alpha, G[j], p.beta * *c);
                         }
                 }
@@ -317,9 +344,9 @@ int num_sms() {
 int pieces_of(int variant) { return variant_pieces(variant); }
 int default_cta_group() { return kDefaultCtaGroup; }
 
-template <int CG, int V>
+template <int CG, int V, int BN, int S>
 static int launch_t(const GemmPlan &pl, cudaStream_t st) {
-    using Cf = Cfg<CG, V>;
+    using Cf = Cfg<CG, V, BN>;
     CUtensorMap tmA, tmB;
     int rc = make_piece_map(&tmA, pl.Ap, pl.k, pl.m, pl.ldap, pl.a_plane, Cf::P, kBM);
     if (rc) return rc;
@@ -330,7 +357,7 @@ static int launch_t(const GemmPlan &pl, cudaStream_t st) {
     kp.alpha = pl.alpha; kp.beta = pl.beta;
     kp.C = pl.C; kp.ldc = pl.ldc; kp.flags = pl.flags; kp.acc = pl.acc;
     kp.tiles_m = (pl.m + Cf::TILE_M - 1) / Cf::TILE_M;
-    kp.tiles_n = (pl.n + kBN - 1) / kBN;
+    kp.tiles_n = (pl.n + BN - 1) / BN;
     kp.nkb = (pl.k + kBK - 1) / kBK;
     const int tiles = kp.tiles_m * kp.tiles_n;
     int units = num_sms() / CG;
@@ -339,7 +366,7 @@ static int launch_t(const GemmPlan &pl, cudaStream_t st) {
 
     static bool attr_set = false;  // per template instance
     if (!attr_set) {
-        if (cudaFuncSetAttribute(gemm_split_kernel<CG, V>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cf::SMEM) !=
+        if (cudaFuncSetAttribute(gemm_split_kernel<CG, V, BN, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cf::SMEM) !=
             cudaSuccess)
             return check_launch("gemm attr");
         attr_set = true;
@@ -356,7 +383,7 @@ static int launch_t(const GemmPlan &pl, cudaStream_t st) {
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cudaError_t e = cudaLaunchKernelEx(&cfg, gemm_split_kernel<CG, V>, tmA, tmB, kp);
+    cudaError_t e = cudaLaunchKernelEx(&cfg, gemm_split_kernel<CG, V, BN, S>, tmA, tmB, kp);
     if (e != cudaSuccess) {
         set_cuda_error(e, "gemm launch");
         return BF16X_ERR_CUDA;
@@ -365,22 +392,33 @@ static int launch_t(const GemmPlan &pl, cudaStream_t st) {
     return check_launch("gemm");
 }
 
+// Stages per promotion interval: 2 (64 values of k) for the 2-CTA kernel, whose promotion
+// round trip (TMEM drain in both CTAs + remote mbarrier arrivals) needs the longer
+// interval to stay hidden behind the MMAs; 1 (32 values of k) otherwise.
+template <int CG, int V>
+static int launch_s(const GemmPlan &pl, cudaStream_t st) {
+    int s = pl.stages_per_interval;
+    if (s != 1 && s != 2) s = (CG == 2) ? 2 : 1;
+    if (s == 2 && Cfg<CG, V, 256>::STAGES < 4) s = 1;
+    return s == 2 ? launch_t<CG, V, 256, 2>(pl, st) : launch_t<CG, V, 256, 1>(pl, st);
+}
+
 int launch_gemm_pieces(const GemmPlan &pl, cudaStream_t st) {
     int cg = pl.cta_group;
     if (cg == 0) cg = kDefaultCtaGroup;
     if (cg == 1) {
         switch (pl.variant) {
-        case 1: return launch_t<1, 1>(pl, st);
-        case 3: return launch_t<1, 3>(pl, st);
-        case 6: return launch_t<1, 6>(pl, st);
-        case 9: return launch_t<1, 9>(pl, st);
+        case 1: return launch_s<1, 1>(pl, st);
+        case 3: return launch_s<1, 3>(pl, st);
+        case 6: return launch_s<1, 6>(pl, st);
+        case 9: return launch_s<1, 9>(pl, st);
         }
     } else {
         switch (pl.variant) {
-        case 1: return launch_t<2, 1>(pl, st);
-        case 3: return launch_t<2, 3>(pl, st);
-        case 6: return launch_t<2, 6>(pl, st);
-        case 9: return launch_t<2, 9>(pl, st);
+        case 1: return launch_s<2, 1>(pl, st);
+        case 3: return launch_s<2, 3>(pl, st);
+        case 6: return launch_s<2, 6>(pl, st);
+        case 9: return launch_s<2, 9>(pl, st);
         }
     }
     return -12;

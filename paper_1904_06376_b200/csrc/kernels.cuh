@@ -22,6 +22,8 @@ struct GemmPlan {
     float *acc;          // carry (ld = ldc) or nullptr
     int cta_group;       // 1 or 2 (0 = choose)
     int max_ctas;        // 0 = all SMs
+    int tile_n;          // reserved (256)
+    int stages_per_interval;  // 0 = choose; 1 or 2 stages of 32 k per promotion interval
 };
 
 int launch_gemm_pieces(const GemmPlan &p, cudaStream_t st);

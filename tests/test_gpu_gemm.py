@@ -17,6 +17,14 @@ pytestmark = pytest.mark.gpu
 RATIO = 2.0   # north-star tolerance on the normwise error ratio GPU / oracle
 
 
+@pytest.fixture(params=[1, 2], ids=["spi1", "spi2"])
+def spi(request):
+    """Stages (of 32 k) per promotion interval; restored to the library default afterwards."""
+    bx.lib().bf16x_tune(0, 0, request.param)
+    yield request.param
+    bx.lib().bf16x_tune(0, 0, 0)
+
+
 def _gpu(A, B, C=None, alpha=1.0, beta=0.0, variant=6, cg=0):
     Ad = torch.from_numpy(np.asfortranarray(A)).cuda()
     Bd = torch.from_numpy(np.asfortranarray(B)).cuda()
@@ -42,7 +50,7 @@ def _check_ratio(orc, A, B, variant, cg, cols=None):
 @pytest.mark.parametrize("cg", [1, 2])
 @pytest.mark.parametrize("variant", [3, 6, 9])
 @pytest.mark.parametrize("shape", [(64, 64, 64), (129, 257, 33), (333, 517, 77), (256, 512, 1000), (20, 600, 48)])
-def test_uniform_shapes(orc, shape, variant, cg):
+def test_uniform_shapes(orc, shape, variant, cg, spi):
     m, n, k = shape
     A = synthetic.uniform(m, k, seed=m + 7 * k)
     B = synthetic.uniform(k, n, seed=n + 11 * k)
@@ -52,7 +60,7 @@ def test_uniform_shapes(orc, shape, variant, cg):
 @pytest.mark.parametrize("cg", [1, 2])
 @pytest.mark.parametrize("dist", ["wide", "gauss"])
 @pytest.mark.parametrize("variant", [3, 6, 9])
-def test_wide_and_gaussian(orc, dist, variant, cg):
+def test_wide_and_gaussian(orc, dist, variant, cg, spi):
     A = synthetic.by_name(dist, 200, 300, seed=5)
     B = synthetic.by_name(dist, 300, 260, seed=6)
     _check_ratio(orc, A, B, variant, cg)
@@ -60,7 +68,7 @@ def test_wide_and_gaussian(orc, dist, variant, cg):
 
 @pytest.mark.parametrize("k", [256, 1024, 4096, 16384])
 @pytest.mark.parametrize("variant", [3, 6, 9])
-def test_k_sweep_wide(orc, k, variant):
+def test_k_sweep_wide(orc, k, variant, spi):
     """Config 3 shape family (k-sweep, wide exponents) at m = n = 256."""
     A = synthetic.wide(256, k, seed=1000 + k)
     B = synthetic.wide(k, 256, seed=2000 + k)
@@ -68,7 +76,7 @@ def test_k_sweep_wide(orc, k, variant):
 
 
 @pytest.mark.parametrize("cg", [1, 2])
-def test_exact_pins(orc, cg):
+def test_exact_pins(orc, cg, spi):
     """Bit-exact cases: A*I = A and A*P = A P for x6/x9 (one nonzero term per piece pair),
     x3 with B = I returns fl32(b0 + b1); 10-bit integers with k <= 16 are exact for x6/x9."""
     A = synthetic.wide(300, 40, seed=8)
