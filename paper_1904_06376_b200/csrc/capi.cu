@@ -21,6 +21,7 @@ static int g_force_cg = 0, g_force_bn = 0, g_force_spi = 0;  // tuning overrides
 void set_cuda_error(cudaError_t e, const char *where) {
     snprintf(g_err, sizeof(g_err), "%s: %s", where, cudaGetErrorString(e));
 }
+void set_error_msg(const char *msg) { snprintf(g_err, sizeof(g_err), "%s", msg); }
 int check_launch(const char *where) {
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) {

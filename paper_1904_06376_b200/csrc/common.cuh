@@ -15,6 +15,7 @@ namespace bf16x {
 // host status plumbing
 // ----------------------------------------------------------------------------------
 void set_cuda_error(cudaError_t e, const char *where);
+void set_error_msg(const char *msg);
 int check_launch(const char *where);     // BF16X_ERR_CUDA on a pending launch error
 void count_launch(uint64_t n = 1);
 cudaStream_t current_stream();

@@ -151,3 +151,40 @@ def test_config2_4096_sampled(orc):
     full64 = Ad.double() @ Bd.double()
     e_full = float(torch.linalg.norm(C.double() - full64) / (torch.linalg.norm(Ad.double()) * torch.linalg.norm(Bd.double())))
     assert e_full <= RATIO * eo * 1.5
+
+
+@pytest.mark.parametrize("k,chunks", [(1024, 4), (1000, 3), (4096, 2)])
+def test_kchunk_carry_bit_identical(orc, k, chunks):
+    """the A broadcast is overlapped by running sub-block 0 over k-chunks with the
+    FP32 promoted accumulator carried between launches (ACC_OUT / ACC_IN).  With chunk edges on
+    the 64-wide promotion grid the result is bit-identical to a one-pass GEMM."""
+    from paper_1904_06376_b200.distributed import gemm_colsharded
+    m, n = 300, 520
+    A = torch.from_numpy(synthetic.uniform(m, k, seed=21)).cuda()
+    B = torch.from_numpy(synthetic.uniform(k, n, seed=22)).cuda()
+    one = bx.gemm(A, B, variant=6)
+    C = torch.empty_strided((m, n), (1, m), dtype=torch.float32, device="cuda")
+    gemm_colsharded(A, B, C, variant=6, k_chunks=chunks)
+    torch.cuda.synchronize()
+    assert torch.equal(one, C)
+
+
+def test_ragged_ld_and_offsets(orc):
+    """lda > m, ldb > k, ldc > m and sub-matrix views (A, B, C inside larger buffers)."""
+    big_A = synthetic.uniform(300, 150, seed=31)
+    big_B = synthetic.uniform(140, 90, seed=32)
+    A, B = big_A[7:207, 3:133], big_B[5:135, 2:82]
+    Ad = torch.from_numpy(big_A).cuda()[7:207, 3:133]
+    Bd = torch.from_numpy(big_B).cuda()[5:135, 2:82]
+    Cbig = torch.zeros((260, 100), dtype=torch.float32).t().contiguous().t().cuda()
+    Cbig = torch.empty_strided((260, 100), (1, 260), dtype=torch.float32, device="cuda").fill_(7.0)
+    Cd = Cbig[11:211, 5:85]
+    bx.gemm(Ad, Bd, Cd, variant=9)
+    torch.cuda.synchronize()
+    G = Cd.cpu().numpy()
+    C64 = orc.dgemm(np.asfortranarray(A), np.asfortranarray(B))
+    eo = orc.normwise_error(orc.gemm(np.asfortranarray(A), np.asfortranarray(B), variant=9), C64, A, B)
+    assert orc.normwise_error(G, C64, A, B) <= RATIO * eo
+    outside = Cbig.cpu().numpy().copy()
+    outside[11:211, 5:85] = 7.0
+    assert np.all(outside == 7.0)
