@@ -395,11 +395,30 @@ static int launch_t(const GemmPlan &pl, cudaStream_t st) {
 // Stages per promotion interval: 2 (64 values of k) for the 2-CTA kernel, whose promotion
 // round trip (TMEM drain in both CTAs + remote mbarrier arrivals) needs the longer
 // interval to stay hidden behind the MMAs; 1 (32 values of k) otherwise.
+//
+// Tile N (2-CTA kernel only): 256, or 192 / 128 when that needs fewer waves-of-work on the
+// persistent grid (wave quantisation: cost ~ ceil(tiles / clusters) * N).
+// Measured (r02, x3/x6/x9 at 4096-16384): N = 192 and 128 lose more per-MMA efficiency than
+// they win on wave quantisation, so 256 is the default; 192 stays available to the tuner.
+int choose_tile_n(int m, int n, int cg, int units, int forced) {
+    (void)m; (void)n; (void)units;
+    if (cg == 1) return 256;
+    if (forced == 192) return 192;
+    return 256;
+}
+
 template <int CG, int V>
 static int launch_s(const GemmPlan &pl, cudaStream_t st) {
     int s = pl.stages_per_interval;
     if (s != 1 && s != 2) s = (CG == 2) ? 2 : 1;
     if (s == 2 && Cfg<CG, V, 256>::STAGES < 4) s = 1;
+    if constexpr (CG == 2) {
+        if (s == 2) {
+            const int units = (pl.max_ctas > 0 ? pl.max_ctas : num_sms()) / CG;
+            const int bn = choose_tile_n(pl.m, pl.n, CG, units, pl.tile_n);
+            if (bn == 192) return launch_t<CG, V, 192, 2>(pl, st);
+        }
+    }
     return s == 2 ? launch_t<CG, V, 256, 2>(pl, st) : launch_t<CG, V, 256, 1>(pl, st);
 }
 

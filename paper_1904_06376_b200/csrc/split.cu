@@ -4,14 +4,54 @@
 //                 K-major B operand of the GEMM, since B is k x n column-major)
 //   split_trans : pieces are written transposed (bf16x_split_t; the K-major A operand)
 // Algorithmic traffic: 4 B read + 2p B written per element (p = pieces kept).
+//
+// Arithmetic: pairs of values whose magnitude is below the b0-overflow band (|x| <
+// 0x7F7F8000, so finite) take the hardware path -- cvt.rn.bf16x2.f32 is IEEE
+// round-to-nearest-even on two values at once and cannot overflow there; the FP32
+// residual subtractions are exact.  Anything else (NaN, Inf, the overflow band) takes the
+// integer path of common.cuh::split3 (saturation R3, NaN -> 0x7FC0 R4).  Both paths are
+// bit-exact against the oracle over all 2^32 patterns (tests/test_gpu_split.py).
 #include "common.cuh"
 #include "kernels.cuh"
 
 namespace bf16x {
 
+__device__ __forceinline__ uint32_t cvt_bf16x2(float hi, float lo) {
+    uint32_t d;
+    asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(d) : "f"(hi), "f"(lo));
+    return d;
+}
+
+__device__ __forceinline__ bool regular(float x) { return (__float_as_uint(x) & 0x7FFFFFFFu) < 0x7F7F8000u; }
+
+// Split two values; packs piece q of (lo, hi) as (hi << 16) | lo in p[q].
+template <int NP>
+__device__ __forceinline__ void split_pair(float lo, float hi, uint32_t (&p)[3]) {
+    if (regular(lo) && regular(hi)) {
+        const uint32_t a = cvt_bf16x2(hi, lo);
+        p[0] = a;
+        if constexpr (NP >= 2) {
+            const float r1lo = __fsub_rn(lo, __uint_as_float(a << 16));
+            const float r1hi = __fsub_rn(hi, __uint_as_float(a & 0xFFFF0000u));
+            const uint32_t b = cvt_bf16x2(r1hi, r1lo);
+            p[1] = b;
+            if constexpr (NP >= 3) {
+                const float r2lo = __fsub_rn(r1lo, __uint_as_float(b << 16));
+                const float r2hi = __fsub_rn(r1hi, __uint_as_float(b & 0xFFFF0000u));
+                p[2] = cvt_bf16x2(r2hi, r2lo);
+            }
+        }
+    } else {
+        const Split3 a = split3(lo), b = split3(hi);
+        p[0] = a.b0 | (b.b0 << 16);
+        p[1] = a.b1 | (b.b1 << 16);
+        p[2] = a.b2 | (b.b2 << 16);
+    }
+}
+
 // ---------------------------------------------------------------------------------
-// same layout: each thread splits 8 consecutive rows of one column; 16-byte vector
-// loads/stores when the whole matrix is 16-byte aligned (vec != 0).
+// same layout: each thread splits 8 consecutive rows of one column per iteration;
+// 16-byte vector loads/stores when the whole matrix is 16-byte aligned (vec != 0).
 // ---------------------------------------------------------------------------------
 template <int NP>
 __global__ void __launch_bounds__(256) split_same_kernel(int64_t rows, int64_t cols, const float *__restrict__ X,
@@ -19,91 +59,104 @@ __global__ void __launch_bounds__(256) split_same_kernel(int64_t rows, int64_t c
                                                          uint16_t *__restrict__ P1, uint16_t *__restrict__ P2,
                                                          int64_t ldp, int vec) {
     const int64_t nchunk = (rows + 7) / 8;
-    for (int64_t col = blockIdx.y; col < cols; col += gridDim.y) {
+    const int64_t total = nchunk * cols;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t col = t / nchunk, ch = t - col * nchunk;
         const float *x = X + col * ldx;
         const int64_t o = col * ldp;
-        for (int64_t ch = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; ch < nchunk;
-             ch += (int64_t)gridDim.x * blockDim.x) {
-            const int64_t r0 = ch * 8;
-            if (vec && r0 + 8 <= rows) {
-                float4 u = __ldcs(reinterpret_cast<const float4 *>(x + r0));
-                float4 w = __ldcs(reinterpret_cast<const float4 *>(x + r0 + 4));
-                float v[8] = {u.x, u.y, u.z, u.w, w.x, w.y, w.z, w.w};
-                uint32_t q0[4], q1[4], q2[4];
-#pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                    Split3 a = split3(v[2 * i]), b = split3(v[2 * i + 1]);
-                    q0[i] = a.b0 | (b.b0 << 16);
-                    q1[i] = a.b1 | (b.b1 << 16);
-                    q2[i] = a.b2 | (b.b2 << 16);
-                }
-                __stcs(reinterpret_cast<uint4 *>(P0 + o + r0), make_uint4(q0[0], q0[1], q0[2], q0[3]));
-                if (NP >= 2) __stcs(reinterpret_cast<uint4 *>(P1 + o + r0), make_uint4(q1[0], q1[1], q1[2], q1[3]));
-                if (NP >= 3) __stcs(reinterpret_cast<uint4 *>(P2 + o + r0), make_uint4(q2[0], q2[1], q2[2], q2[3]));
-            } else {
-                for (int64_t r = r0; r < rows && r < r0 + 8; ++r) {
-                    Split3 s = split3(x[r]);
-                    P0[o + r] = (uint16_t)s.b0;
-                    if (NP >= 2) P1[o + r] = (uint16_t)s.b1;
-                    if (NP >= 3) P2[o + r] = (uint16_t)s.b2;
-                }
+        const int64_t r0 = ch * 8;
+        if (vec && r0 + 8 <= rows) {
+            const float4 u = __ldcs(reinterpret_cast<const float4 *>(x + r0));
+            const float4 w = __ldcs(reinterpret_cast<const float4 *>(x + r0 + 4));
+            uint32_t q[4][3];
+            split_pair<NP>(u.x, u.y, q[0]);
+            split_pair<NP>(u.z, u.w, q[1]);
+            split_pair<NP>(w.x, w.y, q[2]);
+            split_pair<NP>(w.z, w.w, q[3]);
+            __stcs(reinterpret_cast<uint4 *>(P0 + o + r0), make_uint4(q[0][0], q[1][0], q[2][0], q[3][0]));
+            if constexpr (NP >= 2)
+                __stcs(reinterpret_cast<uint4 *>(P1 + o + r0), make_uint4(q[0][1], q[1][1], q[2][1], q[3][1]));
+            if constexpr (NP >= 3)
+                __stcs(reinterpret_cast<uint4 *>(P2 + o + r0), make_uint4(q[0][2], q[1][2], q[2][2], q[3][2]));
+        } else {
+            for (int64_t r = r0; r < rows && r < r0 + 8; ++r) {
+                Split3 s = split3(x[r]);
+                P0[o + r] = (uint16_t)s.b0;
+                if constexpr (NP >= 2) P1[o + r] = (uint16_t)s.b1;
+                if constexpr (NP >= 3) P2[o + r] = (uint16_t)s.b2;
             }
         }
     }
 }
 
 // ---------------------------------------------------------------------------------
-// transposed: 64 x 64 tiles through shared memory.  Reads are coalesced along the
-// rows of the column-major source, writes along its columns (the output's
-// contiguous dimension).
+// transposed: 64 (source rows) x 64 (source columns) tiles.  Warp w loads source columns
+// [8w, 8w+8) of the tile: lane = (row quad mq: 0..15) + 16 * (column pair half); every lane
+// splits pairs of adjacent columns (= adjacent output elements) and stores packed words to
+// shared memory [piece][row][column pair] (row stride 33 words: conflict-free enough), then
+// each warp writes whole output rows: 32 words = 64 bf16 = 128 B per warp store.
 // ---------------------------------------------------------------------------------
 constexpr int TT = 64;
+constexpr int TW = TT / 2 + 1;   // words per smem row (+1 pad)
 template <int NP>
 __global__ void __launch_bounds__(256) split_trans_kernel(int64_t rows, int64_t cols, const float *__restrict__ X,
                                                           int64_t ldx, uint16_t *__restrict__ P0,
                                                           uint16_t *__restrict__ P1, uint16_t *__restrict__ P2,
-                                                          int64_t ldp) {
-    __shared__ uint16_t s[NP][TT][TT + 2];
-    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;   // 32 x 8 threads
+                                                          int64_t ldp, int vec) {
+    __shared__ uint32_t s[NP][TT][TW];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int mq = lane & 15, half = lane >> 4;
     const int64_t tiles_r = (rows + TT - 1) / TT, tiles_c = (cols + TT - 1) / TT;
     uint16_t *P[3] = {P0, P1, P2};
+    const bool out_words = (ldp % 2 == 0) && ((reinterpret_cast<uintptr_t>(P0) & 3u) == 0) &&
+                           (!P1 || (reinterpret_cast<uintptr_t>(P1) & 3u) == 0) &&
+                           (!P2 || (reinterpret_cast<uintptr_t>(P2) & 3u) == 0);
     for (int64_t t = blockIdx.x; t < tiles_r * tiles_c; t += gridDim.x) {
         const int64_t r0 = (t % tiles_r) * TT, c0 = (t / tiles_r) * TT;
-        // load + split: thread covers rows r0+2tx, r0+2tx+1 of columns c0+ty+8i
+        const bool full = (r0 + TT <= rows) && (c0 + TT <= cols) && vec;
 #pragma unroll
-        for (int i = 0; i < TT / 8; ++i) {
-            const int cl = ty + 8 * i;
-            const int64_t c = c0 + cl;
-            const int64_t r = r0 + 2 * tx;
-            float v0 = 0.f, v1 = 0.f;
-            if (c < cols) {
-                const float *x = X + c * ldx + r;
-                if (r < rows) v0 = x[0];
-                if (r + 1 < rows) v1 = x[1];
+        for (int j = 0; j < 2; ++j) {
+            const int cp = wid * 4 + half * 2 + j;        // column pair within the tile (0..31)
+            const int64_t c = c0 + 2 * cp;
+            const int64_t r = r0 + 4 * mq;
+            float a[4], b[4];
+            if (full) {
+                const float4 fa = __ldcs(reinterpret_cast<const float4 *>(X + c * ldx + r));
+                const float4 fb = __ldcs(reinterpret_cast<const float4 *>(X + (c + 1) * ldx + r));
+                a[0] = fa.x; a[1] = fa.y; a[2] = fa.z; a[3] = fa.w;
+                b[0] = fb.x; b[1] = fb.y; b[2] = fb.z; b[3] = fb.w;
+            } else {
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    a[i] = (c < cols && r + i < rows) ? X[c * ldx + r + i] : 0.f;
+                    b[i] = (c + 1 < cols && r + i < rows) ? X[(c + 1) * ldx + r + i] : 0.f;
+                }
             }
-            Split3 a = split3(v0), b = split3(v1);
-            s[0][2 * tx][cl] = (uint16_t)a.b0;
-            s[0][2 * tx + 1][cl] = (uint16_t)b.b0;
-            if constexpr (NP >= 2) { s[1][2 * tx][cl] = (uint16_t)a.b1; s[1][2 * tx + 1][cl] = (uint16_t)b.b1; }
-            if constexpr (NP >= 3) { s[2][2 * tx][cl] = (uint16_t)a.b2; s[2][2 * tx + 1][cl] = (uint16_t)b.b2; }
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                uint32_t q[3];
+                split_pair<NP>(a[i], b[i], q);     // lo = column c, hi = column c+1
+#pragma unroll
+                for (int p = 0; p < NP; ++p) s[p][4 * mq + i][cp] = q[p];
+            }
         }
         __syncthreads();
-        // store: output row (source row) r, contiguous source columns c0 + 2tx, +1
+        // output: row rl of the tile, word `lane` = source columns c0 + 2*lane, +1
 #pragma unroll
         for (int i = 0; i < TT / 8; ++i) {
-            const int rl = ty + 8 * i;
+            const int rl = wid + 8 * i;
             const int64_t r = r0 + rl;
-            const int64_t c = c0 + 2 * tx;
+            const int64_t c = c0 + 2 * lane;
             if (r >= rows) continue;
 #pragma unroll
-            for (int q = 0; q < NP; ++q) {
-                uint16_t *dst = P[q] + r * ldp + c;
-                const uint16_t lo = s[q][rl][2 * tx], hi = s[q][rl][2 * tx + 1];
-                if (c + 1 < cols && ((reinterpret_cast<uintptr_t>(dst) & 3u) == 0)) {
-                    *reinterpret_cast<uint32_t *>(dst) = (uint32_t)lo | ((uint32_t)hi << 16);
+            for (int p = 0; p < NP; ++p) {
+                const uint32_t wv = s[p][rl][lane];
+                uint16_t *dst = P[p] + r * ldp + c;
+                if (out_words && c + 1 < cols) {
+                    __stcs(reinterpret_cast<unsigned int *>(dst), wv);
                 } else {
-                    if (c < cols) dst[0] = lo;
-                    if (c + 1 < cols) dst[1] = hi;
+                    if (c < cols) dst[0] = (uint16_t)(wv & 0xFFFFu);
+                    if (c + 1 < cols) dst[1] = (uint16_t)(wv >> 16);
                 }
             }
         }
@@ -131,27 +184,22 @@ int launch_split(int64_t rows, int64_t cols, const float *X, int64_t ldx, uint16
                          ((reinterpret_cast<uintptr_t>(P0) & 15u) == 0) &&
                          (!P1 || (reinterpret_cast<uintptr_t>(P1) & 15u) == 0) &&
                          (!P2 || (reinterpret_cast<uintptr_t>(P2) & 15u) == 0) && ldp % 8 == 0;
-        const int64_t nchunk = (rows + 7) / 8;
-        int64_t gx = (nchunk + 255) / 256;
-        int64_t gy = cols;
-        // keep roughly 16 waves of 256-thread blocks in flight
-        const int64_t target = (int64_t)sm_count() * 8 * 16;
-        if (gx > target) gx = target;
-        if (gx * gy > target) gy = (target + gx - 1) / gx;
-        if (gy > 65535) gy = 65535;
-        if (gy < 1) gy = 1;
-        dim3 grid((unsigned)gx, (unsigned)gy);
-        if (np == 1) split_same_kernel<1><<<grid, 256, 0, st>>>(rows, cols, X, ldx, P0, P1, P2, ldp, vec);
-        else if (np == 2) split_same_kernel<2><<<grid, 256, 0, st>>>(rows, cols, X, ldx, P0, P1, P2, ldp, vec);
-        else split_same_kernel<3><<<grid, 256, 0, st>>>(rows, cols, X, ldx, P0, P1, P2, ldp, vec);
+        const int64_t total = ((rows + 7) / 8) * cols;
+        int64_t g = (total + 255) / 256;
+        const int64_t cap = (int64_t)sm_count() * 8 * 8;
+        if (g > cap) g = cap;
+        if (np == 1) split_same_kernel<1><<<(unsigned)g, 256, 0, st>>>(rows, cols, X, ldx, P0, P1, P2, ldp, vec);
+        else if (np == 2) split_same_kernel<2><<<(unsigned)g, 256, 0, st>>>(rows, cols, X, ldx, P0, P1, P2, ldp, vec);
+        else split_same_kernel<3><<<(unsigned)g, 256, 0, st>>>(rows, cols, X, ldx, P0, P1, P2, ldp, vec);
     } else {
+        const bool vec = ((reinterpret_cast<uintptr_t>(X) & 15u) == 0) && ldx % 4 == 0;
         const int64_t tiles = ((rows + TT - 1) / TT) * ((cols + TT - 1) / TT);
         int64_t g = tiles;
         const int64_t cap = (int64_t)sm_count() * 8;
         if (g > cap) g = cap;
-        if (np == 1) split_trans_kernel<1><<<(unsigned)g, 256, 0, st>>>(rows, cols, X, ldx, P0, P1, P2, ldp);
-        else if (np == 2) split_trans_kernel<2><<<(unsigned)g, 256, 0, st>>>(rows, cols, X, ldx, P0, P1, P2, ldp);
-        else split_trans_kernel<3><<<(unsigned)g, 256, 0, st>>>(rows, cols, X, ldx, P0, P1, P2, ldp);
+        if (np == 1) split_trans_kernel<1><<<(unsigned)g, 256, 0, st>>>(rows, cols, X, ldx, P0, P1, P2, ldp, vec);
+        else if (np == 2) split_trans_kernel<2><<<(unsigned)g, 256, 0, st>>>(rows, cols, X, ldx, P0, P1, P2, ldp, vec);
+        else split_trans_kernel<3><<<(unsigned)g, 256, 0, st>>>(rows, cols, X, ldx, P0, P1, P2, ldp, vec);
     }
     count_launch();
     return check_launch("split");

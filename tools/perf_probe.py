@@ -18,6 +18,7 @@ sizes = [int(x) for x in (sys.argv[1].split(",") if len(sys.argv) > 1 else ["409
 variants = [int(x) for x in (sys.argv[2].split(",") if len(sys.argv) > 2 else ["1", "3", "6", "9"])]
 cgs = [int(x) for x in (sys.argv[3].split(",") if len(sys.argv) > 3 else ["1", "2"])]
 spis = [int(x) for x in (sys.argv[4].split(",") if len(sys.argv) > 4 else ["0"])]
+tns = [int(x) for x in (sys.argv[5].split(",") if len(sys.argv) > 5 else ["0"])]
 L = bx.lib()
 for n in sizes:
     A = torch.rand(n, n, device="cuda") * 2 - 1
@@ -31,12 +32,13 @@ for n in sizes:
     print(f"split trans n={n}: {ms*1e3:.1f} us  {10*n*n/ms/1e6:.0f} GB/s", flush=True)
     for cg in cgs:
       for bn in spis:
-        L.bf16x_tune(cg, 0, bn)
+       for tn in tns:
+        L.bf16x_tune(cg, tn, bn)
         for v in variants:
             ms = timeit(lambda: bx.gemm(A, B, C, variant=v))
             tf = 2 * n**3 / ms / 1e9
             roof = 1658.0 / v
-            print(f"gemm n={n} v{v} cg{cg} spi{bn}: {ms:.3f} ms  {tf:.1f} eff TFLOPS  ({100*tf/roof:.1f}% of R/{v}; mma {tf*v:.0f} TF)", flush=True)
+            print(f"gemm n={n} v{v} cg{cg} spi{bn} tn{tn}: {ms:.3f} ms  {tf:.1f} eff TFLOPS  ({100*tf/roof:.1f}% of R/{v}; mma {tf*v:.0f} TF)", flush=True)
     L.bf16x_tune(0, 0, 0)
     ms = timeit(lambda: torch.matmul(A.bfloat16(), B.bfloat16()))
     print(f"torch bf16 matmul (incl casts) n={n}: {ms:.3f} ms", flush=True)
