@@ -255,7 +255,8 @@ def run_ours(args):
     mma_flops = v * 2.0 * m * n_loc * k           # algorithmic BF16 MMA flops per GEMM launch
     achieved = mma_flops / (gemm_ms * 1e-3) / 1e12
     workload = cfg["label"].format(v=v)
-    kname = f"gemm_split_kernel<{bx.default_cta_group()},{v}>"
+    cg = bx.default_cta_group()
+    kname = f"gemm_split_kernel<{cg},{v},256,{2 if cg == 2 else 1}>"
     traffic = _ncu_traffic(f"gemm_split_kernel_v{v}", workload, kname)
     split_bytes = (4 + 2 * p) * (m * k + k * n_loc)
 

@@ -70,6 +70,53 @@ struct KParams {
     unsigned flags;
     float *acc;
     int tiles_m, tiles_n, nkb;
+    // schedule: tiles [0, dp_tiles) data-parallel (one cluster per tile); tiles
+    // [dp_tiles, dp_tiles + sk_tiles) stream-K: their sk_tiles * n_int promotion intervals are
+    // split evenly over the clusters; a tile cut in two is finished by the cluster holding its
+    // first intervals ("owner"), which adds the other part's raw FP32 accumulator (sk_ws,
+    // published with sk_flags = epoch) before the epilogue.
+    int dp_tiles, sk_tiles, n_int;
+    float *sk_ws;
+    unsigned int *sk_flags;
+    unsigned int epoch;
+};
+
+struct Work {
+    int tile, i0, i1;      // promotion intervals [i0, i1) of `tile`
+    int role;              // 0 complete tile, 1 owner of a split tile, 2 contributor
+    int sk_slot;           // stream-K tile index (sk workspace slot)
+};
+
+// Identical on every role of a cluster: data-parallel tiles first, then this cluster's
+// contiguous range of stream-K intervals.
+struct WorkIter {
+    int cid, ncl, dp_next, u, u_end;
+    __device__ __forceinline__ WorkIter(const KParams &p, int cid_, int ncl_) : cid(cid_), ncl(ncl_), dp_next(cid_) {
+        const int64_t U = (int64_t)p.sk_tiles * p.n_int;
+        u = (int)(U * cid / ncl);
+        u_end = (int)(U * (cid + 1) / ncl);
+    }
+    __device__ __forceinline__ bool next(const KParams &p, Work &w) {
+        if (dp_next < p.dp_tiles) {
+            w.tile = dp_next;
+            w.i0 = 0;
+            w.i1 = p.n_int;
+            w.role = 0;
+            w.sk_slot = -1;
+            dp_next += ncl;
+            return true;
+        }
+        if (u >= u_end) return false;
+        const int t = u / p.n_int, j0 = u - t * p.n_int;
+        const int j1 = min(p.n_int, j0 + (u_end - u));
+        w.tile = p.dp_tiles + t;
+        w.i0 = j0;
+        w.i1 = j1;
+        w.role = (j0 == 0) ? ((j1 == p.n_int) ? 0 : 1) : 2;
+        w.sk_slot = t;
+        u += j1 - j0;
+        return true;
+    }
 };
 
 __device__ __forceinline__ void tile_coords(int tile, int tiles_m, int tiles_n, int &tm, int &tn) {
@@ -156,7 +203,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
-    const int num_tiles = p.tiles_m * p.tiles_n;
     const int cid = blockIdx.x / CG, ncl = gridDim.x / CG;
 
     if (warp < 4) {
@@ -165,12 +211,15 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (lane == 0) {
                 int stage = 0;
                 uint32_t phase = 0;
-                for (int tile = cid; tile < num_tiles; tile += ncl) {
+                WorkIter it(p, cid, ncl);
+                Work w;
+                while (it.next(p, w)) {
                     int tm, tn;
-                    tile_coords(tile, p.tiles_m, p.tiles_n, tm, tn);
+                    tile_coords(w.tile, p.tiles_m, p.tiles_n, tm, tn);
                     const int a_row = tm * Cf::TILE_M + (int)rank * kBM;
                     const int b_row = tn * BN + (int)rank * Cf::BN_LOCAL;
-                    for (int kb = 0; kb < p.nkb; ++kb) {
+                    const int kb_end = min(p.nkb, w.i1 * S);
+                    for (int kb = w.i0 * S; kb < kb_end; ++kb) {
                         mbar_wait(&empty[stage], phase ^ 1u);
                         uint8_t *a_dst = sA + stage * Cf::A_STAGE;
                         uint8_t *b_dst = sB + stage * Cf::B_STAGE;
@@ -193,9 +242,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const uint32_t idesc = idesc_bf16_f32(kBM * CG, BN);
                 int stage = 0;
                 uint32_t phase = 0, acc_it = 0;
-                for (int tile = cid; tile < num_tiles; tile += ncl) {
-                    for (int kb = 0; kb < p.nkb; kb += S, ++acc_it) {
-                        const int ns = min(S, p.nkb - kb);
+                WorkIter it(p, cid, ncl);
+                Work w;
+                while (it.next(p, w)) {
+                    const int kb_end = min(p.nkb, w.i1 * S);
+                    for (int kb = w.i0 * S; kb < kb_end; kb += S, ++acc_it) {
+                        const int ns = min(S, kb_end - kb);
                         const uint32_t buf = acc_it & 1u, apar = (acc_it >> 1) & 1u;
                         mbar_wait(&acc_empty[buf], apar ^ 1u);
                         uint32_t a_base[S], b_base[S];
@@ -231,13 +283,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int half = ew >> 2;                 // which half of the accumulator columns
         const uint32_t tm_lane = tmem_base + ((uint32_t)(quad * 32) << 16) + half * EC;
         uint32_t acc_it = 0;
-        for (int tile = cid; tile < num_tiles; tile += ncl) {
+        WorkIter it(p, cid, ncl);
+        Work w;
+        while (it.next(p, w)) {
             int tm, tn;
-            tile_coords(tile, p.tiles_m, p.tiles_n, tm, tn);
+            tile_coords(w.tile, p.tiles_m, p.tiles_n, tm, tn);
             const int row = tm * Cf::TILE_M + (int)rank * kBM + quad * 32 + lane;
             const int col0 = tn * BN + half * EC;
             float G[EC];
-            if (p.flags & BF16X_ACC_IN) {
+            if ((p.flags & BF16X_ACC_IN) && w.i0 == 0) {
 #pragma unroll
                 for (int j = 0; j < EC; ++j)
                     G[j] = (row < p.m && col0 + j < p.n) ? p.acc[(int64_t)(col0 + j) * p.ldc + row] : 0.f;
@@ -245,7 +299,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                 for (int j = 0; j < EC; ++j) G[j] = 0.f;
             }
-            for (int kb = 0; kb < p.nkb; kb += S, ++acc_it) {
+            const int kb_end = min(p.nkb, w.i1 * S);
+            for (int kb = w.i0 * S; kb < kb_end; kb += S, ++acc_it) {
                 const uint32_t buf = acc_it & 1u, apar = (acc_it >> 1) & 1u;
                 mbar_wait(&acc_full[buf], apar);
                 tc_fence_after();
@@ -264,6 +319,25 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if (CG == 1 || rank == 0) mbar_arrive(&acc_empty[buf]);
                     else mbar_arrive_cluster(&acc_empty[buf], 0);
                 }
+            }
+            if (w.role != 0) {
+                // stream-K fix-up: slot layout [sk tile][cta rank][column 0..BN)[row 0..127]
+                float *slot = p.sk_ws + ((size_t)w.sk_slot * CG + rank) * (size_t)BN * kBM;
+                const int lrow = quad * 32 + lane;
+                unsigned int *flag = p.sk_flags + (size_t)w.sk_slot * CG + rank;
+                if (w.role == 2) {
+#pragma unroll
+                    for (int j = 0; j < EC; ++j) __stcg(slot + (size_t)(half * EC + j) * kBM + lrow, G[j]);
+                    __threadfence();
+                    asm volatile("bar.sync 1, %0;" ::"n"(kNumEpiWarps * 32));
+                    if (ew == 0 && lane == 0) st_release_u32(flag, p.epoch);
+                    continue;
+                }
+                if (lane == 0)
+                    while (ld_acquire_u32(flag) != p.epoch) __nanosleep(64);
+                __syncwarp();
+#pragma unroll
+                for (int j = 0; j < EC; ++j) G[j] = __fadd_rn(G[j], __ldcg(slot + (size_t)(half * EC + j) * kBM + lrow));
             }
             if (row < p.m) {
                 float *crow = p.C + row;
@@ -330,6 +404,57 @@ static int make_piece_map(CUtensorMap *map, const uint16_t *base, int k, int row
     return r == CUDA_SUCCESS ? BF16X_SUCCESS : BF16X_ERR_CUDA;
 }
 
+// Stream-K fix-up workspace: partial accumulators + per-(tile, CTA) ready flags.  Flags are
+// zeroed when the buffer is (re)allocated and compared against a per-launch epoch, so no
+// per-launch reset is needed.  Launches on one stream are ordered; concurrent launches on
+// different streams would need their own workspace (documented in bf16x.h).
+static std::mutex g_sk_mu;
+static float *g_sk_ws = nullptr;
+static unsigned int *g_sk_flags = nullptr;
+static size_t g_sk_ws_n = 0, g_sk_flags_n = 0;
+static unsigned int g_sk_epoch = 0;
+
+static int sk_workspace(size_t ws_floats, size_t nflags, float **ws, unsigned int **flags, unsigned int *epoch) {
+    std::lock_guard<std::mutex> g(g_sk_mu);
+    if (ws_floats > g_sk_ws_n) {
+        if (g_sk_ws) { cudaDeviceSynchronize(); cudaFree(g_sk_ws); }
+        g_sk_ws = nullptr;
+        g_sk_ws_n = 0;
+        if (cudaMalloc(&g_sk_ws, ws_floats * sizeof(float)) != cudaSuccess) {
+            cudaGetLastError();
+            set_error_msg("stream-K workspace: allocation failed");
+            return BF16X_ERR_ALLOC;
+        }
+        g_sk_ws_n = ws_floats;
+    }
+    if (nflags > g_sk_flags_n) {
+        if (g_sk_flags) { cudaDeviceSynchronize(); cudaFree(g_sk_flags); }
+        g_sk_flags = nullptr;
+        g_sk_flags_n = 0;
+        if (cudaMalloc(&g_sk_flags, nflags * sizeof(unsigned int)) != cudaSuccess ||
+            cudaMemset(g_sk_flags, 0, nflags * sizeof(unsigned int)) != cudaSuccess) {
+            cudaGetLastError();
+            set_error_msg("stream-K flags: allocation failed");
+            return BF16X_ERR_ALLOC;
+        }
+        g_sk_flags_n = nflags;
+    }
+    if (++g_sk_epoch == 0) ++g_sk_epoch;  // never 0 (the reset value)
+    *ws = g_sk_ws;
+    *flags = g_sk_flags;
+    *epoch = g_sk_epoch;
+    return BF16X_SUCCESS;
+}
+
+void release_gemm_workspace() {
+    std::lock_guard<std::mutex> g(g_sk_mu);
+    if (g_sk_ws) cudaFree(g_sk_ws);
+    if (g_sk_flags) cudaFree(g_sk_flags);
+    g_sk_ws = nullptr;
+    g_sk_flags = nullptr;
+    g_sk_ws_n = g_sk_flags_n = 0;
+}
+
 int num_sms() {
     static int n = 0;
     if (!n) {
@@ -363,6 +488,24 @@ static int launch_t(const GemmPlan &pl, cudaStream_t st) {
     int units = num_sms() / CG;
     if (pl.max_ctas > 0) units = std::max(1, pl.max_ctas / CG);
     const int grid = std::min(tiles, units) * CG;
+    // Hybrid schedule: all full waves but the last run data-parallel; the last full wave plus
+    // the partial one are spread over every cluster by promotion interval (stream-K), so the
+    // partial wave no longer idles most of the GPU.  Disabled for accumulator-carry launches.
+    kp.n_int = (kp.nkb + S - 1) / S;
+    kp.dp_tiles = tiles;
+    kp.sk_tiles = 0;
+    kp.sk_ws = nullptr;
+    kp.sk_flags = nullptr;
+    kp.epoch = 0;
+    const int ncl = grid / CG;
+    if (pl.stream_k != 0 && !(pl.flags & (BF16X_ACC_IN | BF16X_ACC_OUT)) && tiles > ncl && tiles % ncl != 0) {
+        const int full = tiles / ncl;
+        kp.dp_tiles = (full - 1) * ncl;
+        kp.sk_tiles = tiles - kp.dp_tiles;
+        int rc2 = sk_workspace((size_t)kp.sk_tiles * CG * BN * kBM, (size_t)kp.sk_tiles * CG, &kp.sk_ws, &kp.sk_flags,
+                               &kp.epoch);
+        if (rc2) return rc2;
+    }
 
     static bool attr_set = false;  // per template instance
     if (!attr_set) {

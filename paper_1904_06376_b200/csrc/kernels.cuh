@@ -24,6 +24,7 @@ struct GemmPlan {
     int max_ctas;        // 0 = all SMs
     int tile_n;          // reserved (256)
     int stages_per_interval;  // 0 = choose; 1 or 2 stages of 32 k per promotion interval
+    int stream_k;        // 0 = data-parallel only, else hybrid stream-K for the last waves
 };
 
 int launch_gemm_pieces(const GemmPlan &p, cudaStream_t st);
@@ -31,5 +32,6 @@ int launch_scale(int m, int n, float beta, float *C, int ldc, cudaStream_t st);
 int pieces_of(int variant);
 int num_sms();
 int default_cta_group();
+void release_gemm_workspace();
 
 }  // namespace bf16x
