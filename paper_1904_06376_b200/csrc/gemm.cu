@@ -133,17 +133,18 @@ __device__ __forceinline__ void tile_coords(int tile, int tiles_m, int tiles_n, 
 // issued over all K=16 halves of the interval's ns stages (ns <= S) before the next,
 // larger band.  The interval's first MMA overwrites the TMEM accumulator.
 template <int CG, int V, int BN, int S>
-__device__ __forceinline__ void issue_interval(uint32_t d_tmem, const uint32_t (&a_base)[S],
-                                               const uint32_t (&b_base)[S], int ns, uint32_t idesc) {
+__device__ __forceinline__ void issue_interval(uint32_t d_tmem, const uint64_t (&a_desc)[S],
+                                               const uint64_t (&b_desc)[S], int ns, uint32_t idesc) {
     using Cf = Cfg<CG, V, BN>;
     constexpr int H = S * (kBK / kUK);     // K=16 halves per interval (max)
     const int nh = ns * (kBK / kUK);
     bool first = true;
+    // descriptor start-address field is in 16-byte units: piece / K-half offsets add directly
     auto mma = [&](int i, int j, int h) {
         const int st = h / (kBK / kUK), kk = h % (kBK / kUK);
-        const uint64_t ad = smem_desc_kmajor(a_base[st] + i * Cf::A_PIECE + kk * (kUK * 2), kSwizzleAtom, 4);
-        const uint64_t bd = smem_desc_kmajor(b_base[st] + j * Cf::B_PIECE + kk * (kUK * 2), kSwizzleAtom, 4);
-        umma_bf16<CG>(d_tmem, ad, bd, idesc, first ? 0u : 1u);
+        const uint64_t ad = a_desc[st] + (uint64_t)((i * Cf::A_PIECE + kk * (kUK * 2)) >> 4);
+        const uint64_t bd = b_desc[st] + (uint64_t)((j * Cf::B_PIECE + kk * (kUK * 2)) >> 4);
+        umma_bf16_elect<CG>(d_tmem, ad, bd, idesc, first ? 0u : 1u);
         first = false;
     };
     if constexpr (V == 9) {
@@ -238,7 +239,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         } else if (warp == 1) {
             // ------------------------------ MMA issuer --------------------------------
-            if (rank == 0 && lane == 0) {
+            if (rank == 0) {   // warp-uniform loop; one elected lane issues (umma_*_elect)
                 const uint32_t idesc = idesc_bf16_f32(kBM * CG, BN);
                 int stage = 0;
                 uint32_t phase = 0, acc_it = 0;
@@ -250,27 +251,27 @@ __global__ void __launch_bounds__(kThreads, 1)
                         const int ns = min(S, kb_end - kb);
                         const uint32_t buf = acc_it & 1u, apar = (acc_it >> 1) & 1u;
                         mbar_wait(&acc_empty[buf], apar ^ 1u);
-                        uint32_t a_base[S], b_base[S];
+                        uint64_t a_desc[S], b_desc[S];
                         int stages[S];
 #pragma unroll
                         for (int q = 0; q < S; ++q) {
                             stages[q] = stage;
                             if (q < ns) {
                                 mbar_wait(&full[stage], phase);
-                                a_base[q] = smem_u32(sA + stage * Cf::A_STAGE);
-                                b_base[q] = smem_u32(sB + stage * Cf::B_STAGE);
+                                a_desc[q] = smem_desc_kmajor(smem_u32(sA + stage * Cf::A_STAGE), kSwizzleAtom, 4);
+                                b_desc[q] = smem_desc_kmajor(smem_u32(sB + stage * Cf::B_STAGE), kSwizzleAtom, 4);
                                 if (++stage == Cf::STAGES) { stage = 0; phase ^= 1u; }
                             } else {
-                                a_base[q] = a_base[0];
-                                b_base[q] = b_base[0];
+                                a_desc[q] = a_desc[0];
+                                b_desc[q] = b_desc[0];
                             }
                         }
                         tc_fence_after();
-                        issue_interval<CG, V, BN, S>(tmem_base + buf * kTmemBufStride, a_base, b_base, ns, idesc);
+                        issue_interval<CG, V, BN, S>(tmem_base + buf * kTmemBufStride, a_desc, b_desc, ns, idesc);
 #pragma unroll
                         for (int q = 0; q < S; ++q)
-                            if (q < ns) umma_commit<CG>(&empty[stages[q]]);
-                        umma_commit<CG>(&acc_full[buf]);
+                            if (q < ns) umma_commit_elect<CG>(&empty[stages[q]]);
+                        umma_commit_elect<CG>(&acc_full[buf]);
                     }
                 }
             }
