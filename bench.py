@@ -208,10 +208,8 @@ def run_ours(args):
             dist.broadcast(A, src=0)
         if ev is not None:
             ev[0].record(st)
-        bx._check(L.bf16x_split_t(m, k, A.data_ptr(), m, a_pl[0], a_pl[1] if p > 1 else None,
-                                  a_pl[2] if p > 2 else None, kp, sh), "split_t")
-        bx._check(L.bf16x_split(k, n_loc, B.data_ptr(), k, b_pl[0], b_pl[1] if p > 1 else None,
-                                b_pl[2] if p > 2 else None, kp, sh), "split")
+        bx._check(L.bf16x_split_operands(m, n_loc, k, A.data_ptr(), m, B.data_ptr(), k, p, Ap.data_ptr(), kp,
+                                         m * kp, Bp.data_ptr(), kp, n_loc * kp, sh), "split_operands")
         if ev is not None:
             ev[1].record(st)
         bx._check(L.bf16x_gemm_ex(m, n_loc, k, 1.0, None, m, None, k, 0.0, C_loc.data_ptr(), m, v, 0,

@@ -69,6 +69,15 @@ int bf16x_split(int64_t rows, int64_t cols, const float *X, int64_t ldx,
 int bf16x_split_t(int64_t rows, int64_t cols, const float *X, int64_t ldx,
                   uint16_t *P0, uint16_t *P1, uint16_t *P2, int64_t ldp, bf16x_stream_t stream);
 
+/* Both GEMM operands in one launch (the pre-pass bf16x_gemm runs): A (m x k, lda) is split
+ * transposed into K-major pieces (element (i,l) of piece q at Ap[q*a_plane + l + i*ldap]),
+ * B (k x n, ldb) in place (element (l,j) of piece q at Bp[q*b_plane + l + j*ldbp]).
+ *   pieces : 1, 2 or 3 (bf16x3 uses 2, bf16x6/x9 use 3)
+ * Errors: -1 m, -2 n, -3 k, -5 lda, -7 ldb, -8 pieces, -9 Ap/ldap/a_plane, -12 Bp/ldbp/b_plane. */
+int bf16x_split_operands(int m, int n, int k, const float *A, int64_t lda, const float *B, int64_t ldb,
+                         int pieces, uint16_t *Ap, int64_t ldap, int64_t a_plane, uint16_t *Bp, int64_t ldbp,
+                         int64_t b_plane, bf16x_stream_t stream);
+
 /* ------------------------------------------------------------------------------------
  * bf16x_gemm -- C = alpha*A*B + beta*C (BLAS sgemm, transa = transb = 'N') with the
  * FP32 product emulated by BF16 x BF16 -> FP32 tensor-core products (section IV-A):

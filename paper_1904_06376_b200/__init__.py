@@ -48,6 +48,7 @@ def lib() -> ctypes.CDLL:
         L = ctypes.CDLL(LIB_PATH)
         L.bf16x_split.argtypes = [_i64, _i64, _vp, _i64, _vp, _vp, _vp, _i64, _vp]
         L.bf16x_split_t.argtypes = [_i64, _i64, _vp, _i64, _vp, _vp, _vp, _i64, _vp]
+        L.bf16x_split_operands.argtypes = [_i, _i, _i, _vp, _i64, _vp, _i64, _i, _vp, _i64, _i64, _vp, _i64, _i64, _vp]
         L.bf16x_gemm.argtypes = [_i, _i, _i, _f, _vp, _i, _vp, _i, _f, _vp, _i, _i]
         L.bf16x_gemm_workspace_size.argtypes = [_i, _i, _i, _i]
         L.bf16x_gemm_workspace_size.restype = ctypes.c_size_t

@@ -107,6 +107,18 @@ int gemm_core(int m, int n, int k, float alpha, const float *A, int lda, const f
             if (rc) return rc;
         }
     }
+    if (!Ap && !Bp) {   // both operands: one fused launch
+        uint16_t *a = (uint16_t *)w;
+        a_plane = (int64_t)m * kp;
+        ldap = kp;
+        uint16_t *b = a + p * a_plane;
+        b_plane = (int64_t)n * kp;
+        ldbp = kp;
+        rc = launch_split_ab(m, n, k, A, lda, a, ldap, a_plane, B, ldb, b, ldbp, b_plane, p, st);
+        if (rc) return rc;
+        Ap = a;
+        Bp = b;
+    }
     if (!Ap) {
         uint16_t *a = (uint16_t *)w;
         a_plane = (int64_t)m * kp;

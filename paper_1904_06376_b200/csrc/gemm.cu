@@ -203,6 +203,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     if constexpr (CG == 2) cluster_sync(); else __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    // Programmatic dependent launch: everything above overlapped the previous kernel's tail;
+    // from here on we read its outputs (the pieces) and may overwrite what it read.
+    asm volatile("griddepcontrol.wait;" ::: "memory");
 
     const int cid = blockIdx.x / CG, ncl = gridDim.x / CG;
 
@@ -520,13 +523,15 @@ static int launch_t(const GemmPlan &pl, cudaStream_t st) {
     cfg.blockDim = dim3(kThreads);
     cfg.dynamicSmemBytes = Cf::SMEM;
     cfg.stream = st;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = CG;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = 2;
     cudaError_t e = cudaLaunchKernelEx(&cfg, gemm_split_kernel<CG, V, BN, S>, tmA, tmB, kp);
     if (e != cudaSuccess) {
         set_cuda_error(e, "gemm launch");

@@ -8,6 +8,9 @@ namespace bf16x {
 int launch_split(int64_t rows, int64_t cols, const float *X, int64_t ldx, uint16_t *P0, uint16_t *P1,
                  uint16_t *P2, int64_t ldp, bool transpose, cudaStream_t st);
 
+int launch_split_ab(int m, int n, int k, const float *A, int64_t lda, uint16_t *Ap, int64_t ldap, int64_t a_plane,
+                    const float *B, int64_t ldb, uint16_t *Bp, int64_t ldbp, int64_t b_plane, int np, cudaStream_t st);
+
 struct GemmPlan {
     int m, n, k;
     float alpha, beta;

@@ -54,13 +54,13 @@ __device__ __forceinline__ void split_pair(float lo, float hi, uint32_t (&p)[3])
 // 16-byte vector loads/stores when the whole matrix is 16-byte aligned (vec != 0).
 // ---------------------------------------------------------------------------------
 template <int NP>
-__global__ void __launch_bounds__(256) split_same_kernel(int64_t rows, int64_t cols, const float *__restrict__ X,
-                                                         int64_t ldx, uint16_t *__restrict__ P0,
-                                                         uint16_t *__restrict__ P1, uint16_t *__restrict__ P2,
-                                                         int64_t ldp, int vec) {
+__device__ __forceinline__ void split_same_body(int64_t rows, int64_t cols, const float *__restrict__ X, int64_t ldx,
+                                                uint16_t *__restrict__ P0, uint16_t *__restrict__ P1,
+                                                uint16_t *__restrict__ P2, int64_t ldp, int vec, int64_t vblock,
+                                                int64_t vgrid) {
     const int64_t nchunk = (rows + 7) / 8;
     const int64_t total = nchunk * cols;
-    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    for (int64_t t = vblock * blockDim.x + threadIdx.x; t < total; t += vgrid * blockDim.x) {
         const int64_t col = t / nchunk, ch = t - col * nchunk;
         const float *x = X + col * ldx;
         const int64_t o = col * ldp;
@@ -89,6 +89,15 @@ __global__ void __launch_bounds__(256) split_same_kernel(int64_t rows, int64_t c
     }
 }
 
+template <int NP>
+__global__ void __launch_bounds__(256) split_same_kernel(int64_t rows, int64_t cols, const float *__restrict__ X,
+                                                         int64_t ldx, uint16_t *__restrict__ P0,
+                                                         uint16_t *__restrict__ P1, uint16_t *__restrict__ P2,
+                                                         int64_t ldp, int vec) {
+    asm volatile("griddepcontrol.launch_dependents;");
+    split_same_body<NP>(rows, cols, X, ldx, P0, P1, P2, ldp, vec, blockIdx.x, gridDim.x);
+}
+
 // ---------------------------------------------------------------------------------
 // transposed: 64 (source rows) x 64 (source columns) tiles.  Warp w loads source columns
 // [8w, 8w+8) of the tile: lane = (row quad mq: 0..15) + 16 * (column pair half); every lane
@@ -99,11 +108,10 @@ __global__ void __launch_bounds__(256) split_same_kernel(int64_t rows, int64_t c
 constexpr int TT = 64;
 constexpr int TW = TT / 2 + 1;   // words per smem row (+1 pad)
 template <int NP>
-__global__ void __launch_bounds__(256) split_trans_kernel(int64_t rows, int64_t cols, const float *__restrict__ X,
-                                                          int64_t ldx, uint16_t *__restrict__ P0,
-                                                          uint16_t *__restrict__ P1, uint16_t *__restrict__ P2,
-                                                          int64_t ldp, int vec) {
-    __shared__ uint32_t s[NP][TT][TW];
+__device__ __forceinline__ void split_trans_body(int64_t rows, int64_t cols, const float *__restrict__ X, int64_t ldx,
+                                                 uint16_t *__restrict__ P0, uint16_t *__restrict__ P1,
+                                                 uint16_t *__restrict__ P2, int64_t ldp, int vec, int64_t vblock,
+                                                 int64_t vgrid, uint32_t (&s)[3][TT][TW]) {
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int mq = lane & 15, half = lane >> 4;
     const int64_t tiles_r = (rows + TT - 1) / TT, tiles_c = (cols + TT - 1) / TT;
@@ -111,7 +119,7 @@ __global__ void __launch_bounds__(256) split_trans_kernel(int64_t rows, int64_t 
     const bool out_words = (ldp % 2 == 0) && ((reinterpret_cast<uintptr_t>(P0) & 3u) == 0) &&
                            (!P1 || (reinterpret_cast<uintptr_t>(P1) & 3u) == 0) &&
                            (!P2 || (reinterpret_cast<uintptr_t>(P2) & 3u) == 0);
-    for (int64_t t = blockIdx.x; t < tiles_r * tiles_c; t += gridDim.x) {
+    for (int64_t t = vblock; t < tiles_r * tiles_c; t += vgrid) {
         const int64_t r0 = (t % tiles_r) * TT, c0 = (t / tiles_r) * TT;
         const bool full = (r0 + TT <= rows) && (c0 + TT <= cols) && vec;
 #pragma unroll
@@ -164,6 +172,35 @@ __global__ void __launch_bounds__(256) split_trans_kernel(int64_t rows, int64_t 
     }
 }
 
+template <int NP>
+__global__ void __launch_bounds__(256) split_trans_kernel(int64_t rows, int64_t cols, const float *__restrict__ X,
+                                                          int64_t ldx, uint16_t *__restrict__ P0,
+                                                          uint16_t *__restrict__ P1, uint16_t *__restrict__ P2,
+                                                          int64_t ldp, int vec) {
+    __shared__ uint32_t s[3][TT][TW];
+    asm volatile("griddepcontrol.launch_dependents;");
+    split_trans_body<NP>(rows, cols, X, ldx, P0, P1, P2, ldp, vec, blockIdx.x, gridDim.x, s);
+}
+
+// Both GEMM operands in one launch: blocks [0, gA) split A transposed (K-major pieces),
+// blocks [gA, grid) split B in place.  One ramp-up/tail instead of two.
+struct SplitArgs {
+    int64_t rows, cols, ldx, ldp;
+    const float *X;
+    uint16_t *P0, *P1, *P2;
+    int vec;
+};
+template <int NP>
+__global__ void __launch_bounds__(256) split_ab_kernel(SplitArgs a, SplitArgs b, int gA) {
+    __shared__ uint32_t s[3][TT][TW];
+    asm volatile("griddepcontrol.launch_dependents;");   // let the GEMM's prologue start early
+    if ((int)blockIdx.x < gA)
+        split_trans_body<NP>(a.rows, a.cols, a.X, a.ldx, a.P0, a.P1, a.P2, a.ldp, a.vec, blockIdx.x, gA, s);
+    else
+        split_same_body<NP>(b.rows, b.cols, b.X, b.ldx, b.P0, b.P1, b.P2, b.ldp, b.vec, blockIdx.x - gA,
+                            gridDim.x - gA);
+}
+
 static int sm_count() {
     static int n = 0;
     if (!n) {
@@ -205,6 +242,25 @@ int launch_split(int64_t rows, int64_t cols, const float *X, int64_t ldx, uint16
     return check_launch("split");
 }
 
+int launch_split_ab(int m, int n, int k, const float *A, int64_t lda, uint16_t *Ap, int64_t ldap, int64_t a_plane,
+                    const float *B, int64_t ldb, uint16_t *Bp, int64_t ldbp, int64_t b_plane, int np, cudaStream_t st) {
+    if (m == 0 || n == 0 || k == 0) return BF16X_SUCCESS;
+    SplitArgs a{m, k, lda, ldap, A, Ap, np > 1 ? Ap + a_plane : nullptr, np > 2 ? Ap + 2 * a_plane : nullptr, 0};
+    SplitArgs b{k, n, ldb, ldbp, B, Bp, np > 1 ? Bp + b_plane : nullptr, np > 2 ? Bp + 2 * b_plane : nullptr, 0};
+    a.vec = ((reinterpret_cast<uintptr_t>(A) & 15u) == 0) && lda % 4 == 0;
+    b.vec = ((reinterpret_cast<uintptr_t>(B) & 15u) == 0) && ldb % 4 == 0 &&
+            ((reinterpret_cast<uintptr_t>(Bp) & 15u) == 0) && ldbp % 8 == 0 && b_plane % 8 == 0;
+    const int64_t grid = (int64_t)sm_count() * 8;
+    const double wa = (double)m * k, wb = (double)k * n;
+    int gA = (int)(grid * wa / (wa + wb));
+    gA = gA < 1 ? 1 : (gA > grid - 1 ? (int)grid - 1 : gA);
+    if (np == 1) split_ab_kernel<1><<<(unsigned)grid, 256, 0, st>>>(a, b, gA);
+    else if (np == 2) split_ab_kernel<2><<<(unsigned)grid, 256, 0, st>>>(a, b, gA);
+    else split_ab_kernel<3><<<(unsigned)grid, 256, 0, st>>>(a, b, gA);
+    count_launch();
+    return check_launch("split_ab");
+}
+
 }  // namespace bf16x
 
 using namespace bf16x;
@@ -227,6 +283,23 @@ extern "C" int bf16x_split(int64_t rows, int64_t cols, const float *X, int64_t l
     int ok = arch_ok();
     if (ok) return ok;
     return launch_split(rows, cols, X, ldx, P0, P1, P2, ldp, false, (cudaStream_t)stream);
+}
+
+extern "C" int bf16x_split_operands(int m, int n, int k, const float *A, int64_t lda, const float *B, int64_t ldb,
+                                    int pieces, uint16_t *Ap, int64_t ldap, int64_t a_plane, uint16_t *Bp,
+                                    int64_t ldbp, int64_t b_plane, bf16x_stream_t stream) {
+    if (m < 0) return -1;
+    if (n < 0) return -2;
+    if (k < 0) return -3;
+    if (lda < (m > 1 ? m : 1)) return -5;
+    if (ldb < (k > 1 ? k : 1)) return -7;
+    if (pieces < 1 || pieces > 3) return -8;
+    if (!Ap || ldap < (k > 1 ? k : 1) || a_plane < ldap * (int64_t)m) return -9;
+    if (!Bp || ldbp < (k > 1 ? k : 1) || b_plane < ldbp * (int64_t)n) return -12;
+    int ok = arch_ok();
+    if (ok) return ok;
+    return launch_split_ab(m, n, k, A, lda, Ap, ldap, a_plane, B, ldb, Bp, ldbp, b_plane, pieces,
+                           (cudaStream_t)stream);
 }
 
 extern "C" int bf16x_split_t(int64_t rows, int64_t cols, const float *X, int64_t ldx, uint16_t *P0, uint16_t *P1,
