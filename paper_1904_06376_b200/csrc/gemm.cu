@@ -354,12 +354,19 @@ __global__ void __launch_bounds__(kThreads, 1)
                     for (int j = 0; j < EC; ++j)
                         if (col0 + j < p.n) __stcs(crow + (int64_t)(col0 + j) * p.ldc, fmaf(p.alpha, G[j], 0.f));
                 } else {
+                    // beta != 0: batch 8 independent loads of C before the FMAs and stores, so
+                    // the old values stream in parallel instead of one round trip per column
 #pragma unroll
-                    for (int j = 0; j < EC; ++j)
-                        if (col0 + j < p.n) {
-                            float *c = crow + (int64_t)(col0 + j) * p.ldc;
-                            *c = fmaf(p.alpha, G[j], p.beta * *c);
-                        }
+                    for (int j0 = 0; j0 < EC; j0 += 8) {
+                        float cold[8];
+#pragma unroll
+                        for (int j = 0; j < 8; ++j)
+                            cold[j] = (col0 + j0 + j < p.n) ? __ldcs(crow + (int64_t)(col0 + j0 + j) * p.ldc) : 0.f;
+#pragma unroll
+                        for (int j = 0; j < 8; ++j)
+                            if (col0 + j0 + j < p.n)
+                                __stcs(crow + (int64_t)(col0 + j0 + j) * p.ldc, fmaf(p.alpha, G[j0 + j], p.beta * cold[j]));
+                    }
                 }
             }
         }

@@ -4,10 +4,9 @@
 // precision").
 //
 //   factor (FP32, in a device copy of A), blocked right-looking, panel width nb:
-//     K4 panel_kernel   cooperative grid, one grid barrier per column: pivot search (argmax |a|,
-//                       ties -> lowest row), L multipliers and the rank-1 updates restricted to
-//                       the panel, rows left in place (pivoted rows are marked instead of
-//                       swapped) -- the LAPACK interchange sequence is derived afterwards
+//     K4 subpanel_kernel    32-column sub-panels on one thread-block cluster (8-16 CTAs, rows in
+//                           shared memory, pivot exchange through DSMEM + cluster barrier);
+//        panel_update_kernel   TRSM + rank-32 update of the rest of the 256-wide panel
 //     K5 laswp_kernel   applies the panel's interchanges to all n columns
 //        trsm_kernel    U12 = L11^-1 A12 (FP32, unit lower)
 //     K2 bf16x GEMM     A22 <- -1 * L21 U12 + 1 * A22 in bf16x<variant>   (the cubic work)
@@ -15,8 +14,12 @@
 //     K6 residual       r = b - A x, deterministic two-phase row sums
 //        trsv_kernel    cooperative blocked forward / backward substitution
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <vector>
+
+#include <cooperative_groups.h>
 
 #include "common.cuh"
 #include "kernels.cuh"
@@ -78,51 +81,74 @@ __device__ __forceinline__ bool better(float v, int i, float bv, int bi) {
     return v > bv || (v == bv && i < bi);  // larger |a|, ties -> lowest row index
 }
 
+// 4-byte global -> shared copy that does not occupy a register until it lands (LDGSTS), so
+// tile-staging loops keep many loads in flight; finish with async_wait_all().
+__device__ __forceinline__ void async_copy_f32(float *dst, const float *src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void async_wait_all() {
+    asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+}
+
 // ------------------------------------------------------------------------------------
-// K4: panel factorisation of columns [j0, j0+jb) over rows [j0, n).  Rows are split into
-// contiguous chunks, one per CTA, held in shared memory for the whole panel ([col][row]).
-// Step t (column c = j0+t):
+// K4: panel factorisation by sub-panels of kSubW columns.  Each sub-panel [s0, s0+w) is
+// factored over rows [s0, n) by one thread-block cluster: the rows are split in contiguous
+// chunks over the cluster's CTAs and held in shared memory ([col][row]).  Step t (column
+// c = s0+t):
 //   (a) unpivoted rows apply step t-1: l = a[i,c-1] / p[c-1] stored in place (the L
-//       multiplier), a[i,c'] -= l * p[c'] for panel columns c' >= c, p = pivot row of step t-1;
-//   (b) local argmax |a[i,c]| over unpivoted rows; the CTA publishes (|a|, row) and that row's
-//       entries c..j0+jb-1; grid barrier;
-//   (c) every CTA reduces the candidates identically (ties -> lowest row, LAPACK isamax on
-//       the unswapped order) and copies the winner's row; the owner marks it pivoted.
-// Rows are not moved: the LAPACK interchange sequence is derived afterwards (build_ipiv).
+//       multiplier), a[i,c'] -= l * p[c'] for c' >= c, p = pivot row of step t-1;
+//   (b) local argmax |a[i,c]| over unpivoted rows (ties -> lowest row, LAPACK isamax on the
+//       unswapped order); the CTA publishes (|a|, row) and that row's entries in its own
+//       shared memory; cluster barrier;
+//   (c) every CTA reads the candidates and the winner's row through distributed shared memory
+//       (identical reduction everywhere); the owner marks its row pivoted.
+// Rows are not moved inside the sub-panel: the LAPACK interchange sequence is derived
+// afterwards (build_ipiv_kernel) and applied to the panel columns (laswp_kernel); the
+// remaining panel columns then receive the sub-panel's TRSM + rank-w update
+// (panel_update_kernel).  All panel arithmetic is FP32.
 // ------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(kLuThreads) panel_kernel(float *LU, int ld, int n, int j0, int jb, int rl_max,
-                                                           PivotCand *cand, float *cand_rows, int *piv_rows,
-                                                           int *info, GridBar gb, unsigned int epoch) {
-    extern __shared__ float sp[];            // [jb][rl_max] panel rows, then prow[jb], then marks
-    float *prow = sp + (size_t)jb * rl_max;
-    unsigned char *smark = reinterpret_cast<unsigned char *>(prow + jb);
-    __shared__ float s_v[kLuThreads / 32];
-    __shared__ int s_i[kLuThreads / 32];
-    __shared__ int s_p, s_owner_e;
-    const int nbk = gridDim.x, b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    const int nw = blockDim.x >> 5;
-    const int R = n - j0;
-    const int r0 = j0 + (int)(((int64_t)R * b) / nbk), r1 = j0 + (int)(((int64_t)R * (b + 1)) / nbk);
+constexpr int kSubW = 32;
+constexpr int kSubThreads = 512;
+
+__global__ void __launch_bounds__(kSubThreads) subpanel_kernel(float *LU, int ld, int n, int s0, int w, int rl_max,
+                                                              int *piv_rows, int *info) {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cl = cg::this_cluster();
+    const int ncta = (int)cl.num_blocks(), rank = (int)cl.block_rank();
+    extern __shared__ float sm[];
+    float *sp = sm;                                  // [w][rl_max]
+    float *prow = sp + (size_t)w * rl_max;           // [w]    pivot row of the current step
+    float *crow = prow + w;                          // [2][w] this CTA's candidate row
+    float *cval = crow + 2 * w;                      // [2]    candidate |a|
+    int *cidx = reinterpret_cast<int *>(cval + 2);   // [2]    candidate row
+    unsigned char *smark = reinterpret_cast<unsigned char *>(cidx + 2);
+    __shared__ float s_v[kSubThreads / 32];
+    __shared__ int s_i[kSubThreads / 32];
+    __shared__ int s_wr, s_gi;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
+    const int R = n - s0;
+    const int r0 = s0 + (int)(((int64_t)R * rank) / ncta), r1 = s0 + (int)(((int64_t)R * (rank + 1)) / ncta);
     const int rl = r1 - r0;
-    for (int cc = wid; cc < jb; cc += nw)
-        for (int e = lane; e < rl; e += 32) sp[cc * rl_max + e] = LU[(int64_t)(j0 + cc) * ld + r0 + e];
+    for (int cc = wid; cc < w; cc += nw)
+        for (int e = lane; e < rl; e += 32) async_copy_f32(sp + cc * rl_max + e, LU + (int64_t)(s0 + cc) * ld + r0 + e);
     for (int e = tid; e < rl; e += blockDim.x) smark[e] = 0;
+    async_wait_all();
     __syncthreads();
-    for (int t = 0; t <= jb; ++t) {
+    for (int t = 0; t <= w; ++t) {
         if (t > 0) {
             const int tp = t - 1;
             const float piv = prow[tp];
             for (int e = tid; e < rl; e += blockDim.x)
                 if (!smark[e]) sp[tp * rl_max + e] = (piv != 0.f) ? sp[tp * rl_max + e] / piv : 0.f;
             __syncthreads();
-            for (int cc = t + wid; cc < jb; cc += nw) {
+            for (int cc = t + wid; cc < w; cc += nw) {
                 const float u = prow[cc];
                 for (int e = lane; e < rl; e += 32)
                     if (!smark[e]) sp[cc * rl_max + e] = sp[cc * rl_max + e] - sp[tp * rl_max + e] * u;
             }
             __syncthreads();
         }
-        if (t == jb) break;
+        if (t == w) break;
         float bv = -1.f;
         int bi = 0x7FFFFFFF;
         for (int e = tid; e < rl; e += blockDim.x) {
@@ -138,48 +164,136 @@ __global__ void __launch_bounds__(kLuThreads) panel_kernel(float *LU, int ld, in
         if (lane == 0) { s_v[wid] = bv; s_i[wid] = bi; }
         __syncthreads();
         if (tid == 0) {
-            for (int w = 1; w < nw; ++w)
-                if (better(s_v[w], s_i[w], bv, bi)) { bv = s_v[w]; bi = s_i[w]; }
-            cand[(t & 1) * nbk + b] = {bv, bi};
-            s_owner_e = (bi >= r0 && bi < r1) ? bi - r0 : -1;
+            for (int q = 1; q < nw; ++q)
+                if (better(s_v[q], s_i[q], bv, bi)) { bv = s_v[q]; bi = s_i[q]; }
+            cval[t & 1] = bv;
+            cidx[t & 1] = bi;
+            s_gi = (bi >= r0 && bi < r1) ? bi - r0 : -1;
         }
         __syncthreads();
-        if (s_owner_e >= 0) {
-            float *dst = cand_rows + ((size_t)(t & 1) * nbk + b) * jb;
-            for (int cc = t + tid; cc < jb; cc += blockDim.x) dst[cc] = sp[cc * rl_max + s_owner_e];
-        }
-        grid_sync(gb, epoch + t);
+        if (s_gi >= 0)
+            for (int cc = t + tid; cc < w; cc += blockDim.x) crow[(t & 1) * w + cc] = sp[cc * rl_max + s_gi];
+        cl.sync();
         if (tid < 32) {
             float gv = -1.f;
-            int gi = 0x7FFFFFFF, gb_ = 0;
-            for (int k = tid; k < nbk; k += 32) {
-                const float2 raw = __ldcg(reinterpret_cast<const float2 *>(cand + (t & 1) * nbk + k));
-                const float v = raw.x;
-                const int i = __float_as_int(raw.y);
-                if (better(v, i, gv, gi)) { gv = v; gi = i; gb_ = k; }
+            int gi = 0x7FFFFFFF, gr = 0;
+            for (int q = tid; q < ncta; q += 32) {
+                const float v = *cl.map_shared_rank(&cval[t & 1], q);
+                const int i = *cl.map_shared_rank(&cidx[t & 1], q);
+                if (better(v, i, gv, gi)) { gv = v; gi = i; gr = q; }
             }
             for (int o = 16; o > 0; o >>= 1) {
                 const float ov = __shfl_xor_sync(0xffffffffu, gv, o);
                 const int oi = __shfl_xor_sync(0xffffffffu, gi, o);
-                const int ob = __shfl_xor_sync(0xffffffffu, gb_, o);
-                if (better(ov, oi, gv, gi)) { gv = ov; gi = oi; gb_ = ob; }
+                const int orr = __shfl_xor_sync(0xffffffffu, gr, o);
+                if (better(ov, oi, gv, gi)) { gv = ov; gi = oi; gr = orr; }
             }
             if (tid == 0) {
-                s_p = gb_;
+                s_wr = gr;
                 if (gi >= r0 && gi < r1) smark[gi - r0] = 1;
-                if (b == 0) {
+                if (rank == 0) {
                     piv_rows[t] = gi;
-                    if (gv == 0.f && *info == 0) *info = j0 + t + 1;
+                    if (gv == 0.f && *info == 0) *info = s0 + t + 1;
                 }
             }
         }
         __syncthreads();
-        const float *src = cand_rows + ((size_t)(t & 1) * nbk + s_p) * jb;
-        for (int cc = t + tid; cc < jb; cc += blockDim.x) prow[cc] = __ldcg(src + cc);
+        const float *src = cl.map_shared_rank(crow, s_wr) + (t & 1) * w;
+        for (int cc = t + tid; cc < w; cc += blockDim.x) prow[cc] = src[cc];
         __syncthreads();
     }
-    for (int cc = wid; cc < jb; cc += nw)
-        for (int e = lane; e < rl; e += 32) LU[(int64_t)(j0 + cc) * ld + r0 + e] = sp[cc * rl_max + e];
+    for (int cc = wid; cc < w; cc += nw)
+        for (int e = lane; e < rl; e += 32) LU[(int64_t)(s0 + cc) * ld + r0 + e] = sp[cc * rl_max + e];
+    cl.sync();   // peers may still read this CTA's candidate row
+}
+
+// After sub-panel [s0, s0+w) (rows already interchanged): remaining panel columns [c1, c2)
+// get U = L11^-1 A[s0:s0+w, c1:c2] (L11 unit lower w x w; every block recomputes it, block 0
+// stores it) and rows [c1, n) get A -= L21 U.  64 rows per block.
+constexpr int kUpdRows = 64;
+__global__ void __launch_bounds__(256) panel_update_kernel(float *LU, int ld, int n, int s0, int w, int c1, int c2) {
+    extern __shared__ float su[];
+    const int nc = c2 - c1;
+    float *sU = su;                           // [w][nc]
+    float *sL11 = sU + (size_t)w * nc;        // [w][w]   (row r, col i) at r*w + i
+    float *sL21 = sL11 + (size_t)w * w;       // [w][kUpdRows] (col t, row r)
+    const int tid = threadIdx.x;
+    for (int e = tid; e < w * nc; e += blockDim.x) {
+        const int r = e % w, c = e / w;
+        async_copy_f32(sU + r * nc + c, LU + (int64_t)(c1 + c) * ld + s0 + r);
+    }
+    for (int e = tid; e < w * w; e += blockDim.x) {
+        const int r = e % w, i = e / w;
+        async_copy_f32(sL11 + r * w + i, LU + (int64_t)(s0 + i) * ld + s0 + r);
+    }
+    const int rb = c1 + blockIdx.x * kUpdRows;
+    const int nr = min(kUpdRows, n - rb);
+    for (int e = tid; e < w * kUpdRows; e += blockDim.x) {
+        const int r = e % kUpdRows, t = e / kUpdRows;
+        if (r < nr) async_copy_f32(sL21 + t * kUpdRows + r, LU + (int64_t)(s0 + t) * ld + rb + r);
+        else sL21[t * kUpdRows + r] = 0.f;
+    }
+    async_wait_all();
+    __syncthreads();
+    for (int c = tid; c < nc; c += blockDim.x)       // forward substitution per column
+        for (int i = 0; i < w - 1; ++i) {
+            const float xi = sU[i * nc + c];
+            for (int r = i + 1; r < w; ++r) sU[r * nc + c] -= sL11[r * w + i] * xi;
+        }
+    __syncthreads();
+    if (blockIdx.x == 0)
+        for (int e = tid; e < w * nc; e += blockDim.x) {
+            const int r = e % w, c = e / w;
+            LU[(int64_t)(c1 + c) * ld + s0 + r] = sU[r * nc + c];
+        }
+    // 8 outputs per round: their old values are loaded together (independent loads in flight)
+    const int nout = kUpdRows * nc;
+    for (int e0 = tid; e0 < nout; e0 += 8 * blockDim.x) {
+        float old[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const int e = e0 + q * blockDim.x;
+            const int r = e % kUpdRows, c = e / kUpdRows;
+            old[q] = (e < nout && r < nr) ? LU[(int64_t)(c1 + c) * ld + rb + r] : 0.f;
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const int e = e0 + q * blockDim.x;
+            const int r = e % kUpdRows, c = e / kUpdRows;
+            if (e >= nout || r >= nr) continue;
+            float acc = 0.f;
+            for (int t = 0; t < w; ++t) acc = fmaf(sL21[t * kUpdRows + r], sU[t * nc + c], acc);
+            LU[(int64_t)(c1 + c) * ld + rb + r] = old[q] - acc;
+        }
+    }
+}
+
+// Gather pairs (dst <- src) for an interchange sequence ipiv[j0 .. j0+jb) applied in order.
+__global__ void build_pairs_kernel(int n, int j0, int jb, const int *ipiv, int *pos, int *row_at, int2 *pairs,
+                                   int *npairs) {
+    for (int i = j0 + threadIdx.x; i < n; i += blockDim.x) { pos[i] = i; row_at[i] = i; }
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    for (int t = 0; t < jb; ++t) {
+        const int here = j0 + t, q = ipiv[here];
+        if (q == here) continue;
+        const int a = row_at[here], b = row_at[q];
+        row_at[here] = b; pos[b] = here;
+        row_at[q] = a; pos[a] = q;
+    }
+    int np = 0;
+    for (int t = 0; t < jb; ++t) {
+        const int here = j0 + t;
+        if (row_at[here] != here) pairs[np++] = make_int2(here, row_at[here]);
+    }
+    for (int t = 0; t < jb; ++t) {
+        const int q = ipiv[j0 + t];
+        if (q >= j0 + jb && row_at[q] != q && pos[q] != -1) {
+            pairs[np++] = make_int2(q, row_at[q]);
+            pos[q] = -1;
+        }
+    }
+    *npairs = np;
 }
 
 // LAPACK interchange sequence from the chosen physical rows: step t swaps position j0+t with
@@ -246,14 +360,18 @@ __global__ void __launch_bounds__(256) trsm_kernel(float *LU, int ld, int j0, in
     const int cb = c0 + blockIdx.x * kTrsmCols;
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;   // 32 columns x 8 row groups
     const bool valid = (cb + tx) < c0 + ncols;
-    for (int r = ty; r < jb; r += 8) sB[r * kTrsmCols + tx] = valid ? LU[(int64_t)(cb + tx) * ld + j0 + r] : 0.f;
+    for (int r = ty; r < jb; r += 8) {
+        if (valid) async_copy_f32(sB + r * kTrsmCols + tx, LU + (int64_t)(cb + tx) * ld + j0 + r);
+        else sB[r * kTrsmCols + tx] = 0.f;
+    }
     for (int i0 = 0; i0 < jb; i0 += 32) {
         const int ib = min(32, jb - i0);
         __syncthreads();
         for (int e = threadIdx.x; e < (jb - i0) * ib; e += blockDim.x) {
             const int r = e % (jb - i0), c = e / (jb - i0);
-            sL[r * 33 + c] = LU[(int64_t)(j0 + i0 + c) * ld + j0 + i0 + r];
+            async_copy_f32(sL + r * 33 + c, LU + (int64_t)(j0 + i0 + c) * ld + j0 + i0 + r);
         }
+        async_wait_all();
         __syncthreads();
         for (int i = 0; i < ib - 1; ++i) {
             const float xi = sB[(i0 + i) * kTrsmCols + tx];
@@ -280,9 +398,13 @@ __global__ void residual_partial_kernel(const float *A, int ld, int n, const dou
     const int j0 = blockIdx.y * kResChunk, j1 = min(n, j0 + kResChunk);
     if (i >= n) return;
     double s = 0.0;
-    for (int j = j0; j < j1; ++j) {
-        const double a = (double)A[(int64_t)j * ld + i];
-        s += absval ? fabs(a) : a * x[j];
+    for (int jb = j0; jb < j1; jb += 16) {
+        float a[16];
+#pragma unroll
+        for (int q = 0; q < 16; ++q) a[q] = (jb + q < j1) ? __ldg(A + (int64_t)(jb + q) * ld + i) : 0.f;
+#pragma unroll
+        for (int q = 0; q < 16; ++q)
+            if (jb + q < j1) s += absval ? fabs((double)a[q]) : (double)a[q] * x[jb + q];
     }
     part[(int64_t)blockIdx.y * n + i] = s;
 }
@@ -331,57 +453,130 @@ __global__ void gather_kernel(int n, const int *perm, const double *v, double *y
     if (i < n) y[i] = v[perm[i]];
 }
 
+constexpr int kTrsvBlock = 128;
+
+constexpr int kTS = kTrsvBlock + 4;   // smem column stride (floats): 16-byte aligned columns
+constexpr int kTrsvSmem = 2 * kTrsvBlock * kTS * sizeof(float) + 3 * kTrsvBlock * sizeof(double);
+
+// acc = sum_{j < pw} LU[(pc0 + j) * ld + r] * sx[j], 16 independent loads in flight per batch
+// acc = sum_{j < pw} LU[(pc0 + j) * ld + r] * sx[j] (pw <= kTrsvBlock): all loads are issued
+// before the first FMA, so the row costs one memory round trip.
+__device__ __forceinline__ double dot_col_block(const float *LU, int64_t ld, int pc0, int pw, int r, const double *sx) {
+    float a[kTrsvBlock];
+#pragma unroll
+    for (int q = 0; q < kTrsvBlock; ++q) a[q] = (q < pw) ? __ldg(LU + (int64_t)(pc0 + q) * ld + r) : 0.f;
+    double acc = 0.0;
+#pragma unroll
+    for (int q = 0; q < kTrsvBlock; ++q) acc = fma((double)a[q], (q < pw) ? sx[q] : 0.0, acc);
+    return acc;
+}
+
+// Asynchronously copy the rows x cols tile LU[r0.., c0..] into smem [col][kTS] (LDGSTS).
+__device__ __forceinline__ void prefetch_tile(float *dst, const float *LU, int64_t ld, int r0, int rows, int c0,
+                                              int cols) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int c = wid; c < cols; c += nw) {
+        const float *src = LU + (int64_t)(c0 + c) * ld + r0;
+        for (int r = lane; r < rows; r += 32)
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst + c * kTS + r)), "l"(src + r)
+                         : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+}
+
 // Blocked triangular solve in FP64 with the FP32 factors, cooperative grid.  lower != 0:
-// L y = y (unit diagonal, forward); else U y = y (backward).  Step s handles block b_s: CTA 0
-// applies the previous block's solution to b_s's rows and solves b_s's diagonal triangle in
-// shared memory, while CTAs 1.. apply the previous block to every other dependent row; one
+// L y = y (unit diagonal, forward); else U y = y (backward).  Step s handles block b_s (128
+// rows): CTA 0 owns the critical path -- the block's diagonal tile and the tile coupling it to
+// the previous block were prefetched into shared memory (cp.async) during the previous
+// barrier, so it applies the previous block to b_s's rows, solves the diagonal triangle and
+// publishes x_{b_s}; CTAs 1.. apply the previous block to every other dependent row.  One
 // grid barrier per block.  y is accessed with L2-coherent loads/stores.
-constexpr int kTrsvBlock = 64;
 __global__ void __launch_bounds__(256) trsv_kernel(const float *LU, int ld, int n, double *y, int lower, GridBar gb,
                                                    unsigned int epoch) {
-    __shared__ double sx[kTrsvBlock];      // solution of the previous block
-    __shared__ double sy[kTrsvBlock];      // right-hand side of the current block (CTA 0)
-    __shared__ float sL[kTrsvBlock][kTrsvBlock + 1];
+    extern __shared__ double sdyn[];
+    double *sx = sdyn;                             // [kTrsvBlock] solution of the previous block
+    double *sy = sx + kTrsvBlock;                  // [kTrsvBlock] current block (CTA 0)
+    double *sp = sy + kTrsvBlock;                  // [kTrsvBlock] partial sums (CTA 0)
+    float *sL = reinterpret_cast<float *>(sp + kTrsvBlock);   // [col][kTS] diagonal tile
+    float *sB = sL + kTrsvBlock * kTS;                        // [col][kTS] coupling tile
     const int nblk = (n + kTrsvBlock - 1) / kTrsvBlock;
-    const int G = gridDim.x;
+    const int G = gridDim.x, tid = threadIdx.x;
+    auto blk = [&](int s, int &c0, int &w) {
+        const int b = lower ? s : nblk - 1 - s;
+        c0 = b * kTrsvBlock;
+        w = min(n, c0 + kTrsvBlock) - c0;
+    };
+    if (blockIdx.x == 0) {
+        int c0, w;
+        blk(0, c0, w);
+        prefetch_tile(sL, LU, ld, c0, w, c0, w);
+    }
     int pc0 = 0, pw = 0;                  // previous block [pc0, pc0+pw)
     for (int s = 0; s < nblk; ++s) {
-        const int bidx = lower ? s : nblk - 1 - s;
-        const int c0 = bidx * kTrsvBlock, c1 = min(n, c0 + kTrsvBlock), w = c1 - c0;
+        int c0, w;
+        blk(s, c0, w);
+        const int c1 = c0 + w;
         if (s > 0) {
-            for (int e = threadIdx.x; e < pw; e += blockDim.x) sx[e] = __ldcg(y + pc0 + e);
+            for (int e = tid; e < pw; e += blockDim.x) sx[e] = __ldcg(y + pc0 + e);
             __syncthreads();
         }
         if (blockIdx.x == 0) {
-            for (int e = threadIdx.x; e < w * w; e += blockDim.x) {
-                const int r = e % w, c = e / w;
-                sL[r][c] = LU[(int64_t)(c0 + c) * ld + c0 + r];
-            }
-            for (int e = threadIdx.x; e < w; e += blockDim.x) {
-                double v = __ldcg(y + c0 + e);
-                for (int j = 0; j < pw; ++j) v -= (double)LU[(int64_t)(pc0 + j) * ld + c0 + e] * sx[j];
-                sy[e] = v;
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
+            __syncthreads();
+            // y_b - (coupling tile) x_prev : 2 threads per row, half of the previous block each
+            if (tid < 2 * w) {
+                const int r = tid % w, hsel = tid / w, half = pw / 2;
+                const int jb = hsel ? half : 0, je = hsel ? pw : half;
+                double part = 0.0;
+                for (int j = jb; j < je; ++j) part = fma((double)sB[j * kTS + r], sx[j], part);
+                if (hsel) sp[r] = part; else sy[r] = part;
             }
             __syncthreads();
-            if (threadIdx.x < 32) {
-                for (int jj = 0; jj < w; ++jj) {
-                    const int j = lower ? jj : w - 1 - jj;
-                    if (!lower && threadIdx.x == 0) sy[j] /= (double)sL[j][j];
-                    __syncwarp();
-                    const double xj = sy[j];
-                    for (int r = threadIdx.x; r < w; r += 32)
-                        if (lower ? (r > j) : (r < j)) sy[r] -= (double)sL[r][j] * xj;
-                    __syncwarp();
+            for (int e = tid; e < w; e += blockDim.x) sy[e] = __ldcg(y + c0 + e) - (sy[e] + sp[e]);
+            __syncthreads();
+            // diagonal triangle: 32-row sub-blocks, each solved by warp 0 in registers with
+            // shuffles, then applied to the rest of the block by all threads
+            const int nsb = (w + 31) / 32;
+            for (int q = 0; q < nsb; ++q) {
+                const int sb = lower ? q * 32 : (nsb - 1 - q) * 32;
+                const int sw = min(32, w - sb);
+                if (tid < 32) {
+                    double v = (tid < sw) ? sy[sb + tid] : 0.0;
+                    if (lower) {
+                        for (int j = 0; j < sw; ++j) {
+                            const double xj = __shfl_sync(0xffffffffu, v, j);
+                            if (tid > j && tid < sw) v -= (double)sL[(sb + j) * kTS + sb + tid] * xj;
+                        }
+                    } else {
+                        for (int j = sw - 1; j >= 0; --j) {
+                            if (tid == j) v /= (double)sL[(sb + j) * kTS + sb + j];
+                            const double xj = __shfl_sync(0xffffffffu, v, j);
+                            if (tid < j) v -= (double)sL[(sb + j) * kTS + sb + tid] * xj;
+                        }
+                    }
+                    if (tid < sw) sy[sb + tid] = v;
                 }
+                __syncthreads();
+                const int lo = lower ? sb + sw : 0, hi = lower ? w : sb;
+                for (int r = lo + tid; r < hi; r += blockDim.x) {
+                    double acc = 0.0;
+                    for (int j = 0; j < sw; ++j) acc = fma((double)sL[(sb + j) * kTS + r], sy[sb + j], acc);
+                    sy[r] -= acc;
+                }
+                __syncthreads();
             }
+            for (int e = tid; e < w; e += blockDim.x) __stcg(y + c0 + e, sy[e]);
             __syncthreads();
-            for (int e = threadIdx.x; e < w; e += blockDim.x) __stcg(y + c0 + e, sy[e]);
+            if (s + 1 < nblk) {          // next step's tiles, in flight during the barrier
+                int n0, nw_;
+                blk(s + 1, n0, nw_);
+                prefetch_tile(sL, LU, ld, n0, nw_, n0, nw_);
+                prefetch_tile(sB, LU, ld, n0, nw_, c0, w);
+            }
         } else if (s > 0) {
-            // rows still depending on the previous block, except the current block's rows
             const int lo = lower ? c1 : 0, hi = lower ? n : c0;
-            for (int r = lo + (blockIdx.x - 1) * blockDim.x + threadIdx.x; r < hi; r += (G - 1) * blockDim.x) {
-                double acc = 0.0;
-                for (int j = 0; j < pw; ++j) acc += (double)LU[(int64_t)(pc0 + j) * ld + r] * sx[j];
+            for (int r = lo + (blockIdx.x - 1) * blockDim.x + tid; r < hi; r += (G - 1) * blockDim.x) {
+                const double acc = dot_col_block(LU, ld, pc0, pw, r, sx);
                 __stcg(y + r, __ldcg(y + r) - acc);
             }
         }
@@ -403,11 +598,10 @@ __global__ void copy_matrix_kernel(int n, const float *A, int lda, float *B, int
 // host driver
 // ------------------------------------------------------------------------------------
 struct LuWork {
-    float *LU = nullptr, *cand_rows = nullptr;
+    float *LU = nullptr;
     int *ipiv = nullptr, *piv_rows = nullptr, *pos = nullptr, *row_at = nullptr, *info = nullptr;
     int *perm = nullptr, *npairs = nullptr;
     int2 *pairs = nullptr;
-    PivotCand *cand = nullptr;
     unsigned int *bar = nullptr;  // [grid] arrive flags + [1] release
     GridBar gb;
     unsigned int epoch = 1;
@@ -435,12 +629,12 @@ static int solve_with_factors(LuWork &w, int n, const double *v, double *out, in
     unsigned int ep = w.epoch;
     void *args[] = {(void *)&LU, (void *)&ld, (void *)&n, (void *)&y, (void *)&lower, (void *)&gb, (void *)&ep};
     const int nblk = (n + kTrsvBlock - 1) / kTrsvBlock;
-    int rc = coop_launch((const void *)trsv_kernel, coop_grid, 256, args, 0, st);
+    int rc = coop_launch((const void *)trsv_kernel, coop_grid, 256, args, kTrsvSmem, st);
     w.epoch += nblk;
     if (rc) return rc;
     lower = 0;
     ep = w.epoch;
-    rc = coop_launch((const void *)trsv_kernel, coop_grid, 256, args, 0, st);
+    rc = coop_launch((const void *)trsv_kernel, coop_grid, 256, args, kTrsvSmem, st);
     w.epoch += nblk;
     return rc;
 }
@@ -476,19 +670,29 @@ extern "C" int bf16x_gesv_ir(int n, const float *A, int lda, const double *b, do
     if (max_iter <= 0) max_iter = 30;
     cudaStream_t st = current_stream();
     const int coop_grid = num_sms();
-    // panel rows per CTA held in shared memory for the whole panel
-    const int rl_max = (n + coop_grid - 1) / coop_grid + 1;
-    const size_t panel_smem = (size_t)nb * rl_max * sizeof(float) + (size_t)nb * sizeof(float) + rl_max + 16;
-    if (panel_smem > 200 * 1024 || (size_t)n * sizeof(int) > 200 * 1024) {
-        set_error_msg("gesv_ir: n * nb too large for the shared-memory panel (n/148 * nb * 4 B <= 200 KB)");
+    // sub-panel rows per cluster CTA in shared memory: cluster of 8 (portable) or 16
+    int cl = 16;                           // non-portable cluster size (falls back to 8)
+    int rl_max = (n + cl - 1) / cl + 1;
+    auto sub_smem = [&](int rl) {
+        return (size_t)kSubW * rl * sizeof(float) + (size_t)3 * kSubW * sizeof(float) + 16 + (size_t)rl + 16;
+    };
+    if (sub_smem(rl_max) > 200 * 1024) {
+        cl = 16;
+        rl_max = (n + cl - 1) / cl + 1;
+    }
+    if (sub_smem(rl_max) > 200 * 1024 || (size_t)n * sizeof(int) > 200 * 1024) {
+        set_error_msg("gesv_ir: n too large for the shared-memory sub-panel (n <= ~51000)");
         return -1;
     }
     {
         static bool attr = false;
         if (!attr) {
-            cudaFuncSetAttribute(panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024 + 1024);
+            cudaFuncSetAttribute(subpanel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024 + 1024);
+            cudaFuncSetAttribute(subpanel_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
             cudaFuncSetAttribute(build_perm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024 + 1024);
             cudaFuncSetAttribute(trsm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024 + 1024);
+            cudaFuncSetAttribute(panel_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024 + 1024);
+            cudaFuncSetAttribute(trsv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTrsvSmem);
             attr = true;
         }
     }
@@ -504,14 +708,12 @@ extern "C" int bf16x_gesv_ir(int n, const float *A, int lda, const double *b, do
     alloc((void **)&w.LU, sizeof(float) * (size_t)n * n);
     alloc((void **)&w.ipiv, sizeof(int) * n);
     alloc((void **)&w.perm, sizeof(int) * n);
-    alloc((void **)&w.piv_rows, sizeof(int) * (size_t)nb);
+    alloc((void **)&w.piv_rows, sizeof(int) * (size_t)kSubW);
     alloc((void **)&w.pos, sizeof(int) * n);
     alloc((void **)&w.row_at, sizeof(int) * n);
     alloc((void **)&w.info, sizeof(int));
     alloc((void **)&w.npairs, sizeof(int));
     alloc((void **)&w.pairs, sizeof(int2) * 2 * (size_t)nb);
-    alloc((void **)&w.cand, sizeof(PivotCand) * 2 * (size_t)coop_grid);
-    alloc((void **)&w.cand_rows, sizeof(float) * 2 * (size_t)coop_grid * nb);
     alloc((void **)&w.bar, sizeof(unsigned int) * ((size_t)coop_grid + 1));
     alloc((void **)&w.r, sizeof(double) * n);
     alloc((void **)&w.d, sizeof(double) * n);
@@ -519,8 +721,8 @@ extern "C" int bf16x_gesv_ir(int n, const float *A, int lda, const double *b, do
     alloc((void **)&w.scal, sizeof(double) * 4);
     auto cleanup = [&]() {
         cudaFree(w.LU); cudaFree(w.ipiv); cudaFree(w.perm); cudaFree(w.piv_rows); cudaFree(w.pos);
-        cudaFree(w.row_at); cudaFree(w.info); cudaFree(w.npairs); cudaFree(w.pairs); cudaFree(w.cand);
-        cudaFree(w.cand_rows); cudaFree(w.bar); cudaFree(w.r); cudaFree(w.d); cudaFree(w.part); cudaFree(w.scal);
+        cudaFree(w.row_at); cudaFree(w.info); cudaFree(w.npairs); cudaFree(w.pairs);
+        cudaFree(w.bar); cudaFree(w.r); cudaFree(w.d); cudaFree(w.part); cudaFree(w.scal);
     };
     if (rc) {
         cleanup();
@@ -538,24 +740,67 @@ extern "C" int bf16x_gesv_ir(int n, const float *A, int lda, const double *b, do
     copy_matrix_kernel<<<num_sms() * 8, 256, 0, st>>>(n, A, lda, w.LU, n);
     count_launch();
     const int ld = n;
+    auto laswp = [&](int c0, int c1, int pair_cap) {
+        if (c1 <= c0) return;
+        laswp_kernel<<<(c1 - c0 + 7) / 8, 256, 8 * (size_t)pair_cap * sizeof(float), st>>>(w.LU, ld, c0, c1, w.pairs,
+                                                                                          w.npairs);
+        count_launch();
+    };
     for (int j0 = 0; j0 < n && !rc; j0 += nb) {
         const int jb = std::min(nb, n - j0);
-        {
-            float *LU = w.LU, *cand_rows = w.cand_rows;
-            int ldv = ld, nv = n, j0v = j0, jbv = jb, rlv = rl_max;
-            PivotCand *cand = w.cand;
-            int *piv = w.piv_rows, *info = w.info;
-            GridBar gb = w.gb;
-            unsigned int ep = w.epoch;
-            void *args[] = {&LU, &ldv, &nv, &j0v, &jbv, &rlv, &cand, &cand_rows, &piv, &info, &gb, &ep};
-            const size_t smem = (size_t)jb * rl_max * sizeof(float) + (size_t)jb * sizeof(float) + rl_max + 16;
-            rc = coop_launch((const void *)panel_kernel, coop_grid, kLuThreads, args, smem, st);
-            w.epoch += jb;
-            if (rc) break;
+        for (int s0 = j0; s0 < j0 + jb && !rc; s0 += kSubW) {
+            const int sw = std::min(kSubW, j0 + jb - s0);
+            // (1) sub-panel factorisation on one cluster
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3(cl);
+            cfg.blockDim = dim3(kSubThreads);
+            cfg.dynamicSmemBytes = sub_smem(rl_max);
+            cfg.stream = st;
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeClusterDimension;
+            at[0].val.clusterDim.x = cl;
+            at[0].val.clusterDim.y = 1;
+            at[0].val.clusterDim.z = 1;
+            cfg.attrs = at;
+            cfg.numAttrs = 1;
+            cudaError_t e = cudaLaunchKernelEx(&cfg, subpanel_kernel, w.LU, ld, n, s0, sw, rl_max, w.piv_rows, w.info);
+            if (e != cudaSuccess && cl == 16) {    // 16-CTA clusters unavailable: use 8
+                cudaGetLastError();
+                cl = 8;
+                rl_max = (n + cl - 1) / cl + 1;
+                if (sub_smem(rl_max) <= 200 * 1024) {
+                    cfg.gridDim = dim3(cl);
+                    at[0].val.clusterDim.x = cl;
+                    cfg.dynamicSmemBytes = sub_smem(rl_max);
+                    e = cudaLaunchKernelEx(&cfg, subpanel_kernel, w.LU, ld, n, s0, sw, rl_max, w.piv_rows, w.info);
+                }
+            }
+            if (e != cudaSuccess) {
+                set_cuda_error(e, "subpanel launch");
+                rc = BF16X_ERR_CUDA;
+                break;
+            }
+            count_launch();
+            // (2) its interchanges, applied to the panel columns
+            build_ipiv_kernel<<<1, 1024, 0, st>>>(n, s0, sw, w.piv_rows, w.ipiv, w.pos, w.row_at, w.pairs, w.npairs);
+            count_launch();
+            laswp(j0, j0 + jb, 2 * sw);
+            // (3) TRSM + rank-sw update of the rest of the panel
+            const int c1 = s0 + sw, c2 = j0 + jb;
+            if (c1 < c2) {
+                const size_t smem = ((size_t)sw * (c2 - c1) + (size_t)sw * sw + (size_t)sw * kUpdRows) * sizeof(float);
+                panel_update_kernel<<<(n - c1 + kUpdRows - 1) / kUpdRows, 256, smem, st>>>(w.LU, ld, n, s0, sw, c1,
+                                                                                            c2);
+                count_launch();
+            }
+            rc = check_launch("panel");
         }
-        build_ipiv_kernel<<<1, 1024, 0, st>>>(n, j0, jb, w.piv_rows, w.ipiv, w.pos, w.row_at, w.pairs, w.npairs);
-        laswp_kernel<<<(n + 7) / 8, 256, 8 * 2 * (size_t)jb * sizeof(float), st>>>(w.LU, ld, 0, n, w.pairs, w.npairs);
-        count_launch(2);
+        if (rc) break;
+        // the panel's whole interchange sequence on the columns outside it
+        build_pairs_kernel<<<1, 1024, 0, st>>>(n, j0, jb, w.ipiv, w.pos, w.row_at, w.pairs, w.npairs);
+        count_launch();
+        laswp(0, j0, 2 * jb);
+        laswp(j0 + jb, n, 2 * jb);
         const int j1 = j0 + jb, rest = n - j1;
         if (rest > 0) {
             trsm_kernel<<<(rest + kTrsmCols - 1) / kTrsmCols, 256, (size_t)jb * (kTrsmCols + 33) * sizeof(float), st>>>(
