@@ -138,6 +138,18 @@ __device__ __forceinline__ void tma_load_3d_2sm(void *smem_dst, const CUtensorMa
         : "memory");
 }
 
+// 2-CTA multicast form: the box lands at the same smem offset in every CTA of `mask`; each
+// destination signals the barrier at this offset in its pair's leader (even) CTA.
+__device__ __forceinline__ void tma_load_3d_2sm_mc(void *smem_dst, const CUtensorMap *map, uint64_t *bar, int c0,
+                                                   int c1, int c2, uint16_t mask) {
+    uint32_t b = smem_u32(bar) & 0xFEFFFFFFu;
+    asm volatile(
+        "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+        " [%0], [%1, {%3, %4, %5}], [%2], %6;" ::"r"(smem_u32(smem_dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(b), "r"(c0), "r"(c1), "r"(c2), "h"(mask)
+        : "memory");
+}
+
 // ---- tcgen05 ----
 template <int CG>
 __device__ __forceinline__ void tmem_alloc(uint32_t *smem_result, uint32_t ncols) {
@@ -208,6 +220,16 @@ __device__ __forceinline__ void umma_commit_elect(uint64_t *bar) {
                 smem_u32(bar)),
             "h"((uint16_t)3)
             : "memory");
+}
+
+// 2-CTA commit arriving on the barrier at this offset in every CTA of `mask`.
+__device__ __forceinline__ void umma_commit2_mask_elect(uint64_t *bar, uint16_t mask) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}" ::"r"(
+            smem_u32(bar)),
+        "h"(mask)
+        : "memory");
 }
 
 // Make `bar` track completion of all prior tcgen05 async ops of this thread.

@@ -165,11 +165,15 @@ __device__ __forceinline__ void issue_interval(uint32_t d_tmem, const uint64_t (
     for (int h = 0; h < H; ++h) if (h < nh) mma(0, 0, h);                                  // bin 0
 }
 
-template <int CG, int V, int BN, int S>
+// MC = number of CTA pairs per cluster sharing the B tile (1, or 2: two vertically adjacent
+// 256 x BN tiles; each pair loads half of every B slice and multicasts it to both pairs).
+template <int CG, int V, int BN, int S, int MC>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_split_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                       const KParams p) {
     using Cf = Cfg<CG, V, BN>;
+    constexpr int CL = CG * MC;   // cluster size
+    static_assert(MC == 1 || CG == 2, "multicast needs 2-CTA pairs");
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t *sA = smem;
@@ -181,7 +185,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(acc_empty + 2);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t rank = (CG == 2) ? cluster_ctarank() : 0u;
+    const uint32_t crank = (CL > 1) ? cluster_ctarank() : 0u;   // rank in the cluster
+    const uint32_t rank = crank % CG;                            // rank in the CTA pair
+    const uint32_t pair = crank / CG;                            // which pair of the cluster
 
     if (warp == 0 && lane == 0) {
         prefetch_tmap(&tmA);
@@ -190,7 +196,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (warp == 1 && lane == 0) {
         for (int s = 0; s < Cf::STAGES; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], 1);
+            mbar_init(&empty[s], MC);     // one commit per pair reading the (shared) stage
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(&acc_full[b], 1);
@@ -200,14 +206,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     if (warp == 2) tmem_alloc<CG>(tmem_slot, kTmemCols);
     tc_fence_before();
-    if constexpr (CG == 2) cluster_sync(); else __syncthreads();
+    if constexpr (CL > 1) cluster_sync(); else __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
     // Programmatic dependent launch: everything above overlapped the previous kernel's tail;
     // from here on we read its outputs (the pieces) and may overwrite what it read.
     asm volatile("griddepcontrol.wait;" ::: "memory");
 
-    const int cid = blockIdx.x / CG, ncl = gridDim.x / CG;
+    const int cid = blockIdx.x / CL, ncl = gridDim.x / CL;
 
     if (warp < 4) {
         if (warp == 0) {
@@ -220,6 +226,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 while (it.next(p, w)) {
                     int tm, tn;
                     tile_coords(w.tile, p.tiles_m, p.tiles_n, tm, tn);
+                    tm = tm * MC + (int)pair;
                     const int a_row = tm * Cf::TILE_M + (int)rank * kBM;
                     const int b_row = tn * BN + (int)rank * Cf::BN_LOCAL;
                     const int kb_end = min(p.nkb, w.i1 * S);
@@ -234,7 +241,17 @@ __global__ void __launch_bounds__(kThreads, 1)
                         } else {
                             if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * Cf::STAGE);
                             tma_load_3d_2sm(a_dst, &tmA, &full[stage], kb * kBK, a_row, 0);
-                            tma_load_3d_2sm(b_dst, &tmB, &full[stage], kb * kBK, b_row, 0);
+                            if constexpr (MC == 1) {
+                                tma_load_3d_2sm(b_dst, &tmB, &full[stage], kb * kBK, b_row, 0);
+                            } else {
+                                // this pair's half of the B slice, piece by piece, to both pairs
+                                constexpr int HB = Cf::BN_LOCAL / MC;
+                                const uint16_t mask = (uint16_t)((1u << rank) | (1u << (CG + rank)));
+#pragma unroll
+                                for (int q = 0; q < Cf::P; ++q)
+                                    tma_load_3d_2sm_mc(b_dst + q * Cf::B_PIECE + (int)pair * HB * kRowBytes, &tmB,
+                                                       &full[stage], kb * kBK, b_row + (int)pair * HB, q, mask);
+                            }
                         }
                         if (++stage == Cf::STAGES) { stage = 0; phase ^= 1u; }
                     }
@@ -273,8 +290,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                         issue_interval<CG, V, BN, S>(tmem_base + buf * kTmemBufStride, a_desc, b_desc, ns, idesc);
 #pragma unroll
                         for (int q = 0; q < S; ++q)
-                            if (q < ns) umma_commit_elect<CG>(&empty[stages[q]]);
-                        umma_commit_elect<CG>(&acc_full[buf]);
+                            if (q < ns) {
+                                if constexpr (MC == 1) umma_commit_elect<CG>(&empty[stages[q]]);
+                                else umma_commit2_mask_elect(&empty[stages[q]], (uint16_t)((1u << CL) - 1));
+                            }
+                        if constexpr (MC == 1) umma_commit_elect<CG>(&acc_full[buf]);
+                        else umma_commit2_mask_elect(&acc_full[buf], (uint16_t)(3u << (CG * pair)));
                     }
                 }
             }
@@ -292,6 +313,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         while (it.next(p, w)) {
             int tm, tn;
             tile_coords(w.tile, p.tiles_m, p.tiles_n, tm, tn);
+            tm = tm * MC + (int)pair;
             const int row = tm * Cf::TILE_M + (int)rank * kBM + quad * 32 + lane;
             const int col0 = tn * BN + half * EC;
             float G[EC];
@@ -321,14 +343,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                 __syncwarp();
                 if (lane == 0) {
                     if (CG == 1 || rank == 0) mbar_arrive(&acc_empty[buf]);
-                    else mbar_arrive_cluster(&acc_empty[buf], 0);
+                    else mbar_arrive_cluster(&acc_empty[buf], pair * CG);
                 }
             }
             if (w.role != 0) {
                 // stream-K fix-up: slot layout [sk tile][cta rank][column 0..BN)[row 0..127]
-                float *slot = p.sk_ws + ((size_t)w.sk_slot * CG + rank) * (size_t)BN * kBM;
+                float *slot = p.sk_ws + ((size_t)w.sk_slot * CL + crank) * (size_t)BN * kBM;
                 const int lrow = quad * 32 + lane;
-                unsigned int *flag = p.sk_flags + (size_t)w.sk_slot * CG + rank;
+                unsigned int *flag = p.sk_flags + (size_t)w.sk_slot * CL + crank;
                 if (w.role == 2) {
 #pragma unroll
                     for (int j = 0; j < EC; ++j) __stcg(slot + (size_t)(half * EC + j) * kBM + lrow, G[j]);
@@ -373,7 +395,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
 
     tc_fence_before();
-    if constexpr (CG == 2) cluster_sync(); else __syncthreads();
+    if constexpr (CL > 1) cluster_sync(); else __syncthreads();
     if (warp == 2) {
         tc_fence_after();
         tmem_dealloc<CG>(tmem_base, kTmemCols);
@@ -402,12 +424,13 @@ static EncodeTiledFn encode_fn() {
 
 // 3D map over p K-major piece planes: dims (k, rows, p), box (BK, box_rows, p).
 static int make_piece_map(CUtensorMap *map, const uint16_t *base, int k, int rows, int64_t ld, int64_t plane,
-                          int p, int box_rows) {
+                          int p, int box_rows, int box_p = 0) {
+    if (box_p <= 0) box_p = p;
     EncodeTiledFn enc = encode_fn();
     if (!enc) return BF16X_ERR_CUDA;
     cuuint64_t dims[3] = {(cuuint64_t)k, (cuuint64_t)rows, (cuuint64_t)p};
     cuuint64_t strides[2] = {(cuuint64_t)ld * 2, (cuuint64_t)plane * 2};
-    cuuint32_t box[3] = {(cuuint32_t)kBK, (cuuint32_t)box_rows, (cuuint32_t)p};
+    cuuint32_t box[3] = {(cuuint32_t)kBK, (cuuint32_t)box_rows, (cuuint32_t)box_p};
     cuuint32_t estr[3] = {1, 1, 1};
     CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<uint16_t *>(base), dims, strides, box, estr,
                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -480,25 +503,53 @@ int num_sms() {
 int pieces_of(int variant) { return variant_pieces(variant); }
 int default_cta_group() { return kDefaultCtaGroup; }
 
-template <int CG, int V, int BN, int S>
+template <int CG, int V, int BN, int S, int MC>
 static int launch_t(const GemmPlan &pl, cudaStream_t st) {
     using Cf = Cfg<CG, V, BN>;
+    constexpr int CL = CG * MC;
     CUtensorMap tmA, tmB;
     int rc = make_piece_map(&tmA, pl.Ap, pl.k, pl.m, pl.ldap, pl.a_plane, Cf::P, kBM);
     if (rc) return rc;
-    rc = make_piece_map(&tmB, pl.Bp, pl.k, pl.n, pl.ldbp, pl.b_plane, Cf::P, Cf::BN_LOCAL);
+    if (MC == 1) rc = make_piece_map(&tmB, pl.Bp, pl.k, pl.n, pl.ldbp, pl.b_plane, Cf::P, Cf::BN_LOCAL);
+    else rc = make_piece_map(&tmB, pl.Bp, pl.k, pl.n, pl.ldbp, pl.b_plane, Cf::P, Cf::BN_LOCAL / MC, 1);
     if (rc) return rc;
     KParams kp;
     kp.m = pl.m; kp.n = pl.n; kp.k = pl.k;
     kp.alpha = pl.alpha; kp.beta = pl.beta;
     kp.C = pl.C; kp.ldc = pl.ldc; kp.flags = pl.flags; kp.acc = pl.acc;
-    kp.tiles_m = (pl.m + Cf::TILE_M - 1) / Cf::TILE_M;
+    kp.tiles_m = ((pl.m + Cf::TILE_M - 1) / Cf::TILE_M + MC - 1) / MC;   // rows of (MC-tall) super-tiles
     kp.tiles_n = (pl.n + BN - 1) / BN;
     kp.nkb = (pl.k + kBK - 1) / kBK;
     const int tiles = kp.tiles_m * kp.tiles_n;
-    int units = num_sms() / CG;
-    if (pl.max_ctas > 0) units = std::max(1, pl.max_ctas / CG);
-    const int grid = std::min(tiles, units) * CG;
+    int units = num_sms() / CL;
+    if (pl.max_ctas > 0) units = std::max(1, pl.max_ctas / CL);
+    if constexpr (CL > 2) {
+        // clusters of 4 do not tile every GPC: only co-resident clusters may be launched
+        static int max_clusters = -1;
+        if (max_clusters < 0) {
+            cudaFuncSetAttribute(gemm_split_kernel<CG, V, BN, S, MC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 Cf::SMEM);
+            cudaLaunchConfig_t qc = {};
+            qc.gridDim = dim3(units * CL);
+            qc.blockDim = dim3(kThreads);
+            qc.dynamicSmemBytes = Cf::SMEM;
+            cudaLaunchAttribute qa[1];
+            qa[0].id = cudaLaunchAttributeClusterDimension;
+            qa[0].val.clusterDim.x = CL;
+            qa[0].val.clusterDim.y = 1;
+            qa[0].val.clusterDim.z = 1;
+            qc.attrs = qa;
+            qc.numAttrs = 1;
+            int nclu = 0;
+            if (cudaOccupancyMaxActiveClusters(&nclu, gemm_split_kernel<CG, V, BN, S, MC>, &qc) != cudaSuccess) {
+                cudaGetLastError();
+                nclu = 0;
+            }
+            max_clusters = nclu;
+        }
+        if (max_clusters > 0) units = std::min(units, max_clusters);
+    }
+    const int grid = std::min(tiles, units) * CL;
     // Hybrid schedule: all full waves but the last run data-parallel; the last full wave plus
     // the partial one are spread over every cluster by promotion interval (stream-K), so the
     // partial wave no longer idles most of the GPU.  Disabled for accumulator-carry launches.
@@ -508,19 +559,19 @@ static int launch_t(const GemmPlan &pl, cudaStream_t st) {
     kp.sk_ws = nullptr;
     kp.sk_flags = nullptr;
     kp.epoch = 0;
-    const int ncl = grid / CG;
+    const int ncl = grid / CL;
     if (pl.stream_k != 0 && !(pl.flags & (BF16X_ACC_IN | BF16X_ACC_OUT)) && tiles > ncl && tiles % ncl != 0) {
         const int full = tiles / ncl;
         kp.dp_tiles = (full - 1) * ncl;
         kp.sk_tiles = tiles - kp.dp_tiles;
-        int rc2 = sk_workspace((size_t)kp.sk_tiles * CG * BN * kBM, (size_t)kp.sk_tiles * CG, &kp.sk_ws, &kp.sk_flags,
+        int rc2 = sk_workspace((size_t)kp.sk_tiles * CL * BN * kBM, (size_t)kp.sk_tiles * CL, &kp.sk_ws, &kp.sk_flags,
                                &kp.epoch);
         if (rc2) return rc2;
     }
 
     static bool attr_set = false;  // per template instance
     if (!attr_set) {
-        if (cudaFuncSetAttribute(gemm_split_kernel<CG, V, BN, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cf::SMEM) !=
+        if (cudaFuncSetAttribute(gemm_split_kernel<CG, V, BN, S, MC>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cf::SMEM) !=
             cudaSuccess)
             return check_launch("gemm attr");
         attr_set = true;
@@ -532,14 +583,14 @@ static int launch_t(const GemmPlan &pl, cudaStream_t st) {
     cfg.stream = st;
     cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = CG;
+    attr[0].val.clusterDim.x = CL;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 2;
-    cudaError_t e = cudaLaunchKernelEx(&cfg, gemm_split_kernel<CG, V, BN, S>, tmA, tmB, kp);
+    cudaError_t e = cudaLaunchKernelEx(&cfg, gemm_split_kernel<CG, V, BN, S, MC>, tmA, tmB, kp);
     if (e != cudaSuccess) {
         set_cuda_error(e, "gemm launch");
         return BF16X_ERR_CUDA;
@@ -572,10 +623,16 @@ static int launch_s(const GemmPlan &pl, cudaStream_t st) {
         if (s == 2) {
             const int units = (pl.max_ctas > 0 ? pl.max_ctas : num_sms()) / CG;
             const int bn = choose_tile_n(pl.m, pl.n, CG, units, pl.tile_n);
-            if (bn == 192) return launch_t<CG, V, 192, 2>(pl, st);
+            if (bn == 192) return launch_t<CG, V, 192, 2, 1>(pl, st);
+            // Two pairs per cluster sharing B (TMA multicast) cut L2->SM and DRAM traffic by a
+            // quarter but clusters of 4 leave 16 SMs idle; measured (r05) a win only for large
+            // outputs, where the kernel runs long enough to be power-limited (16384^3: x3 +17 %,
+            // x6 +7 %), and a loss at 8192^3.  Auto: multicast for m*n >= 12288^2.
+            const bool mc2 = pl.multicast == 2 || (pl.multicast == 0 && (int64_t)pl.m * pl.n >= 12288LL * 12288LL);
+            if (mc2) return launch_t<CG, V, 256, 2, 2>(pl, st);
         }
     }
-    return s == 2 ? launch_t<CG, V, 256, 2>(pl, st) : launch_t<CG, V, 256, 1>(pl, st);
+    return s == 2 ? launch_t<CG, V, 256, 2, 1>(pl, st) : launch_t<CG, V, 256, 1, 1>(pl, st);
 }
 
 int launch_gemm_pieces(const GemmPlan &pl, cudaStream_t st) {

@@ -25,6 +25,14 @@ def spi(request):
     bx.lib().bf16x_tune(0, 0, 0)
 
 
+@pytest.fixture(params=[1, 2], ids=["mc1", "mc2"])
+def mc(request):
+    """CTA pairs per cluster sharing B tiles through TMA multicast (2-CTA kernel)."""
+    bx.lib().bf16x_multicast(request.param)
+    yield request.param
+    bx.lib().bf16x_multicast(0)
+
+
 def _gpu(A, B, C=None, alpha=1.0, beta=0.0, variant=6, cg=0):
     Ad = torch.from_numpy(np.asfortranarray(A)).cuda()
     Bd = torch.from_numpy(np.asfortranarray(B)).cuda()
@@ -49,8 +57,9 @@ def _check_ratio(orc, A, B, variant, cg, cols=None):
 
 @pytest.mark.parametrize("cg", [1, 2])
 @pytest.mark.parametrize("variant", [3, 6, 9])
-@pytest.mark.parametrize("shape", [(64, 64, 64), (129, 257, 33), (333, 517, 77), (256, 512, 1000), (20, 600, 48)])
-def test_uniform_shapes(orc, shape, variant, cg, spi):
+@pytest.mark.parametrize("shape", [(64, 64, 64), (129, 257, 33), (333, 517, 77), (256, 512, 1000), (20, 600, 48),
+                                   (700, 300, 200)])
+def test_uniform_shapes(orc, shape, variant, cg, spi, mc):
     m, n, k = shape
     A = synthetic.uniform(m, k, seed=m + 7 * k)
     B = synthetic.uniform(k, n, seed=n + 11 * k)
@@ -68,7 +77,7 @@ def test_wide_and_gaussian(orc, dist, variant, cg, spi):
 
 @pytest.mark.parametrize("k", [256, 1024, 4096, 16384])
 @pytest.mark.parametrize("variant", [3, 6, 9])
-def test_k_sweep_wide(orc, k, variant, spi):
+def test_k_sweep_wide(orc, k, variant, spi, mc):
     """Config 3 shape family (k-sweep, wide exponents) at m = n = 256."""
     A = synthetic.wide(256, k, seed=1000 + k)
     B = synthetic.wide(k, 256, seed=2000 + k)
@@ -76,7 +85,7 @@ def test_k_sweep_wide(orc, k, variant, spi):
 
 
 @pytest.mark.parametrize("cg", [1, 2])
-def test_exact_pins(orc, cg, spi):
+def test_exact_pins(orc, cg, spi, mc):
     """Bit-exact cases: A*I = A and A*P = A P for x6/x9 (one nonzero term per piece pair),
     x3 with B = I returns fl32(b0 + b1); 10-bit integers with k <= 16 are exact for x6/x9."""
     A = synthetic.wide(300, 40, seed=8)
@@ -191,7 +200,7 @@ def test_ragged_ld_and_offsets(orc):
 
 
 @pytest.mark.parametrize("m,n,k", [(2560, 2560, 1000), (4096, 1536, 333), (2304, 4608, 64)])
-def test_stream_k_schedule(orc, m, n, k):
+def test_stream_k_schedule(orc, m, n, k, mc):
     """Hybrid stream-K (tiles > clusters, partial last wave): split tiles are finished by the
     cluster holding their first promotion intervals, which adds the other part's raw FP32
     accumulator.  Checked on sampled columns against the oracle (ratio <= 2) and against the
