@@ -83,15 +83,16 @@ int bf16x_split_operands(int m, int n, int k, const float *A, int64_t lda, const
  * FP32 product emulated by BF16 x BF16 -> FP32 tensor-core products (section IV-A):
  *   variant 3: pieces 0-1, products {00,01,10}            ("pair of BF16s")
  *   variant 6: pieces 0-2, products {00,01,10,02,11,20}   (Z_2)
+ *   variant 8: eight products, bins 0..3 = the paper's Z_3
  *   variant 9: all nine products                          (R9)
  *   variant 1: b0 only, one product (debug / plain-BF16 peak)
  * Products are accumulated smallest bin first into an FP32 tensor-memory
  * partial that is added, with FP32 round-to-nearest, into a promoted accumulator every
- * BK = 32 values of k.  alpha/beta follow BLAS (R19):
+ * 64 values of k ("promotion").  alpha/beta follow BLAS (R19):
  * beta == 0 never reads C; alpha == 0 or k == 0 returns beta*C.
  *   A: m x k, lda >= max(1,m);  B: k x n, ldb >= max(1,k);  C: m x n, ldc >= max(1,m).
  * Runs on the library stream (bf16x_set_stream).  Errors: -1 m, -2 n, -3 k, -6 lda,
- * -8 ldb, -11 ldc, -12 variant; BF16X_ERR_ALLOC if the workspace cannot grow.
+ * -8 ldb, -11 ldc, -12 variant (not 1/3/6/8/9); BF16X_ERR_ALLOC if the workspace cannot grow.
  * ---------------------------------------------------------------------------------- */
 int bf16x_gemm(int m, int n, int k, float alpha, const float *A, int lda,
                const float *B, int ldb, float beta, float *C, int ldc, int variant);

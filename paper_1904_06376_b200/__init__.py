@@ -19,8 +19,8 @@ HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "bf16x.h")
 
 SUCCESS, ERR_CUDA, ERR_ALLOC, ERR_ARCH, ERR_SINGULAR, NOT_CONVERGED = 0, 1, 2, 3, 4, 5
 ACC_IN, ACC_OUT = 1, 2
-VARIANTS = (1, 3, 6, 9)
-PIECES = {1: 1, 3: 2, 6: 3, 9: 3}
+VARIANTS = (1, 3, 6, 8, 9)
+PIECES = {1: 1, 3: 2, 6: 3, 8: 3, 9: 3}
 
 
 class Bf16xError(RuntimeError):

@@ -81,7 +81,7 @@ static int gemm_args(int m, int n, int k, int lda, int ldb, int ldc, int variant
     if (lda < (m > 1 ? m : 1)) return -6;
     if (ldb < (k > 1 ? k : 1)) return -8;
     if (ldc < (m > 1 ? m : 1)) return -11;
-    if (variant != 1 && variant != 3 && variant != 6 && variant != 9) return -12;
+    if (variant != 1 && variant != 3 && variant != 6 && variant != 8 && variant != 9) return -12;
     return 0;
 }
 
@@ -171,7 +171,7 @@ int bf16x_gemm(int m, int n, int k, float alpha, const float *A, int lda, const 
 
 size_t bf16x_gemm_workspace_size(int m, int n, int k, int variant) {
     if (m < 0 || n < 0 || k < 0) return 0;
-    int v = (variant == 1 || variant == 3 || variant == 6 || variant == 9) ? variant : 9;
+    int v = (variant == 1 || variant == 3 || variant == 6 || variant == 8 || variant == 9) ? variant : 9;
     return 2ull * (size_t)pieces_of(v) * ((size_t)m + (size_t)n) * (size_t)round_up8(k);
 }
 

@@ -150,6 +150,8 @@ __device__ __forceinline__ void issue_interval(uint32_t d_tmem, const uint64_t (
     if constexpr (V == 9) {
 #pragma unroll
         for (int h = 0; h < H; ++h) if (h < nh) mma(2, 2, h);                              // bin 4: 2^-32
+    }
+    if constexpr (V >= 8) {   // x8 = the paper's Z_3: bins 0..3
 #pragma unroll
         for (int h = 0; h < H; ++h) if (h < nh) { mma(1, 2, h); mma(2, 1, h); }           // bin 3: 2^-24
     }
@@ -643,6 +645,7 @@ int launch_gemm_pieces(const GemmPlan &pl, cudaStream_t st) {
         case 1: return launch_s<1, 1>(pl, st);
         case 3: return launch_s<1, 3>(pl, st);
         case 6: return launch_s<1, 6>(pl, st);
+        case 8: return launch_s<1, 8>(pl, st);
         case 9: return launch_s<1, 9>(pl, st);
         }
     } else {
@@ -650,6 +653,7 @@ int launch_gemm_pieces(const GemmPlan &pl, cudaStream_t st) {
         case 1: return launch_s<2, 1>(pl, st);
         case 3: return launch_s<2, 3>(pl, st);
         case 6: return launch_s<2, 6>(pl, st);
+        case 8: return launch_s<2, 8>(pl, st);
         case 9: return launch_s<2, 9>(pl, st);
         }
     }

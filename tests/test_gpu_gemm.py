@@ -68,7 +68,7 @@ def test_uniform_shapes(orc, shape, variant, cg, spi, mc):
 
 @pytest.mark.parametrize("cg", [1, 2])
 @pytest.mark.parametrize("dist", ["wide", "gauss"])
-@pytest.mark.parametrize("variant", [3, 6, 9])
+@pytest.mark.parametrize("variant", [3, 6, 8, 9])
 def test_wide_and_gaussian(orc, dist, variant, cg, spi):
     A = synthetic.by_name(dist, 200, 300, seed=5)
     B = synthetic.by_name(dist, 300, 260, seed=6)
@@ -76,7 +76,7 @@ def test_wide_and_gaussian(orc, dist, variant, cg, spi):
 
 
 @pytest.mark.parametrize("k", [256, 1024, 4096, 16384])
-@pytest.mark.parametrize("variant", [3, 6, 9])
+@pytest.mark.parametrize("variant", [3, 6, 8, 9])
 def test_k_sweep_wide(orc, k, variant, spi, mc):
     """Config 3 shape family (k-sweep, wide exponents) at m = n = 256."""
     A = synthetic.wide(256, k, seed=1000 + k)
@@ -91,7 +91,7 @@ def test_exact_pins(orc, cg, spi, mc):
     A = synthetic.wide(300, 40, seed=8)
     I = np.eye(40, dtype=np.float32)
     P = I[:, np.random.default_rng(0).permutation(40)]
-    for v in (6, 9):
+    for v in (6, 8, 9):
         assert np.array_equal(_gpu(A, I, variant=v, cg=cg), A)
         assert np.array_equal(_gpu(A, P, variant=v, cg=cg), A @ P)
     b0, b1, _ = orc.split(A)
