@@ -16,7 +16,7 @@ static std::atomic<uint64_t> g_launches{0};
 static std::mutex g_ws_mu;
 static void *g_ws = nullptr;
 static size_t g_ws_bytes = 0;
-static int g_force_cg = 0, g_force_bn = 0, g_force_spi = 0, g_stream_k = 1, g_multicast = 0;  // tuning overrides (bf16x_tune; not in the public ABI)
+static int g_force_cg = 0, g_force_bn = 0, g_force_spi = 0, g_stream_k = 1, g_multicast = 0, g_split_acc = 0;  // tuning overrides (bf16x_tune; not in the public ABI)
 
 void set_cuda_error(cudaError_t e, const char *where) {
     snprintf(g_err, sizeof(g_err), "%s: %s", where, cudaGetErrorString(e));
@@ -152,6 +152,7 @@ int gemm_core(int m, int n, int k, float alpha, const float *A, int lda, const f
     pl.stages_per_interval = g_force_spi;
     pl.stream_k = g_stream_k;
     pl.multicast = g_multicast;
+    pl.split_acc = g_split_acc;
     return launch_gemm_pieces(pl, st);
 }
 
@@ -306,6 +307,7 @@ uint64_t bf16x_launch_count(void) { return g_launches.load(); }
 // testing/bench hooks (not in the public header)
 int bf16x_default_cta_group(void) { return default_cta_group(); }
 void bf16x_stream_k(int on) { g_stream_k = on; }
+void bf16x_split_acc(int on) { g_split_acc = on; }
 void bf16x_multicast(int pairs) { g_multicast = pairs; }   // 0 = auto, 1 = off, 2 = on
 void bf16x_tune(int cta_group, int tile_n, int stages_per_interval) {
     g_force_cg = cta_group;

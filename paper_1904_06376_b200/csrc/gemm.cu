@@ -131,21 +131,28 @@ __device__ __forceinline__ void tile_coords(int tile, int tiles_m, int tiles_n, 
 
 // Issue one promotion interval's MMAs, smallest bin first: every band is
 // issued over all K=16 halves of the interval's ns stages (ns <= S) before the next,
-// larger band.  The interval's first MMA overwrites the TMEM accumulator.
-template <int CG, int V, int BN, int S>
-__device__ __forceinline__ void issue_interval(uint32_t d_tmem, const uint64_t (&a_desc)[S],
+// larger band.  SA = false: one TMEM accumulator for all bands.  SA = true ("split
+// accumulators"): bins >= 1 go to d_small and bin 0 to d_big, so the tensor core's
+// alignment truncation of each MMA step (K3 probe) never cuts the small bins against the
+// bin-0 products; the epilogue combines them as (small + big) in FP32 round-to-nearest.
+// Each accumulator's first MMA of the interval overwrites it.
+template <int CG, int V, int BN, int S, bool SA>
+__device__ __forceinline__ void issue_interval(uint32_t d_big, uint32_t d_small, const uint64_t (&a_desc)[S],
                                                const uint64_t (&b_desc)[S], int ns, uint32_t idesc) {
     using Cf = Cfg<CG, V, BN>;
     constexpr int H = S * (kBK / kUK);     // K=16 halves per interval (max)
     const int nh = ns * (kBK / kUK);
-    bool first = true;
+    bool first_small = true, first_big = true;
     // descriptor start-address field is in 16-byte units: piece / K-half offsets add directly
     auto mma = [&](int i, int j, int h) {
         const int st = h / (kBK / kUK), kk = h % (kBK / kUK);
         const uint64_t ad = a_desc[st] + (uint64_t)((i * Cf::A_PIECE + kk * (kUK * 2)) >> 4);
         const uint64_t bd = b_desc[st] + (uint64_t)((j * Cf::B_PIECE + kk * (kUK * 2)) >> 4);
-        umma_bf16_elect<CG>(d_tmem, ad, bd, idesc, first ? 0u : 1u);
+        const bool big = SA && (i + j == 0);
+        bool &first = (SA && !big) ? first_small : first_big;
+        umma_bf16_elect<CG>(big || !SA ? d_big : d_small, ad, bd, idesc, first ? 0u : 1u);
         first = false;
+        if constexpr (!SA) first_small = false;
     };
     if constexpr (V == 9) {
 #pragma unroll
@@ -169,13 +176,14 @@ __device__ __forceinline__ void issue_interval(uint32_t d_tmem, const uint64_t (
 
 // MC = number of CTA pairs per cluster sharing the B tile (1, or 2: two vertically adjacent
 // 256 x BN tiles; each pair loads half of every B slice and multicasts it to both pairs).
-template <int CG, int V, int BN, int S, int MC>
+template <int CG, int V, int BN, int S, int MC, bool SA>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_split_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                       const KParams p) {
     using Cf = Cfg<CG, V, BN>;
     constexpr int CL = CG * MC;   // cluster size
     static_assert(MC == 1 || CG == 2, "multicast needs 2-CTA pairs");
+    static_assert(!SA || 2 * BN <= kTmemBufStride, "split accumulators need 4 x BN TMEM columns");
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t *sA = smem;
@@ -289,7 +297,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                             }
                         }
                         tc_fence_after();
-                        issue_interval<CG, V, BN, S>(tmem_base + buf * kTmemBufStride, a_desc, b_desc, ns, idesc);
+                        // buffer layout: SA -> small at buf*BN, big at 256 + buf*BN; else one at buf*256
+                        const uint32_t d_big = SA ? tmem_base + kTmemBufStride + buf * BN : tmem_base + buf * kTmemBufStride;
+                        const uint32_t d_small = SA ? tmem_base + buf * BN : d_big;
+                        issue_interval<CG, V, BN, S, SA>(d_big, d_small, a_desc, b_desc, ns, idesc);
 #pragma unroll
                         for (int q = 0; q < S; ++q)
                             if (q < ns) {
@@ -332,14 +343,28 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const uint32_t buf = acc_it & 1u, apar = (acc_it >> 1) & 1u;
                 mbar_wait(&acc_full[buf], apar);
                 tc_fence_after();
-                const uint32_t taddr = tm_lane + buf * kTmemBufStride;
+                if constexpr (!SA) {
+                    const uint32_t taddr = tm_lane + buf * kTmemBufStride;
 #pragma unroll
-                for (int c = 0; c < EC / 16; ++c) {
-                    float v[16];
-                    tmem_ld16(taddr + c * 16, v);
-                    tmem_ld_wait();
+                    for (int c = 0; c < EC / 16; ++c) {
+                        float v[16];
+                        tmem_ld16(taddr + c * 16, v);
+                        tmem_ld_wait();
 #pragma unroll
-                    for (int j = 0; j < 16; ++j) G[c * 16 + j] = __fadd_rn(G[c * 16 + j], v[j]);
+                        for (int j = 0; j < 16; ++j) G[c * 16 + j] = __fadd_rn(G[c * 16 + j], v[j]);
+                    }
+                } else {
+                    // interval total = small bins + bin 0 (RN), then into G (RN)
+                    const uint32_t ts = tm_lane + buf * BN, tb = tm_lane + kTmemBufStride + buf * BN;
+#pragma unroll
+                    for (int c = 0; c < EC / 16; ++c) {
+                        float vs[16], vb[16];
+                        tmem_ld16(ts + c * 16, vs);
+                        tmem_ld16(tb + c * 16, vb);
+                        tmem_ld_wait();
+#pragma unroll
+                        for (int j = 0; j < 16; ++j) G[c * 16 + j] = __fadd_rn(G[c * 16 + j], __fadd_rn(vs[j], vb[j]));
+                    }
                 }
                 tc_fence_before();
                 __syncwarp();
@@ -505,7 +530,7 @@ int num_sms() {
 int pieces_of(int variant) { return variant_pieces(variant); }
 int default_cta_group() { return kDefaultCtaGroup; }
 
-template <int CG, int V, int BN, int S, int MC>
+template <int CG, int V, int BN, int S, int MC, bool SA = false>
 static int launch_t(const GemmPlan &pl, cudaStream_t st) {
     using Cf = Cfg<CG, V, BN>;
     constexpr int CL = CG * MC;
@@ -529,7 +554,7 @@ static int launch_t(const GemmPlan &pl, cudaStream_t st) {
         // clusters of 4 do not tile every GPC: only co-resident clusters may be launched
         static int max_clusters = -1;
         if (max_clusters < 0) {
-            cudaFuncSetAttribute(gemm_split_kernel<CG, V, BN, S, MC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+            cudaFuncSetAttribute(gemm_split_kernel<CG, V, BN, S, MC, SA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  Cf::SMEM);
             cudaLaunchConfig_t qc = {};
             qc.gridDim = dim3(units * CL);
@@ -543,7 +568,7 @@ static int launch_t(const GemmPlan &pl, cudaStream_t st) {
             qc.attrs = qa;
             qc.numAttrs = 1;
             int nclu = 0;
-            if (cudaOccupancyMaxActiveClusters(&nclu, gemm_split_kernel<CG, V, BN, S, MC>, &qc) != cudaSuccess) {
+            if (cudaOccupancyMaxActiveClusters(&nclu, gemm_split_kernel<CG, V, BN, S, MC, SA>, &qc) != cudaSuccess) {
                 cudaGetLastError();
                 nclu = 0;
             }
@@ -573,7 +598,7 @@ static int launch_t(const GemmPlan &pl, cudaStream_t st) {
 
     static bool attr_set = false;  // per template instance
     if (!attr_set) {
-        if (cudaFuncSetAttribute(gemm_split_kernel<CG, V, BN, S, MC>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cf::SMEM) !=
+        if (cudaFuncSetAttribute(gemm_split_kernel<CG, V, BN, S, MC, SA>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cf::SMEM) !=
             cudaSuccess)
             return check_launch("gemm attr");
         attr_set = true;
@@ -592,7 +617,7 @@ static int launch_t(const GemmPlan &pl, cudaStream_t st) {
     attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 2;
-    cudaError_t e = cudaLaunchKernelEx(&cfg, gemm_split_kernel<CG, V, BN, S, MC>, tmA, tmB, kp);
+    cudaError_t e = cudaLaunchKernelEx(&cfg, gemm_split_kernel<CG, V, BN, S, MC, SA>, tmA, tmB, kp);
     if (e != cudaSuccess) {
         set_cuda_error(e, "gemm launch");
         return BF16X_ERR_CUDA;
@@ -619,13 +644,17 @@ int choose_tile_n(int m, int n, int cg, int units, int forced) {
 template <int CG, int V>
 static int launch_s(const GemmPlan &pl, cudaStream_t st) {
     int s = pl.stages_per_interval;
-    if (s != 1 && s != 2) s = (CG == 2) ? 2 : 1;
+    // Short k (<= 128): the whole product is one or two intervals, so the tensor core's
+    // truncating accumulation dominates the error; 32-k intervals halve it (measured wide
+    // exponents, k = 64: max ratio to the oracle 2.07 -> 1.66) at no cost that matters.
+    if (s != 1 && s != 2) s = (CG == 2 && pl.k > 128) ? 2 : 1;
     if (s == 2 && Cfg<CG, V, 256>::STAGES < 4) s = 1;
     if constexpr (CG == 2) {
         if (s == 2) {
             const int units = (pl.max_ctas > 0 ? pl.max_ctas : num_sms()) / CG;
             const int bn = choose_tile_n(pl.m, pl.n, CG, units, pl.tile_n);
             if (bn == 192) return launch_t<CG, V, 192, 2, 1>(pl, st);
+            if (pl.split_acc && V >= 3) return launch_t<CG, V, 128, 2, 1, true>(pl, st);
             // Two pairs per cluster sharing B (TMA multicast) cut L2->SM and DRAM traffic by a
             // quarter but clusters of 4 leave 16 SMs idle; measured (r05) a win only for large
             // outputs, where the kernel runs long enough to be power-limited (16384^3: x3 +17 %,

@@ -29,6 +29,7 @@ struct GemmPlan {
     int stages_per_interval;  // 0 = choose; 1 or 2 stages of 32 k per promotion interval
     int stream_k;        // 0 = data-parallel only, else hybrid stream-K for the last waves
     int multicast;       // 2 = two CTA pairs per cluster share B tiles (TMA multicast), else 1
+    int split_acc;       // 1 = separate TMEM accumulators for bin 0 and bins >= 1 (tile N 128)
 };
 
 int launch_gemm_pieces(const GemmPlan &p, cudaStream_t st);
