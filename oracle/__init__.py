@@ -8,8 +8,9 @@ The arithmetic lives in ``bf16x_oracle.c`` (plain C99, one IEEE FP32 operation
 per source operation, no FTZ); this module is argument marshalling plus the
 plain-numpy error metrics and the iterative-refinement loop (§III), each
 citing the passage it follows.  Pins: ``tests/test_oracle_*.py``; see DESIGN.md
-"Oracle pins" for the list (the LU-IR convergence statistics are *parity
-unpinned*: the paper's table is for single-BF16/FP16 LU).
+"Oracle pins" for the list (the LU-IR and GMRES-IR convergence statistics are
+*parity unpinned*: the paper's tables are for single-BF16/FP16 LU; GMRES
+itself is pinned by Krylov theory and brute-force least squares, test_oracle_gmres.py).
 """
 from __future__ import annotations
 
@@ -262,3 +263,116 @@ def gesv_ir(A, b, variant=3, nb=64, max_iter=30):
             break
         x = x + lu_solve_f64(LU, ipiv, r)
     return dict(x=x, converged=converged, iterations=it, info=0, history=hist)
+
+
+# --------------------------------------------------------------------------
+# O-8: GMRES and GMRES-IR (§III "combining Iterative Refinement with an
+# Iterative Solver like GMRES [iterativerefinement-fp16][templates]"
+# §IV-B "apply GMRES instead of iterative refinement, and use the LU decomposition
+# in the lower precision ... as a pre-conditioner")
+# --------------------------------------------------------------------------
+def gmres(matvec, psolve, b, x0=None, restart=None, tol=1e-10, max_cycles=1):
+    """Left-preconditioned restarted GMRES(m) in FP64, step by step as in the paper's
+    cited GMRES template (Barrett et al., "Templates for the Solution of Linear Systems",
+    section 2.3.4): Arnoldi with modified Gram-Schmidt on M^-1 A, Givens rotations on the
+    Hessenberg column, least-squares update x += V y at the end of each cycle.
+
+    Solves M^-1 A x = M^-1 b.  matvec(v) = A v, psolve(v) = M^-1 v (both FP64).  A cycle
+    ends after `restart` Arnoldi steps, on an exact breakdown (h_{j+1,j} == 0: the
+    Krylov space is invariant, the least-squares solution is exact), or when the rotated
+    residual |s_{j+1}| <= tol * ||M^-1 (b - A x0)||_2 (reading R25).
+    Returns dict(x, iterations = Arnoldi steps, history = [|s_{j+1}|], converged)."""
+    b = np.asarray(b, dtype=np.float64)
+    n = b.size
+    m = n if restart is None else max(1, min(int(restart), n))
+    x = np.zeros(n) if x0 is None else np.array(x0, dtype=np.float64)
+    r = psolve(b - matvec(x))
+    beta0 = float(np.linalg.norm(r))
+    hist = []
+    steps = 0
+    if beta0 == 0.0:
+        return dict(x=x, iterations=0, history=[0.0], converged=True)
+    converged = False
+    for _cycle in range(max_cycles):
+        beta = float(np.linalg.norm(r))
+        V = np.zeros((n, m + 1))
+        H = np.zeros((m + 1, m))
+        cs = np.zeros(m)
+        sn = np.zeros(m)
+        s = np.zeros(m + 1)
+        s[0] = beta
+        V[:, 0] = r / beta
+        jm = 0
+        for j in range(m):
+            w = psolve(matvec(V[:, j]))
+            for i in range(j + 1):                      # modified Gram-Schmidt
+                H[i, j] = float(w @ V[:, i])
+                w = w - H[i, j] * V[:, i]
+            hnext = float(np.linalg.norm(w))
+            H[j + 1, j] = hnext
+            if hnext != 0.0:
+                V[:, j + 1] = w / hnext
+            for i in range(j):                          # previous rotations on column j
+                t = cs[i] * H[i, j] + sn[i] * H[i + 1, j]
+                H[i + 1, j] = -sn[i] * H[i, j] + cs[i] * H[i + 1, j]
+                H[i, j] = t
+            d = float(np.hypot(H[j, j], H[j + 1, j]))  # new rotation annihilates H[j+1, j]
+            cs[j] = H[j, j] / d
+            sn[j] = H[j + 1, j] / d
+            H[j, j] = d
+            H[j + 1, j] = 0.0
+            s[j + 1] = -sn[j] * s[j]
+            s[j] = cs[j] * s[j]
+            steps += 1
+            jm = j + 1
+            hist.append(abs(float(s[j + 1])))
+            if abs(s[j + 1]) <= tol * beta0 or hnext == 0.0:
+                converged = True
+                break
+        y = np.zeros(jm)                                 # back substitution H y = s
+        for i in range(jm - 1, -1, -1):
+            y[i] = (s[i] - H[i, i + 1:jm] @ y[i + 1:jm]) / H[i, i]
+        x = x + V[:, :jm] @ y
+        if converged:
+            break
+        r = psolve(b - matvec(x))
+    return dict(x=x, iterations=steps, history=hist, converged=converged)
+
+
+def gmres_ir(A, b, variant=3, nb=64, restart=200, inner_tol=1e-10, max_iter=30):
+    """GMRES-IR: factor once in low precision (getrf, the split-GEMM trailing updates of
+    P:406); outer loop as gesv_ir (r = b - A x in FP64, same stopping and stagnation rules,
+    R14), but the correction equation A d = r is solved by one cycle of FP64 GMRES left-
+    preconditioned with the low-precision factors (reading R25), x0 = 0.
+    Returns dict(x, converged, iterations = outer corrections, inner_iterations = total
+    Arnoldi steps, info, history)."""
+    A = _colmajor_f32(A)
+    n = A.shape[0]
+    LU, ipiv, info = getrf(A, variant=variant, nb=nb)
+    if info != 0:
+        return dict(x=np.zeros(n), converged=False, iterations=0, inner_iterations=0, info=info, history=[])
+    anrm = float(np.max(np.sum(np.abs(A.astype(np.float64)), axis=1)))
+    eps = 2.0 ** -53
+    zero = np.zeros(n)
+    matvec = lambda v: -residual_f64(A, zero, v)          # A v, FP64 sums of FP32 A
+    psolve = lambda v: lu_solve_f64(LU, ipiv, v)
+    x = np.zeros(n)
+    hist = []
+    converged = False
+    inner = 0
+    it = 0
+    for it in range(0, max_iter + 1):
+        r = residual_f64(A, b, x)
+        rn = float(np.max(np.abs(r)))
+        hist.append(rn)
+        if rn <= np.sqrt(n) * float(np.max(np.abs(x))) * anrm * eps:
+            converged = True
+            break
+        if it == max_iter:
+            break
+        if len(hist) >= 4 and hist[-1] > 0.5 * hist[-4]:
+            break
+        g = gmres(matvec, psolve, r, restart=restart, tol=inner_tol, max_cycles=1)
+        inner += g["iterations"]
+        x = x + g["x"]
+    return dict(x=x, converged=converged, iterations=it, inner_iterations=inner, info=0, history=hist)
