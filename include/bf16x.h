@@ -150,10 +150,46 @@ typedef struct {
     double tol;              /* threshold the test compared ||r||_inf against */
     double factor_ms;        /* device time of the LU factorisation */
     double refine_ms;        /* device time of the refinement loop */
+    int inner_iterations;    /* bf16x_gesv_gmres_ir: total Arnoldi steps (0 for bf16x_gesv_ir) */
 } bf16x_ir_report;
 
 int bf16x_gesv_ir(int n, const float *A, int lda, const double *b, double *x, int variant,
                   int nb, int max_iter, double *residual_history, bf16x_ir_report *report);
+
+/* ------------------------------------------------------------------------------------
+ * bf16x_gesv_gmres_ir -- GMRES-IR (section III: "combining Iterative Refinement with
+ * an Iterative Solver like GMRES"; section IV-B: "apply GMRES instead of iterative
+ * refinement, and use the LU decomposition in the lower precision ... as a pre-conditioner").
+ * Same factorisation and outer loop as bf16x_gesv_ir (x0 = 0; r = b - A x in FP64; the same
+ * stopping and stagnation rules, R14), but each correction A d = r is solved by one cycle
+ * of FP64 GMRES on M^-1 A d = M^-1 r with M^-1 = U^-1 L^-1 P from the bf16x factors:
+ * Arnoldi by classical Gram-Schmidt applied twice, Givens rotations, cycle ends after
+ * `restart` steps, on breakdown, or when the rotated residual <= inner_tol * ||M^-1 r||_2
+ * (reading R25).  Synchronous.
+ *   n, A, lda, b, x, variant, nb, max_iter, residual_history, report: as bf16x_gesv_ir
+ *     (report->iterations = outer corrections, report->inner_iterations = Arnoldi steps)
+ *   restart   : Arnoldi steps per correction (<= 0: 200; capped at n and at 8190)
+ *   inner_tol : relative tolerance of each GMRES cycle (0: 1e-10; < 0 or NaN: error -9)
+ * Device workspace: n*(restart+1) doubles for the Krylov basis on top of bf16x_gesv_ir's.
+ * Returns as bf16x_gesv_ir; errors -1 n, -3 lda, -6 variant, -9 inner_tol,
+ * -12 report NULL. */
+int bf16x_gesv_gmres_ir(int n, const float *A, int lda, const double *b, double *x, int variant,
+                        int nb, int restart, double inner_tol, int max_iter,
+                        double *residual_history, bf16x_ir_report *report);
+
+/* ------------------------------------------------------------------------------------
+ * bf16x_getrf -- the factorisation alone (LAPACK sgetrf semantics, "a SGETRF
+ * based on triplets of BF16s and six products"): P A = L U in place, right-looking blocked,
+ * FP32 panel + TRSM, trailing updates A22 -= L21 U12 in bf16x_gemm(variant).
+ *   A    : n x n FP32 DEVICE, lda >= max(1,n); overwritten by L (unit, below the diagonal)
+ *          and U (on and above)
+ *   ipiv : DEVICE int32[n], 0-based: row j was interchanged with row ipiv[j] (in order)
+ *   variant : 1, 3, 6, 8 or 9;  nb : panel width (<= 0: 256)
+ *   info : HOST, nullable; 0 or the 1-based column of the first exact zero pivot
+ * Synchronous.  Returns BF16X_SUCCESS, BF16X_ERR_SINGULAR (factorisation continued past
+ * the zero pivot as LAPACK does only for the remaining columns' interchanges), or -1 n,
+ * -2 A NULL, -3 lda, -4 ipiv NULL, -5 variant. */
+int bf16x_getrf(int n, float *A, int lda, int *ipiv, int variant, int nb, int *info);
 
 /* ------------------------------------------------------------------------------------
  * Library state.

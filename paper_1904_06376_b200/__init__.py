@@ -32,7 +32,8 @@ class Bf16xError(RuntimeError):
 class IRReport(ctypes.Structure):
     _fields_ = [("converged", ctypes.c_int), ("iterations", ctypes.c_int), ("info", ctypes.c_int),
                 ("final_residual", ctypes.c_double), ("backward_error", ctypes.c_double),
-                ("tol", ctypes.c_double), ("factor_ms", ctypes.c_double), ("refine_ms", ctypes.c_double)]
+                ("tol", ctypes.c_double), ("factor_ms", ctypes.c_double), ("refine_ms", ctypes.c_double),
+                ("inner_iterations", ctypes.c_int)]
 
 
 _lib = None
@@ -57,6 +58,9 @@ def lib() -> ctypes.CDLL:
         L.bf16x_gemm_cg.argtypes = [_i, _i, _i, _f, _vp, _i, _vp, _i, _f, _vp, _i, _i, _i, _vp]
         L.bf16x_gemm_host.argtypes = [_i, _i, _i, _f, _vp, _i, _vp, _i, _f, _vp, _i, _i]
         L.bf16x_gesv_ir.argtypes = [_i, _vp, _i, _vp, _vp, _i, _i, _i, _vp, ctypes.POINTER(IRReport)]
+        L.bf16x_gesv_gmres_ir.argtypes = [_i, _vp, _i, _vp, _vp, _i, _i, _i, ctypes.c_double, _i, _vp,
+                                          ctypes.POINTER(IRReport)]
+        L.bf16x_getrf.argtypes = [_i, _vp, _i, _vp, _i, _i, ctypes.POINTER(ctypes.c_int)]
         L.bf16x_set_stream.argtypes = [_vp]
         L.bf16x_get_stream.restype = _vp
         L.bf16x_status_string.argtypes = [_i]
@@ -261,3 +265,47 @@ def gesv_ir(A, b, variant: int = 3, nb: int = 256, max_iter: int = 30):
     if rc not in (SUCCESS, NOT_CONVERGED, ERR_SINGULAR):
         _check(rc, "bf16x_gesv_ir")
     return x, rep, hist[: rep.iterations + 1]
+
+
+def _square_colmajor(A):
+    cm = _colmajor(A)
+    if cm is None:
+        A = A.t().contiguous().t()
+        cm = _colmajor(A)
+    return A, cm
+
+
+def gesv_gmres_ir(A, b, variant: int = 3, nb: int = 256, restart: int = 200, inner_tol: float = 1e-10,
+                  max_iter: int = 30):
+    """GMRES-IR (bf16x_gesv_gmres_ir): LU with bf16x trailing updates as the preconditioner of
+    FP64 GMRES corrections.  Arguments as gesv_ir plus restart / inner_tol.
+    Returns (x, report, history); report.inner_iterations = total Arnoldi steps."""
+    import torch
+    n = A.shape[0]
+    A, cm = _square_colmajor(A)
+    x = torch.empty(n, dtype=torch.float64, device=A.device)
+    b = b.to(torch.float64).contiguous()
+    hist = np.zeros(max(1, max_iter) + 1, dtype=np.float64)
+    rep = IRReport()
+    rc = lib().bf16x_gesv_gmres_ir(n, cm[0], cm[3], _ptr(b), _ptr(x), variant, nb, restart, float(inner_tol),
+                                   max_iter, hist.ctypes.data, ctypes.byref(rep))
+    if rc not in (SUCCESS, NOT_CONVERGED, ERR_SINGULAR):
+        _check(rc, "bf16x_gesv_gmres_ir")
+    return x, rep, hist[: rep.iterations + 1]
+
+
+def getrf(A, variant: int = 3, nb: int = 256):
+    """P A = L U of a square float32 CUDA matrix (bf16x_getrf).  Returns (LU, ipiv, info):
+    LU a column-major float32 CUDA tensor (a copy; A is not modified), ipiv int32 CUDA
+    (0-based interchange sequence), info the 1-based first zero-pivot column or 0."""
+    import torch
+    n = A.shape[0]
+    LU = torch.empty_strided((n, n), (1, max(1, n)), dtype=torch.float32, device=A.device)
+    LU.copy_(A)
+    cm = _colmajor(LU)
+    ipiv = torch.zeros(max(1, n), dtype=torch.int32, device=A.device)
+    info = ctypes.c_int(0)
+    rc = lib().bf16x_getrf(n, cm[0], cm[3], _ptr(ipiv), variant, nb, ctypes.byref(info))
+    if rc not in (SUCCESS, ERR_SINGULAR):
+        _check(rc, "bf16x_getrf")
+    return LU, ipiv[:n], int(info.value)

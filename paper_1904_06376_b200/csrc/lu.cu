@@ -453,136 +453,160 @@ __global__ void gather_kernel(int n, const int *perm, const double *v, double *y
     if (i < n) y[i] = v[perm[i]];
 }
 
-constexpr int kTrsvBlock = 128;
+// ------------------------------------------------------------------------------------
+// K6b: triangular solves in FP64 with the FP32 factors widened exactly ("do the solve
+// in a higher precision like FP64").  Two kernels:
+//   diag_inverse_kernel  once per factorisation: the FP64 inverse of every 128 x 128
+//                        diagonal block of L (unit lower) and U (upper), by row-oriented
+//                        substitution (all columns of a row in parallel).
+//   trsv_kernel          per solve: block b's CTA accumulates sum_{b' before b} T_{b,b'} x_{b'}
+//                        as each x_{b'} is published (per-block ready flags, no grid barrier;
+//                        the tiles are streamed into shared memory with cp.async before their
+//                        x arrives), then x_b = inv(T_bb) (y_b - sum) -- one 128 x 128 FP64
+//                        product on the critical path instead of a 128-step substitution.
+// Blocks are numbered in processing order p (lower: b = p; upper: b = nblk-1-p), so both
+// solves have the same dependency pattern: p depends on every p' < p.
+// ------------------------------------------------------------------------------------
+constexpr int kTB = 128;                 // rows / columns per block
+constexpr int kTChunk = 64;              // tile columns per streamed chunk
+constexpr int kTrsvThreads = 256;
+constexpr size_t kTinvBlock = (size_t)kTB * kTB;                         // doubles per inverse
+constexpr int kTrsvSmem = (int)(kTinvBlock * sizeof(double) + 2 * (size_t)kTChunk * kTB * sizeof(float) +
+                                4 * kTB * sizeof(double));
 
-constexpr int kTS = kTrsvBlock + 4;   // smem column stride (floats): 16-byte aligned columns
-constexpr int kTrsvSmem = 2 * kTrsvBlock * kTS * sizeof(float) + 3 * kTrsvBlock * sizeof(double);
-
-// acc = sum_{j < pw} LU[(pc0 + j) * ld + r] * sx[j], 16 independent loads in flight per batch
-// acc = sum_{j < pw} LU[(pc0 + j) * ld + r] * sx[j] (pw <= kTrsvBlock): all loads are issued
-// before the first FMA, so the row costs one memory round trip.
-__device__ __forceinline__ double dot_col_block(const float *LU, int64_t ld, int pc0, int pw, int r, const double *sx) {
-    float a[kTrsvBlock];
-#pragma unroll
-    for (int q = 0; q < kTrsvBlock; ++q) a[q] = (q < pw) ? __ldg(LU + (int64_t)(pc0 + q) * ld + r) : 0.f;
-    double acc = 0.0;
-#pragma unroll
-    for (int q = 0; q < kTrsvBlock; ++q) acc = fma((double)a[q], (q < pw) ? sx[q] : 0.0, acc);
-    return acc;
-}
-
-// Asynchronously copy the rows x cols tile LU[r0.., c0..] into smem [col][kTS] (LDGSTS).
-__device__ __forceinline__ void prefetch_tile(float *dst, const float *LU, int64_t ld, int r0, int rows, int c0,
-                                              int cols) {
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    for (int c = wid; c < cols; c += nw) {
-        const float *src = LU + (int64_t)(c0 + c) * ld + r0;
-        for (int r = lane; r < rows; r += 32)
-            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst + c * kTS + r)), "l"(src + r)
-                         : "memory");
+// Tinv layout: [tri][block][col][row] FP64 (tri 0 = inv(L_bb), 1 = inv(U_bb)); entries outside
+// a ragged block's w x w are 0.
+__global__ void __launch_bounds__(kTB) diag_inverse_kernel(const float *LU, int ld, int n, double *Tinv) {
+    extern __shared__ double sx_inv[];   // X [row][col] (kTB x kTB) then T [row][col] as FP32
+    float *sT = reinterpret_cast<float *>(sx_inv + kTinvBlock);
+    const int b = blockIdx.x, upper = blockIdx.y, j = threadIdx.x;
+    const int c0 = b * kTB, w = min(n, c0 + kTB) - c0;
+    for (int r = 0; r < kTB; ++r) {
+        sT[r * kTB + j] = (r < w && j < w) ? LU[(int64_t)(c0 + j) * ld + c0 + r] : 0.f;
+        sx_inv[r * kTB + j] = 0.0;
     }
-    asm volatile("cp.async.commit_group;" ::: "memory");
-}
-
-// Blocked triangular solve in FP64 with the FP32 factors, cooperative grid.  lower != 0:
-// L y = y (unit diagonal, forward); else U y = y (backward).  Step s handles block b_s (128
-// rows): CTA 0 owns the critical path -- the block's diagonal tile and the tile coupling it to
-// the previous block were prefetched into shared memory (cp.async) during the previous
-// barrier, so it applies the previous block to b_s's rows, solves the diagonal triangle and
-// publishes x_{b_s}; CTAs 1.. apply the previous block to every other dependent row.  One
-// grid barrier per block.  y is accessed with L2-coherent loads/stores.
-__global__ void __launch_bounds__(256) trsv_kernel(const float *LU, int ld, int n, double *y, int lower, GridBar gb,
-                                                   unsigned int epoch) {
-    extern __shared__ double sdyn[];
-    double *sx = sdyn;                             // [kTrsvBlock] solution of the previous block
-    double *sy = sx + kTrsvBlock;                  // [kTrsvBlock] current block (CTA 0)
-    double *sp = sy + kTrsvBlock;                  // [kTrsvBlock] partial sums (CTA 0)
-    float *sL = reinterpret_cast<float *>(sp + kTrsvBlock);   // [col][kTS] diagonal tile
-    float *sB = sL + kTrsvBlock * kTS;                        // [col][kTS] coupling tile
-    const int nblk = (n + kTrsvBlock - 1) / kTrsvBlock;
-    const int G = gridDim.x, tid = threadIdx.x;
-    auto blk = [&](int s, int &c0, int &w) {
-        const int b = lower ? s : nblk - 1 - s;
-        c0 = b * kTrsvBlock;
-        w = min(n, c0 + kTrsvBlock) - c0;
-    };
-    if (blockIdx.x == 0) {
-        int c0, w;
-        blk(0, c0, w);
-        prefetch_tile(sL, LU, ld, c0, w, c0, w);
-    }
-    int pc0 = 0, pw = 0;                  // previous block [pc0, pc0+pw)
-    for (int s = 0; s < nblk; ++s) {
-        int c0, w;
-        blk(s, c0, w);
-        const int c1 = c0 + w;
-        if (s > 0) {
-            for (int e = tid; e < pw; e += blockDim.x) sx[e] = __ldcg(y + pc0 + e);
+    __syncthreads();
+    if (!upper) {
+        // X = L^-1 (unit lower): X[i][i] = 1, X[i][j] = -sum_{k=j}^{i-1} L[i][k] X[k][j] (j < i)
+        for (int i = 0; i < w; ++i) {
+            if (j < i) {
+                double acc = 0.0;
+                for (int k = j; k < i; ++k) acc = fma((double)sT[i * kTB + k], sx_inv[k * kTB + j], acc);
+                sx_inv[i * kTB + j] = -acc;
+            } else if (j == i) {
+                sx_inv[i * kTB + j] = 1.0;
+            }
             __syncthreads();
         }
-        if (blockIdx.x == 0) {
-            asm volatile("cp.async.wait_group 0;" ::: "memory");
-            __syncthreads();
-            // y_b - (coupling tile) x_prev : 2 threads per row, half of the previous block each
-            if (tid < 2 * w) {
-                const int r = tid % w, hsel = tid / w, half = pw / 2;
-                const int jb = hsel ? half : 0, je = hsel ? pw : half;
-                double part = 0.0;
-                for (int j = jb; j < je; ++j) part = fma((double)sB[j * kTS + r], sx[j], part);
-                if (hsel) sp[r] = part; else sy[r] = part;
+    } else {
+        // X = U^-1: X[i][i] = 1/U[i][i], X[i][j] = -(sum_{k=i+1}^{j} U[i][k] X[k][j]) / U[i][i] (j > i)
+        for (int i = w - 1; i >= 0; --i) {
+            const double d = (double)sT[i * kTB + i];
+            if (j > i && j < w) {
+                double acc = 0.0;
+                for (int k = i + 1; k <= j; ++k) acc = fma((double)sT[i * kTB + k], sx_inv[k * kTB + j], acc);
+                sx_inv[i * kTB + j] = -acc / d;
+            } else if (j == i) {
+                sx_inv[i * kTB + j] = 1.0 / d;
             }
             __syncthreads();
-            for (int e = tid; e < w; e += blockDim.x) sy[e] = __ldcg(y + c0 + e) - (sy[e] + sp[e]);
-            __syncthreads();
-            // diagonal triangle: 32-row sub-blocks, each solved by warp 0 in registers with
-            // shuffles, then applied to the rest of the block by all threads
-            const int nsb = (w + 31) / 32;
-            for (int q = 0; q < nsb; ++q) {
-                const int sb = lower ? q * 32 : (nsb - 1 - q) * 32;
-                const int sw = min(32, w - sb);
-                if (tid < 32) {
-                    double v = (tid < sw) ? sy[sb + tid] : 0.0;
-                    if (lower) {
-                        for (int j = 0; j < sw; ++j) {
-                            const double xj = __shfl_sync(0xffffffffu, v, j);
-                            if (tid > j && tid < sw) v -= (double)sL[(sb + j) * kTS + sb + tid] * xj;
-                        }
-                    } else {
-                        for (int j = sw - 1; j >= 0; --j) {
-                            if (tid == j) v /= (double)sL[(sb + j) * kTS + sb + j];
-                            const double xj = __shfl_sync(0xffffffffu, v, j);
-                            if (tid < j) v -= (double)sL[(sb + j) * kTS + sb + tid] * xj;
-                        }
-                    }
-                    if (tid < sw) sy[sb + tid] = v;
-                }
-                __syncthreads();
-                const int lo = lower ? sb + sw : 0, hi = lower ? w : sb;
-                for (int r = lo + tid; r < hi; r += blockDim.x) {
-                    double acc = 0.0;
-                    for (int j = 0; j < sw; ++j) acc = fma((double)sL[(sb + j) * kTS + r], sy[sb + j], acc);
-                    sy[r] -= acc;
-                }
-                __syncthreads();
-            }
-            for (int e = tid; e < w; e += blockDim.x) __stcg(y + c0 + e, sy[e]);
-            __syncthreads();
-            if (s + 1 < nblk) {          // next step's tiles, in flight during the barrier
-                int n0, nw_;
-                blk(s + 1, n0, nw_);
-                prefetch_tile(sL, LU, ld, n0, nw_, n0, nw_);
-                prefetch_tile(sB, LU, ld, n0, nw_, c0, w);
-            }
-        } else if (s > 0) {
-            const int lo = lower ? c1 : 0, hi = lower ? n : c0;
-            for (int r = lo + (blockIdx.x - 1) * blockDim.x + tid; r < hi; r += (G - 1) * blockDim.x) {
-                const double acc = dot_col_block(LU, ld, pc0, pw, r, sx);
-                __stcg(y + r, __ldcg(y + r) - acc);
-            }
         }
-        grid_sync(gb, epoch + s);
-        pc0 = c0;
-        pw = w;
+    }
+    const int nblk = (n + kTB - 1) / kTB;
+    double *out = Tinv + ((size_t)upper * nblk + b) * kTinvBlock;
+    for (int c = 0; c < kTB; ++c) out[(size_t)c * kTB + j] = sx_inv[j * kTB + c];   // [col][row]
+}
+
+__device__ __forceinline__ void cp_async16(void *dst, const void *src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// y <- T^-1 y in place (T = L unit lower if lower, else U), y FP64 of length n.  LU: ld % 4
+// == 0, 16-byte aligned.  flags[p] = epoch once block p's solution is in y.  Cooperative launch
+// (all CTAs co-resident: CTA g owns blocks p = g, g + G, ...).
+__global__ void __launch_bounds__(kTrsvThreads) trsv_kernel(const float *LU, int ld, int n, double *y, int lower,
+                                                            const double *Tinv, unsigned int *flags,
+                                                            unsigned int epoch) {
+    extern __shared__ double sm_tr[];
+    double *sTi = sm_tr;                                           // [col][row] inverse of T_bb
+    float *sC = reinterpret_cast<float *>(sTi + kTinvBlock);        // [2][kTChunk][kTB] tile chunks
+    double *sx = reinterpret_cast<double *>(sC + 2 * kTChunk * kTB);   // [kTB] x of the current dependency
+    double *sacc = sx + kTB;                                       // [2][kTB] half sums
+    double *sy = sacc + 2 * kTB;                                   // [kTB] y_b - sum
+    const int nblk = (n + kTB - 1) / kTB;
+    const int tid = threadIdx.x, r = tid & (kTB - 1), h = tid >> 7;
+    const int nchk = kTB / kTChunk;
+    for (int p = blockIdx.x; p < nblk; p += gridDim.x) {
+        const int b = lower ? p : nblk - 1 - p;
+        const int r0 = b * kTB, w = min(n, r0 + kTB) - r0;
+        const int wg = (w + 3) >> 2;                               // 16-byte row groups to copy
+        // this block's inverse (consumed last; lands while the dependencies stream)
+        const double *ti = Tinv + ((size_t)(lower ? 0 : 1) * nblk + b) * kTinvBlock;
+        for (int e = tid; e < (int)(kTinvBlock / 2); e += kTrsvThreads) cp_async16(sTi + 2 * e, ti + 2 * e);
+        cp_async_commit();
+        auto issue = [&](int s) {        // chunk s of the dependency stream into buffer s & 1
+            const int pd = s / nchk, q = s % nchk;
+            const int bd = lower ? pd : nblk - 1 - pd;
+            const int cc0 = bd * kTB + q * kTChunk;
+            const int ncol = max(0, min(kTChunk, min(n, bd * kTB + kTB) - cc0));
+            float *dst = sC + (s & 1) * kTChunk * kTB;
+            for (int e = tid; e < ncol * wg; e += kTrsvThreads) {
+                const int c = e / wg, g = e % wg;
+                cp_async16(dst + c * kTB + 4 * g, LU + (int64_t)(cc0 + c) * ld + r0 + 4 * g);
+            }
+            cp_async_commit();
+        };
+        double acc = 0.0;
+        const int nsteps = p * nchk;
+        if (nsteps > 0) issue(0);
+        for (int s = 0; s < nsteps; ++s) {
+            const int pd = s / nchk, q = s % nchk;
+            if (s + 1 < nsteps) {
+                issue(s + 1);
+                cp_async_wait<1>();
+            } else {
+                cp_async_wait<0>();
+            }
+            if (q == 0) {                 // dependency pd's solution: wait for its flag
+                if (tid == 0) {
+                    while (ld_acquire(flags + pd) < epoch) {}
+                    __threadfence();
+                }
+                __syncthreads();
+                const int bd = lower ? pd : nblk - 1 - pd;
+                const int wd = min(n, bd * kTB + kTB) - bd * kTB;
+                if (tid < kTB) sx[tid] = (tid < wd) ? __ldcg(y + bd * kTB + tid) : 0.0;
+            }
+            __syncthreads();
+            const int bd = lower ? pd : nblk - 1 - pd;
+            const int ncol = max(0, min(kTChunk, min(n, bd * kTB + kTB) - (bd * kTB + q * kTChunk)));
+            const float *cb = sC + (s & 1) * kTChunk * kTB;
+            const int ca = h * (kTChunk / 2), ce = min(ncol, ca + kTChunk / 2);
+#pragma unroll 8
+            for (int c = ca; c < ce; ++c) acc = fma((double)cb[c * kTB + r], sx[q * kTChunk + c], acc);
+            __syncthreads();              // buffer s & 1 is refilled by issue(s + 2)
+        }
+        if (nsteps == 0) cp_async_wait<0>();
+        sacc[h * kTB + r] = acc;
+        __syncthreads();
+        if (tid < kTB) sy[tid] = (tid < w) ? y[r0 + tid] - (sacc[tid] + sacc[kTB + tid]) : 0.0;
+        __syncthreads();
+        // x_b = inv(T_bb) y_b : two threads per row, half of the columns each
+        double xv = 0.0;
+        const int ka = h * (kTB / 2);
+#pragma unroll 8
+        for (int k = ka; k < ka + kTB / 2; ++k) xv = fma(sTi[(size_t)k * kTB + r], sy[k], xv);
+        sacc[h * kTB + r] = xv;
+        __syncthreads();
+        if (tid < w) __stcg(y + r0 + tid, sacc[tid] + sacc[kTB + tid]);
+        __syncthreads();
+        if (tid == 0) {
+            __threadfence();
+            st_release(flags + p, epoch);
+        }
     }
 }
 
@@ -595,10 +619,92 @@ __global__ void copy_matrix_kernel(int n, const float *A, int lda, float *B, int
 }
 
 // ------------------------------------------------------------------------------------
+// N1: GMRES-IR kernels.  The Krylov basis V (n x (m+1) FP64, ld n) is
+// small (m <= a few hundred) and L2-resident; the dominant costs per Arnoldi step are the
+// FP32-A matvec (HBM) and the two triangular solves.
+// ------------------------------------------------------------------------------------
+constexpr int kArnThreads = 256;
+
+// One Arnoldi step, classical Gram-Schmidt applied twice (CGS2), on a cooperative grid.
+// Column j+1 of V holds w = M^-1 A v_j on entry; on exit it holds v_{j+1} = w' / ||w'||
+// (w' = w orthogonalised against v_0..v_j) and hcol[0..j+1] holds Hessenberg column j
+// (h_ij = sum of both passes' projections, h_{j+1,j} = ||w'||_2).  j = -1 normalises column 0
+// (hcol[0] = its norm).  Rows are split in contiguous chunks over the CTAs; each reduction
+// goes through per-CTA partials that every CTA sums in the same order (deterministic).
+//   part : [3][gridDim.x][pstride] FP64 scratch, pstride >= j + 2
+__global__ void __launch_bounds__(kArnThreads) arnoldi_kernel(double *V, int n, int j, double *part, int pstride,
+                                                              double *hcol, GridBar gb, unsigned int epoch) {
+    extern __shared__ double sh[];                 // [pstride] projections of the current pass
+    __shared__ double sred[kArnThreads / 32];
+    const int G = gridDim.x, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = kArnThreads / 32;
+    const int chunk = (n + G - 1) / G;
+    const int r0 = min(n, blockIdx.x * chunk), r1 = min(n, r0 + chunk);
+    double *w = V + (int64_t)(j + 1) * n;
+    for (int pass = 0; pass < 2 && j >= 0; ++pass) {
+        double *pp = part + (size_t)pass * G * pstride;
+        for (int c = wid; c <= j; c += nw) {       // partial dots over this CTA's rows
+            const double *vc = V + (int64_t)c * n;
+            double acc = 0.0;
+            for (int r = r0 + lane; r < r1; r += 32) acc = fma(vc[r], w[r], acc);
+            for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+            if (lane == 0) pp[(size_t)blockIdx.x * pstride + c] = acc;
+        }
+        grid_sync(gb, epoch++);
+        for (int c = tid; c <= j; c += kArnThreads) {
+            double h = 0.0;
+            for (int g = 0; g < G; ++g) h += __ldcg(pp + (size_t)g * pstride + c);
+            sh[c] = h;
+            if (blockIdx.x == 0) hcol[c] = pass ? hcol[c] + h : h;
+        }
+        __syncthreads();
+        for (int r = r0 + tid; r < r1; r += kArnThreads) {   // w -= V h on this CTA's rows
+            double acc = 0.0;
+#pragma unroll 8
+            for (int c = 0; c <= j; ++c) acc = fma(V[(int64_t)c * n + r], sh[c], acc);
+            w[r] -= acc;
+        }
+        __syncthreads();
+    }
+    double *pn = part + (size_t)2 * G * pstride;
+    double ss = 0.0;
+    for (int r = r0 + tid; r < r1; r += kArnThreads) ss = fma(w[r], w[r], ss);
+    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    if (lane == 0) sred[wid] = ss;
+    __syncthreads();
+    if (tid == 0) {
+        double t = 0.0;
+        for (int q = 0; q < nw; ++q) t += sred[q];
+        pn[blockIdx.x] = t;
+    }
+    grid_sync(gb, epoch++);
+    if (tid == 0) {
+        double t = 0.0;
+        for (int g = 0; g < G; ++g) t += __ldcg(pn + g);
+        sred[0] = sqrt(t);
+        if (blockIdx.x == 0) hcol[j + 1] = sred[0];
+    }
+    __syncthreads();
+    const double nrm = sred[0];
+    if (nrm > 0.0)
+        for (int r = r0 + tid; r < r1; r += kArnThreads) w[r] = w[r] / nrm;
+}
+
+// x += V[:, 0:jm] y  (y: jm FP64 on the device)
+__global__ void krylov_update_kernel(int n, int jm, const double *V, const double *y, double *x) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double acc = 0.0;
+    for (int c = 0; c < jm; ++c) acc = fma(V[(int64_t)c * n + i], y[c], acc);
+    x[i] += acc;
+}
+
+// ------------------------------------------------------------------------------------
 // host driver
 // ------------------------------------------------------------------------------------
 struct LuWork {
     float *LU = nullptr;
+    int ld = 0;
+    bool own_LU = true, own_ipiv = true;
     int *ipiv = nullptr, *piv_rows = nullptr, *pos = nullptr, *row_at = nullptr, *info = nullptr;
     int *perm = nullptr, *npairs = nullptr;
     int2 *pairs = nullptr;
@@ -606,7 +712,15 @@ struct LuWork {
     GridBar gb;
     unsigned int epoch = 1;
     double *r = nullptr, *d = nullptr, *part = nullptr, *scal = nullptr;
+    double *tinv = nullptr;       // FP64 inverses of the diagonal blocks (solves only)
+    unsigned int *tflags = nullptr, tepoch = 0;
+    int n = 0, nb = 0, cl = 16, rl_max = 0, coop_grid = 0;
+    std::vector<void *> extra;    // further device buffers owned by the solve
 };
+
+static size_t sub_smem(int rl) {
+    return (size_t)kSubW * rl * sizeof(float) + (size_t)3 * kSubW * sizeof(float) + 16 + (size_t)rl + 16;
+}
 
 static int coop_launch(const void *fn, int grid, int threads, void **args, size_t smem, cudaStream_t st) {
     cudaError_t e = cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(threads), args, smem, st);
@@ -618,128 +732,97 @@ static int coop_launch(const void *fn, int grid, int threads, void **args, size_
     return BF16X_SUCCESS;
 }
 
-static int solve_with_factors(LuWork &w, int n, const double *v, double *out, int coop_grid, cudaStream_t st) {
-    // out = U^-1 L^-1 P v
-    gather_kernel<<<(n + 255) / 256, 256, 0, st>>>(n, w.perm, v, out);
-    count_launch();
-    int ld = n, lower = 1;
-    const float *LU = w.LU;
-    double *y = out;
-    GridBar gb = w.gb;
-    unsigned int ep = w.epoch;
-    void *args[] = {(void *)&LU, (void *)&ld, (void *)&n, (void *)&y, (void *)&lower, (void *)&gb, (void *)&ep};
-    const int nblk = (n + kTrsvBlock - 1) / kTrsvBlock;
-    int rc = coop_launch((const void *)trsv_kernel, coop_grid, 256, args, kTrsvSmem, st);
-    w.epoch += nblk;
-    if (rc) return rc;
-    lower = 0;
-    ep = w.epoch;
-    rc = coop_launch((const void *)trsv_kernel, coop_grid, 256, args, kTrsvSmem, st);
-    w.epoch += nblk;
-    return rc;
+static void lu_free(LuWork &w) {
+    if (w.own_LU) cudaFree(w.LU);
+    if (w.own_ipiv) cudaFree(w.ipiv);
+    cudaFree(w.perm); cudaFree(w.piv_rows); cudaFree(w.pos);
+    cudaFree(w.row_at); cudaFree(w.info); cudaFree(w.npairs); cudaFree(w.pairs);
+    cudaFree(w.bar); cudaFree(w.r); cudaFree(w.d); cudaFree(w.part); cudaFree(w.scal);
+    cudaFree(w.tinv); cudaFree(w.tflags);
+    for (void *p : w.extra) cudaFree(p);
+    w = LuWork{};
 }
 
-static void residual(const float *A, int lda, int n, const double *x, const double *b, double *r, double *part,
-                     int absval, cudaStream_t st) {
-    const int nchunk = (n + kResChunk - 1) / kResChunk;
-    dim3 grid((n + kResRows - 1) / kResRows, nchunk);
-    residual_partial_kernel<<<grid, kResRows, 0, st>>>(A, lda, n, x, part, absval);
-    residual_final_kernel<<<(n + 255) / 256, 256, 0, st>>>(n, nchunk, part, b, r);
-    count_launch(2);
+static int dev_alloc(void **p, size_t bytes) {
+    if (cudaMalloc(p, bytes) != cudaSuccess) {
+        cudaGetLastError();
+        *p = nullptr;
+        return BF16X_ERR_ALLOC;
+    }
+    return BF16X_SUCCESS;
 }
 
-}  // namespace bf16x
-
-using namespace bf16x;
-
-extern "C" int bf16x_gesv_ir(int n, const float *A, int lda, const double *b, double *x, int variant, int nb,
-                             int max_iter, double *residual_history, bf16x_ir_report *report) {
-    if (n < 0) return -1;
-    if (lda < (n > 1 ? n : 1)) return -3;
-    if (variant != 3 && variant != 6 && variant != 9) return -6;
-    if (!report) return -10;
-    *report = bf16x_ir_report{0, 0, 0, 0.0, 0.0, 0.0, 0.0, 0.0};
-    int rc = arch_ok();
-    if (rc) return rc;
-    if (n == 0) {
-        report->converged = 1;
-        return BF16X_SUCCESS;
-    }
-    if (nb <= 0) nb = 256;
-    nb = std::min(nb, n);
-    if (max_iter <= 0) max_iter = 30;
-    cudaStream_t st = current_stream();
-    const int coop_grid = num_sms();
-    // sub-panel rows per cluster CTA in shared memory: cluster of 8 (portable) or 16
-    int cl = 16;                           // non-portable cluster size (falls back to 8)
-    int rl_max = (n + cl - 1) / cl + 1;
-    auto sub_smem = [&](int rl) {
-        return (size_t)kSubW * rl * sizeof(float) + (size_t)3 * kSubW * sizeof(float) + 16 + (size_t)rl + 16;
-    };
-    if (sub_smem(rl_max) > 200 * 1024) {
-        cl = 16;
-        rl_max = (n + cl - 1) / cl + 1;
-    }
-    if (sub_smem(rl_max) > 200 * 1024 || (size_t)n * sizeof(int) > 200 * 1024) {
-        set_error_msg("gesv_ir: n too large for the shared-memory sub-panel (n <= ~51000)");
+// Configure and allocate the factorisation state for order n.  LU/ipiv: caller buffers
+// (factor in place) or nullptr (allocated here, ld = n rounded up to 4 floats for the
+// 16-byte tile copies of the solves).  solves: also allocate the triangular-solve state.
+static int lu_prepare(LuWork &w, int n, int nb, float *LU, int ld, int *ipiv, bool solves, cudaStream_t st) {
+    w.n = n;
+    w.nb = std::min(nb <= 0 ? 256 : nb, n);
+    w.coop_grid = num_sms();
+    w.cl = 16;                                   // non-portable cluster size (falls back to 8)
+    w.rl_max = (n + w.cl - 1) / w.cl + 1;
+    if (sub_smem(w.rl_max) > 200 * 1024 || (size_t)n * sizeof(int) > 200 * 1024) {
+        set_error_msg("LU: n too large for the shared-memory sub-panel (n <= ~51000)");
         return -1;
     }
-    {
-        static bool attr = false;
-        if (!attr) {
-            cudaFuncSetAttribute(subpanel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024 + 1024);
-            cudaFuncSetAttribute(subpanel_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-            cudaFuncSetAttribute(build_perm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024 + 1024);
-            cudaFuncSetAttribute(trsm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024 + 1024);
-            cudaFuncSetAttribute(panel_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024 + 1024);
-            cudaFuncSetAttribute(trsv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTrsvSmem);
-            attr = true;
-        }
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(subpanel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024 + 1024);
+        cudaFuncSetAttribute(subpanel_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        cudaFuncSetAttribute(build_perm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024 + 1024);
+        cudaFuncSetAttribute(trsm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024 + 1024);
+        cudaFuncSetAttribute(panel_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024 + 1024);
+        cudaFuncSetAttribute(trsv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTrsvSmem);
+        cudaFuncSetAttribute(diag_inverse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)(kTinvBlock * sizeof(double) + kTinvBlock * sizeof(float)));
+        attr = true;
     }
-    LuWork w;
-    const int nchunk = (n + kResChunk - 1) / kResChunk;
+    int rc = BF16X_SUCCESS;
     auto alloc = [&](void **p, size_t bytes) {
-        if (rc) return;
-        if (cudaMalloc(p, bytes) != cudaSuccess) {
-            cudaGetLastError();
-            rc = BF16X_ERR_ALLOC;
-        }
+        if (!rc) rc = dev_alloc(p, bytes);
     };
-    alloc((void **)&w.LU, sizeof(float) * (size_t)n * n);
-    alloc((void **)&w.ipiv, sizeof(int) * n);
+    w.own_LU = (LU == nullptr);
+    w.own_ipiv = (ipiv == nullptr);
+    if (LU) {
+        w.LU = LU;
+        w.ld = ld;
+    } else {
+        w.ld = (n + 3) & ~3;
+        alloc((void **)&w.LU, sizeof(float) * (size_t)w.ld * n);
+    }
+    if (ipiv) w.ipiv = ipiv; else alloc((void **)&w.ipiv, sizeof(int) * n);
+    const int nchunk = (n + kResChunk - 1) / kResChunk;
     alloc((void **)&w.perm, sizeof(int) * n);
     alloc((void **)&w.piv_rows, sizeof(int) * (size_t)kSubW);
     alloc((void **)&w.pos, sizeof(int) * n);
     alloc((void **)&w.row_at, sizeof(int) * n);
     alloc((void **)&w.info, sizeof(int));
     alloc((void **)&w.npairs, sizeof(int));
-    alloc((void **)&w.pairs, sizeof(int2) * 2 * (size_t)nb);
-    alloc((void **)&w.bar, sizeof(unsigned int) * ((size_t)coop_grid + 1));
+    alloc((void **)&w.pairs, sizeof(int2) * 2 * (size_t)w.nb);
+    alloc((void **)&w.bar, sizeof(unsigned int) * ((size_t)w.coop_grid + 1));
     alloc((void **)&w.r, sizeof(double) * n);
     alloc((void **)&w.d, sizeof(double) * n);
     alloc((void **)&w.part, sizeof(double) * (size_t)n * nchunk);
     alloc((void **)&w.scal, sizeof(double) * 4);
-    auto cleanup = [&]() {
-        cudaFree(w.LU); cudaFree(w.ipiv); cudaFree(w.perm); cudaFree(w.piv_rows); cudaFree(w.pos);
-        cudaFree(w.row_at); cudaFree(w.info); cudaFree(w.npairs); cudaFree(w.pairs);
-        cudaFree(w.bar); cudaFree(w.r); cudaFree(w.d); cudaFree(w.part); cudaFree(w.scal);
-    };
-    if (rc) {
-        cleanup();
-        return rc;
+    const int nblk = (n + kTB - 1) / kTB;
+    if (solves) {
+        alloc((void **)&w.tinv, sizeof(double) * 2 * kTinvBlock * nblk);
+        alloc((void **)&w.tflags, sizeof(unsigned int) * nblk);
     }
+    if (rc) return rc;
+    if (solves) cudaMemsetAsync(w.tflags, 0, sizeof(unsigned int) * nblk, st);
     w.gb.arrive = w.bar;
-    w.gb.release = w.bar + coop_grid;
-    cudaMemsetAsync(w.bar, 0, sizeof(unsigned int) * ((size_t)coop_grid + 1), st);
+    w.gb.release = w.bar + w.coop_grid;
+    cudaMemsetAsync(w.bar, 0, sizeof(unsigned int) * ((size_t)w.coop_grid + 1), st);
     cudaMemsetAsync(w.info, 0, sizeof(int), st);
-    cudaEvent_t e0, e1, e2;
-    cudaEventCreate(&e0); cudaEventCreate(&e1); cudaEventCreate(&e2);
-    cudaEventRecord(e0, st);
+    return BF16X_SUCCESS;
+}
 
-    // ---------------- factorisation ----------------
-    copy_matrix_kernel<<<num_sms() * 8, 256, 0, st>>>(n, A, lda, w.LU, n);
-    count_launch();
-    const int ld = n;
+// Factor w.LU (order w.n, ld w.ld) in place: P A = L U, ipiv 0-based, perm for the solves.
+// Enqueued on st; the zero-pivot column lands in w.info (device).
+static int lu_factor(LuWork &w, int variant, cudaStream_t st) {
+    const int n = w.n, nb = w.nb, ld = w.ld;
+    int rc = BF16X_SUCCESS;
     auto laswp = [&](int c0, int c1, int pair_cap) {
         if (c1 <= c0) return;
         laswp_kernel<<<(c1 - c0 + 7) / 8, 256, 8 * (size_t)pair_cap * sizeof(float), st>>>(w.LU, ld, c0, c1, w.pairs,
@@ -752,27 +835,27 @@ extern "C" int bf16x_gesv_ir(int n, const float *A, int lda, const double *b, do
             const int sw = std::min(kSubW, j0 + jb - s0);
             // (1) sub-panel factorisation on one cluster
             cudaLaunchConfig_t cfg = {};
-            cfg.gridDim = dim3(cl);
+            cfg.gridDim = dim3(w.cl);
             cfg.blockDim = dim3(kSubThreads);
-            cfg.dynamicSmemBytes = sub_smem(rl_max);
+            cfg.dynamicSmemBytes = sub_smem(w.rl_max);
             cfg.stream = st;
             cudaLaunchAttribute at[1];
             at[0].id = cudaLaunchAttributeClusterDimension;
-            at[0].val.clusterDim.x = cl;
+            at[0].val.clusterDim.x = w.cl;
             at[0].val.clusterDim.y = 1;
             at[0].val.clusterDim.z = 1;
             cfg.attrs = at;
             cfg.numAttrs = 1;
-            cudaError_t e = cudaLaunchKernelEx(&cfg, subpanel_kernel, w.LU, ld, n, s0, sw, rl_max, w.piv_rows, w.info);
-            if (e != cudaSuccess && cl == 16) {    // 16-CTA clusters unavailable: use 8
+            cudaError_t e = cudaLaunchKernelEx(&cfg, subpanel_kernel, w.LU, ld, n, s0, sw, w.rl_max, w.piv_rows, w.info);
+            if (e != cudaSuccess && w.cl == 16) {    // 16-CTA clusters unavailable: use 8
                 cudaGetLastError();
-                cl = 8;
-                rl_max = (n + cl - 1) / cl + 1;
-                if (sub_smem(rl_max) <= 200 * 1024) {
-                    cfg.gridDim = dim3(cl);
-                    at[0].val.clusterDim.x = cl;
-                    cfg.dynamicSmemBytes = sub_smem(rl_max);
-                    e = cudaLaunchKernelEx(&cfg, subpanel_kernel, w.LU, ld, n, s0, sw, rl_max, w.piv_rows, w.info);
+                w.cl = 8;
+                w.rl_max = (n + w.cl - 1) / w.cl + 1;
+                if (sub_smem(w.rl_max) <= 200 * 1024) {
+                    cfg.gridDim = dim3(w.cl);
+                    at[0].val.clusterDim.x = w.cl;
+                    cfg.dynamicSmemBytes = sub_smem(w.rl_max);
+                    e = cudaLaunchKernelEx(&cfg, subpanel_kernel, w.LU, ld, n, s0, sw, w.rl_max, w.piv_rows, w.info);
                 }
             }
             if (e != cudaSuccess) {
@@ -817,44 +900,153 @@ extern "C" int bf16x_gesv_ir(int n, const float *A, int lda, const double *b, do
     if (rc == BF16X_SUCCESS) {
         build_perm_kernel<<<1, 1024, (size_t)n * sizeof(int), st>>>(n, w.ipiv, w.perm);
         count_launch();
+        if (w.tinv) {
+            diag_inverse_kernel<<<dim3((n + kTB - 1) / kTB, 2), kTB, kTinvBlock * (sizeof(double) + sizeof(float)),
+                                  st>>>(w.LU, ld, n, w.tinv);
+            count_launch();
+        }
         rc = check_launch("lu");
     }
+    return rc;
+}
+
+// Wait for the factorisation; *info = first zero-pivot column (1-based) or 0.
+static int lu_sync_info(LuWork &w, cudaStream_t st, int *info) {
+    *info = 0;
+    cudaMemcpyAsync(info, w.info, sizeof(int), cudaMemcpyDeviceToHost, st);
+    if (cudaStreamSynchronize(st) != cudaSuccess) return check_launch("lu sync");
+    return *info ? BF16X_ERR_SINGULAR : BF16X_SUCCESS;
+}
+
+static int solve_with_factors(LuWork &w, int n, const double *v, double *out, int coop_grid, cudaStream_t st) {
+    // out = U^-1 L^-1 P v
+    gather_kernel<<<(n + 255) / 256, 256, 0, st>>>(n, w.perm, v, out);
+    count_launch();
+    int ld = w.ld, lower = 1;
+    const float *LU = w.LU;
+    const double *ti = w.tinv;
+    unsigned int *fl = w.tflags;
+    double *y = out;
+    unsigned int ep = ++w.tepoch;
+    void *args[] = {(void *)&LU, (void *)&ld, (void *)&n, (void *)&y, (void *)&lower, (void *)&ti, (void *)&fl,
+                    (void *)&ep};
+    const int grid = std::min((n + kTB - 1) / kTB, coop_grid);
+    int rc = coop_launch((const void *)trsv_kernel, grid, kTrsvThreads, args, kTrsvSmem, st);
+    if (rc) return rc;
+    lower = 0;
+    ep = ++w.tepoch;
+    return coop_launch((const void *)trsv_kernel, grid, kTrsvThreads, args, kTrsvSmem, st);
+}
+
+// r = b - A x (b != nullptr), r = A x (b == nullptr), or row abs sums (absval).
+static void residual(const float *A, int lda, int n, const double *x, const double *b, double *r, double *part,
+                     int absval, cudaStream_t st) {
+    const int nchunk = (n + kResChunk - 1) / kResChunk;
+    dim3 grid((n + kResRows - 1) / kResRows, nchunk);
+    residual_partial_kernel<<<grid, kResRows, 0, st>>>(A, lda, n, x, part, absval);
+    residual_final_kernel<<<(n + 255) / 256, 256, 0, st>>>(n, nchunk, part, b, r);
+    count_launch(2);
+}
+
+static double inf_norm_A(LuWork &w, const float *A, int lda, int n, cudaStream_t st) {
+    residual(A, lda, n, nullptr, nullptr, w.r, w.part, 1, st);
+    absmax_kernel<<<1, 256, 0, st>>>(n, w.r, w.scal + 2);
+    count_launch();
+    double anrm = 0.0;
+    cudaMemcpyAsync(&anrm, w.scal + 2, sizeof(double), cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    return anrm;
+}
+
+// ||b - A x||_inf and ||x||_inf (synchronises).
+static int residual_norms(LuWork &w, const float *A, int lda, int n, const double *x, const double *b,
+                          cudaStream_t st, double *rn, double *xn) {
+    residual(A, lda, n, x, b, w.r, w.part, 0, st);
+    absmax_kernel<<<1, 256, 0, st>>>(n, w.r, w.scal);
+    absmax_kernel<<<1, 256, 0, st>>>(n, x, w.scal + 1);
+    count_launch(2);
+    double h[2];
+    cudaMemcpyAsync(h, w.scal, 2 * sizeof(double), cudaMemcpyDeviceToHost, st);
+    if (cudaStreamSynchronize(st) != cudaSuccess) return check_launch("ir sync");
+    *rn = h[0];
+    *xn = h[1];
+    return BF16X_SUCCESS;
+}
+
+static int check_common(int n, int lda, int variant) {
+    if (n < 0) return -1;
+    if (lda < (n > 1 ? n : 1)) return -3;
+    if (variant != 3 && variant != 6 && variant != 9) return -6;
+    return BF16X_SUCCESS;
+}
+
+}  // namespace bf16x
+
+using namespace bf16x;
+
+extern "C" int bf16x_getrf(int n, float *A, int lda, int *ipiv, int variant, int nb, int *info) {
+    if (n < 0) return -1;
+    if (n > 0 && !A) return -2;
+    if (lda < (n > 1 ? n : 1)) return -3;
+    if (n > 0 && !ipiv) return -4;
+    if (variant != 1 && variant != 3 && variant != 6 && variant != 8 && variant != 9) return -5;
+    if (info) *info = 0;
+    int rc = arch_ok();
+    if (rc || n == 0) return rc;
+    cudaStream_t st = current_stream();
+    LuWork w;
+    rc = lu_prepare(w, n, nb, A, lda, ipiv, false, st);
+    if (!rc) rc = lu_factor(w, variant, st);
+    int inf = 0;
+    if (!rc) rc = lu_sync_info(w, st, &inf);
+    if (info) *info = inf;
+    lu_free(w);
+    return rc;
+}
+
+extern "C" int bf16x_gesv_ir(int n, const float *A, int lda, const double *b, double *x, int variant, int nb,
+                             int max_iter, double *residual_history, bf16x_ir_report *report) {
+    if (!report) return -10;
+    *report = bf16x_ir_report{};
+    int rc = check_common(n, lda, variant);
+    if (rc) return rc;
+    rc = arch_ok();
+    if (rc) return rc;
+    if (n == 0) {
+        report->converged = 1;
+        return BF16X_SUCCESS;
+    }
+    if (max_iter <= 0) max_iter = 30;
+    cudaStream_t st = current_stream();
+    LuWork w;
+    rc = lu_prepare(w, n, nb, nullptr, 0, nullptr, true, st);
+    if (rc) {
+        lu_free(w);
+        return rc;
+    }
+    cudaEvent_t e0, e1, e2;
+    cudaEventCreate(&e0); cudaEventCreate(&e1); cudaEventCreate(&e2);
+    cudaEventRecord(e0, st);
+    copy_matrix_kernel<<<num_sms() * 8, 256, 0, st>>>(n, A, lda, w.LU, w.ld);
+    count_launch();
+    rc = lu_factor(w, variant, st);
     cudaEventRecord(e1, st);
     int info = 0;
-    if (rc == BF16X_SUCCESS) {
-        cudaMemcpyAsync(&info, w.info, sizeof(int), cudaMemcpyDeviceToHost, st);
-        if (cudaStreamSynchronize(st) != cudaSuccess) rc = check_launch("lu sync");
-    }
+    if (rc == BF16X_SUCCESS) rc = lu_sync_info(w, st, &info);
     report->info = info;
-    if (rc == BF16X_SUCCESS && info != 0) rc = BF16X_ERR_SINGULAR;
 
-    // ---------------- refinement ----------------
+    // ---------------- refinement (P:406) ----------------
     if (rc == BF16X_SUCCESS) {
-        // ||A||_inf (row abs sums)
-        residual(A, lda, n, nullptr, nullptr, w.r, w.part, 1, st);
-        absmax_kernel<<<1, 256, 0, st>>>(n, w.r, w.scal + 2);
-        count_launch();
-        double anrm = 0.0;
-        cudaMemcpyAsync(&anrm, w.scal + 2, sizeof(double), cudaMemcpyDeviceToHost, st);
-        rc = solve_with_factors(w, n, b, x, coop_grid, st);
+        const double anrm = inf_norm_A(w, A, lda, n, st);
+        rc = solve_with_factors(w, n, b, x, w.coop_grid, st);
         const double eps = std::ldexp(1.0, -53);
         std::vector<double> hist;
         int it = 0;
         bool converged = false;
         double rn = 0.0, xn = 0.0;
         for (; rc == BF16X_SUCCESS; ++it) {
-            residual(A, lda, n, x, b, w.r, w.part, 0, st);
-            absmax_kernel<<<1, 256, 0, st>>>(n, w.r, w.scal);
-            absmax_kernel<<<1, 256, 0, st>>>(n, x, w.scal + 1);
-            count_launch(2);
-            double h[2];
-            cudaMemcpyAsync(h, w.scal, 2 * sizeof(double), cudaMemcpyDeviceToHost, st);
-            if (cudaStreamSynchronize(st) != cudaSuccess) {
-                rc = check_launch("ir sync");
-                break;
-            }
-            rn = h[0];
-            xn = h[1];
+            rc = residual_norms(w, A, lda, n, x, b, st, &rn, &xn);
+            if (rc) break;
             hist.push_back(rn);
             report->tol = std::sqrt((double)n) * xn * anrm * eps;
             if (rn <= report->tol) {
@@ -863,7 +1055,7 @@ extern "C" int bf16x_gesv_ir(int n, const float *A, int lda, const double *b, do
             }
             if (it >= max_iter) break;
             if (hist.size() >= 4 && hist.back() > 0.5 * hist[hist.size() - 4]) break;  // stagnation
-            rc = solve_with_factors(w, n, w.r, w.d, coop_grid, st);
+            rc = solve_with_factors(w, n, w.r, w.d, w.coop_grid, st);
             if (rc) break;
             axpy_kernel<<<(n + 255) / 256, 256, 0, st>>>(n, x, w.d);
             count_launch();
@@ -884,6 +1076,164 @@ extern "C" int bf16x_gesv_ir(int n, const float *A, int lda, const double *b, do
     report->factor_ms = f_ms;
     report->refine_ms = r_ms;
     cudaEventDestroy(e0); cudaEventDestroy(e1); cudaEventDestroy(e2);
-    cleanup();
+    lu_free(w);
+    return rc;
+}
+
+extern "C" int bf16x_gesv_gmres_ir(int n, const float *A, int lda, const double *b, double *x, int variant, int nb,
+                                   int restart, double inner_tol, int max_iter, double *residual_history,
+                                   bf16x_ir_report *report) {
+    if (!report) return -12;
+    *report = bf16x_ir_report{};
+    int rc = check_common(n, lda, variant);
+    if (rc) return rc;
+    if (inner_tol < 0.0 || inner_tol != inner_tol) return -9;
+    rc = arch_ok();
+    if (rc) return rc;
+    if (n == 0) {
+        report->converged = 1;
+        return BF16X_SUCCESS;
+    }
+    if (max_iter <= 0) max_iter = 30;
+    if (inner_tol == 0.0) inner_tol = 1e-10;
+    const int m = std::min(std::min(restart <= 0 ? 200 : restart, n), 8190);   // shared-memory projections
+    cudaStream_t st = current_stream();
+    LuWork w;
+    rc = lu_prepare(w, n, nb, nullptr, 0, nullptr, true, st);
+    double *V = nullptr, *part = nullptr, *hcol = nullptr, *ydev = nullptr, *t = nullptr;
+    const int pstride = m + 2;
+    if (!rc) rc = dev_alloc((void **)&V, sizeof(double) * (size_t)n * (m + 1));
+    if (!rc) rc = dev_alloc((void **)&part, sizeof(double) * 3 * (size_t)w.coop_grid * pstride);
+    if (!rc) rc = dev_alloc((void **)&hcol, sizeof(double) * pstride);
+    if (!rc) rc = dev_alloc((void **)&ydev, sizeof(double) * (m + 1));
+    if (!rc) rc = dev_alloc((void **)&t, sizeof(double) * n);
+    for (void *p : {(void *)V, (void *)part, (void *)hcol, (void *)ydev, (void *)t}) w.extra.push_back(p);
+    if (rc) {
+        lu_free(w);
+        return rc;
+    }
+    {
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(arnoldi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+            attr = true;
+        }
+    }
+    cudaEvent_t e0, e1, e2;
+    cudaEventCreate(&e0); cudaEventCreate(&e1); cudaEventCreate(&e2);
+    cudaEventRecord(e0, st);
+    copy_matrix_kernel<<<num_sms() * 8, 256, 0, st>>>(n, A, lda, w.LU, w.ld);
+    count_launch();
+    rc = lu_factor(w, variant, st);
+    cudaEventRecord(e1, st);
+    int info = 0;
+    if (rc == BF16X_SUCCESS) rc = lu_sync_info(w, st, &info);
+    report->info = info;
+
+    auto arnoldi = [&](int j) -> int {
+        double *Vp = V, *pp = part, *hp = hcol;
+        int nn = n, jj = j, ps = pstride;
+        GridBar gb = w.gb;
+        unsigned int ep = w.epoch;
+        void *args[] = {(void *)&Vp, (void *)&nn, (void *)&jj, (void *)&pp, (void *)&ps, (void *)&hp, (void *)&gb,
+                        (void *)&ep};
+        const int rc2 = coop_launch((const void *)arnoldi_kernel, w.coop_grid, kArnThreads, args,
+                                    (size_t)pstride * sizeof(double), st);
+        w.epoch += (j >= 0) ? 3 : 1;
+        return rc2;
+    };
+
+    // ---------------- GMRES-IR (reading R25) ----------------
+    if (rc == BF16X_SUCCESS) {
+        const double anrm = inf_norm_A(w, A, lda, n, st);
+        const double eps = std::ldexp(1.0, -53);
+        cudaMemsetAsync(x, 0, sizeof(double) * n, st);
+        std::vector<double> hist, H((size_t)(m + 1) * m), cs(m), sn(m), g(m + 1), y(m), hc(m + 2);
+        int it = 0, inner = 0;
+        bool converged = false;
+        double rn = 0.0, xn = 0.0;
+        for (; rc == BF16X_SUCCESS; ++it) {
+            rc = residual_norms(w, A, lda, n, x, b, st, &rn, &xn);
+            if (rc) break;
+            hist.push_back(rn);
+            report->tol = std::sqrt((double)n) * xn * anrm * eps;
+            if (rn <= report->tol) {
+                converged = true;
+                break;
+            }
+            if (it >= max_iter) break;
+            if (hist.size() >= 4 && hist.back() > 0.5 * hist[hist.size() - 4]) break;  // stagnation
+            // one GMRES cycle on M^-1 A d = M^-1 r, d0 = 0
+            rc = solve_with_factors(w, n, w.r, V, w.coop_grid, st);
+            if (!rc) rc = arnoldi(-1);
+            double beta = 0.0;
+            if (!rc) {
+                cudaMemcpyAsync(&beta, hcol, sizeof(double), cudaMemcpyDeviceToHost, st);
+                if (cudaStreamSynchronize(st) != cudaSuccess) rc = check_launch("gmres sync");
+            }
+            if (rc || beta == 0.0) break;
+            std::fill(g.begin(), g.end(), 0.0);
+            g[0] = beta;
+            int jm = 0;
+            for (int j = 0; j < m && !rc; ++j) {
+                // w = M^-1 A v_j into column j+1, then CGS2 + normalisation
+                residual(A, lda, n, V + (int64_t)j * n, nullptr, t, w.part, 0, st);
+                rc = solve_with_factors(w, n, t, V + (int64_t)(j + 1) * n, w.coop_grid, st);
+                if (!rc) rc = arnoldi(j);
+                if (!rc) {
+                    cudaMemcpyAsync(hc.data(), hcol, sizeof(double) * (j + 2), cudaMemcpyDeviceToHost, st);
+                    if (cudaStreamSynchronize(st) != cudaSuccess) rc = check_launch("gmres sync");
+                }
+                if (rc) break;
+                // Givens rotations on Hessenberg column j (host, FP64), as the oracle's template
+                double *Hc = H.data() + (size_t)j * (m + 1);      // column j, rows 0..j+1
+                for (int i = 0; i <= j + 1; ++i) Hc[i] = hc[i];
+                const double hnext = hc[j + 1];
+                for (int i = 0; i < j; ++i) {
+                    const double a = cs[i] * Hc[i] + sn[i] * Hc[i + 1];
+                    Hc[i + 1] = -sn[i] * Hc[i] + cs[i] * Hc[i + 1];
+                    Hc[i] = a;
+                }
+                const double dd = std::hypot(Hc[j], Hc[j + 1]);
+                cs[j] = Hc[j] / dd;
+                sn[j] = Hc[j + 1] / dd;
+                Hc[j] = dd;
+                Hc[j + 1] = 0.0;
+                g[j + 1] = -sn[j] * g[j];
+                g[j] = cs[j] * g[j];
+                ++inner;
+                jm = j + 1;
+                if (std::fabs(g[j + 1]) <= inner_tol * beta || hnext == 0.0) break;
+            }
+            if (rc) break;
+            // least squares: H(0:jm, 0:jm) y = g, then x += V y
+            for (int i = jm - 1; i >= 0; --i) {
+                double s = g[i];
+                for (int c = i + 1; c < jm; ++c) s -= H[(size_t)c * (m + 1) + i] * y[c];
+                y[i] = s / H[(size_t)i * (m + 1) + i];
+            }
+            cudaMemcpyAsync(ydev, y.data(), sizeof(double) * jm, cudaMemcpyHostToDevice, st);
+            krylov_update_kernel<<<(n + 255) / 256, 256, 0, st>>>(n, jm, V, ydev, x);
+            count_launch();
+            rc = check_launch("gmres update");
+        }
+        report->converged = converged ? 1 : 0;
+        report->iterations = it;
+        report->inner_iterations = inner;
+        report->final_residual = rn;
+        report->backward_error = (anrm > 0 && xn > 0) ? rn / (anrm * xn) : 0.0;
+        if (residual_history)
+            for (size_t q = 0; q < hist.size() && q <= (size_t)max_iter; ++q) residual_history[q] = hist[q];
+        if (rc == BF16X_SUCCESS && !converged) rc = BF16X_NOT_CONVERGED;
+    }
+    cudaEventRecord(e2, st);
+    cudaEventSynchronize(e2);
+    float f_ms = 0.f, r_ms = 0.f;
+    cudaEventElapsedTime(&f_ms, e0, e1);
+    cudaEventElapsedTime(&r_ms, e1, e2);
+    report->factor_ms = f_ms;
+    report->refine_ms = r_ms;
+    cudaEventDestroy(e0); cudaEventDestroy(e1); cudaEventDestroy(e2);
+    lu_free(w);
     return rc;
 }

@@ -68,3 +68,26 @@ def test_no_cpu_fallback_without_gpu():
     rc = L.bf16x_gemm(4, 4, 4, 1.0, None, 4, None, 4, 0.0, None, 4, 6)
     assert rc == bx.ERR_ARCH
     assert b"sm_100" in L.bf16x_status_string(rc)
+
+
+def test_solver_argument_errors():
+    L = bx.lib()
+    rep = bx.IRReport()
+    g = L.bf16x_gesv_gmres_ir
+    assert g(-1, None, 1, None, None, 3, 0, 0, 0.0, 0, None, ctypes.byref(rep)) == -1
+    assert g(4, None, 3, None, None, 3, 0, 0, 0.0, 0, None, ctypes.byref(rep)) == -3
+    assert g(4, None, 4, None, None, 7, 0, 0, 0.0, 0, None, ctypes.byref(rep)) == -6
+    assert g(4, None, 4, None, None, 3, 0, 0, -1.0, 0, None, ctypes.byref(rep)) == -9
+    assert g(4, None, 4, None, None, 3, 0, 0, 0.0, 0, None, None) == -12
+    assert L.bf16x_gesv_ir(4, None, 3, None, None, 3, 0, 0, None, ctypes.byref(rep)) == -3
+    info = ctypes.c_int(0)
+    f = L.bf16x_getrf
+    assert f(-1, None, 1, None, 3, 0, ctypes.byref(info)) == -1
+    assert f(4, None, 4, None, 3, 0, ctypes.byref(info)) == -2
+    assert f(4, 16, 3, None, 3, 0, ctypes.byref(info)) == -3
+    assert f(4, 16, 4, None, 3, 0, ctypes.byref(info)) == -4
+    assert f(4, 16, 4, 32, 4, 0, ctypes.byref(info)) == -5
+    import torch
+    if not torch.cuda.is_available():
+        assert f(4, 16, 4, 32, 3, 0, ctypes.byref(info)) == bx.ERR_ARCH
+        assert g(4, 16, 4, 32, 48, 3, 0, 0, 0.0, 0, None, ctypes.byref(rep)) == bx.ERR_ARCH

@@ -12,6 +12,7 @@ import paper_1904_06376_b200 as bx
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 8192
 variant = int(sys.argv[2]) if len(sys.argv) > 2 else 3
 kappas = [float(x) for x in (sys.argv[3].split(",") if len(sys.argv) > 3 else ["1e1", "1e2", "1e4", "1e6", "1e8", "1e10", "1e12"])]
+solvers = (sys.argv[4].split(",") if len(sys.argv) > 4 else ["ir", "gmres"])
 dev = torch.device("cuda")
 g = torch.Generator(device=dev)
 for kappa in kappas:
@@ -31,15 +32,20 @@ for kappa in kappas:
         kappa_meas = float(sv[0] / sv[-1])
     x_true = torch.randn(n, dtype=torch.float64, device=dev, generator=g)
     b = A.double() @ x_true
-    torch.cuda.synchronize()
-    t0 = time.time()
-    x, rep, hist = bx.gesv_ir(A, b, variant=variant, nb=256, max_iter=30)
-    torch.cuda.synchronize()
-    wall = time.time() - t0
-    fe = float(torch.linalg.norm(x - x_true) / torch.linalg.norm(x_true))
-    print(json.dumps({"n": n, "variant": variant, "kappa_target": kappa, "kappa_measured": kappa_meas,
-                      "converged": bool(rep.converged), "iterations": rep.iterations, "info": rep.info,
-                      "forward_error": fe, "backward_error": rep.backward_error,
-                      "final_residual_inf": rep.final_residual, "tol": rep.tol,
-                      "factor_ms": rep.factor_ms, "refine_ms": rep.refine_ms, "wall_s": wall,
-                      "history": [float(h) for h in hist]}), flush=True)
+    for solver in solvers:
+        torch.cuda.synchronize()
+        t0 = time.time()
+        if solver == "gmres":
+            x, rep, hist = bx.gesv_gmres_ir(A, b, variant=variant, nb=256, restart=200, max_iter=30)
+        else:
+            x, rep, hist = bx.gesv_ir(A, b, variant=variant, nb=256, max_iter=30)
+        torch.cuda.synchronize()
+        wall = time.time() - t0
+        fe = float(torch.linalg.norm(x - x_true) / torch.linalg.norm(x_true))
+        print(json.dumps({"n": n, "solver": solver, "variant": variant, "kappa_target": kappa,
+                          "kappa_measured": kappa_meas, "converged": bool(rep.converged),
+                          "iterations": rep.iterations, "inner_iterations": rep.inner_iterations, "info": rep.info,
+                          "forward_error": fe, "backward_error": rep.backward_error,
+                          "final_residual_inf": rep.final_residual, "tol": rep.tol,
+                          "factor_ms": rep.factor_ms, "refine_ms": rep.refine_ms, "wall_s": wall,
+                          "history": [float(h) for h in hist]}), flush=True)
