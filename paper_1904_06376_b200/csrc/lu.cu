@@ -93,118 +93,243 @@ __device__ __forceinline__ void async_wait_all() {
 // ------------------------------------------------------------------------------------
 // K4: panel factorisation by sub-panels of kSubW columns.  Each sub-panel [s0, s0+w) is
 // factored over rows [s0, n) by one thread-block cluster: the rows are split in contiguous
-// chunks over the cluster's CTAs and held in shared memory ([col][row]).  Step t (column
-// c = s0+t):
-//   (a) unpivoted rows apply step t-1: l = a[i,c-1] / p[c-1] stored in place (the L
-//       multiplier), a[i,c'] -= l * p[c'] for c' >= c, p = pivot row of step t-1;
-//   (b) local argmax |a[i,c]| over unpivoted rows (ties -> lowest row, LAPACK isamax on the
-//       unswapped order); the CTA publishes (|a|, row) and that row's entries in its own
-//       shared memory; cluster barrier;
-//   (c) every CTA reads the candidates and the winner's row through distributed shared memory
-//       (identical reduction everywhere); the owner marks its row pivoted.
-// Rows are not moved inside the sub-panel: the LAPACK interchange sequence is derived
-// afterwards (build_ipiv_kernel) and applied to the panel columns (laswp_kernel); the
-// remaining panel columns then receive the sub-panel's TRSM + rank-w update
-// (panel_update_kernel).  All panel arithmetic is FP32.
+// chunks over the cluster's CTAs and held in shared memory ([col][row]); thread e owns rows
+// e, e + 512, ... of its CTA, so the per-column work needs no CTA barrier.  Step t (column
+// c = s0+t), per owned unpivoted row:
+//   (a) apply step t-1: l = a[i,c-1] / p[c-1] stored in place (the L multiplier),
+//       a[i,c'] -= l * p[c'] for c' >= c (p = pivot row of step t-1);
+//   (b) candidate |a[i,c]| (ties -> lowest row, LAPACK isamax on the unswapped order); warp
+//       0 reduces the warps' candidates and PUSHES the CTA's (|a|, row, row entries) into
+//       every peer's receive slot with st.async, completing bytes on the peer's mbarrier;
+//   (c) warp 0 waits on its own mbarrier for all peers' records (no cluster barrier, no
+//       GPU-scope fence per column), picks the same winner everywhere and stores its row as p.
+// Rows are not moved inside the sub-panel: at the end CTA 0 turns the chosen rows into the
+// LAPACK interchange sequence (ipiv) and the equivalent gather pairs, which laswp_kernel
+// then applies to all n columns.  All panel arithmetic is FP32.
 // ------------------------------------------------------------------------------------
 constexpr int kSubW = 32;
 constexpr int kSubThreads = 512;
+constexpr int kSubWarps = kSubThreads / 32;
+constexpr int kSubRec = 36;              // receive record: |a|, row index, 2 pad, 32 row entries
+constexpr int kSubMaxCl = 16;
 
-__global__ void __launch_bounds__(kSubThreads) subpanel_kernel(float *LU, int ld, int n, int s0, int w, int rl_max,
-                                                              int *piv_rows, int *info) {
+__device__ __forceinline__ uint32_t mapa_u32(uint32_t a, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void st_async_v4(uint32_t raddr, uint32_t a, uint32_t b, uint32_t c, uint32_t d,
+                                            uint32_t rbar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(
+                     raddr),
+                 "r"(a), "r"(b), "r"(c), "r"(d), "r"(rbar)
+                 : "memory");
+}
+
+// Candidate key: |a| (non-negative float bits, monotone as unsigned) in the high word, the
+// complemented row index in the low word, so the largest key is the largest |a| with ties
+// going to the lowest row (LAPACK isamax on the unswapped order).  0 = no candidate.
+__device__ __forceinline__ uint64_t cand_key(uint32_t vbits, uint32_t row) {
+    return ((uint64_t)vbits << 32) | (uint64_t)(0xFFFFFFFFu - row);
+}
+// warp-wide maximum of (hi, lo) pairs with two redux operations
+__device__ __forceinline__ uint64_t warp_max_key(uint32_t hi, uint32_t lo) {
+    const uint32_t mh = __reduce_max_sync(0xffffffffu, hi);
+    const uint32_t ml = __reduce_max_sync(0xffffffffu, hi == mh ? lo : 0u);
+    return ((uint64_t)mh << 32) | ml;
+}
+
+template <int RPT>
+__global__ void __launch_bounds__(kSubThreads) subpanel_kernel(float *LU, int ld, int n, int s0, int w, int *ipiv,
+                                                              int2 *pairs, int *npairs, int *info) {
     namespace cg = cooperative_groups;
     cg::cluster_group cl = cg::this_cluster();
     const int ncta = (int)cl.num_blocks(), rank = (int)cl.block_rank();
-    extern __shared__ float sm[];
-    float *sp = sm;                                  // [w][rl_max]
-    float *prow = sp + (size_t)w * rl_max;           // [w]    pivot row of the current step
-    float *crow = prow + w;                          // [2][w] this CTA's candidate row
-    float *cval = crow + 2 * w;                      // [2]    candidate |a|
-    int *cidx = reinterpret_cast<int *>(cval + 2);   // [2]    candidate row
-    unsigned char *smark = reinterpret_cast<unsigned char *>(cidx + 2);
-    __shared__ float s_v[kSubThreads / 32];
-    __shared__ int s_i[kSubThreads / 32];
-    __shared__ int s_wr, s_gi;
-    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
+    __shared__ __align__(16) uint64_t rbar[2];                   // receive barriers
+    __shared__ __align__(16) float rbuf[2 * kSubMaxCl * kSubRec];  // [2][cluster][record]
+    __shared__ __align__(16) float wslot[kSubWarps * kSubW];      // each warp's candidate row
+    __shared__ __align__(16) float prow[kSubW];                   // pivot row, columns t.. (shifted)
+    __shared__ unsigned long long s_key[2];                       // CTA candidate (atomicMax)
+    __shared__ int s_rows[kSubW];                                 // chosen rows, step order
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const int R = n - s0;
     const int r0 = s0 + (int)(((int64_t)R * rank) / ncta), r1 = s0 + (int)(((int64_t)R * (rank + 1)) / ncta);
     const int rl = r1 - r0;
-    for (int cc = wid; cc < w; cc += nw)
-        for (int e = lane; e < rl; e += 32) async_copy_f32(sp + cc * rl_max + e, LU + (int64_t)(s0 + cc) * ld + r0 + e);
-    for (int e = tid; e < rl; e += blockDim.x) smark[e] = 0;
-    async_wait_all();
-    __syncthreads();
+    // The thread's rows (e = tid + k * 512) live in registers for the whole sub-panel, SHIFTED:
+    // at step t, a[k][j] holds column s0 + t + j, so every index is a compile-time constant.
+    // Multipliers go to global memory as they are produced; a row's U part when it is chosen.
+    float a[RPT][kSubW];
+    bool live[RPT];
+#pragma unroll
+    for (int k = 0; k < RPT; ++k) {
+        const int e = tid + k * kSubThreads;
+        live[k] = e < rl;
+#pragma unroll
+        for (int cc = 0; cc < kSubW; ++cc)
+            a[k][cc] = (live[k] && cc < w) ? LU[(int64_t)(s0 + cc) * ld + r0 + e] : 0.f;
+    }
+    if (tid == 0) {
+        mbar_init(&rbar[0], 1);
+        mbar_init(&rbar[1], 1);
+        fence_barrier_init();
+        s_key[0] = 0ull;
+        s_key[1] = 0ull;
+    }
+    cl.sync();                                       // barriers initialised cluster-wide
+    const uint32_t rbar_s = smem_u32(rbar), rbuf_s = smem_u32(rbuf);
+    // interchange bookkeeping (CTA 0, warp 1, overlapped with the exchange): rows are at their
+    // own positions when the sub-panel starts; step t swaps position s0+t with the current
+    // position of row s_rows[t].  Only <= 2w positions are touched: a (position -> row) map of
+    // <= 64 entries held two per lane (identity elsewhere), searched with ballots.
+    const bool book = (rank == 0 && wid == 1);
+    int mp[2] = {-1, -1}, mr[2] = {-1, -1}, nm = 0;
+    auto book_step = [&](int t) {
+        const unsigned FULL = 0xffffffffu;
+        auto find = [&](const int *key, int v) -> int {
+            const unsigned b0 = __ballot_sync(FULL, key[0] == v), b1 = __ballot_sync(FULL, key[1] == v);
+            return b0 ? __ffs(b0) - 1 : (b1 ? 32 + __ffs(b1) - 1 : -1);
+        };
+        auto get = [&](const int *arr, int k) -> int {
+            const int v0 = __shfl_sync(FULL, arr[0], k & 31), v1 = __shfl_sync(FULL, arr[1], k & 31);
+            return k < 32 ? v0 : v1;
+        };
+        auto set = [&](int p, int r) {
+            int k = find(mp, p);
+            if (k < 0) k = nm++;
+            if (lane == (k & 31)) {
+                if (k < 32) { mp[0] = p; mr[0] = r; } else { mp[1] = p; mr[1] = r; }
+            }
+            __syncwarp();
+        };
+        const int r = s_rows[t], here = s0 + t;
+        const int kr = find(mr, r);
+        const int q = kr >= 0 ? get(mp, kr) : r;          // current position of row r
+        const int kh = find(mp, here);
+        const int other = kh >= 0 ? get(mr, kh) : here;   // row currently at s0+t
+        if (lane == 0) ipiv[here] = q;
+        set(q, other);
+        set(here, r);
+    };
     for (int t = 0; t <= w; ++t) {
         if (t > 0) {
-            const int tp = t - 1;
-            const float piv = prow[tp];
-            for (int e = tid; e < rl; e += blockDim.x)
-                if (!smark[e]) sp[tp * rl_max + e] = (piv != 0.f) ? sp[tp * rl_max + e] / piv : 0.f;
-            __syncthreads();
-            for (int cc = t + wid; cc < w; cc += nw) {
-                const float u = prow[cc];
-                for (int e = lane; e < rl; e += 32)
-                    if (!smark[e]) sp[cc * rl_max + e] = sp[cc * rl_max + e] - sp[tp * rl_max + e] * u;
+            // apply step t-1: l = a[i,c-1] / p[c-1] (stored), a[i,c'] -= l * p[c'], shift by one
+            const float piv = prow[0];
+#pragma unroll
+            for (int k = 0; k < RPT; ++k) {
+                if (!live[k]) continue;
+                const float l = (piv != 0.f) ? a[k][0] / piv : 0.f;
+                LU[(int64_t)(s0 + t - 1) * ld + r0 + tid + k * kSubThreads] = l;
+#pragma unroll
+                for (int c4 = 0; c4 < kSubW / 4; ++c4) {
+                    const float4 q = reinterpret_cast<const float4 *>(prow)[c4];
+                    const float pq[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int j = 4 * c4 + u;
+                        if (j >= 1) a[k][j - 1] = a[k][j] - l * pq[u];
+                    }
+                }
+                a[k][kSubW - 1] = 0.f;
             }
-            __syncthreads();
         }
         if (t == w) break;
-        float bv = -1.f;
-        int bi = 0x7FFFFFFF;
-        for (int e = tid; e < rl; e += blockDim.x) {
-            if (smark[e]) continue;
-            const float v = fabsf(sp[t * rl_max + e]);
-            if (better(v, r0 + e, bv, bi)) { bv = v; bi = r0 + e; }
+        // this thread's best live row, then the warp's (two redux), then the CTA's (smem atomic)
+        uint32_t bh = 0u, bl = 0u;
+        int bk = -1;
+#pragma unroll
+        for (int k = 0; k < RPT; ++k) {
+            if (!live[k]) continue;
+            float v = fabsf(a[k][0]);
+            if (!(v >= 0.f)) v = INFINITY;           // NaN: chosen (and propagated), never skipped
+            const uint32_t vh = __float_as_uint(v), vl = 0xFFFFFFFFu - (uint32_t)(r0 + tid + k * kSubThreads);
+            if (vh > bh || (vh == bh && vl > bl) || bk < 0) { bh = vh; bl = vl; bk = k; }
         }
-        for (int o = 16; o > 0; o >>= 1) {
-            const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
-            const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-            if (better(ov, oi, bv, bi)) { bv = ov; bi = oi; }
+        const uint64_t wk = warp_max_key(bh, bk >= 0 ? bl : 0u);
+        if (bk >= 0 && wk == (((uint64_t)bh << 32) | bl)) {   // this lane holds the warp's best row
+#pragma unroll
+            for (int k = 0; k < RPT; ++k)
+                if (k == bk) {
+#pragma unroll
+                    for (int c4 = 0; c4 < kSubW / 4; ++c4)
+                        reinterpret_cast<float4 *>(wslot + wid * kSubW)[c4] =
+                            make_float4(a[k][4 * c4], a[k][4 * c4 + 1], a[k][4 * c4 + 2], a[k][4 * c4 + 3]);
+                }
         }
-        if (lane == 0) { s_v[wid] = bv; s_i[wid] = bi; }
+        if (lane == 0 && (uint32_t)wk != 0u) atomicMax(&s_key[t & 1], (unsigned long long)wk);
         __syncthreads();
-        if (tid == 0) {
-            for (int q = 1; q < nw; ++q)
-                if (better(s_v[q], s_i[q], bv, bi)) { bv = s_v[q]; bi = s_i[q]; }
-            cval[t & 1] = bv;
-            cidx[t & 1] = bi;
-            s_gi = (bi >= r0 && bi < r1) ? bi - r0 : -1;
-        }
-        __syncthreads();
-        if (s_gi >= 0)
-            for (int cc = t + tid; cc < w; cc += blockDim.x) crow[(t & 1) * w + cc] = sp[cc * rl_max + s_gi];
-        cl.sync();
-        if (tid < 32) {
-            float gv = -1.f;
-            int gi = 0x7FFFFFFF, gr = 0;
-            for (int q = tid; q < ncta; q += 32) {
-                const float v = *cl.map_shared_rank(&cval[t & 1], q);
-                const int i = *cl.map_shared_rank(&cidx[t & 1], q);
-                if (better(v, i, gv, gi)) { gv = v; gi = i; gr = q; }
-            }
-            for (int o = 16; o > 0; o >>= 1) {
-                const float ov = __shfl_xor_sync(0xffffffffu, gv, o);
-                const int oi = __shfl_xor_sync(0xffffffffu, gi, o);
-                const int orr = __shfl_xor_sync(0xffffffffu, gr, o);
-                if (better(ov, oi, gv, gi)) { gv = ov; gi = oi; gr = orr; }
-            }
-            if (tid == 0) {
-                s_wr = gr;
-                if (gi >= r0 && gi < r1) smark[gi - r0] = 1;
-                if (rank == 0) {
-                    piv_rows[t] = gi;
-                    if (gv == 0.f && *info == 0) *info = s0 + t + 1;
+        if (wid == 0) {
+            const int buf = t & 1;
+            const uint64_t ck = s_key[buf];
+            const int crow = (int)(0xFFFFFFFFu - (uint32_t)ck);
+            const int cw = ((uint32_t)ck != 0u) ? ((crow - r0) % kSubThreads) / 32 : 0;   // winner warp
+            if (lane == 0) mbar_arrive_expect_tx(&rbar[buf], (uint32_t)(ncta * kSubRec * 4));
+            // lane q pushes the whole record (key, row entries; 9 x 16 B) into slot `rank` of
+            // CTA q's receive buffer
+            if (lane < ncta) {
+                const uint32_t slot = rbuf_s + (uint32_t)((buf * kSubMaxCl + rank) * kSubRec) * 4u;
+                const uint32_t rs = mapa_u32(slot, lane), rb = mapa_u32(rbar_s + (uint32_t)buf * 8u, lane);
+                st_async_v4(rs, (uint32_t)ck, (uint32_t)(ck >> 32), 0u, 0u, rb);
+                const float4 *src = reinterpret_cast<const float4 *>(wslot + cw * kSubW);
+#pragma unroll
+                for (int c4 = 0; c4 < kSubW / 4; ++c4) {
+                    const float4 r4 = src[c4];
+                    st_async_v4(rs + 16u + 16u * c4, __float_as_uint(r4.x), __float_as_uint(r4.y),
+                                __float_as_uint(r4.z), __float_as_uint(r4.w), rb);
                 }
             }
+            if (lane == 0) s_key[buf ^ 1] = 0ull;   // next step's accumulator (all atomics of
+                                                    // step t - 1 finished before this step's sync)
+            {   // spin (no suspend): this wait is on the factorisation's critical path
+                const uint32_t par = (uint32_t)((t >> 1) & 1);
+                uint32_t done = 0;
+                while (!done)
+                    asm volatile(
+                        "{\n\t.reg .pred p;\n\t"
+                        "mbarrier.test_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+                        "selp.u32 %0, 1, 0, p;\n\t}"
+                        : "=r"(done)
+                        : "r"(rbar_s + (uint32_t)buf * 8u), "r"(par)
+                        : "memory");
+            }
+            // the cluster's winner, identical in every CTA: lane q holds record q
+            const float *rec = rbuf + buf * kSubMaxCl * kSubRec;
+            const uint32_t ql = (lane < ncta) ? __float_as_uint(rec[lane * kSubRec]) : 0u;
+            const uint32_t qh = (lane < ncta) ? __float_as_uint(rec[lane * kSubRec + 1]) : 0u;
+            const uint64_t gk = warp_max_key(qh, ql);
+            const unsigned hit = __ballot_sync(0xffffffffu, lane < ncta && qh == (uint32_t)(gk >> 32) &&
+                                                                ql == (uint32_t)gk);
+            const int gq = __ffs(hit) - 1;
+            prow[lane] = rec[gq * kSubRec + 4 + lane];
+            if (lane == 0) {
+                s_rows[t] = (int)(0xFFFFFFFFu - (uint32_t)gk);
+                if (rank == 0 && (uint32_t)(gk >> 32) == 0u && *info == 0) *info = s0 + t + 1;
+            }
+        } else if (book && t > 0) {
+            book_step(t - 1);
         }
         __syncthreads();
-        const float *src = cl.map_shared_rank(crow, s_wr) + (t & 1) * w;
-        for (int cc = t + tid; cc < w; cc += blockDim.x) prow[cc] = src[cc];
-        __syncthreads();
+        const int gi = s_rows[t];                    // the owner retires its pivot row: U part
+#pragma unroll
+        for (int k = 0; k < RPT; ++k)
+            if (live[k] && r0 + tid + k * kSubThreads == gi) {
+                live[k] = false;
+#pragma unroll
+                for (int j = 0; j < kSubW; ++j)
+                    if (j < w - t) LU[(int64_t)(s0 + t + j) * ld + gi] = a[k][j];
+            }
     }
-    for (int cc = wid; cc < w; cc += nw)
-        for (int e = lane; e < rl; e += 32) LU[(int64_t)(s0 + cc) * ld + r0 + e] = sp[cc * rl_max + e];
-    cl.sync();   // peers may still read this CTA's candidate row
+    if (book) {
+        if (w > 0) book_step(w - 1);
+        int np = 0;
+        for (int h = 0; h < 2; ++h) {
+            const bool emit = mp[h] >= 0 && mr[h] != mp[h];
+            const unsigned bal = __ballot_sync(0xffffffffu, emit);
+            if (emit) pairs[np + __popc(bal & ((1u << lane) - 1))] = make_int2(mp[h], mr[h]);
+            np += __popc(bal);
+        }
+        if (lane == 0) *npairs = np;
+    }
+    cl.sync();   // no CTA exits while a peer may still push into it
 }
 
 // After sub-panel [s0, s0+w) (rows already interchanged): remaining panel columns [c1, c2)
@@ -266,70 +391,6 @@ __global__ void __launch_bounds__(256) panel_update_kernel(float *LU, int ld, in
             LU[(int64_t)(c1 + c) * ld + rb + r] = old[q] - acc;
         }
     }
-}
-
-// Gather pairs (dst <- src) for an interchange sequence ipiv[j0 .. j0+jb) applied in order.
-__global__ void build_pairs_kernel(int n, int j0, int jb, const int *ipiv, int *pos, int *row_at, int2 *pairs,
-                                   int *npairs) {
-    for (int i = j0 + threadIdx.x; i < n; i += blockDim.x) { pos[i] = i; row_at[i] = i; }
-    __syncthreads();
-    if (threadIdx.x != 0) return;
-    for (int t = 0; t < jb; ++t) {
-        const int here = j0 + t, q = ipiv[here];
-        if (q == here) continue;
-        const int a = row_at[here], b = row_at[q];
-        row_at[here] = b; pos[b] = here;
-        row_at[q] = a; pos[a] = q;
-    }
-    int np = 0;
-    for (int t = 0; t < jb; ++t) {
-        const int here = j0 + t;
-        if (row_at[here] != here) pairs[np++] = make_int2(here, row_at[here]);
-    }
-    for (int t = 0; t < jb; ++t) {
-        const int q = ipiv[j0 + t];
-        if (q >= j0 + jb && row_at[q] != q && pos[q] != -1) {
-            pairs[np++] = make_int2(q, row_at[q]);
-            pos[q] = -1;
-        }
-    }
-    *npairs = np;
-}
-
-// LAPACK interchange sequence from the chosen physical rows: step t swaps position j0+t with
-// the current position of row piv_rows[t] (ipiv, 0-based).  The net effect on the touched
-// positions is emitted as gather pairs (dst <- src) for laswp.  One CTA: parallel init, the
-// jb-step simulation on thread 0.
-__global__ void build_ipiv_kernel(int n, int j0, int jb, const int *piv_rows, int *ipiv, int *pos, int *row_at,
-                                  int2 *pairs, int *npairs) {
-    for (int i = j0 + threadIdx.x; i < n; i += blockDim.x) { pos[i] = i; row_at[i] = i; }
-    __syncthreads();
-    if (threadIdx.x != 0) return;
-    int np = 0;
-    for (int t = 0; t < jb; ++t) {
-        const int r = piv_rows[t];
-        const int q = pos[r];              // where the chosen row currently is
-        const int here = j0 + t;
-        const int other = row_at[here];    // row currently at the target position
-        ipiv[here] = q;
-        row_at[q] = other;
-        pos[other] = q;
-        row_at[here] = r;
-        pos[r] = here;
-    }
-    // touched positions: j0..j0+jb-1 and every q that received a displaced row
-    for (int t = 0; t < jb; ++t) {
-        const int here = j0 + t;
-        if (row_at[here] != here) pairs[np++] = make_int2(here, row_at[here]);
-    }
-    for (int t = 0; t < jb; ++t) {
-        const int q = ipiv[j0 + t];
-        if (q >= j0 + jb && row_at[q] != q && pos[q] != -1) {
-            pairs[np++] = make_int2(q, row_at[q]);
-            pos[q] = -1;                   // pos is dead after the simulation: reuse as "emitted"
-        }
-    }
-    *npairs = np;
 }
 
 // K5a: apply the panel's row interchanges to columns [c0, c1) as a gather through shared
@@ -705,7 +766,7 @@ struct LuWork {
     float *LU = nullptr;
     int ld = 0;
     bool own_LU = true, own_ipiv = true;
-    int *ipiv = nullptr, *piv_rows = nullptr, *pos = nullptr, *row_at = nullptr, *info = nullptr;
+    int *ipiv = nullptr, *info = nullptr;
     int *perm = nullptr, *npairs = nullptr;
     int2 *pairs = nullptr;
     unsigned int *bar = nullptr;  // [grid] arrive flags + [1] release
@@ -714,12 +775,36 @@ struct LuWork {
     double *r = nullptr, *d = nullptr, *part = nullptr, *scal = nullptr;
     double *tinv = nullptr;       // FP64 inverses of the diagonal blocks (solves only)
     unsigned int *tflags = nullptr, tepoch = 0;
-    int n = 0, nb = 0, cl = 16, rl_max = 0, coop_grid = 0;
+    int n = 0, nb = 0, cl = 16, coop_grid = 0;
     std::vector<void *> extra;    // further device buffers owned by the solve
 };
 
-static size_t sub_smem(int rl) {
-    return (size_t)kSubW * rl * sizeof(float) + (size_t)3 * kSubW * sizeof(float) + 16 + (size_t)rl + 16;
+// rows per thread of the register-resident sub-panel for a cluster of cl CTAs (0: too large)
+static int sub_rpt(int n, int cl) {
+    const int rl = (n + cl - 1) / cl;            // max rows of one CTA (contiguous split)
+    for (int r : {1, 2, 4})
+        if (rl <= r * kSubThreads) return r;
+    return 0;
+}
+
+static cudaError_t launch_subpanel(const LuWork &w, int s0, int sw, cudaStream_t st) {
+    const int rpt = sub_rpt(w.n, w.cl);
+    if (rpt == 0) return cudaErrorInvalidValue;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(w.cl);
+    cfg.blockDim = dim3(kSubThreads);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = w.cl;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    if (rpt == 1) return cudaLaunchKernelEx(&cfg, subpanel_kernel<1>, w.LU, w.ld, w.n, s0, sw, w.ipiv, w.pairs, w.npairs, w.info);
+    if (rpt == 2) return cudaLaunchKernelEx(&cfg, subpanel_kernel<2>, w.LU, w.ld, w.n, s0, sw, w.ipiv, w.pairs, w.npairs, w.info);
+    return cudaLaunchKernelEx(&cfg, subpanel_kernel<4>, w.LU, w.ld, w.n, s0, sw, w.ipiv, w.pairs, w.npairs, w.info);
 }
 
 static int coop_launch(const void *fn, int grid, int threads, void **args, size_t smem, cudaStream_t st) {
@@ -735,8 +820,7 @@ static int coop_launch(const void *fn, int grid, int threads, void **args, size_
 static void lu_free(LuWork &w) {
     if (w.own_LU) cudaFree(w.LU);
     if (w.own_ipiv) cudaFree(w.ipiv);
-    cudaFree(w.perm); cudaFree(w.piv_rows); cudaFree(w.pos);
-    cudaFree(w.row_at); cudaFree(w.info); cudaFree(w.npairs); cudaFree(w.pairs);
+    cudaFree(w.perm); cudaFree(w.info); cudaFree(w.npairs); cudaFree(w.pairs);
     cudaFree(w.bar); cudaFree(w.r); cudaFree(w.d); cudaFree(w.part); cudaFree(w.scal);
     cudaFree(w.tinv); cudaFree(w.tflags);
     for (void *p : w.extra) cudaFree(p);
@@ -760,15 +844,15 @@ static int lu_prepare(LuWork &w, int n, int nb, float *LU, int ld, int *ipiv, bo
     w.nb = std::min(nb <= 0 ? 256 : nb, n);
     w.coop_grid = num_sms();
     w.cl = 16;                                   // non-portable cluster size (falls back to 8)
-    w.rl_max = (n + w.cl - 1) / w.cl + 1;
-    if (sub_smem(w.rl_max) > 200 * 1024 || (size_t)n * sizeof(int) > 200 * 1024) {
-        set_error_msg("LU: n too large for the shared-memory sub-panel (n <= ~51000)");
+    if (sub_rpt(n, 8) == 0) {
+        set_error_msg("LU: n too large for the register-resident sub-panel (n <= 16384)");
         return -1;
     }
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(subpanel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024 + 1024);
-        cudaFuncSetAttribute(subpanel_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        cudaFuncSetAttribute(subpanel_kernel<1>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        cudaFuncSetAttribute(subpanel_kernel<2>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        cudaFuncSetAttribute(subpanel_kernel<4>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         cudaFuncSetAttribute(build_perm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024 + 1024);
         cudaFuncSetAttribute(trsm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024 + 1024);
         cudaFuncSetAttribute(panel_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024 + 1024);
@@ -793,9 +877,6 @@ static int lu_prepare(LuWork &w, int n, int nb, float *LU, int ld, int *ipiv, bo
     if (ipiv) w.ipiv = ipiv; else alloc((void **)&w.ipiv, sizeof(int) * n);
     const int nchunk = (n + kResChunk - 1) / kResChunk;
     alloc((void **)&w.perm, sizeof(int) * n);
-    alloc((void **)&w.piv_rows, sizeof(int) * (size_t)kSubW);
-    alloc((void **)&w.pos, sizeof(int) * n);
-    alloc((void **)&w.row_at, sizeof(int) * n);
     alloc((void **)&w.info, sizeof(int));
     alloc((void **)&w.npairs, sizeof(int));
     alloc((void **)&w.pairs, sizeof(int2) * 2 * (size_t)w.nb);
@@ -833,30 +914,12 @@ static int lu_factor(LuWork &w, int variant, cudaStream_t st) {
         const int jb = std::min(nb, n - j0);
         for (int s0 = j0; s0 < j0 + jb && !rc; s0 += kSubW) {
             const int sw = std::min(kSubW, j0 + jb - s0);
-            // (1) sub-panel factorisation on one cluster
-            cudaLaunchConfig_t cfg = {};
-            cfg.gridDim = dim3(w.cl);
-            cfg.blockDim = dim3(kSubThreads);
-            cfg.dynamicSmemBytes = sub_smem(w.rl_max);
-            cfg.stream = st;
-            cudaLaunchAttribute at[1];
-            at[0].id = cudaLaunchAttributeClusterDimension;
-            at[0].val.clusterDim.x = w.cl;
-            at[0].val.clusterDim.y = 1;
-            at[0].val.clusterDim.z = 1;
-            cfg.attrs = at;
-            cfg.numAttrs = 1;
-            cudaError_t e = cudaLaunchKernelEx(&cfg, subpanel_kernel, w.LU, ld, n, s0, sw, w.rl_max, w.piv_rows, w.info);
+            // (1) sub-panel factorisation on one cluster (rows in registers, RPT per thread)
+            cudaError_t e = launch_subpanel(w, s0, sw, st);
             if (e != cudaSuccess && w.cl == 16) {    // 16-CTA clusters unavailable: use 8
                 cudaGetLastError();
                 w.cl = 8;
-                w.rl_max = (n + w.cl - 1) / w.cl + 1;
-                if (sub_smem(w.rl_max) <= 200 * 1024) {
-                    cfg.gridDim = dim3(w.cl);
-                    at[0].val.clusterDim.x = w.cl;
-                    cfg.dynamicSmemBytes = sub_smem(w.rl_max);
-                    e = cudaLaunchKernelEx(&cfg, subpanel_kernel, w.LU, ld, n, s0, sw, w.rl_max, w.piv_rows, w.info);
-                }
+                e = launch_subpanel(w, s0, sw, st);
             }
             if (e != cudaSuccess) {
                 set_cuda_error(e, "subpanel launch");
@@ -864,10 +927,8 @@ static int lu_factor(LuWork &w, int variant, cudaStream_t st) {
                 break;
             }
             count_launch();
-            // (2) its interchanges, applied to the panel columns
-            build_ipiv_kernel<<<1, 1024, 0, st>>>(n, s0, sw, w.piv_rows, w.ipiv, w.pos, w.row_at, w.pairs, w.npairs);
-            count_launch();
-            laswp(j0, j0 + jb, 2 * sw);
+            // (2) its interchanges (emitted by the sub-panel kernel), applied to all n columns
+            laswp(0, n, 2 * sw);
             // (3) TRSM + rank-sw update of the rest of the panel
             const int c1 = s0 + sw, c2 = j0 + jb;
             if (c1 < c2) {
@@ -879,11 +940,6 @@ static int lu_factor(LuWork &w, int variant, cudaStream_t st) {
             rc = check_launch("panel");
         }
         if (rc) break;
-        // the panel's whole interchange sequence on the columns outside it
-        build_pairs_kernel<<<1, 1024, 0, st>>>(n, j0, jb, w.ipiv, w.pos, w.row_at, w.pairs, w.npairs);
-        count_launch();
-        laswp(0, j0, 2 * jb);
-        laswp(j0 + jb, n, 2 * jb);
         const int j1 = j0 + jb, rest = n - j1;
         if (rest > 0) {
             trsm_kernel<<<(rest + kTrsmCols - 1) / kTrsmCols, 256, (size_t)jb * (kTrsmCols + 33) * sizeof(float), st>>>(
