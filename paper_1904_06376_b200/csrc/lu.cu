@@ -333,74 +333,112 @@ __global__ void __launch_bounds__(kSubThreads) subpanel_kernel(float *LU, int ld
 }
 
 // After sub-panel [s0, s0+w) (rows already interchanged): remaining panel columns [c1, c2)
-// get U = L11^-1 A[s0:s0+w, c1:c2] (L11 unit lower w x w; every block recomputes it, block 0
-// stores it) and rows [c1, n) get A -= L21 U.  64 rows per block.
+// get U = L11^-1 A[s0:s0+w, c1:c2] (L11 unit lower w x w; every block recomputes it with one
+// column per thread held in registers, block 0 stores it) and rows [c1, n) get A -= L21 U,
+// 64 rows per block, 4 x 4 outputs per thread from shared-memory tiles.
 constexpr int kUpdRows = 64;
+static size_t panel_update_smem(int nc) {
+    const int ncp = (nc + 3) & ~3;
+    return ((size_t)kSubW * ncp + (size_t)kSubW * (kSubW + 1) + (size_t)kSubW * kUpdRows) * sizeof(float);
+}
 __global__ void __launch_bounds__(256) panel_update_kernel(float *LU, int ld, int n, int s0, int w, int c1, int c2) {
-    extern __shared__ float su[];
-    const int nc = c2 - c1;
-    float *sU = su;                           // [w][nc]
-    float *sL11 = sU + (size_t)w * nc;        // [w][w]   (row r, col i) at r*w + i
-    float *sL21 = sL11 + (size_t)w * w;       // [w][kUpdRows] (col t, row r)
+    extern __shared__ __align__(16) float su[];
+    const int nc = c2 - c1, ncp = (nc + 3) & ~3;
+    float *sU = su;                                   // [kSubW][ncp]      row r of the w x nc block
+    float *sL11 = sU + (size_t)kSubW * ncp;           // [kSubW][kSubW+1]  L11[r][i]
+    float *sL21 = sL11 + kSubW * (kSubW + 1);         // [kSubW][kUpdRows] (col t, row r)
     const int tid = threadIdx.x;
-    for (int e = tid; e < w * nc; e += blockDim.x) {
-        const int r = e % w, c = e / w;
-        async_copy_f32(sU + r * nc + c, LU + (int64_t)(c1 + c) * ld + s0 + r);
+    for (int e = tid; e < kSubW * ncp; e += blockDim.x) {
+        const int r = e % kSubW, c = e / kSubW;
+        if (r < w && c < nc) async_copy_f32(sU + r * ncp + c, LU + (int64_t)(c1 + c) * ld + s0 + r);
+        else sU[r * ncp + c] = 0.f;
     }
-    for (int e = tid; e < w * w; e += blockDim.x) {
-        const int r = e % w, i = e / w;
-        async_copy_f32(sL11 + r * w + i, LU + (int64_t)(s0 + i) * ld + s0 + r);
+    for (int e = tid; e < kSubW * kSubW; e += blockDim.x) {
+        const int r = e % kSubW, i = e / kSubW;
+        if (r < w && i < w && r > i) async_copy_f32(sL11 + r * (kSubW + 1) + i, LU + (int64_t)(s0 + i) * ld + s0 + r);
+        else sL11[r * (kSubW + 1) + i] = 0.f;
     }
     const int rb = c1 + blockIdx.x * kUpdRows;
     const int nr = min(kUpdRows, n - rb);
-    for (int e = tid; e < w * kUpdRows; e += blockDim.x) {
+    for (int e = tid; e < kSubW * kUpdRows; e += blockDim.x) {
         const int r = e % kUpdRows, t = e / kUpdRows;
-        if (r < nr) async_copy_f32(sL21 + t * kUpdRows + r, LU + (int64_t)(s0 + t) * ld + rb + r);
+        if (r < nr && t < w) async_copy_f32(sL21 + t * kUpdRows + r, LU + (int64_t)(s0 + t) * ld + rb + r);
         else sL21[t * kUpdRows + r] = 0.f;
     }
     async_wait_all();
     __syncthreads();
-    for (int c = tid; c < nc; c += blockDim.x)       // forward substitution per column
-        for (int i = 0; i < w - 1; ++i) {
-            const float xi = sU[i * nc + c];
-            for (int r = i + 1; r < w; ++r) sU[r * nc + c] -= sL11[r * w + i] * xi;
-        }
+    for (int c = tid; c < nc; c += blockDim.x) {      // forward substitution, column in registers
+        float x[kSubW];
+#pragma unroll
+        for (int r = 0; r < kSubW; ++r) x[r] = sU[r * ncp + c];
+#pragma unroll
+        for (int i = 0; i < kSubW - 1; ++i)
+#pragma unroll
+            for (int r = i + 1; r < kSubW; ++r) x[r] = x[r] - sL11[r * (kSubW + 1) + i] * x[i];
+#pragma unroll
+        for (int r = 0; r < kSubW; ++r) sU[r * ncp + c] = x[r];
+        if (blockIdx.x == 0)
+#pragma unroll
+            for (int r = 0; r < kSubW; ++r)
+                if (r < w) LU[(int64_t)(c1 + c) * ld + s0 + r] = x[r];
+    }
     __syncthreads();
-    if (blockIdx.x == 0)
-        for (int e = tid; e < w * nc; e += blockDim.x) {
-            const int r = e % w, c = e / w;
-            LU[(int64_t)(c1 + c) * ld + s0 + r] = sU[r * nc + c];
-        }
-    // 8 outputs per round: their old values are loaded together (independent loads in flight)
-    const int nout = kUpdRows * nc;
-    for (int e0 = tid; e0 < nout; e0 += 8 * blockDim.x) {
-        float old[8];
+    // A[rb + 4ty + i, c1 + cq + j] -= sum_t L21[., t] U[t, .]
+    const int ty = tid >> 4, tx = tid & 15;
+    for (int cq = 4 * tx; cq < nc; cq += 64) {
+        float old[4][4];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
-            const int e = e0 + q * blockDim.x;
-            const int r = e % kUpdRows, c = e / kUpdRows;
-            old[q] = (e < nout && r < nr) ? LU[(int64_t)(c1 + c) * ld + rb + r] : 0.f;
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int r = 4 * ty + i;
+                old[j][i] = (cq + j < nc && r < nr) ? LU[(int64_t)(c1 + cq + j) * ld + rb + r] : 0.f;
+            }
+        float acc[4][4] = {};
+#pragma unroll 8
+        for (int t = 0; t < kSubW; ++t) {
+            const float4 l = *reinterpret_cast<const float4 *>(sL21 + t * kUpdRows + 4 * ty);
+            const float4 u = *reinterpret_cast<const float4 *>(sU + t * ncp + cq);
+            const float lv[4] = {l.x, l.y, l.z, l.w}, uv[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+#pragma unroll
+                for (int i = 0; i < 4; ++i) acc[j][i] = fmaf(lv[i], uv[j], acc[j][i]);
         }
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
-            const int e = e0 + q * blockDim.x;
-            const int r = e % kUpdRows, c = e / kUpdRows;
-            if (e >= nout || r >= nr) continue;
-            float acc = 0.f;
-            for (int t = 0; t < w; ++t) acc = fmaf(sL21[t * kUpdRows + r], sU[t * nc + c], acc);
-            LU[(int64_t)(c1 + c) * ld + rb + r] = old[q] - acc;
-        }
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int r = 4 * ty + i;
+                if (cq + j < nc && r < nr) LU[(int64_t)(c1 + cq + j) * ld + rb + r] = old[j][i] - acc[j][i];
+            }
     }
 }
 
 // K5a: apply the panel's row interchanges to columns [c0, c1) as a gather through shared
-// memory: one warp per column, lanes over the (dst <- src) pairs.
+// memory: one warp per column, lanes over the (dst <- src) pairs.  Block 0 also applies them
+// to the row permutation perm (perm[i] = original row now at position i), so the solves'
+// P never has to be rebuilt from ipiv.
 __global__ void __launch_bounds__(256) laswp_kernel(float *LU, int ld, int c0, int c1, const int2 *pairs,
-                                                    const int *npairs) {
+                                                    const int *npairs, int *perm) {
     extern __shared__ float sv[];          // [8 warps][np]
     const int np = *npairs;
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int c = c0 + blockIdx.x * 8 + wid;
+    if (np > 0 && perm && blockIdx.x == 0 && wid == 0) {   // np <= 2 * kSubW = 64
+        int pv[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int e = h * 32 + lane;
+            pv[h] = (e < np) ? perm[pairs[e].y] : 0;
+        }
+        __syncwarp();
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int e = h * 32 + lane;
+            if (e < np) perm[pairs[e].x] = pv[h];
+        }
+    }
     if (np == 0 || c >= c1) return;
     float *col = LU + (int64_t)c * ld;
     float *buf = sv + wid * np;
@@ -411,38 +449,76 @@ __global__ void __launch_bounds__(256) laswp_kernel(float *LU, int ld, int c0, i
 
 // K5b: U12 = L11^-1 A12 with L11 = unit lower jb x jb at (j0, j0), A12 = rows j0..j0+jb of
 // columns [c0, c0 + ncols).  One CTA per 32 columns held in shared memory; L11 is staged in
-// 32-column chunks: each chunk's 32x32 diagonal triangle is solved step by step, then the
-// rows below it take the chunk's contribution as one small product (no barrier per row).
+// 32-column chunks.  Per chunk: the 32 x 32 diagonal triangle is solved by warp shuffles
+// (warp w owns 4 columns, lanes are rows: no CTA barrier per row), then the rows below take
+// the chunk's contribution as a small product, 4 rows per thread from a transposed L tile.
 constexpr int kTrsmCols = 32;
+static size_t trsm_smem(int jb) {
+    const int jbp = (jb + 3) & ~3;
+    return ((size_t)jb * kTrsmCols + 32 * 33 + (size_t)32 * jbp) * sizeof(float);
+}
 __global__ void __launch_bounds__(256) trsm_kernel(float *LU, int ld, int j0, int jb, int c0, int ncols) {
-    extern __shared__ float sm[];
-    float *sB = sm;                                   // [jb][32]
-    float *sL = sm + (size_t)jb * kTrsmCols;          // [jb][33]: rows i0.., chunk columns
+    extern __shared__ __align__(16) float sm[];
+    const int jbp = (jb + 3) & ~3;
+    float *sB = sm;                                   // [jb][32]   (row r, column c)
+    float *sLd = sB + (size_t)jb * kTrsmCols;         // [32][33]   L[i0+r][i0+i]
+    float *sLt = sLd + 32 * 33;                       // [32][jbp]  L[i0+ib+r][i0+i] at i*jbp + r
     const int cb = c0 + blockIdx.x * kTrsmCols;
-    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;   // 32 columns x 8 row groups
+    const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5, lane = tx;
     const bool valid = (cb + tx) < c0 + ncols;
     for (int r = ty; r < jb; r += 8) {
         if (valid) async_copy_f32(sB + r * kTrsmCols + tx, LU + (int64_t)(cb + tx) * ld + j0 + r);
         else sB[r * kTrsmCols + tx] = 0.f;
     }
     for (int i0 = 0; i0 < jb; i0 += 32) {
-        const int ib = min(32, jb - i0);
+        const int ib = min(32, jb - i0), below = jb - i0 - ib;
         __syncthreads();
-        for (int e = threadIdx.x; e < (jb - i0) * ib; e += blockDim.x) {
-            const int r = e % (jb - i0), c = e / (jb - i0);
-            async_copy_f32(sL + r * 33 + c, LU + (int64_t)(j0 + i0 + c) * ld + j0 + i0 + r);
+        for (int e = tid; e < 32 * 32; e += blockDim.x) {
+            const int r = e & 31, i = e >> 5;
+            if (r < ib && i < ib && r > i) async_copy_f32(sLd + r * 33 + i, LU + (int64_t)(j0 + i0 + i) * ld + j0 + i0 + r);
+            else sLd[r * 33 + i] = 0.f;
         }
+        for (int i = ty; i < ib; i += 8)
+            for (int r = lane; r < below; r += 32)
+                async_copy_f32(sLt + i * jbp + r, LU + (int64_t)(j0 + i0 + i) * ld + j0 + i0 + ib + r);
         async_wait_all();
         __syncthreads();
-        for (int i = 0; i < ib - 1; ++i) {
-            const float xi = sB[(i0 + i) * kTrsmCols + tx];
-            for (int r = i + 1 + ty; r < ib; r += 8) sB[(i0 + r) * kTrsmCols + tx] -= sL[r * 33 + i] * xi;
-            __syncthreads();
+        {   // diagonal triangle: warp ty owns columns 4ty .. 4ty+3, lane = row
+            float v[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) v[q] = (lane < ib) ? sB[(i0 + lane) * kTrsmCols + 4 * ty + q] : 0.f;
+            for (int i = 0; i < ib - 1; ++i) {
+                const float l = sLd[lane * 33 + i];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const float xi = __shfl_sync(0xffffffffu, v[q], i);
+                    if (lane > i) v[q] -= l * xi;
+                }
+            }
+            if (lane < ib)
+#pragma unroll
+                for (int q = 0; q < 4; ++q) sB[(i0 + lane) * kTrsmCols + 4 * ty + q] = v[q];
         }
-        for (int r = i0 + ib + ty; r < jb; r += 8) {
-            float acc = 0.f;
-            for (int i = 0; i < ib; ++i) acc = fmaf(sL[(r - i0) * 33 + i], sB[(i0 + i) * kTrsmCols + tx], acc);
-            sB[r * kTrsmCols + tx] -= acc;
+        __syncthreads();
+        if (below > 0) {  // rows below the chunk: column tx, 4 rows per step
+            float x[32];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) x[i] = (i < ib) ? sB[(i0 + i) * kTrsmCols + tx] : 0.f;
+            for (int rq = 4 * ty; rq < below; rq += 32) {
+                float acc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+                for (int i = 0; i < 32; ++i) {
+                    if (i >= ib) break;
+                    const float4 l4 = *reinterpret_cast<const float4 *>(sLt + i * jbp + rq);
+                    acc[0] = fmaf(l4.x, x[i], acc[0]);
+                    acc[1] = fmaf(l4.y, x[i], acc[1]);
+                    acc[2] = fmaf(l4.z, x[i], acc[2]);
+                    acc[3] = fmaf(l4.w, x[i], acc[3]);
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    if (rq + u < below) sB[(i0 + ib + rq + u) * kTrsmCols + tx] -= acc[u];
+            }
         }
     }
     __syncthreads();
@@ -496,18 +572,10 @@ __global__ void axpy_kernel(int n, double *x, const double *d) {
     if (i < n) x[i] += d[i];
 }
 
-// perm[i] = source index of y[i] in y = P v (interchanges applied in order); one CTA.
-__global__ void build_perm_kernel(int n, const int *ipiv, int *perm) {
-    extern __shared__ int sp_i[];
-    for (int i = threadIdx.x; i < n; i += blockDim.x) sp_i[i] = i;
-    __syncthreads();
-    if (threadIdx.x == 0)
-        for (int j = 0; j < n; ++j) {
-            const int q = ipiv[j];
-            if (q != j) { const int t = sp_i[j]; sp_i[j] = sp_i[q]; sp_i[q] = t; }
-        }
-    __syncthreads();
-    for (int i = threadIdx.x; i < n; i += blockDim.x) perm[i] = sp_i[i];
+// perm[i] = original row now at position i (the interchanges composed by laswp_kernel)
+__global__ void iota_kernel(int n, int *perm) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) perm[i] = i;
 }
 __global__ void gather_kernel(int n, const int *perm, const double *v, double *y) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -853,7 +921,6 @@ static int lu_prepare(LuWork &w, int n, int nb, float *LU, int ld, int *ipiv, bo
         cudaFuncSetAttribute(subpanel_kernel<1>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         cudaFuncSetAttribute(subpanel_kernel<2>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         cudaFuncSetAttribute(subpanel_kernel<4>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-        cudaFuncSetAttribute(build_perm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024 + 1024);
         cudaFuncSetAttribute(trsm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024 + 1024);
         cudaFuncSetAttribute(panel_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024 + 1024);
         cudaFuncSetAttribute(trsv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTrsvSmem);
@@ -907,9 +974,11 @@ static int lu_factor(LuWork &w, int variant, cudaStream_t st) {
     auto laswp = [&](int c0, int c1, int pair_cap) {
         if (c1 <= c0) return;
         laswp_kernel<<<(c1 - c0 + 7) / 8, 256, 8 * (size_t)pair_cap * sizeof(float), st>>>(w.LU, ld, c0, c1, w.pairs,
-                                                                                          w.npairs);
+                                                                                          w.npairs, w.perm);
         count_launch();
     };
+    iota_kernel<<<(n + 255) / 256, 256, 0, st>>>(n, w.perm);
+    count_launch();
     for (int j0 = 0; j0 < n && !rc; j0 += nb) {
         const int jb = std::min(nb, n - j0);
         for (int s0 = j0; s0 < j0 + jb && !rc; s0 += kSubW) {
@@ -932,7 +1001,7 @@ static int lu_factor(LuWork &w, int variant, cudaStream_t st) {
             // (3) TRSM + rank-sw update of the rest of the panel
             const int c1 = s0 + sw, c2 = j0 + jb;
             if (c1 < c2) {
-                const size_t smem = ((size_t)sw * (c2 - c1) + (size_t)sw * sw + (size_t)sw * kUpdRows) * sizeof(float);
+                const size_t smem = panel_update_smem(c2 - c1);
                 panel_update_kernel<<<(n - c1 + kUpdRows - 1) / kUpdRows, 256, smem, st>>>(w.LU, ld, n, s0, sw, c1,
                                                                                             c2);
                 count_launch();
@@ -942,7 +1011,7 @@ static int lu_factor(LuWork &w, int variant, cudaStream_t st) {
         if (rc) break;
         const int j1 = j0 + jb, rest = n - j1;
         if (rest > 0) {
-            trsm_kernel<<<(rest + kTrsmCols - 1) / kTrsmCols, 256, (size_t)jb * (kTrsmCols + 33) * sizeof(float), st>>>(
+            trsm_kernel<<<(rest + kTrsmCols - 1) / kTrsmCols, 256, trsm_smem(jb), st>>>(
                 w.LU, ld, j0, jb, j1, rest);
             count_launch();
             rc = check_launch("trsm");
@@ -954,8 +1023,6 @@ static int lu_factor(LuWork &w, int variant, cudaStream_t st) {
         }
     }
     if (rc == BF16X_SUCCESS) {
-        build_perm_kernel<<<1, 1024, (size_t)n * sizeof(int), st>>>(n, w.ipiv, w.perm);
-        count_launch();
         if (w.tinv) {
             diag_inverse_kernel<<<dim3((n + kTB - 1) / kTB, 2), kTB, kTinvBlock * (sizeof(double) + sizeof(float)),
                                   st>>>(w.LU, ld, n, w.tinv);
