@@ -119,8 +119,12 @@ int bf16x_gemm_ex(int m, int n, int k, float alpha, const float *A, int lda,
                   void *workspace, size_t ws_bytes, bf16x_stream_t stream);
 
 /* Host-buffer GEMM (synchronous): copies A, B (and C when beta != 0) from host memory
- * into cached device buffers, runs bf16x_gemm_ex, copies C back.  Same arguments and
- * errors as bf16x_gemm with HOST pointers.  Pinned host memory gives full PCIe speed. */
+ * into cached device buffers, runs the split GEMM, copies C back.  Same arguments and
+ * errors as bf16x_gemm with HOST pointers.  Large problems (m*k >= 2^20, n >= 1024) are
+ * pipelined over column chunks of B/C (width n / min(8, n/512) rounded up to 256): A is
+ * copied and split once, each chunk's B copy overlaps the previous chunk's GEMM and each
+ * chunk's C copy-back overlaps the next; every chunk equals bf16x_gemm on that column block.
+ * Pinned host memory is needed for the copies to overlap (pageable memory still works). */
 int bf16x_gemm_host(int m, int n, int k, float alpha, const float *A_host, int lda,
                     const float *B_host, int ldb, float beta, float *C_host, int ldc, int variant);
 

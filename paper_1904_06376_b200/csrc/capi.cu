@@ -204,8 +204,12 @@ int bf16x_gemm_cg(int m, int n, int k, float alpha, const float *A, int lda, con
 }
 
 static std::mutex g_host_mu;
-static float *g_hA = nullptr, *g_hB = nullptr, *g_hC = nullptr;
-static size_t g_hA_n = 0, g_hB_n = 0, g_hC_n = 0;
+static float *g_hA = nullptr, *g_hB = nullptr, *g_hC = nullptr, *g_hAp = nullptr;   // g_hAp: A's pieces
+static size_t g_hA_n = 0, g_hB_n = 0, g_hC_n = 0, g_hAp_n = 0;
+// host-path pipeline: copy-in / copy-out streams and per-chunk events (created once)
+constexpr int kHostChunks = 8;
+static cudaStream_t g_s_in = nullptr, g_s_out = nullptr;
+static cudaEvent_t g_ev_a = nullptr, g_ev_b[kHostChunks], g_ev_c[kHostChunks], g_ev_done = nullptr;
 
 static int ensure(float **p, size_t *cap, size_t n) {
     if (n <= *cap) return BF16X_SUCCESS;
@@ -220,6 +224,31 @@ static int ensure(float **p, size_t *cap, size_t n) {
     return BF16X_SUCCESS;
 }
 
+static int host_pipeline_init() {
+    if (g_s_in) return BF16X_SUCCESS;
+    cudaError_t e = cudaStreamCreateWithFlags(&g_s_in, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&g_s_out, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&g_ev_a, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&g_ev_done, cudaEventDisableTiming);
+    for (int j = 0; j < kHostChunks && e == cudaSuccess; ++j) {
+        e = cudaEventCreateWithFlags(&g_ev_b[j], cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&g_ev_c[j], cudaEventDisableTiming);
+    }
+    if (e != cudaSuccess) {
+        set_cuda_error(e, "gemm_host streams");
+        return BF16X_ERR_CUDA;
+    }
+    return BF16X_SUCCESS;
+}
+
+// Host-buffer GEMM.  Small problems: copy in, GEMM, copy out on the library stream.  Large ones
+// are pipelined over column chunks of B and C so the PCIe transfers overlap the device work:
+//   copy-in stream : A, then B chunk 0, 1, ... (and C chunks when beta != 0)
+//   library stream : split A once (K-major pieces); per chunk, once its B has landed: split the
+//                    chunk and run the GEMM on the pre-split A
+//   copy-out stream: C chunk j as soon as its GEMM is done (overlaps the next chunks' copy-in)
+// Each chunk is an independent GEMM: its columns equal bf16x_gemm on that column block (chunk
+// width: n / min(8, n / 512) rounded up to 256 columns when m*k >= 2^20 and n >= 1024).
 int bf16x_gemm_host(int m, int n, int k, float alpha, const float *A_host, int lda, const float *B_host, int ldb,
                     float beta, float *C_host, int ldc, int variant) {
     int a = gemm_args(m, n, k, lda, ldb, ldc, variant);
@@ -232,28 +261,90 @@ int bf16x_gemm_host(int m, int n, int k, float alpha, const float *A_host, int l
     if ((rc = ensure(&g_hA, &g_hA_n, (size_t)m * (k > 0 ? k : 1))) ||
         (rc = ensure(&g_hB, &g_hB_n, (size_t)(k > 0 ? k : 1) * n)) || (rc = ensure(&g_hC, &g_hC_n, (size_t)m * n)))
         return rc;
-    cudaError_t e = cudaSuccess;
-    if (k > 0) {
-        e = cudaMemcpy2DAsync(g_hA, (size_t)m * 4, A_host, (size_t)lda * 4, (size_t)m * 4, k, cudaMemcpyHostToDevice,
-                              st);
-        if (e == cudaSuccess)
-            e = cudaMemcpy2DAsync(g_hB, (size_t)k * 4, B_host, (size_t)ldb * 4, (size_t)k * 4, n,
-                                  cudaMemcpyHostToDevice, st);
+    const int p = pieces_of(variant);
+    const int64_t kp = round_up8(k);
+    // chunk width: a multiple of 256 columns, >= 512, at most kHostChunks chunks
+    int nchunk = 1;
+    if (k > 0 && alpha != 0.f && (int64_t)m * k >= (1 << 20) && n >= 1024)
+        nchunk = std::min(kHostChunks, n / 512);
+    if (nchunk > 1) {
+        if ((rc = host_pipeline_init())) return rc;
+        if ((rc = ensure(&g_hAp, &g_hAp_n, ((size_t)p * m * kp + 1) / 2))) return rc;
     }
-    if (e == cudaSuccess && beta != 0.f)
-        e = cudaMemcpy2DAsync(g_hC, (size_t)m * 4, C_host, (size_t)ldc * 4, (size_t)m * 4, n, cudaMemcpyHostToDevice,
+    cudaError_t e = cudaSuccess;
+    if (nchunk == 1) {
+        if (k > 0) {
+            e = cudaMemcpy2DAsync(g_hA, (size_t)m * 4, A_host, (size_t)lda * 4, (size_t)m * 4, k,
+                                  cudaMemcpyHostToDevice, st);
+            if (e == cudaSuccess)
+                e = cudaMemcpy2DAsync(g_hB, (size_t)k * 4, B_host, (size_t)ldb * 4, (size_t)k * 4, n,
+                                      cudaMemcpyHostToDevice, st);
+        }
+        if (e == cudaSuccess && beta != 0.f)
+            e = cudaMemcpy2DAsync(g_hC, (size_t)m * 4, C_host, (size_t)ldc * 4, (size_t)m * 4, n,
+                                  cudaMemcpyHostToDevice, st);
+        if (e != cudaSuccess) {
+            set_cuda_error(e, "gemm_host h2d");
+            return BF16X_ERR_CUDA;
+        }
+        rc = gemm_core(m, n, k, alpha, g_hA, m, g_hB, k > 0 ? k : 1, beta, g_hC, m, variant, 0u, nullptr, 0, 0,
+                       nullptr, 0, 0, nullptr, nullptr, 0, st, 0);
+        if (rc) return rc;
+        e = cudaMemcpy2DAsync(C_host, (size_t)ldc * 4, g_hC, (size_t)m * 4, (size_t)m * 4, n, cudaMemcpyDeviceToHost,
                               st);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+        if (e != cudaSuccess) {
+            set_cuda_error(e, "gemm_host d2h");
+            return BF16X_ERR_CUDA;
+        }
+        return BF16X_SUCCESS;
+    }
+    const int cw = ((n + nchunk - 1) / nchunk + 255) / 256 * 256;
+    nchunk = (n + cw - 1) / cw;
+    uint16_t *ap = reinterpret_cast<uint16_t *>(g_hAp);
+    const int64_t a_plane = (int64_t)m * kp;
+    // the caller's stream may still be using the device buffers / host arrays
+    e = cudaEventRecord(g_ev_done, st);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(g_s_in, g_ev_done, 0);
+    if (e == cudaSuccess)
+        e = cudaMemcpy2DAsync(g_hA, (size_t)m * 4, A_host, (size_t)lda * 4, (size_t)m * 4, k, cudaMemcpyHostToDevice,
+                              g_s_in);
+    if (e == cudaSuccess) e = cudaEventRecord(g_ev_a, g_s_in);
+    for (int j = 0; j < nchunk && e == cudaSuccess; ++j) {
+        const int c0 = j * cw, nj = std::min(cw, n - c0);
+        e = cudaMemcpy2DAsync(g_hB + (size_t)c0 * k, (size_t)k * 4, B_host + (size_t)c0 * ldb, (size_t)ldb * 4,
+                              (size_t)k * 4, nj, cudaMemcpyHostToDevice, g_s_in);
+        if (e == cudaSuccess && beta != 0.f)
+            e = cudaMemcpy2DAsync(g_hC + (size_t)c0 * m, (size_t)m * 4, C_host + (size_t)c0 * ldc, (size_t)ldc * 4,
+                                  (size_t)m * 4, nj, cudaMemcpyHostToDevice, g_s_in);
+        if (e == cudaSuccess) e = cudaEventRecord(g_ev_b[j], g_s_in);
+    }
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(st, g_ev_a, 0);
     if (e != cudaSuccess) {
         set_cuda_error(e, "gemm_host h2d");
         return BF16X_ERR_CUDA;
     }
-    rc = gemm_core(m, n, k, alpha, g_hA, m, g_hB, k > 0 ? k : 1, beta, g_hC, m, variant, 0u, nullptr, 0, 0, nullptr,
-                   0, 0, nullptr, nullptr, 0, st, 0);
+    rc = launch_split(m, k, g_hA, m, ap, p > 1 ? ap + a_plane : nullptr, p > 2 ? ap + 2 * a_plane : nullptr, kp, true,
+                      st);
+    for (int j = 0; j < nchunk && rc == BF16X_SUCCESS; ++j) {
+        const int c0 = j * cw, nj = std::min(cw, n - c0);
+        e = cudaStreamWaitEvent(st, g_ev_b[j], 0);
+        if (e != cudaSuccess) break;
+        rc = gemm_core(m, nj, k, alpha, nullptr, m, g_hB + (size_t)c0 * k, k, beta, g_hC + (size_t)c0 * m, m, variant,
+                       0u, ap, kp, a_plane, nullptr, 0, 0, nullptr, nullptr, 0, st, 0);
+        if (rc) break;
+        e = cudaEventRecord(g_ev_c[j], st);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(g_s_out, g_ev_c[j], 0);
+        if (e == cudaSuccess)
+            e = cudaMemcpy2DAsync(C_host + (size_t)c0 * ldc, (size_t)ldc * 4, g_hC + (size_t)c0 * m, (size_t)m * 4,
+                                  (size_t)m * 4, nj, cudaMemcpyDeviceToHost, g_s_out);
+        if (e != cudaSuccess) break;
+    }
     if (rc) return rc;
-    e = cudaMemcpy2DAsync(C_host, (size_t)ldc * 4, g_hC, (size_t)m * 4, (size_t)m * 4, n, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(g_s_out);
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) {
-        set_cuda_error(e, "gemm_host d2h");
+        set_cuda_error(e, "gemm_host pipeline");
         return BF16X_ERR_CUDA;
     }
     return BF16X_SUCCESS;
@@ -276,8 +367,9 @@ void bf16x_release(void) {
     if (g_hA) cudaFree(g_hA);
     if (g_hB) cudaFree(g_hB);
     if (g_hC) cudaFree(g_hC);
-    g_hA = g_hB = g_hC = nullptr;
-    g_hA_n = g_hB_n = g_hC_n = 0;
+    if (g_hAp) cudaFree(g_hAp);
+    g_hA = g_hB = g_hC = g_hAp = nullptr;
+    g_hA_n = g_hB_n = g_hC_n = g_hAp_n = 0;
 }
 
 const char *bf16x_status_string(int status) {

@@ -150,6 +150,31 @@ def test_row_major_torch_and_host_api(orc):
     assert orc.normwise_error(Cr.cpu().numpy(), C64, A, B) <= RATIO * eo
 
 
+@pytest.mark.parametrize("beta", [0.0, 0.75])
+def test_host_api_pipelined_chunks(orc, beta):
+    """bf16x_gemm_host's chunked pipeline (m*k >= 2^20, n >= 1024): every column chunk equals
+    the device GEMM on that column block bit for bit; sampled columns meet the oracle bar."""
+    m, k, n = 1024, 1100, 2600
+    A = synthetic.uniform(m, k, seed=21)
+    B = synthetic.uniform(k, n, seed=22)
+    C0 = synthetic.uniform(m, n, seed=23)
+    Gh = bx.gemm_host(A, B, C=np.asfortranarray(C0.copy()), alpha=1.25, beta=beta, variant=6)
+    nchunk = min(8, n // 512)
+    cw = ((n + nchunk - 1) // nchunk + 255) // 256 * 256
+    Ad = torch.from_numpy(np.asfortranarray(A)).cuda()
+    for c0 in range(0, n, cw):
+        c1 = min(n, c0 + cw)
+        Bd = torch.from_numpy(np.asfortranarray(B[:, c0:c1])).cuda()
+        Cd = torch.from_numpy(np.asfortranarray(C0[:, c0:c1])).cuda()
+        Gd = bx.gemm(Ad, Bd, C=Cd, alpha=1.25, beta=beta, variant=6).cpu().numpy()
+        assert np.array_equal(Gh[:, c0:c1], Gd), c0
+    cols = np.array([0, 767, 768, 1999, 2599])
+    O = orc.gemm(A, B, C=C0, alpha=1.25, beta=beta, variant=6, cols=cols)
+    C64 = orc.dgemm(A, B, cols=cols) * 1.25 + beta * C0[:, cols].astype(np.float64)
+    eo = orc.normwise_error(O, C64, A, B[:, cols])
+    assert orc.normwise_error(Gh[:, cols], C64, A, B[:, cols]) <= RATIO * eo
+
+
 def test_config2_4096_sampled(orc):
     """configs[1]: 4096^3 bf16x6, U[-1,1], in the launch configuration bench.py times
     (2-CTA persistent).  The oracle computes 24 sampled output columns one by one; the whole
