@@ -376,3 +376,38 @@ def gmres_ir(A, b, variant=3, nb=64, restart=200, inner_tol=1e-10, max_iter=30):
         inner += g["iterations"]
         x = x + g["x"]
     return dict(x=x, converged=converged, iterations=it, inner_iterations=inner, info=0, history=hist)
+
+
+# --------------------------------------------------------------------------
+# O-9: the Fig. 5 SGETRF accuracy measure (§IV-A: "SGETRF vs BFLOAT16x3_6 LU
+# Decomposition: Element errors average improvement ... The comparison points were results
+# from DGETRF on the same input data")
+# --------------------------------------------------------------------------
+def lu_nopivot_f64(M) -> np.ndarray:
+    """Right-looking LU without pivoting in FP64 (the textbook elimination), L unit lower and
+    U packed in one array.  Applied to P A with the pivots of the factorisation under test, it
+    is the FP64 (DGETRF) factorisation that factorisation approximates element by element."""
+    M = np.array(M, dtype=np.float64, copy=True)
+    n = M.shape[0]
+    for j in range(n):
+        M[j + 1:, j] /= M[j, j]
+        M[j + 1:, j + 1:] -= np.outer(M[j + 1:, j], M[j, j + 1:])
+    return M
+
+
+def row_permutation(ipiv) -> np.ndarray:
+    """p such that (P A) = A[p]: the LAPACK interchange sequence applied in order."""
+    ipiv = np.asarray(ipiv)
+    p = np.arange(ipiv.size)
+    for j, q in enumerate(ipiv):
+        p[[j, q]] = p[[q, j]]
+    return p
+
+
+def lu_element_error(A, LU, ipiv) -> float:
+    """Mean over all entries of |LU - D| / |D|, D = FP64 LU of P A with the same pivots (R26)."""
+    A = np.asarray(A, dtype=np.float64)
+    D = lu_nopivot_f64(A[row_permutation(ipiv)])
+    den = np.abs(D)
+    mask = den > 0
+    return float(np.mean(np.abs(np.asarray(LU, dtype=np.float64)[mask] - D[mask]) / den[mask]))
