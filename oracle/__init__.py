@@ -132,7 +132,7 @@ def partials(A, B, cols=None) -> np.ndarray:
 def gemm(A, B, C=None, alpha=1.0, beta=0.0, variant=6, cols=None) -> np.ndarray:
     """Split GEMM C_out = alpha*A*B + beta*C (BLAS scaling R19).
 
-    variant in {1, 3, 6, 8, 9}.  Returns the m x len(cols) FP32 result."""
+    variant in {1, 3, 5, 6, 7, 8, 9}.  Returns the m x len(cols) FP32 result."""
     A = _colmajor_f32(A)
     B = _colmajor_f32(B)
     m, k = A.shape

@@ -207,6 +207,11 @@ int orc_partials(int m, int n, int k, const float *A, int lda, const float *B, i
  *    x8 (Z_3):                            Z0 + (Z1 + (Z2 + Z3))
  *    x9 (all nine, R9, "bins ... added from smallest to largest"):
  *                                                Z0 + (Z1 + (Z2 + (Z3 + Z4)))
+ *    x7 ("computing at least 7 products instead of just 6": x6 plus the
+ *        2^-24-bin term a1*b2 of the worked example, R27):
+ *                                                Z0 + (Z1 + (Z2 + Z^(1,2)))
+ *    x5 (A split in two, B in three: "taking only the a1 b1 and a0 b2 terms
+ *        from the 2^-16 bin", R27):               Z0 + (Z1 + (Z^(0,2) + Z^(1,1)))
  *    1  (single BF16, debug):             Z0
  * all in FP32 round-to-nearest.
  * O-5  C = alpha*Z + beta*C (BLAS, R19): beta == 0 never reads C, the product
@@ -214,7 +219,7 @@ int orc_partials(int m, int n, int k, const float *A, int lda, const float *B, i
  * ------------------------------------------------------------------------ */
 static int variant_pieces(int variant)
 {
-    switch (variant) { case 1: return 1; case 3: return 2; case 6: case 8: case 9: return 3; }
+    switch (variant) { case 1: return 1; case 3: return 2; case 5: case 6: case 7: case 8: case 9: return 3; }
     return 0;
 }
 
@@ -228,7 +233,9 @@ static float combine_bins(int variant, const float Z[3][3])
     switch (variant) {
     case 1: return Z0;
     case 3: return Z0 + Z1;
+    case 5: return Z0 + (Z1 + (Z[0][2] + Z[1][1]));
     case 6: return Z0 + (Z1 + Z2);
+    case 7: return Z0 + (Z1 + (Z2 + Z[1][2]));
     case 8: return Z0 + (Z1 + (Z2 + Z3));
     case 9: return Z0 + (Z1 + (Z2 + (Z3 + Z4)));
     }
@@ -240,7 +247,9 @@ static int product_needed(int variant, int i, int j)
     switch (variant) {
     case 1: return i + j == 0;
     case 3: return i + j <= 1;
+    case 5: return i <= 1 && i + j <= 2;   /* A has pieces 0, 1 only */
     case 6: return i + j <= 2;
+    case 7: return i + j <= 2 || (i == 1 && j == 2);
     case 8: return i + j <= 3;
     case 9: return 1;
     }

@@ -71,6 +71,46 @@ def test_multiply_sets_by_value(orc):
     assert orc.gemm(x, x, variant=6)[0, 0] == 1 + 2 * 2 ** -9 + 3 * 2 ** -18
 
 
+def test_variant_product_sets_by_value(orc):
+    """N2 product sets (reading R27), pinned by value with k = 2 and an exact
+    cancellation of bin 0: x = y = (1 + 2^-9 + 2^-18, -1) . (1 + 2^-9 + 2^-18, 1) has pieces
+    (1, 2^-9, 2^-18) and (-1, 0, 0) / (1, 0, 0), so Z00 = 0 and every other Z^(i,j) is
+    2^-9(i+j) (each a single term), and the result is the sum of the products the variant
+    takes, exactly (all spans <= 24 bits):
+      x3 = 2*2^-9;  x5 = 2*2^-9 + 2*2^-18 (A has no third piece: Z20 absent);
+      x6 = 2*2^-9 + 3*2^-18;  x7 = x6 + 2^-27 (Z12 only);  x8 = x6 + 2*2^-27."""
+    t = 1 + 2 ** -9 + 2 ** -18
+    A = np.array([[t, -1.0]], dtype=np.float32)
+    B = np.array([[t], [1.0]], dtype=np.float32)
+    want = {3: 2 * 2 ** -9, 5: 2 * 2 ** -9 + 2 * 2 ** -18, 6: 2 * 2 ** -9 + 3 * 2 ** -18,
+            7: 2 * 2 ** -9 + 3 * 2 ** -18 + 2 ** -27, 8: 2 * 2 ** -9 + 3 * 2 ** -18 + 2 * 2 ** -27}
+    for v, val in want.items():
+        assert float(orc.gemm(A, B, variant=v)[0, 0]) == val, v
+    # x5's asymmetry: with B = (1 + 2^-9, 1) (pieces 1, 2^-9, 0) only Z11 and Z20 are nonzero
+    # in bin 2; x5 drops Z20 (A's third piece), x6 keeps both
+    B2 = np.array([[1 + 2 ** -9], [1.0]], dtype=np.float32)
+    assert float(orc.gemm(A, B2, variant=5)[0, 0]) == 2 ** -8 + 2 ** -18
+    assert float(orc.gemm(A, B2, variant=6)[0, 0]) == 2 ** -8 + 2 * 2 ** -18
+
+
+def test_x5_x7_identity_closed_forms(orc):
+    """A*I under x5 (A in two pieces) is fl32(a0 + a1) -- the third piece is dropped -- and
+    under x7 it is A exactly; I*B is B exactly under both (B keeps three pieces).  x5 equals
+    x6 bit for bit when A's values carry <= 16 significant bits (a2 == 0)."""
+    rng = np.random.default_rng(5)
+    A = synthetic.uniform(19, 13, seed=int(rng.integers(1 << 30)))
+    I = np.eye(13, dtype=np.float32)
+    a0, a1, _ = (orc.widen(p) for p in orc.split(A))
+    assert np.array_equal(orc.gemm(A, I, variant=5), (a0 + a1).astype(np.float32))
+    assert np.array_equal(orc.gemm(A, I, variant=7), A)
+    B = synthetic.uniform(13, 11, seed=int(rng.integers(1 << 30)))
+    for v in (5, 7):
+        assert np.array_equal(orc.gemm(I, B, variant=v), B)
+    A16 = (a0 + a1).astype(np.float32)                       # exactly two BF16 pieces
+    assert np.all(orc.widen(orc.split(A16)[2]) == 0)
+    assert np.array_equal(orc.gemm(A16, B, variant=5), orc.gemm(A16, B, variant=6))
+
+
 def test_paper_worked_example_xy(orc):
     """P:376 worked example (tests/golden/paper_xy_example.txt): with 6 products the result is
     less accurate than FP32 (the 2^-24-bin term a1*b2 matters); with all 9 products the FP32
@@ -85,7 +125,9 @@ def test_paper_worked_example_xy(orc):
     x6 = float(orc.gemm(A, B, variant=6)[0, 0])
     x9 = float(orc.gemm(A, B, variant=9)[0, 0])
     x8 = float(orc.gemm(A, B, variant=8)[0, 0])
+    x7 = float(orc.gemm(A, B, variant=7)[0, 0])
     assert f32 == float(np.float32(exact))           # one rounding
+    assert abs(x7 - exact) <= abs(f32 - exact)       # "computing at least 7 products"
     assert abs(x6 - exact) > abs(f32 - exact)
     assert abs(x9 - exact) <= abs(f32 - exact)
     assert abs(x8 - exact) <= abs(f32 - exact)
