@@ -83,8 +83,10 @@ int bf16x_split_operands(int m, int n, int k, const float *A, int64_t lda, const
  * FP32 product emulated by BF16 x BF16 -> FP32 tensor-core products (section IV-A):
  *   variant 3: pieces 0-1, products {00,01,10}            ("pair of BF16s")
  *   variant 6: pieces 0-2, products {00,01,10,02,11,20}   (Z_2)
+ *   variant 7: x6 + a1*b2 (the 2^-24-bin term of P:376's example: "at least 7 products"; R27)
  *   variant 8: eight products, bins 0..3 = the paper's Z_3
  *   variant 9: all nine products                          (R9)
+ *   variant 5: A in two pieces, B in three, products {00,01,10,02,11} (R27)
  *   variant 1: b0 only, one product (debug / plain-BF16 peak)
  * Products are accumulated smallest bin first into an FP32 tensor-memory
  * partial that is added, with FP32 round-to-nearest, into a promoted accumulator every
@@ -92,21 +94,22 @@ int bf16x_split_operands(int m, int n, int k, const float *A, int64_t lda, const
  * beta == 0 never reads C; alpha == 0 or k == 0 returns beta*C.
  *   A: m x k, lda >= max(1,m);  B: k x n, ldb >= max(1,k);  C: m x n, ldc >= max(1,m).
  * Runs on the library stream (bf16x_set_stream).  Errors: -1 m, -2 n, -3 k, -6 lda,
- * -8 ldb, -11 ldc, -12 variant (not 1/3/6/8/9); BF16X_ERR_ALLOC if the workspace cannot grow.
+ * -8 ldb, -11 ldc, -12 variant (not 1/3/5/6/7/8/9); BF16X_ERR_ALLOC if the workspace cannot grow.
  * ---------------------------------------------------------------------------------- */
 int bf16x_gemm(int m, int n, int k, float alpha, const float *A, int lda,
                const float *B, int ldb, float beta, float *C, int ldc, int variant);
 
-/* Bytes of caller workspace bf16x_gemm_ex needs: 2 * p * (m + n) * round_up(k, 8). */
+/* Bytes of caller workspace bf16x_gemm_ex needs: 2 * (pA * m + pB * n) * round_up(k, 8), with
+ * (pA, pB) the variant's pieces per operand: x1 (1,1), x3 (2,2), x5 (2,3), others (3,3). */
 size_t bf16x_gemm_workspace_size(int m, int n, int k, int variant);
 
 /* Extended GEMM: explicit stream, caller workspace (NULL = library cache), optional
  * pre-split pieces, optional accumulator carry.
- *   A_pieces : NULL, or the base of p K-major piece planes of A as written by
+ *   A_pieces : NULL, or the base of pA K-major piece planes of A as written by
  *              bf16x_split_t: element (i,l) of piece q at A_pieces[q*a_plane + l + i*ldap],
  *              ldap >= k, ldap % 8 == 0, a_plane % 8 == 0, 16-byte aligned base;
  *              then A may be NULL.
- *   B_pieces : NULL, or the base of p piece planes of B as written by bf16x_split:
+ *   B_pieces : NULL, or the base of pB piece planes of B as written by bf16x_split:
  *              element (l,j) of piece q at B_pieces[q*b_plane + l + j*ldbp], ldbp >= k,
  *              ldbp % 8 == 0, b_plane % 8 == 0; then B may be NULL.
  *   acc_carry: m x n FP32 (ld = ldc) used by BF16X_ACC_IN / BF16X_ACC_OUT.
@@ -188,7 +191,7 @@ int bf16x_gesv_gmres_ir(int n, const float *A, int lda, const double *b, double 
  *   A    : n x n FP32 DEVICE, lda >= max(1,n); overwritten by L (unit, below the diagonal)
  *          and U (on and above)
  *   ipiv : DEVICE int32[n], 0-based: row j was interchanged with row ipiv[j] (in order)
- *   variant : 1, 3, 6, 8 or 9;  nb : panel width (<= 0: 256)
+ *   variant : 1, 3, 5, 6, 7, 8 or 9;  nb : panel width (<= 0: 256)
  *   info : HOST, nullable; 0 or the 1-based column of the first exact zero pivot
  * Synchronous.  Returns BF16X_SUCCESS, BF16X_ERR_SINGULAR (factorisation continued past
  * the zero pivot as LAPACK does only for the remaining columns' interchanges), or -1 n,

@@ -19,7 +19,7 @@ HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "bf16x.h")
 
 SUCCESS, ERR_CUDA, ERR_ALLOC, ERR_ARCH, ERR_SINGULAR, NOT_CONVERGED = 0, 1, 2, 3, 4, 5
 ACC_IN, ACC_OUT = 1, 2
-VARIANTS = (1, 3, 6, 8, 9)
+VARIANTS = (1, 3, 5, 6, 7, 8, 9)
 PIECES = {1: 1, 3: 2, 6: 3, 8: 3, 9: 3}
 
 

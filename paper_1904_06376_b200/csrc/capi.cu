@@ -74,6 +74,8 @@ static void *workspace(size_t bytes, int *rc) {
     return g_ws;
 }
 
+static bool variant_ok(int v) { return v == 1 || v == 3 || v == 5 || v == 6 || v == 7 || v == 8 || v == 9; }
+
 static int gemm_args(int m, int n, int k, int lda, int ldb, int ldc, int variant) {
     if (m < 0) return -1;
     if (n < 0) return -2;
@@ -81,7 +83,7 @@ static int gemm_args(int m, int n, int k, int lda, int ldb, int ldc, int variant
     if (lda < (m > 1 ? m : 1)) return -6;
     if (ldb < (k > 1 ? k : 1)) return -8;
     if (ldc < (m > 1 ? m : 1)) return -11;
-    if (variant != 1 && variant != 3 && variant != 6 && variant != 8 && variant != 9) return -12;
+    if (!variant_ok(variant)) return -12;
     return 0;
 }
 
@@ -94,9 +96,9 @@ int gemm_core(int m, int n, int k, float alpha, const float *A, int lda, const f
     if (m == 0 || n == 0) return BF16X_SUCCESS;
     if ((alpha == 0.f || k == 0) && !(flags & (BF16X_ACC_IN | BF16X_ACC_OUT)))
         return launch_scale(m, n, beta, C, ldc, st);
-    const int p = pieces_of(variant);
+    const int pa = pieces_a(variant), pb = pieces_b(variant);
     const int64_t kp = round_up8(k);
-    const size_t need = 2ull * p * ((Ap ? 0 : (size_t)m) + (Bp ? 0 : (size_t)n)) * (size_t)kp;
+    const size_t need = 2ull * ((Ap ? 0 : (size_t)pa * m) + (Bp ? 0 : (size_t)pb * n)) * (size_t)kp;
     uint8_t *w = nullptr;
     if (need) {
         if (ws) {
@@ -111,10 +113,10 @@ int gemm_core(int m, int n, int k, float alpha, const float *A, int lda, const f
         uint16_t *a = (uint16_t *)w;
         a_plane = (int64_t)m * kp;
         ldap = kp;
-        uint16_t *b = a + p * a_plane;
+        uint16_t *b = a + pa * a_plane;
         b_plane = (int64_t)n * kp;
         ldbp = kp;
-        rc = launch_split_ab(m, n, k, A, lda, a, ldap, a_plane, B, ldb, b, ldbp, b_plane, p, st);
+        rc = launch_split_ab(m, n, k, A, lda, a, ldap, a_plane, B, ldb, b, ldbp, b_plane, pa, pb, st);
         if (rc) return rc;
         Ap = a;
         Bp = b;
@@ -123,17 +125,17 @@ int gemm_core(int m, int n, int k, float alpha, const float *A, int lda, const f
         uint16_t *a = (uint16_t *)w;
         a_plane = (int64_t)m * kp;
         ldap = kp;
-        rc = launch_split(m, k, A, lda, a, p > 1 ? a + a_plane : nullptr, p > 2 ? a + 2 * a_plane : nullptr, ldap,
+        rc = launch_split(m, k, A, lda, a, pa > 1 ? a + a_plane : nullptr, pa > 2 ? a + 2 * a_plane : nullptr, ldap,
                           true, st);
         if (rc) return rc;
         Ap = a;
-        w += 2ull * p * (size_t)a_plane;
+        w += 2ull * pa * (size_t)a_plane;
     }
     if (!Bp) {
         uint16_t *b = (uint16_t *)w;
         b_plane = (int64_t)n * kp;
         ldbp = kp;
-        rc = launch_split(k, n, B, ldb, b, p > 1 ? b + b_plane : nullptr, p > 2 ? b + 2 * b_plane : nullptr, ldbp,
+        rc = launch_split(k, n, B, ldb, b, pb > 1 ? b + b_plane : nullptr, pb > 2 ? b + 2 * b_plane : nullptr, ldbp,
                           false, st);
         if (rc) return rc;
         Bp = b;
@@ -172,8 +174,8 @@ int bf16x_gemm(int m, int n, int k, float alpha, const float *A, int lda, const 
 
 size_t bf16x_gemm_workspace_size(int m, int n, int k, int variant) {
     if (m < 0 || n < 0 || k < 0) return 0;
-    int v = (variant == 1 || variant == 3 || variant == 6 || variant == 8 || variant == 9) ? variant : 9;
-    return 2ull * (size_t)pieces_of(v) * ((size_t)m + (size_t)n) * (size_t)round_up8(k);
+    const int v = variant_ok(variant) ? variant : 9;
+    return 2ull * ((size_t)pieces_a(v) * m + (size_t)pieces_b(v) * n) * (size_t)round_up8(k);
 }
 
 int bf16x_gemm_ex(int m, int n, int k, float alpha, const float *A, int lda, const float *B, int ldb, float beta,
@@ -261,7 +263,7 @@ int bf16x_gemm_host(int m, int n, int k, float alpha, const float *A_host, int l
     if ((rc = ensure(&g_hA, &g_hA_n, (size_t)m * (k > 0 ? k : 1))) ||
         (rc = ensure(&g_hB, &g_hB_n, (size_t)(k > 0 ? k : 1) * n)) || (rc = ensure(&g_hC, &g_hC_n, (size_t)m * n)))
         return rc;
-    const int p = pieces_of(variant);
+    const int p = pieces_a(variant);
     const int64_t kp = round_up8(k);
     // chunk width: a multiple of 256 columns, >= 512, at most kHostChunks chunks
     int nchunk = 1;

@@ -41,18 +41,20 @@ constexpr int kGroupM = 8;            // tile raster: 8 m-tiles per group for L2
 constexpr int kDefaultCtaGroup = 2;   // 2-CTA pairs, 64-k promotion interval
 constexpr int kSmemBudget = 224 * 1024;
 
-__host__ __device__ constexpr int variant_pieces(int v) { return v == 1 ? 1 : (v == 3 ? 2 : 3); }
+// pieces per operand: x1 1; x3 2; x5 A 2, B 3; x6 / x7 / x8 / x9 3
+__host__ __device__ constexpr int variant_pieces_a(int v) { return v == 1 ? 1 : ((v == 3 || v == 5) ? 2 : 3); }
+__host__ __device__ constexpr int variant_pieces_b(int v) { return v == 1 ? 1 : (v == 3 ? 2 : 3); }
 
 template <int CG, int V, int BN>
 struct Cfg {
-    static constexpr int P = variant_pieces(V);
+    static constexpr int PA = variant_pieces_a(V), PB = variant_pieces_b(V);
     static constexpr int TILE_M = kBM * CG;
     static constexpr int BN_LOCAL = BN / CG;          // B rows (output columns) loaded per CTA
     static constexpr int EPI_COLS = BN / 2;           // accumulator columns per epilogue warp
     static constexpr int A_PIECE = kBM * kRowBytes;
     static constexpr int B_PIECE = BN_LOCAL * kRowBytes;
-    static constexpr int A_STAGE = P * A_PIECE;
-    static constexpr int B_STAGE = P * B_PIECE;
+    static constexpr int A_STAGE = PA * A_PIECE;
+    static constexpr int B_STAGE = PB * B_PIECE;
     static constexpr int STAGE = A_STAGE + B_STAGE;
     static constexpr int BAR_BYTES = 256;
     static constexpr int STAGES_RAW = (kSmemBudget - BAR_BYTES - 1024) / STAGE;
@@ -162,9 +164,17 @@ __device__ __forceinline__ void issue_interval(uint32_t d_big, uint32_t d_small,
 #pragma unroll
         for (int h = 0; h < H; ++h) if (h < nh) { mma(1, 2, h); mma(2, 1, h); }           // bin 3: 2^-24
     }
+    if constexpr (V == 7) {   // x7: x6 + the a1*b2 term ("at least 7 products"; R27)
+#pragma unroll
+        for (int h = 0; h < H; ++h) if (h < nh) mma(1, 2, h);
+    }
     if constexpr (V >= 6) {
 #pragma unroll
         for (int h = 0; h < H; ++h) if (h < nh) { mma(0, 2, h); mma(1, 1, h); mma(2, 0, h); }  // bin 2: 2^-16
+    }
+    if constexpr (V == 5) {   // x5: A in two pieces, bin 2 = {02, 11} (R27)
+#pragma unroll
+        for (int h = 0; h < H; ++h) if (h < nh) { mma(0, 2, h); mma(1, 1, h); }
     }
     if constexpr (V >= 3) {
 #pragma unroll
@@ -258,7 +268,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                                 constexpr int HB = Cf::BN_LOCAL / MC;
                                 const uint16_t mask = (uint16_t)((1u << rank) | (1u << (CG + rank)));
 #pragma unroll
-                                for (int q = 0; q < Cf::P; ++q)
+                                for (int q = 0; q < Cf::PB; ++q)
                                     tma_load_3d_2sm_mc(b_dst + q * Cf::B_PIECE + (int)pair * HB * kRowBytes, &tmB,
                                                        &full[stage], kb * kBK, b_row + (int)pair * HB, q, mask);
                             }
@@ -527,7 +537,8 @@ int num_sms() {
     return n;
 }
 
-int pieces_of(int variant) { return variant_pieces(variant); }
+int pieces_a(int variant) { return variant_pieces_a(variant); }
+int pieces_b(int variant) { return variant_pieces_b(variant); }
 int default_cta_group() { return kDefaultCtaGroup; }
 
 template <int CG, int V, int BN, int S, int MC, bool SA = false>
@@ -535,10 +546,10 @@ static int launch_t(const GemmPlan &pl, cudaStream_t st) {
     using Cf = Cfg<CG, V, BN>;
     constexpr int CL = CG * MC;
     CUtensorMap tmA, tmB;
-    int rc = make_piece_map(&tmA, pl.Ap, pl.k, pl.m, pl.ldap, pl.a_plane, Cf::P, kBM);
+    int rc = make_piece_map(&tmA, pl.Ap, pl.k, pl.m, pl.ldap, pl.a_plane, Cf::PA, kBM);
     if (rc) return rc;
-    if (MC == 1) rc = make_piece_map(&tmB, pl.Bp, pl.k, pl.n, pl.ldbp, pl.b_plane, Cf::P, Cf::BN_LOCAL);
-    else rc = make_piece_map(&tmB, pl.Bp, pl.k, pl.n, pl.ldbp, pl.b_plane, Cf::P, Cf::BN_LOCAL / MC, 1);
+    if (MC == 1) rc = make_piece_map(&tmB, pl.Bp, pl.k, pl.n, pl.ldbp, pl.b_plane, Cf::PB, Cf::BN_LOCAL);
+    else rc = make_piece_map(&tmB, pl.Bp, pl.k, pl.n, pl.ldbp, pl.b_plane, Cf::PB, Cf::BN_LOCAL / MC, 1);
     if (rc) return rc;
     KParams kp;
     kp.m = pl.m; kp.n = pl.n; kp.k = pl.k;
@@ -673,7 +684,9 @@ int launch_gemm_pieces(const GemmPlan &pl, cudaStream_t st) {
         switch (pl.variant) {
         case 1: return launch_s<1, 1>(pl, st);
         case 3: return launch_s<1, 3>(pl, st);
+        case 5: return launch_s<1, 5>(pl, st);
         case 6: return launch_s<1, 6>(pl, st);
+        case 7: return launch_s<1, 7>(pl, st);
         case 8: return launch_s<1, 8>(pl, st);
         case 9: return launch_s<1, 9>(pl, st);
         }
@@ -681,7 +694,9 @@ int launch_gemm_pieces(const GemmPlan &pl, cudaStream_t st) {
         switch (pl.variant) {
         case 1: return launch_s<2, 1>(pl, st);
         case 3: return launch_s<2, 3>(pl, st);
+        case 5: return launch_s<2, 5>(pl, st);
         case 6: return launch_s<2, 6>(pl, st);
+        case 7: return launch_s<2, 7>(pl, st);
         case 8: return launch_s<2, 8>(pl, st);
         case 9: return launch_s<2, 9>(pl, st);
         }

@@ -9,7 +9,8 @@ int launch_split(int64_t rows, int64_t cols, const float *X, int64_t ldx, uint16
                  uint16_t *P2, int64_t ldp, bool transpose, cudaStream_t st);
 
 int launch_split_ab(int m, int n, int k, const float *A, int64_t lda, uint16_t *Ap, int64_t ldap, int64_t a_plane,
-                    const float *B, int64_t ldb, uint16_t *Bp, int64_t ldbp, int64_t b_plane, int np, cudaStream_t st);
+                    const float *B, int64_t ldb, uint16_t *Bp, int64_t ldbp, int64_t b_plane, int npa, int npb,
+                    cudaStream_t st);
 
 struct GemmPlan {
     int m, n, k;
@@ -34,7 +35,8 @@ struct GemmPlan {
 
 int launch_gemm_pieces(const GemmPlan &p, cudaStream_t st);
 int launch_scale(int m, int n, float beta, float *C, int ldc, cudaStream_t st);
-int pieces_of(int variant);
+int pieces_a(int variant);   // BF16 pieces of A / B for a variant (x5: 2 / 3)
+int pieces_b(int variant);
 int num_sms();
 int default_cta_group();
 void release_gemm_workspace();

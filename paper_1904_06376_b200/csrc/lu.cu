@@ -1112,7 +1112,8 @@ extern "C" int bf16x_getrf(int n, float *A, int lda, int *ipiv, int variant, int
     if (n > 0 && !A) return -2;
     if (lda < (n > 1 ? n : 1)) return -3;
     if (n > 0 && !ipiv) return -4;
-    if (variant != 1 && variant != 3 && variant != 6 && variant != 8 && variant != 9) return -5;
+    if (variant != 1 && variant != 3 && variant != 5 && variant != 6 && variant != 7 && variant != 8 && variant != 9)
+        return -5;
     if (info) *info = 0;
     int rc = arch_ok();
     if (rc || n == 0) return rc;

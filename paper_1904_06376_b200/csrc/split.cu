@@ -190,15 +190,15 @@ struct SplitArgs {
     uint16_t *P0, *P1, *P2;
     int vec;
 };
-template <int NP>
+template <int NPA, int NPB>
 __global__ void __launch_bounds__(256) split_ab_kernel(SplitArgs a, SplitArgs b, int gA) {
     __shared__ uint32_t s[3][TT][TW];
     asm volatile("griddepcontrol.launch_dependents;");   // let the GEMM's prologue start early
     if ((int)blockIdx.x < gA)
-        split_trans_body<NP>(a.rows, a.cols, a.X, a.ldx, a.P0, a.P1, a.P2, a.ldp, a.vec, blockIdx.x, gA, s);
+        split_trans_body<NPA>(a.rows, a.cols, a.X, a.ldx, a.P0, a.P1, a.P2, a.ldp, a.vec, blockIdx.x, gA, s);
     else
-        split_same_body<NP>(b.rows, b.cols, b.X, b.ldx, b.P0, b.P1, b.P2, b.ldp, b.vec, blockIdx.x - gA,
-                            gridDim.x - gA);
+        split_same_body<NPB>(b.rows, b.cols, b.X, b.ldx, b.P0, b.P1, b.P2, b.ldp, b.vec, blockIdx.x - gA,
+                             gridDim.x - gA);
 }
 
 static int sm_count() {
@@ -243,10 +243,11 @@ int launch_split(int64_t rows, int64_t cols, const float *X, int64_t ldx, uint16
 }
 
 int launch_split_ab(int m, int n, int k, const float *A, int64_t lda, uint16_t *Ap, int64_t ldap, int64_t a_plane,
-                    const float *B, int64_t ldb, uint16_t *Bp, int64_t ldbp, int64_t b_plane, int np, cudaStream_t st) {
+                    const float *B, int64_t ldb, uint16_t *Bp, int64_t ldbp, int64_t b_plane, int npa, int npb,
+                    cudaStream_t st) {
     if (m == 0 || n == 0 || k == 0) return BF16X_SUCCESS;
-    SplitArgs a{m, k, lda, ldap, A, Ap, np > 1 ? Ap + a_plane : nullptr, np > 2 ? Ap + 2 * a_plane : nullptr, 0};
-    SplitArgs b{k, n, ldb, ldbp, B, Bp, np > 1 ? Bp + b_plane : nullptr, np > 2 ? Bp + 2 * b_plane : nullptr, 0};
+    SplitArgs a{m, k, lda, ldap, A, Ap, npa > 1 ? Ap + a_plane : nullptr, npa > 2 ? Ap + 2 * a_plane : nullptr, 0};
+    SplitArgs b{k, n, ldb, ldbp, B, Bp, npb > 1 ? Bp + b_plane : nullptr, npb > 2 ? Bp + 2 * b_plane : nullptr, 0};
     a.vec = ((reinterpret_cast<uintptr_t>(A) & 15u) == 0) && lda % 4 == 0;
     b.vec = ((reinterpret_cast<uintptr_t>(B) & 15u) == 0) && ldb % 4 == 0 &&
             ((reinterpret_cast<uintptr_t>(Bp) & 15u) == 0) && ldbp % 8 == 0 && b_plane % 8 == 0;
@@ -254,9 +255,10 @@ int launch_split_ab(int m, int n, int k, const float *A, int64_t lda, uint16_t *
     const double wa = (double)m * k, wb = (double)k * n;
     int gA = (int)(grid * wa / (wa + wb));
     gA = gA < 1 ? 1 : (gA > grid - 1 ? (int)grid - 1 : gA);
-    if (np == 1) split_ab_kernel<1><<<(unsigned)grid, 256, 0, st>>>(a, b, gA);
-    else if (np == 2) split_ab_kernel<2><<<(unsigned)grid, 256, 0, st>>>(a, b, gA);
-    else split_ab_kernel<3><<<(unsigned)grid, 256, 0, st>>>(a, b, gA);
+    if (npa == 1 && npb == 1) split_ab_kernel<1, 1><<<(unsigned)grid, 256, 0, st>>>(a, b, gA);
+    else if (npa == 2 && npb == 2) split_ab_kernel<2, 2><<<(unsigned)grid, 256, 0, st>>>(a, b, gA);
+    else if (npa == 2 && npb == 3) split_ab_kernel<2, 3><<<(unsigned)grid, 256, 0, st>>>(a, b, gA);
+    else split_ab_kernel<3, 3><<<(unsigned)grid, 256, 0, st>>>(a, b, gA);
     count_launch();
     return check_launch("split_ab");
 }
@@ -298,7 +300,7 @@ extern "C" int bf16x_split_operands(int m, int n, int k, const float *A, int64_t
     if (!Bp || ldbp < (k > 1 ? k : 1) || b_plane < ldbp * (int64_t)n) return -12;
     int ok = arch_ok();
     if (ok) return ok;
-    return launch_split_ab(m, n, k, A, lda, Ap, ldap, a_plane, B, ldb, Bp, ldbp, b_plane, pieces,
+    return launch_split_ab(m, n, k, A, lda, Ap, ldap, a_plane, B, ldb, Bp, ldbp, b_plane, pieces, pieces,
                            (cudaStream_t)stream);
 }
 

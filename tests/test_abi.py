@@ -34,7 +34,7 @@ def test_gemm_argument_errors():
     assert f(4, 4, 4, 1.0, None, 3, None, 4, 0.0, None, 4, 6) == -6
     assert f(4, 4, 4, 1.0, None, 4, None, 3, 0.0, None, 4, 6) == -8
     assert f(4, 4, 4, 1.0, None, 4, None, 4, 0.0, None, 3, 6) == -11
-    assert f(4, 4, 4, 1.0, None, 4, None, 4, 0.0, None, 4, 7) == -12
+    assert f(4, 4, 4, 1.0, None, 4, None, 4, 0.0, None, 4, 4) == -12
     ex = L.bf16x_gemm_ex
     assert ex(4, 4, 4, 1.0, None, 4, None, 4, 0.0, None, 4, 6, 8, None, 0, 0, None, 0, 0, None, None, 0, None) == -13
     assert ex(4, 4, 4, 1.0, None, 4, None, 4, 0.0, None, 4, 6, 0, 16, 3, 32, None, 0, 0, None, None, 0, None) == -14
@@ -58,6 +58,7 @@ def test_workspace_size_formula():
     # 2 bytes * p pieces * (m + n) rows * round_up(k, 8)
     assert bx.workspace_size(100, 50, 33, 6) == 2 * 3 * 150 * 40
     assert bx.workspace_size(100, 50, 33, 3) == 2 * 2 * 150 * 40
+    assert bx.workspace_size(100, 50, 33, 5) == 2 * (2 * 100 + 3 * 50) * 40
 
 
 def test_no_cpu_fallback_without_gpu():

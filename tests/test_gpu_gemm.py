@@ -56,7 +56,7 @@ def _check_ratio(orc, A, B, variant, cg, cols=None):
 
 
 @pytest.mark.parametrize("cg", [1, 2])
-@pytest.mark.parametrize("variant", [3, 6, 9])
+@pytest.mark.parametrize("variant", [3, 5, 6, 7, 9])
 @pytest.mark.parametrize("shape", [(64, 64, 64), (129, 257, 33), (333, 517, 77), (256, 512, 1000), (20, 600, 48),
                                    (700, 300, 200)])
 def test_uniform_shapes(orc, shape, variant, cg, spi, mc):
@@ -102,9 +102,15 @@ def test_exact_pins(orc, cg, spi, mc):
     A = synthetic.wide(300, 40, seed=8)
     I = np.eye(40, dtype=np.float32)
     P = I[:, np.random.default_rng(0).permutation(40)]
-    for v in (6, 8, 9):
+    for v in (6, 7, 8, 9):
         assert np.array_equal(_gpu(A, I, variant=v, cg=cg), A)
         assert np.array_equal(_gpu(A, P, variant=v, cg=cg), A @ P)
+    # x5 keeps A's first two pieces: A*I = a0 + a1 (<= 16 significant bits: exact in FP32);
+    # as the B operand (three pieces) the matrix is reproduced exactly
+    a0, a1, _ = (orc.widen(q) for q in orc.split(A))
+    assert np.array_equal(_gpu(A, I, variant=5, cg=cg), (a0 + a1).astype(np.float32))
+    AT = np.asfortranarray(A.T)
+    assert np.array_equal(_gpu(I, AT, variant=5, cg=cg), AT)
     b0, b1, _ = orc.split(A)
     assert np.array_equal(_gpu(A, I, variant=3, cg=cg), (orc.widen(b0) + orc.widen(b1)).astype(np.float32))
     Ai = synthetic.small_ints(130, 16, seed=3, bound=1000)
