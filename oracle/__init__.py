@@ -59,6 +59,11 @@ def lib() -> ctypes.CDLL:
         L.orc_lu_solve_f64.argtypes = [ctypes.c_int, _vp, ctypes.c_int, _vp, _vp]
         L.orc_residual_f64.argtypes = [ctypes.c_int, _vp, ctypes.c_int, _vp, _vp, _vp]
         L.orc_num_threads.restype = ctypes.c_int
+        L.orc_fp16_round.argtypes = [ctypes.c_float]
+        L.orc_fp16_round.restype = ctypes.c_uint16
+        L.orc_fp16_widen.argtypes = [ctypes.c_uint16]
+        L.orc_fp16_widen.restype = ctypes.c_float
+        L.orc_getrf16.argtypes = [ctypes.c_int, _vp, ctypes.c_int, _vp, ctypes.c_int, ctypes.c_int]
         _lib = L
     return _lib
 
@@ -411,3 +416,60 @@ def lu_element_error(A, LU, ipiv) -> float:
     den = np.abs(D)
     mask = den > 0
     return float(np.mean(np.abs(np.asarray(LU, dtype=np.float64)[mask] - D[mask]) / den[mask]))
+
+
+# --------------------------------------------------------------------------
+# O-10: fully 16-bit LU and its refinement (N4; §IV-B, reading R28)
+# --------------------------------------------------------------------------
+FORMATS = {"fp32": 0, "bf16": 1, "fp16": 2}
+
+
+def fp16_round(x: float) -> int:
+    """IEEE binary16 RNE of one FP32 value -> 16-bit pattern (overflow -> Inf, subnormals kept)."""
+    return int(lib().orc_fp16_round(ctypes.c_float(float(np.float32(x)))))
+
+
+def fp16_widen(h: int) -> float:
+    return float(lib().orc_fp16_widen(ctypes.c_uint16(h)))
+
+
+def getrf16(A, fmt="bf16", pivot=True):
+    """Gaussian elimination with every stored result rounded to the working format.
+    Returns (LU, ipiv, info); LU holds format values (widened to FP32)."""
+    LU = np.array(A, dtype=np.float32, order="F", copy=True)
+    n = LU.shape[0]
+    ipiv = np.zeros(n, dtype=np.int32)
+    info = lib().orc_getrf16(n, _ptr(LU), max(1, n), _ptr(ipiv), FORMATS[fmt], int(bool(pivot)))
+    return LU, ipiv, int(info)
+
+
+def norm2_seq(v) -> float:
+    """||v||_2 as a plain sequential FP64 sum of squares (fixed order, reproducible)."""
+    s = 0.0
+    for t in np.asarray(v, dtype=np.float64):
+        s += float(t) * float(t)
+    return float(np.sqrt(s))
+
+
+def gesv16_ir(A, b, fmt="bf16", pivot=True, tol=None, max_iter=100):
+    """The §IV-B refinement experiment: factor in the working format, then loop
+    { r = b - A x in FP64; x += U^-1 L^-1 P r in FP64 } from x0 = U^-1 L^-1 P b, converged
+    when ||r||_2 <= tol ||b||_2 with tol = cond(A) * 2^-53 ("a residual tolerance of
+    cond(A)*eps"; the caller passes cond(A)*2^-53).  Returns dict(x, converged,
+    iterations = corrections applied, info)."""
+    A = _colmajor_f32(A)
+    n = A.shape[0]
+    b = np.ascontiguousarray(b, dtype=np.float64)
+    LU, ipiv, info = getrf16(A, fmt=fmt, pivot=pivot)
+    if info != 0:
+        return dict(x=np.zeros(n), converged=False, iterations=0, info=info)
+    nb = norm2_seq(b)
+    x = lu_solve_f64(LU, ipiv, b)
+    for it in range(max_iter + 1):
+        r = residual_f64(A, b, x)
+        if norm2_seq(r) <= tol * nb:
+            return dict(x=x, converged=True, iterations=it, info=0)
+        if it == max_iter or not np.all(np.isfinite(x)):
+            break
+        x = x + lu_solve_f64(LU, ipiv, r)
+    return dict(x=x, converged=False, iterations=it, info=0)

@@ -496,3 +496,106 @@ int orc_num_threads(void)
     return 1;
 #endif
 }
+
+/* ------------------------------------------------------------------------ */
+/* O-10  Fully 16-bit LU (N4; §IV-B: "For iterative refinement on
+ * solutions to Ax = b with LU, using lower precision ... comparing FP32, with
+ * FP16 and bfloat16").  Working formats (reading R28):
+ *   fmt 0: FP32 (no extra rounding);
+ *   fmt 1: BF16 = the (B16) operator above (RNE, saturating);
+ *   fmt 2: IEEE binary16 ("reduce the exponent to 5 bits"): 1 sign,
+ *          5 exponent (bias 15), 10 mantissa bits, round to nearest even,
+ *          gradual underflow, overflow to +-Inf.
+ * ------------------------------------------------------------------------ */
+uint16_t orc_fp16_round(float x)
+{
+    uint32_t u = bits_of(x);
+    uint32_t sign = (u >> 16) & 0x8000u;
+    uint32_t exponent = (u >> 23) & 0xFFu;
+    uint32_t mantissa = u & 0x7FFFFFu;
+    if (exponent == 0xFFu) return (uint16_t)(sign | (mantissa ? 0x7E00u : 0x7C00u));
+    /* value = 1.m * 2^(exponent-127); binary16 normal exponents are -14..15 */
+    int e = (int)exponent - 127;
+    uint32_t sig = (exponent ? (mantissa | 0x800000u) : mantissa);   /* 24-bit significand */
+    if (exponent == 0) e = -126;                                      /* FP32 subnormal */
+    /* number of low significand bits to drop so the result has the binary16 ulp:
+       normal: ulp 2^(e-10) -> drop (e - 10) - (e - 23) = 13 bits; below 2^-14 the
+       ulp is fixed at 2^-24 -> drop 13 + (-14 - e) bits */
+    int drop = (e >= -14) ? 13 : 13 + (-14 - e);
+    if (drop > 25) return (uint16_t)sign;                             /* < 2^-25: rounds to 0 */
+    uint32_t kept = sig >> drop;
+    uint32_t rem = sig & ((1u << drop) - 1u), half = 1u << (drop - 1);
+    if (rem > half || (rem == half && (kept & 1u))) kept += 1u;
+    /* kept is the significand in units of the result ulp; rebuild the pattern */
+    uint32_t out;
+    if (e >= -14) {
+        int ee = e;
+        if (kept >= 0x800u) { kept >>= 1; ee += 1; }                  /* carry into the exponent */
+        if (ee > 15) return (uint16_t)(sign | 0x7C00u);               /* overflow */
+        out = ((uint32_t)(ee + 15) << 10) | (kept & 0x3FFu);
+    } else {
+        out = kept;                                                   /* subnormal (or carry to 2^-14) */
+    }
+    return (uint16_t)(sign | out);
+}
+
+float orc_fp16_widen(uint16_t h)
+{
+    uint32_t sign = (uint32_t)(h & 0x8000u) << 16;
+    uint32_t e = (h >> 10) & 0x1Fu, m = h & 0x3FFu;
+    if (e == 0x1Fu) return float_of(sign | 0x7F800000u | (m << 13));
+    if (e == 0) {                                                     /* subnormal: m * 2^-24 */
+        float v = (float)m * 5.9604644775390625e-8f;
+        return sign ? -v : v;
+    }
+    return float_of(sign | ((e - 15 + 127) << 23) | (m << 13));
+}
+
+/* round an FP32 value to the working format and back (exactly representable result) */
+static float work_round(int fmt, float x)
+{
+    if (fmt == 1) return orc_bf16_widen(orc_bf16_round(x));
+    if (fmt == 2) return orc_fp16_widen(orc_fp16_round(x));
+    return x;
+}
+
+/* Unblocked right-looking Gaussian elimination in the working format: the input is
+ * stored in the format, and every stored result -- each multiplier l = a/p and each
+ * updated entry a - l*u (one FP32 product, one FP32 subtraction) -- is rounded to it.
+ * pivot != 0: partial pivoting on the stored values (largest |a|, lowest row on ties);
+ * pivot == 0: no interchanges (ipiv[j] = j).  Returns 0, or j+1 for the first exact
+ * zero pivot. */
+int orc_getrf16(int n, float *A, int lda, int *ipiv, int fmt, int pivot)
+{
+    for (int c = 0; c < n; ++c)
+        for (int i = 0; i < n; ++i) A[i + (int64_t)c * lda] = work_round(fmt, A[i + (int64_t)c * lda]);
+    for (int j = 0; j < n; ++j) {
+        int p = j;
+        if (pivot) {
+            float best = fabsf(A[j + (int64_t)j * lda]);
+            for (int i = j + 1; i < n; ++i) {
+                float v = fabsf(A[i + (int64_t)j * lda]);
+                if (v > best) { best = v; p = i; }
+            }
+        }
+        ipiv[j] = p;
+        if (A[p + (int64_t)j * lda] == 0.0f) return j + 1;
+        if (p != j)
+            for (int c = 0; c < n; ++c) {
+                float t = A[j + (int64_t)c * lda];
+                A[j + (int64_t)c * lda] = A[p + (int64_t)c * lda];
+                A[p + (int64_t)c * lda] = t;
+            }
+        float piv = A[j + (int64_t)j * lda];
+        for (int i = j + 1; i < n; ++i)
+            A[i + (int64_t)j * lda] = work_round(fmt, A[i + (int64_t)j * lda] / piv);
+        for (int c = j + 1; c < n; ++c) {
+            float u = A[j + (int64_t)c * lda];
+            for (int i = j + 1; i < n; ++i) {
+                float prod = A[i + (int64_t)j * lda] * u;
+                A[i + (int64_t)c * lda] = work_round(fmt, A[i + (int64_t)c * lda] - prod);
+            }
+        }
+    }
+    return 0;
+}
