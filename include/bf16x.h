@@ -185,6 +185,30 @@ int bf16x_gesv_gmres_ir(int n, const float *A, int lda, const double *b, double 
                         double *residual_history, bf16x_ir_report *report);
 
 /* ------------------------------------------------------------------------------------
+ * bf16x_gesv16_batched -- the paper's refinement experiment (section IV-B: "100
+ * tests for unsymmetric dense matrices of order 50, setting the condition number and using
+ * a residual tolerance of cond(A)*eps"; N4, reading R28) for a batch of small systems, one
+ * thread block each.  Gaussian elimination in the working `format` with every stored result
+ * rounded to it, then FP64 refinement: x0 = U^-1 L^-1 P b; loop { r = b - A x;
+ * converged if ||r||_2 <= tol[s] * ||b||_2; stop after max_iter corrections or a non-finite
+ * x; x += U^-1 L^-1 P r }.  Bit-identical to the oracle's gesv16_ir.  Asynchronous (stream).
+ *   n        : order, 0..64;  batch : number of systems (>= 0)
+ *   A        : DEVICE FP32, system s at A + s*strideA, column-major with lda >= max(1,n),
+ *              strideA >= lda*n; not modified
+ *   b, x     : DEVICE FP64, system s at b + s*strideb / x + s*stridex (strides >= n)
+ *   format   : 0 FP32, 1 BF16 (the (B16) operator of P:177-179), 2 IEEE binary16
+ *   pivot    : nonzero = partial pivoting on the stored values, 0 = none
+ *   max_iter : corrections allowed (>= 0);  tol : DEVICE FP64[batch] (e.g. cond(A)*2^-53)
+ *   converged, iterations, info : DEVICE int[batch] outputs (info = 1-based column of an
+ *              exact zero pivot, then x = 0 and converged = 0)
+ * Errors: -1 n, -2 batch, -3 NULL pointer, -4 lda, -5 strideA, -7 strideb, -9 stridex,
+ * -10 format, -12 max_iter. */
+int bf16x_gesv16_batched(int n, int batch, const float *A, int lda, int64_t strideA, const double *b,
+                         int64_t strideb, double *x, int64_t stridex, int format, int pivot, int max_iter,
+                         const double *tol, int *converged, int *iterations, int *info,
+                         bf16x_stream_t stream);
+
+/* ------------------------------------------------------------------------------------
  * bf16x_getrf -- the factorisation alone (LAPACK sgetrf semantics, "a SGETRF
  * based on triplets of BF16s and six products"): P A = L U in place, right-looking blocked,
  * FP32 panel + TRSM, trailing updates A22 -= L21 U12 in bf16x_gemm(variant).

@@ -61,6 +61,8 @@ def lib() -> ctypes.CDLL:
         L.bf16x_gesv_gmres_ir.argtypes = [_i, _vp, _i, _vp, _vp, _i, _i, _i, ctypes.c_double, _i, _vp,
                                           ctypes.POINTER(IRReport)]
         L.bf16x_getrf.argtypes = [_i, _vp, _i, _vp, _i, _i, ctypes.POINTER(ctypes.c_int)]
+        L.bf16x_gesv16_batched.argtypes = [_i, _i, _vp, _i, _i64, _vp, _i64, _vp, _i64, _i, _i, _i, _vp, _vp, _vp,
+                                           _vp, _vp]
         L.bf16x_set_stream.argtypes = [_vp]
         L.bf16x_get_stream.restype = _vp
         L.bf16x_status_string.argtypes = [_i]
@@ -309,3 +311,26 @@ def getrf(A, variant: int = 3, nb: int = 256):
     if rc not in (SUCCESS, ERR_SINGULAR):
         _check(rc, "bf16x_getrf")
     return LU, ipiv[:n], int(info.value)
+
+
+FORMATS16 = {"fp32": 0, "bf16": 1, "fp16": 2}
+
+
+def gesv16_batched(A, b, tol, fmt: str = "bf16", pivot: bool = True, max_iter: int = 100, stream=None):
+    """bf16x_gesv16_batched on CUDA tensors: A (batch, n, n) float32 (A[s] is system s, any
+    layout: copied column-major), b (batch, n) float64, tol (batch,) float64.
+    Returns (x (batch, n) float64, converged, iterations, info) as CUDA tensors."""
+    import torch
+    batch, n, _ = A.shape
+    Acm = A.transpose(1, 2).contiguous()            # column-major per system, lda = n
+    b = b.to(torch.float64).contiguous()
+    tol = tol.to(torch.float64).contiguous()
+    x = torch.empty(batch, n, dtype=torch.float64, device=A.device)
+    conv = torch.empty(batch, dtype=torch.int32, device=A.device)
+    its = torch.empty_like(conv)
+    info = torch.empty_like(conv)
+    st = _stream(stream)
+    _check(lib().bf16x_gesv16_batched(n, batch, _ptr(Acm), max(1, n), n * n, _ptr(b), n, _ptr(x), n,
+                                      FORMATS16[fmt], int(bool(pivot)), max_iter, _ptr(tol), _ptr(conv), _ptr(its),
+                                      _ptr(info), st), "bf16x_gesv16_batched")
+    return x, conv, its, info
