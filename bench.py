@@ -230,12 +230,23 @@ def run_ours(args):
     torch.cuda.synchronize()
     launches0 = bx.launch_count()
     with ClockSampler(local) as clk:
+        # timed region: K steps back to back, no event between the launches (an event record
+        # between the split and the PDL-launched GEMM would cost the programmatic overlap)
         t_start.record(st)
         for i in range(args.steps):
-            step(i, evs[i])
+            step(i)
         t_end.record(st)
         torch.cuda.synchronize()
     launches = bx.launch_count() - launches0
+    # per-kernel durations for the roofline: the same K steps with CUDA events around every
+    # launch on the launching stream, after a pause that lets the board's power budget recover
+    # (back-to-back, the second ~60 ms of tensor load runs ~10 % slower on these boards)
+    time.sleep(1.0)
+    if world > 1:
+        dist.barrier()
+    for i in range(args.steps):
+        step(i, evs[i])
+    torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     total_ms = t_start.elapsed_time(t_end)
@@ -297,7 +308,7 @@ def run_ours(args):
         "roofline": {"bound": "tensor", "kernel": kname, "achieved": achieved,
                      "peak": peak_burst, "unit": "TFLOP/s", "frac": achieved / peak_burst, "traffic": traffic,
                      "peak_source": f"{peak_src} bf16 burst (MEASURED_PEAKS.json bf16_tflops)",
-                     "achieved_def": f"{v} products x 2mnk BF16 MMA flops per launch / mean CUDA-event launch time",
+                     "achieved_def": f"{v} products x 2mnk BF16 MMA flops per launch / mean CUDA-event launch time (events around each launch, in a second pass of the same K steps after a 1 s pause)",
                      "frac_of_sustained": achieved / peak_sust},
         "e2e": {"value": e2e_value, "unit": "TFLOPS", "h2d_bytes_per_step": 4 * (m * k + k * n_loc),
                 "d2h_bytes_per_step": 4 * m * n_loc, "steps": e2e_steps,
