@@ -270,3 +270,56 @@ def test_stream_k_schedule(orc, m, n, k, mc):
     # tiles owned entirely by one cluster are bit-identical between the two schedules
     same = torch.isclose(Csk, Cdp, rtol=0, atol=0).float().mean().item()
     assert same > 0.2
+
+
+@pytest.mark.parametrize("variant", [3, 6, 9])
+def test_nan_inf_propagation(orc, variant):
+    """Non-finite inputs propagate as in the oracle (R4: pieces of a non-finite x are
+    (bf16(x), 0, 0), so Inf * 0 in the cross products yields NaN exactly where the oracle's
+    does): the NaN and +-Inf masks of the output match the oracle's element for element and
+    the finite part meets the 2x bar."""
+    A = synthetic.uniform(70, 50, seed=31)
+    B = synthetic.uniform(50, 40, seed=32)
+    A[3, 7] = np.nan
+    A[10, 2] = np.inf
+    A[11, 9] = -np.inf
+    B[4, 5] = np.inf
+    B[6, 20] = np.nan
+    G = _gpu(A, B, variant=variant)
+    O = orc.gemm(A, B, variant=variant)
+    assert np.array_equal(np.isnan(G), np.isnan(O))
+    assert np.array_equal(np.isposinf(G), np.isposinf(O)) and np.array_equal(np.isneginf(G), np.isneginf(O))
+    fin = np.isfinite(O)
+    rows = np.all(fin, axis=1)
+    cols = np.all(fin, axis=0)
+    C64 = orc.dgemm(A[rows][:, :], B[:, cols])
+    eg = orc.normwise_error(G[rows][:, cols], C64, A[rows], B[:, cols])
+    eo = orc.normwise_error(O[rows][:, cols], C64, A[rows], B[:, cols])
+    assert eg <= RATIO * eo
+
+
+@pytest.mark.parametrize("shape", [(1, 1, 1), (1, 1000, 3), (1000, 1, 7), (5, 3, 40000), (2, 300, 1)])
+@pytest.mark.parametrize("variant", [3, 6, 9])
+def test_degenerate_shapes(orc, shape, variant):
+    m, n, k = shape
+    A = synthetic.uniform(m, k, seed=m * 7 + k)
+    B = synthetic.uniform(k, n, seed=n * 5 + k)
+    G = _gpu(A, B, variant=variant)
+    O = orc.gemm(A, B, variant=variant)
+    C64 = orc.dgemm(A, B)
+    eg, eo = orc.normwise_error(G, C64, A, B), orc.normwise_error(O, C64, A, B)
+    assert eg <= RATIO * eo or eg <= 2.0 ** -30, (eg, eo)
+
+
+@pytest.mark.parametrize("e", [-60, -64, -70])
+def test_underflow_range(orc, e):
+    """Inputs scaled by 2^e so the products (and for e <= -64 the results) fall into FP32's
+    subnormal range (section II-F's territory): the tensor core keeps subnormal products (no
+    flush to zero), so the GPU error tracks the oracle's gradual-underflow error."""
+    A = (synthetic.uniform(64, 64, seed=1) * 2.0 ** e).astype(np.float32)
+    B = (synthetic.uniform(64, 64, seed=2) * 2.0 ** e).astype(np.float32)
+    G = _gpu(A, B, variant=6)
+    O = orc.gemm(A, B, variant=6)
+    C64 = orc.dgemm(A, B)
+    assert np.count_nonzero(G) == np.count_nonzero(O)
+    assert orc.normwise_error(G, C64, A, B) <= RATIO * orc.normwise_error(O, C64, A, B)
