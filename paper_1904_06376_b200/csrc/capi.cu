@@ -16,7 +16,7 @@ static std::atomic<uint64_t> g_launches{0};
 static std::mutex g_ws_mu;
 static void *g_ws = nullptr;
 static size_t g_ws_bytes = 0;
-static int g_force_cg = 0, g_force_bn = 0, g_force_spi = 0, g_stream_k = 1, g_multicast = 0, g_split_acc = 0;  // tuning overrides (bf16x_tune; not in the public ABI)
+static int g_force_cg = 0, g_force_bn = 0, g_force_spi = 0, g_stream_k = 1, g_multicast = 0, g_split_acc = 0, g_fused = 0;  // tuning overrides (bf16x_tune; not in the public ABI)
 
 void set_cuda_error(cudaError_t e, const char *where) {
     snprintf(g_err, sizeof(g_err), "%s: %s", where, cudaGetErrorString(e));
@@ -109,7 +109,26 @@ int gemm_core(int m, int n, int k, float alpha, const float *A, int lda, const f
             if (rc) return rc;
         }
     }
-    if (!Ap && !Bp) {   // both operands: one fused launch
+    GemmPlan pl;
+    pl.m = m; pl.n = n; pl.k = k;
+    pl.alpha = alpha; pl.beta = beta;
+    pl.C = C; pl.ldc = ldc;
+    pl.variant = variant; pl.flags = flags;
+    pl.acc = acc;
+    pl.cta_group = cta_group ? cta_group : g_force_cg;
+    pl.max_ctas = 0;
+    pl.tile_n = g_force_bn;
+    pl.stages_per_interval = g_force_spi;
+    pl.stream_k = g_stream_k;
+    pl.multicast = g_multicast;
+    pl.split_acc = g_split_acc;
+    pl.Af = A; pl.Bf = B; pl.lda = lda; pl.ldb = ldb;
+    if (!Ap && !Bp && g_fused) {   // split inside the GEMM when the plan qualifies
+        pl.Ap = nullptr; pl.Bp = nullptr;
+        const int frc = launch_gemm_fused(pl, st);
+        if (frc != -1) return frc;
+    }
+    if (!Ap && !Bp) {   // both operands: one pre-pass launch
         uint16_t *a = (uint16_t *)w;
         a_plane = (int64_t)m * kp;
         ldap = kp;
@@ -140,21 +159,8 @@ int gemm_core(int m, int n, int k, float alpha, const float *A, int lda, const f
         if (rc) return rc;
         Bp = b;
     }
-    GemmPlan pl;
-    pl.m = m; pl.n = n; pl.k = k;
-    pl.alpha = alpha; pl.beta = beta;
-    pl.C = C; pl.ldc = ldc;
-    pl.variant = variant; pl.flags = flags;
     pl.Ap = Ap; pl.ldap = ldap; pl.a_plane = a_plane;
     pl.Bp = Bp; pl.ldbp = ldbp; pl.b_plane = b_plane;
-    pl.acc = acc;
-    pl.cta_group = cta_group ? cta_group : g_force_cg;
-    pl.max_ctas = 0;
-    pl.tile_n = g_force_bn;
-    pl.stages_per_interval = g_force_spi;
-    pl.stream_k = g_stream_k;
-    pl.multicast = g_multicast;
-    pl.split_acc = g_split_acc;
     return launch_gemm_pieces(pl, st);
 }
 
@@ -402,6 +408,7 @@ uint64_t bf16x_launch_count(void) { return g_launches.load(); }
 int bf16x_default_cta_group(void) { return default_cta_group(); }
 void bf16x_stream_k(int on) { g_stream_k = on; }
 void bf16x_split_acc(int on) { g_split_acc = on; }
+void bf16x_fused_split(int on) { g_fused = on; }   // 1: split inside the GEMM when eligible (default 0)
 void bf16x_multicast(int pairs) { g_multicast = pairs; }   // 0 = auto, 1 = off, 2 = on
 void bf16x_tune(int cta_group, int tile_n, int stages_per_interval) {
     g_force_cg = cta_group;

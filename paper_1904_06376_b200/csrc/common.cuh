@@ -54,6 +54,62 @@ __device__ __forceinline__ Split3 split3(float x) {
     return s;
 }
 
+// Hardware fast path of the split for two values below the b0-overflow band (shared by the
+// split pre-pass and the GEMM's in-kernel transform): cvt.rn.bf16x2.f32 is IEEE RNE on two
+// values, the FP32 residual subtractions are exact; anything else takes split3.
+__device__ __forceinline__ uint32_t cvt_bf16x2(float hi, float lo) {
+    uint32_t d;
+    asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(d) : "f"(hi), "f"(lo));
+    return d;
+}
+
+__device__ __forceinline__ bool regular(float x) { return (__float_as_uint(x) & 0x7FFFFFFFu) < 0x7F7F8000u; }
+
+// Fast path only (both values known to be below the b0-overflow band): branch-free, so many
+// pairs' dependency chains interleave.
+template <int NP>
+__device__ __forceinline__ void split_pair_fast(float lo, float hi, uint32_t (&p)[3]) {
+    const uint32_t a = cvt_bf16x2(hi, lo);
+    p[0] = a;
+    if constexpr (NP >= 2) {
+        const float r1lo = __fsub_rn(lo, __uint_as_float(a << 16));
+        const float r1hi = __fsub_rn(hi, __uint_as_float(a & 0xFFFF0000u));
+        const uint32_t b = cvt_bf16x2(r1hi, r1lo);
+        p[1] = b;
+        if constexpr (NP >= 3) {
+            const float r2lo = __fsub_rn(r1lo, __uint_as_float(b << 16));
+            const float r2hi = __fsub_rn(r1hi, __uint_as_float(b & 0xFFFF0000u));
+            p[2] = cvt_bf16x2(r2hi, r2lo);
+        }
+    }
+}
+
+// Split two values; packs piece q of (lo, hi) as (hi << 16) | lo in p[q].
+template <int NP>
+__device__ __forceinline__ void split_pair(float lo, float hi, uint32_t (&p)[3]) {
+    if (regular(lo) && regular(hi)) {
+        const uint32_t a = cvt_bf16x2(hi, lo);
+        p[0] = a;
+        if constexpr (NP >= 2) {
+            const float r1lo = __fsub_rn(lo, __uint_as_float(a << 16));
+            const float r1hi = __fsub_rn(hi, __uint_as_float(a & 0xFFFF0000u));
+            const uint32_t b = cvt_bf16x2(r1hi, r1lo);
+            p[1] = b;
+            if constexpr (NP >= 3) {
+                const float r2lo = __fsub_rn(r1lo, __uint_as_float(b << 16));
+                const float r2hi = __fsub_rn(r1hi, __uint_as_float(b & 0xFFFF0000u));
+                p[2] = cvt_bf16x2(r2hi, r2lo);
+            }
+        }
+    } else {
+        const Split3 a = split3(lo), b = split3(hi);
+        p[0] = a.b0 | (b.b0 << 16);
+        p[1] = a.b1 | (b.b1 << 16);
+        p[2] = a.b2 | (b.b2 << 16);
+    }
+}
+
+
 // ----------------------------------------------------------------------------------
 // PTX wrappers: shared-memory addresses, mbarrier, TMA, tcgen05
 // ----------------------------------------------------------------------------------
@@ -115,6 +171,40 @@ __device__ __forceinline__ void st_release_u32(unsigned int *p, unsigned int v) 
 
 __device__ __forceinline__ void prefetch_tmap(const CUtensorMap *m) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(m)) : "memory");
+}
+
+// explicit shared-space accesses (32-bit shared addresses): keep the transform's loads and
+// stores on the LDS/STS path instead of generic addressing
+__device__ __forceinline__ float lds_f32(uint32_t a) {
+    float v;
+    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ float4 lds_f32x4(uint32_t a) {
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ void sts_u32x4(uint32_t a, uint32_t x, uint32_t y, uint32_t z, uint32_t w) {
+    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(x), "r"(y), "r"(z), "r"(w));
+}
+
+// 2D TMA tile load into this CTA's shared memory, completion counted on `bar` (local).
+__device__ __forceinline__ void tma_load_2d(void *smem_dst, const CUtensorMap *map, uint64_t *bar, int c0, int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(smem_dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+        : "memory");
+}
+// arrive with release semantics at cluster scope on the barrier at the same smem offset in
+// CTA `cta` (publishes this thread's prior shared-memory writes to that CTA's waiters)
+__device__ __forceinline__ void mbar_arrive_release_cluster(uint64_t *bar, uint32_t cta) {
+    asm volatile(
+        "{\n\t.reg .b32 ra;\n\tmapa.shared::cluster.u32 ra, %0, %1;\n\t"
+        "mbarrier.arrive.release.cluster.shared::cluster.b64 _, [ra];\n\t}" ::"r"(smem_u32(bar)),
+        "r"(cta)
+        : "memory");
 }
 
 // 3D TMA tile load into this CTA's shared memory, completion counted on `bar`.

@@ -35,6 +35,9 @@ constexpr int kRowBytes = kBK * 2;    // 64 B rows -> SWIZZLE_64B
 constexpr int kSwizzleAtom = 8 * kRowBytes;  // 8 rows x 64 B: stride between row groups (SBO)
 constexpr int kNumEpiWarps = 8;       // 2 per TMEM lane quadrant, BN/2 columns each
 constexpr int kThreads = (4 + kNumEpiWarps) * 32;
+constexpr int kNumXfWarps = 8;        // fused split: warps 12..19 convert FP32 tiles to pieces
+constexpr int kThreadsFused = kThreads + kNumXfWarps * 32;
+constexpr int kF32Tile = kBM * kBK * 4;   // one FP32 operand tile per CTA per stage (16 KB)
 constexpr int kTmemCols = 512;        // two accumulator buffers at column 0 and 256
 constexpr int kTmemBufStride = 256;
 constexpr int kGroupM = 8;            // tile raster: 8 m-tiles per group for L2 reuse
@@ -62,6 +65,20 @@ struct Cfg {
     static constexpr int SMEM = STAGES * STAGE + BAR_BYTES + 1024;
     static_assert(STAGES >= 2, "need at least two pipeline stages");
     static_assert(BN % (16 * CG) == 0 && BN <= 256 && EPI_COLS % 32 == 0, "invalid tile N");
+};
+
+// Fused-split configuration (2-CTA pairs, tile N 256, one stage per promotion interval): a ring
+// of FSTAGES FP32 stages (TMA destination: A rows x 32 k and B rows x 32 k per CTA) feeding a
+// ring of STAGES piece stages (MMA source), converted by the transform warps.
+template <int V>
+struct CfgF {
+    using Cf = Cfg<2, V, 256>;
+    static constexpr int FSTAGES = 2;
+    static constexpr int F32_STAGE = 2 * kF32Tile;
+    static constexpr int STAGES_RAW = (kSmemBudget - 256 - 1024 - FSTAGES * F32_STAGE) / Cf::STAGE;
+    static constexpr int STAGES = STAGES_RAW > 6 ? 6 : STAGES_RAW;
+    static constexpr int SMEM = STAGES * Cf::STAGE + FSTAGES * F32_STAGE + 256 + 1024;
+    static_assert(STAGES >= 2, "fused split needs two piece stages");
 };
 
 struct KParams {
@@ -186,23 +203,32 @@ __device__ __forceinline__ void issue_interval(uint32_t d_big, uint32_t d_small,
 
 // MC = number of CTA pairs per cluster sharing the B tile (1, or 2: two vertically adjacent
 // 256 x BN tiles; each pair loads half of every B slice and multicasts it to both pairs).
-template <int CG, int V, int BN, int S, int MC, bool SA>
-__global__ void __launch_bounds__(kThreads, 1)
+// FU (fused split): tmA / tmB are FP32 maps of A and B; warp 0 loads FP32 tiles, warps
+// 12..15 convert them into the piece ring (the MMA reads exactly what the pre-pass + TMA path
+// would have placed there), and the piece-ring "full" barrier counts the converters' arrivals.
+template <int CG, int V, int BN, int S, int MC, bool SA, bool FU = false>
+__global__ void __launch_bounds__(FU ? kThreadsFused : kThreads, 1)
     gemm_split_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                       const KParams p) {
     using Cf = Cfg<CG, V, BN>;
+    constexpr int NST = FU ? CfgF<V>::STAGES : Cf::STAGES;     // piece ring stages
+    constexpr int NF = FU ? CfgF<V>::FSTAGES : 0;              // FP32 ring stages
+    static_assert(!FU || (CG == 2 && BN == 256 && S == 1 && MC == 1 && !SA), "fused split: 2-CTA, N 256, S 1");
     constexpr int CL = CG * MC;   // cluster size
     static_assert(MC == 1 || CG == 2, "multicast needs 2-CTA pairs");
     static_assert(!SA || 2 * BN <= kTmemBufStride, "split accumulators need 4 x BN TMEM columns");
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t *sA = smem;
-    uint8_t *sB = smem + Cf::STAGES * Cf::A_STAGE;
-    uint64_t *full = reinterpret_cast<uint64_t *>(smem + Cf::STAGES * Cf::STAGE);
-    uint64_t *empty = full + Cf::STAGES;
-    uint64_t *acc_full = empty + Cf::STAGES;
+    uint8_t *sB = smem + NST * Cf::A_STAGE;
+    uint8_t *f32 = smem + NST * Cf::STAGE;                      // FU: [NF][A tile | B tile]
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem + NST * Cf::STAGE + NF * 2 * kF32Tile);
+    uint64_t *empty = full + NST;
+    uint64_t *acc_full = empty + NST;
     uint64_t *acc_empty = acc_full + 2;
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(acc_empty + 2);
+    uint64_t *f32_full = acc_empty + 2;
+    uint64_t *f32_empty = f32_full + 2;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(f32_empty + 2);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t crank = (CL > 1) ? cluster_ctarank() : 0u;   // rank in the cluster
@@ -214,14 +240,19 @@ __global__ void __launch_bounds__(kThreads, 1)
         prefetch_tmap(&tmB);
     }
     if (warp == 1 && lane == 0) {
-        for (int s = 0; s < Cf::STAGES; ++s) {
-            mbar_init(&full[s], 1);
+        for (int s = 0; s < NST; ++s) {
+            mbar_init(&full[s], FU ? kNumXfWarps * CG : 1);
             mbar_init(&empty[s], MC);     // one commit per pair reading the (shared) stage
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(&acc_full[b], 1);
             mbar_init(&acc_empty[b], kNumEpiWarps * CG);
         }
+        if constexpr (FU)
+            for (int b = 0; b < NF; ++b) {
+                mbar_init(&f32_full[b], 1);
+                mbar_init(&f32_empty[b], kNumXfWarps);
+            }
         fence_barrier_init();
     }
     if (warp == 2) tmem_alloc<CG>(tmem_slot, kTmemCols);
@@ -232,10 +263,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     // Programmatic dependent launch: everything above overlapped the previous kernel's tail;
     // from here on we read its outputs (the pieces) and may overwrite what it read.
     asm volatile("griddepcontrol.wait;" ::: "memory");
+    // FU register split (per warpgroup, at the top of each role): the epilogue warpgroups hold
+    // G (160 registers), producer / MMA and the two transform warpgroups need few (48); the sum
+    // must not exceed the launch allocation (96 x 640), or the increase waits forever
 
     const int cid = blockIdx.x / CL, ncl = gridDim.x / CL;
 
     if (warp < 4) {
+        if constexpr (FU) asm volatile("setmaxnreg.dec.sync.aligned.u32 48;" ::: "memory");
         if (warp == 0) {
             // ------------------------------ TMA producer ------------------------------
             if (lane == 0) {
@@ -250,6 +285,18 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const int a_row = tm * Cf::TILE_M + (int)rank * kBM;
                     const int b_row = tn * BN + (int)rank * Cf::BN_LOCAL;
                     const int kb_end = min(p.nkb, w.i1 * S);
+                    if constexpr (FU) {
+                        // FP32 tiles of this CTA's 128 A rows and 128 B rows, local completion
+                        for (int kb = w.i0 * S; kb < kb_end; ++kb) {
+                            mbar_wait(&f32_empty[stage], phase ^ 1u);
+                            mbar_arrive_expect_tx(&f32_full[stage], 2 * kF32Tile);
+                            uint8_t *dst = f32 + stage * 2 * kF32Tile;
+                            tma_load_2d(dst, &tmA, &f32_full[stage], a_row, kb * kBK);
+                            tma_load_2d(dst + kF32Tile, &tmB, &f32_full[stage], kb * kBK, b_row);
+                            if (++stage == NF) { stage = 0; phase ^= 1u; }
+                        }
+                        continue;
+                    }
                     for (int kb = w.i0 * S; kb < kb_end; ++kb) {
                         mbar_wait(&empty[stage], phase ^ 1u);
                         uint8_t *a_dst = sA + stage * Cf::A_STAGE;
@@ -273,7 +320,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                                                        &full[stage], kb * kBK, b_row + (int)pair * HB, q, mask);
                             }
                         }
-                        if (++stage == Cf::STAGES) { stage = 0; phase ^= 1u; }
+                        if (++stage == NST) { stage = 0; phase ^= 1u; }
                     }
                 }
             }
@@ -300,7 +347,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                                 mbar_wait(&full[stage], phase);
                                 a_desc[q] = smem_desc_kmajor(smem_u32(sA + stage * Cf::A_STAGE), kSwizzleAtom, 4);
                                 b_desc[q] = smem_desc_kmajor(smem_u32(sB + stage * Cf::B_STAGE), kSwizzleAtom, 4);
-                                if (++stage == Cf::STAGES) { stage = 0; phase ^= 1u; }
+                                if (++stage == NST) { stage = 0; phase ^= 1u; }
                             } else {
                                 a_desc[q] = a_desc[0];
                                 b_desc[q] = b_desc[0];
@@ -323,7 +370,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
             }
         }
-    } else {
+    } else if (warp < 4 + kNumEpiWarps) {
+        if constexpr (FU) asm volatile("setmaxnreg.inc.sync.aligned.u32 160;" ::: "memory");
         // ------------------------- promotion + epilogue ---------------------------
         constexpr int EC = Cf::EPI_COLS;
         const int ew = warp - 4;
@@ -429,6 +477,93 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
             }
         }
+    } else if constexpr (FU) {
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 48;" ::: "memory");
+        // ----------------------- fused split: FP32 tiles -> pieces ----------------------
+        // Threads 0..127 of the transform warps convert row t of the A tile ([k][128 rows] FP32,
+        // no swizzle), threads 128..255 row t of the B tile ([128 rows][32 k] FP32, 128-byte
+        // swizzle), 8 values of k at a time, into the K-major piece planes with the 64-byte
+        // swizzle the MMA descriptors expect (16-byte chunk c of row r at chunk
+        // c ^ ((r >> 1) & 3)): exactly the bytes the pre-pass + TMA would have written.
+        const int tx = threadIdx.x - (4 + kNumEpiWarps) * 32;
+        const bool isA = tx < kBM;
+        const int t = isA ? tx : tx - kBM;
+        const uint32_t swz = (uint32_t)((t >> 1) & 3);
+        const uint32_t f32_s = smem_u32(f32), sA_s = smem_u32(sA), sB_s = smem_u32(sB);
+        int fs = 0, ps = 0;
+        uint32_t fph = 0, pph = 0;
+        WorkIter it(p, cid, ncl);
+        Work w;
+        while (it.next(p, w)) {
+            const int kb_end = min(p.nkb, w.i1 * S);
+            for (int kb = w.i0 * S; kb < kb_end; ++kb) {
+                mbar_wait(&f32_full[fs], fph);
+                mbar_wait(&empty[ps], pph ^ 1u);
+                const uint32_t fbase = f32_s + (uint32_t)(fs * 2 * kF32Tile);
+                if (isA) {
+                    const uint32_t fa = fbase + (uint32_t)t * 4u;           // element (t, k) at k*512 + 4t
+                    const uint32_t pa = sA_s + (uint32_t)(ps * Cf::A_STAGE) + (uint32_t)t * kRowBytes;
+#pragma unroll
+                    for (int hh = 0; hh < 4; ++hh) {
+                        float x[8];
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) x[j] = lds_f32(fa + (uint32_t)((hh * 8 + j) * kBM * 4));
+                        uint32_t q[4][3];
+                        bool ok = true;                     // one branch per 8 values
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) ok = ok && regular(x[j]);
+                        if (ok) {
+#pragma unroll
+                            for (int j = 0; j < 4; ++j) split_pair_fast<Cf::PA>(x[2 * j], x[2 * j + 1], q[j]);
+                        } else {
+#pragma unroll
+                            for (int j = 0; j < 4; ++j) split_pair<Cf::PA>(x[2 * j], x[2 * j + 1], q[j]);
+                        }
+#pragma unroll
+                        for (int pc = 0; pc < Cf::PA; ++pc)
+                            sts_u32x4(pa + (uint32_t)(pc * Cf::A_PIECE) + (((uint32_t)hh ^ swz) << 4), q[0][pc], q[1][pc],
+                                      q[2][pc], q[3][pc]);
+                    }
+                } else {
+                    const uint32_t fb = fbase + (uint32_t)kF32Tile + (uint32_t)t * (kBK * 4);
+                    const uint32_t pb = sB_s + (uint32_t)(ps * Cf::B_STAGE) + (uint32_t)t * kRowBytes;
+#pragma unroll
+                    for (int hh = 0; hh < 4; ++hh) {
+                        float x[8];
+#pragma unroll
+                        for (int c2 = 0; c2 < 2; ++c2) {
+                            const uint32_t c = (uint32_t)(hh * 2 + c2);
+                            const float4 v = lds_f32x4(fb + ((c ^ (uint32_t)(t & 7)) << 4));
+                            x[4 * c2] = v.x; x[4 * c2 + 1] = v.y; x[4 * c2 + 2] = v.z; x[4 * c2 + 3] = v.w;
+                        }
+                        uint32_t q[4][3];
+                        bool ok = true;
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) ok = ok && regular(x[j]);
+                        if (ok) {
+#pragma unroll
+                            for (int j = 0; j < 4; ++j) split_pair_fast<Cf::PB>(x[2 * j], x[2 * j + 1], q[j]);
+                        } else {
+#pragma unroll
+                            for (int j = 0; j < 4; ++j) split_pair<Cf::PB>(x[2 * j], x[2 * j + 1], q[j]);
+                        }
+#pragma unroll
+                        for (int pc = 0; pc < Cf::PB; ++pc)
+                            sts_u32x4(pb + (uint32_t)(pc * Cf::B_PIECE) + (((uint32_t)hh ^ swz) << 4), q[0][pc], q[1][pc],
+                                      q[2][pc], q[3][pc]);
+                    }
+                }
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // visible to the tensor core
+                __syncwarp();
+                if (lane == 0) {
+                    mbar_arrive(&f32_empty[fs]);
+                    if (rank == 0) mbar_arrive(&full[ps]);
+                    else mbar_arrive_release_cluster(&full[ps], pair * CG);
+                }
+                if (++fs == NF) { fs = 0; fph ^= 1u; }
+                if (++ps == NST) { ps = 0; pph ^= 1u; }
+            }
+        }
     }
 
     tc_fence_before();
@@ -471,6 +606,22 @@ static int make_piece_map(CUtensorMap *map, const uint16_t *base, int k, int row
     cuuint32_t estr[3] = {1, 1, 1};
     CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<uint16_t *>(base), dims, strides, box, estr,
                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? BF16X_SUCCESS : BF16X_ERR_CUDA;
+}
+
+// 2D map over a column-major FP32 matrix: dims (rows [inner], cols), box (box_rows, box_cols);
+// out-of-range elements read as zero (they become zero pieces).
+static int make_f32_map(CUtensorMap *map, const float *base, int rows, int cols, int64_t ld, int box_rows,
+                        int box_cols, CUtensorMapSwizzle swz) {
+    EncodeTiledFn enc = encode_fn();
+    if (!enc) return BF16X_ERR_CUDA;
+    cuuint64_t dims[2] = {(cuuint64_t)rows, (cuuint64_t)cols};
+    cuuint64_t strides[1] = {(cuuint64_t)ld * 4};
+    cuuint32_t box[2] = {(cuuint32_t)box_rows, (cuuint32_t)box_cols};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(base), dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS ? BF16X_SUCCESS : BF16X_ERR_CUDA;
 }
@@ -541,15 +692,25 @@ int pieces_a(int variant) { return variant_pieces_a(variant); }
 int pieces_b(int variant) { return variant_pieces_b(variant); }
 int default_cta_group() { return kDefaultCtaGroup; }
 
-template <int CG, int V, int BN, int S, int MC, bool SA = false>
+template <int CG, int V, int BN, int S, int MC, bool SA = false, bool FU = false>
 static int launch_t(const GemmPlan &pl, cudaStream_t st) {
     using Cf = Cfg<CG, V, BN>;
     constexpr int CL = CG * MC;
+    constexpr int THREADS = FU ? kThreadsFused : kThreads;
+    constexpr int SMEM = FU ? CfgF<V>::SMEM : Cf::SMEM;
+    auto kern = gemm_split_kernel<CG, V, BN, S, MC, SA, FU>;
     CUtensorMap tmA, tmB;
-    int rc = make_piece_map(&tmA, pl.Ap, pl.k, pl.m, pl.ldap, pl.a_plane, Cf::PA, kBM);
-    if (rc) return rc;
-    if (MC == 1) rc = make_piece_map(&tmB, pl.Bp, pl.k, pl.n, pl.ldbp, pl.b_plane, Cf::PB, Cf::BN_LOCAL);
-    else rc = make_piece_map(&tmB, pl.Bp, pl.k, pl.n, pl.ldbp, pl.b_plane, Cf::PB, Cf::BN_LOCAL / MC, 1);
+    int rc;
+    if constexpr (FU) {
+        rc = make_f32_map(&tmA, pl.Af, pl.m, pl.k, pl.lda, kBM, kBK, CU_TENSOR_MAP_SWIZZLE_NONE);
+        if (rc) return rc;
+        rc = make_f32_map(&tmB, pl.Bf, pl.k, pl.n, pl.ldb, kBK, Cf::BN_LOCAL, CU_TENSOR_MAP_SWIZZLE_128B);
+    } else {
+        rc = make_piece_map(&tmA, pl.Ap, pl.k, pl.m, pl.ldap, pl.a_plane, Cf::PA, kBM);
+        if (rc) return rc;
+        if (MC == 1) rc = make_piece_map(&tmB, pl.Bp, pl.k, pl.n, pl.ldbp, pl.b_plane, Cf::PB, Cf::BN_LOCAL);
+        else rc = make_piece_map(&tmB, pl.Bp, pl.k, pl.n, pl.ldbp, pl.b_plane, Cf::PB, Cf::BN_LOCAL / MC, 1);
+    }
     if (rc) return rc;
     KParams kp;
     kp.m = pl.m; kp.n = pl.n; kp.k = pl.k;
@@ -565,12 +726,11 @@ static int launch_t(const GemmPlan &pl, cudaStream_t st) {
         // clusters of 4 do not tile every GPC: only co-resident clusters may be launched
         static int max_clusters = -1;
         if (max_clusters < 0) {
-            cudaFuncSetAttribute(gemm_split_kernel<CG, V, BN, S, MC, SA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 Cf::SMEM);
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
             cudaLaunchConfig_t qc = {};
             qc.gridDim = dim3(units * CL);
-            qc.blockDim = dim3(kThreads);
-            qc.dynamicSmemBytes = Cf::SMEM;
+            qc.blockDim = dim3(THREADS);
+            qc.dynamicSmemBytes = SMEM;
             cudaLaunchAttribute qa[1];
             qa[0].id = cudaLaunchAttributeClusterDimension;
             qa[0].val.clusterDim.x = CL;
@@ -579,7 +739,7 @@ static int launch_t(const GemmPlan &pl, cudaStream_t st) {
             qc.attrs = qa;
             qc.numAttrs = 1;
             int nclu = 0;
-            if (cudaOccupancyMaxActiveClusters(&nclu, gemm_split_kernel<CG, V, BN, S, MC, SA>, &qc) != cudaSuccess) {
+            if (cudaOccupancyMaxActiveClusters(&nclu, kern, &qc) != cudaSuccess) {
                 cudaGetLastError();
                 nclu = 0;
             }
@@ -609,15 +769,14 @@ static int launch_t(const GemmPlan &pl, cudaStream_t st) {
 
     static bool attr_set = false;  // per template instance
     if (!attr_set) {
-        if (cudaFuncSetAttribute(gemm_split_kernel<CG, V, BN, S, MC, SA>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cf::SMEM) !=
-            cudaSuccess)
+        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM) != cudaSuccess)
             return check_launch("gemm attr");
         attr_set = true;
     }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(kThreads);
-    cfg.dynamicSmemBytes = Cf::SMEM;
+    cfg.blockDim = dim3(THREADS);
+    cfg.dynamicSmemBytes = SMEM;
     cfg.stream = st;
     cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -628,7 +787,7 @@ static int launch_t(const GemmPlan &pl, cudaStream_t st) {
     attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 2;
-    cudaError_t e = cudaLaunchKernelEx(&cfg, gemm_split_kernel<CG, V, BN, S, MC, SA>, tmA, tmB, kp);
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, tmA, tmB, kp);
     if (e != cudaSuccess) {
         set_cuda_error(e, "gemm launch");
         return BF16X_ERR_CUDA;
@@ -675,6 +834,30 @@ static int launch_s(const GemmPlan &pl, cudaStream_t st) {
         }
     }
     return s == 2 ? launch_t<CG, V, 256, 2, 1>(pl, st) : launch_t<CG, V, 256, 1, 1>(pl, st);
+}
+
+// Fused split: 2-CTA pairs, tile N 256, one 32-k stage per promotion interval, FP32 operands
+// read by TMA (16-byte aligned, leading dimensions multiples of 4 floats).  Not used where the
+// pre-split kernel is configured differently on purpose: forced CTA mode 1 / tile N / 2-stage
+// intervals, split accumulators, or the multicast schedule of large outputs.
+int launch_gemm_fused(const GemmPlan &pl, cudaStream_t st) {
+    const int cg = pl.cta_group ? pl.cta_group : kDefaultCtaGroup;
+    const bool aligned = pl.Af && pl.Bf && ((reinterpret_cast<uintptr_t>(pl.Af) | reinterpret_cast<uintptr_t>(pl.Bf)) & 15u) == 0 &&
+                         pl.lda % 4 == 0 && pl.ldb % 4 == 0;
+    const bool mc2 = pl.multicast == 2 || (pl.multicast == 0 && (int64_t)pl.m * pl.n >= 12288LL * 12288LL);
+    if (!aligned || cg != 2 || pl.split_acc || mc2 || (pl.tile_n && pl.tile_n != 256) ||
+        pl.stages_per_interval == 2 || pl.k <= 0)
+        return -1;
+    switch (pl.variant) {
+    case 1: return launch_t<2, 1, 256, 1, 1, false, true>(pl, st);
+    case 3: return launch_t<2, 3, 256, 1, 1, false, true>(pl, st);
+    case 5: return launch_t<2, 5, 256, 1, 1, false, true>(pl, st);
+    case 6: return launch_t<2, 6, 256, 1, 1, false, true>(pl, st);
+    case 7: return launch_t<2, 7, 256, 1, 1, false, true>(pl, st);
+    case 8: return launch_t<2, 8, 256, 1, 1, false, true>(pl, st);
+    case 9: return launch_t<2, 9, 256, 1, 1, false, true>(pl, st);
+    }
+    return -1;
 }
 
 int launch_gemm_pieces(const GemmPlan &pl, cudaStream_t st) {

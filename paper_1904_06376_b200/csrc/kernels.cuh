@@ -31,9 +31,15 @@ struct GemmPlan {
     int stream_k;        // 0 = data-parallel only, else hybrid stream-K for the last waves
     int multicast;       // 2 = two CTA pairs per cluster share B tiles (TMA multicast), else 1
     int split_acc;       // 1 = separate TMEM accumulators for bin 0 and bins >= 1 (tile N 128)
+    // fused split (Ap == Bp == nullptr): the FP32 operands, converted to pieces inside the GEMM
+    const float *Af, *Bf;   // A (m x k, lda), B (k x n, ldb), column-major, 16-byte aligned
+    int64_t lda, ldb;
 };
 
 int launch_gemm_pieces(const GemmPlan &p, cudaStream_t st);
+// The fused-split GEMM for this plan's FP32 operands: BF16X_SUCCESS, or -1 if the plan does not
+// qualify (then the caller splits in a pre-pass and calls launch_gemm_pieces).
+int launch_gemm_fused(const GemmPlan &p, cudaStream_t st);
 int launch_scale(int m, int n, float beta, float *C, int ldc, cudaStream_t st);
 int pieces_a(int variant);   // BF16 pieces of A / B for a variant (x5: 2 / 3)
 int pieces_b(int variant);

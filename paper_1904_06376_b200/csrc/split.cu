@@ -16,39 +16,6 @@
 
 namespace bf16x {
 
-__device__ __forceinline__ uint32_t cvt_bf16x2(float hi, float lo) {
-    uint32_t d;
-    asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(d) : "f"(hi), "f"(lo));
-    return d;
-}
-
-__device__ __forceinline__ bool regular(float x) { return (__float_as_uint(x) & 0x7FFFFFFFu) < 0x7F7F8000u; }
-
-// Split two values; packs piece q of (lo, hi) as (hi << 16) | lo in p[q].
-template <int NP>
-__device__ __forceinline__ void split_pair(float lo, float hi, uint32_t (&p)[3]) {
-    if (regular(lo) && regular(hi)) {
-        const uint32_t a = cvt_bf16x2(hi, lo);
-        p[0] = a;
-        if constexpr (NP >= 2) {
-            const float r1lo = __fsub_rn(lo, __uint_as_float(a << 16));
-            const float r1hi = __fsub_rn(hi, __uint_as_float(a & 0xFFFF0000u));
-            const uint32_t b = cvt_bf16x2(r1hi, r1lo);
-            p[1] = b;
-            if constexpr (NP >= 3) {
-                const float r2lo = __fsub_rn(r1lo, __uint_as_float(b << 16));
-                const float r2hi = __fsub_rn(r1hi, __uint_as_float(b & 0xFFFF0000u));
-                p[2] = cvt_bf16x2(r2hi, r2lo);
-            }
-        }
-    } else {
-        const Split3 a = split3(lo), b = split3(hi);
-        p[0] = a.b0 | (b.b0 << 16);
-        p[1] = a.b1 | (b.b1 << 16);
-        p[2] = a.b2 | (b.b2 << 16);
-    }
-}
-
 // ---------------------------------------------------------------------------------
 // same layout: each thread splits 8 consecutive rows of one column per iteration;
 // 16-byte vector loads/stores when the whole matrix is 16-byte aligned (vec != 0).

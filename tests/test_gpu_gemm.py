@@ -323,3 +323,57 @@ def test_underflow_range(orc, e):
     C64 = orc.dgemm(A, B)
     assert np.count_nonzero(G) == np.count_nonzero(O)
     assert orc.normwise_error(G, C64, A, B) <= RATIO * orc.normwise_error(O, C64, A, B)
+
+
+@pytest.fixture
+def fused_on():
+    L = bx.lib()
+    L.bf16x_fused_split(1)
+    yield L
+    L.bf16x_fused_split(0)
+    L.bf16x_tune(0, 0, 0)
+
+
+@pytest.mark.parametrize("variant", [3, 5, 6, 7, 9])
+@pytest.mark.parametrize("shape", [(256, 256, 64), (300, 700, 333), (1024, 2048, 1000), (130, 260, 37)])
+def test_fused_split_matches_prepass(orc, fused_on, shape, variant):
+    """The opt-in fused split (FP32 tiles converted inside the GEMM by transform warps) places
+    exactly the pre-pass's pieces in shared memory: with the same 32-k promotion interval the
+    two paths are bit-identical, and both meet the oracle bar."""
+    m, n, k = shape
+    A = synthetic.uniform(m, k, seed=m + k)
+    B = synthetic.uniform(k, n, seed=n + 3 * k)
+    L = fused_on
+    L.bf16x_tune(2, 0, 1)
+    L.bf16x_fused_split(1)
+    Gf = _gpu(A, B, variant=variant)
+    L.bf16x_fused_split(0)
+    Gp = _gpu(A, B, variant=variant)
+    assert np.array_equal(Gf, Gp)
+    C64 = orc.dgemm(A, B)
+    eo = orc.normwise_error(orc.gemm(A, B, variant=variant), C64, A, B)
+    assert orc.normwise_error(Gf, C64, A, B) <= RATIO * eo
+
+
+def test_fused_split_nonfinite_and_ragged(orc, fused_on):
+    """Non-finite and overflow-band inputs take the transform's exact slow path (R3, R4); the
+    NaN / Inf masks match the oracle's."""
+    A = synthetic.wide(200, 96, seed=41)
+    B = synthetic.wide(96, 150, seed=42)
+    A[5, 3] = np.nan
+    A[7, 50] = np.inf
+    B[10, 20] = -np.inf
+    fused_on.bf16x_fused_split(1)
+    G = _gpu(A, B, variant=6)
+    O = orc.gemm(A, B, variant=6)
+    assert np.array_equal(np.isnan(G), np.isnan(O))
+    assert np.array_equal(np.isinf(G), np.isinf(O))
+    # overflow band (b0 saturates, R3) and the section II-F / subnormal values: A * I equals the
+    # oracle's (which reproduces A except where the split itself loses bits, P:340-350)
+    Aw = synthetic.uniform(64, 48, seed=43)
+    Aw[1, 2] = np.float32(3.4e38)
+    Aw[3, 4] = np.float32(-3.39e38)
+    Aw[5, 6] = np.float32(1.1938613e-38)
+    Aw[7, 8] = np.float32(2.0 ** -140)
+    I = np.eye(48, dtype=np.float32)
+    assert np.array_equal(_gpu(Aw, I, variant=6), orc.gemm(Aw, I, variant=6))
