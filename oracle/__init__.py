@@ -50,6 +50,11 @@ def lib() -> ctypes.CDLL:
         L.orc_partials.argtypes = [ctypes.c_int] * 3 + [_vp, ctypes.c_int, _vp, ctypes.c_int, _vp, ctypes.c_int, _vp]
         L.orc_gemm_split_cols.argtypes = ([ctypes.c_int] * 3 + [ctypes.c_float, _vp, ctypes.c_int, _vp, ctypes.c_int,
                                           ctypes.c_float, _vp, ctypes.c_int, ctypes.c_int, _vp, ctypes.c_int, _vp])
+        L.orc_split_scaled.argtypes = [ctypes.c_int64, _vp, _vp, _vp, _vp]
+        L.orc_split_scaled_patterns.argtypes = [ctypes.c_uint64, ctypes.c_int64, _vp, _vp, _vp]
+        L.orc_gemm_split_ex_cols.argtypes = ([ctypes.c_int] * 3 + [ctypes.c_float, _vp, ctypes.c_int, _vp, ctypes.c_int,
+                                             ctypes.c_float, _vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, _vp,
+                                             ctypes.c_int, _vp])
         L.orc_gemm_split.argtypes = ([ctypes.c_int] * 3 + [ctypes.c_float, _vp, ctypes.c_int, _vp, ctypes.c_int,
                                      ctypes.c_float, _vp, ctypes.c_int, ctypes.c_int])
         L.orc_sgemm_fma_cols.argtypes = ([ctypes.c_int] * 3 + [ctypes.c_float, _vp, ctypes.c_int, _vp, ctypes.c_int,
@@ -112,6 +117,24 @@ def split_patterns(first: int, count: int):
     return tuple(out)
 
 
+def split_scaled(x) -> tuple[np.ndarray, np.ndarray, np.ndarray]:
+    """N2 scaled split (R29): b0, b1' = (B16)(2^8 (x - b0)), b2' = (B16)(2^8 (2^8 (x - b0) - b1')).
+
+    x = b0 + 2^-8 b1' + 2^-16 b2' for every finite x (pinned in test_oracle_scaled.py)."""
+    x = np.ascontiguousarray(np.asarray(x, dtype=np.float32))
+    flat = x.reshape(-1)
+    out = [np.empty(flat.shape, dtype=np.uint16) for _ in range(3)]
+    lib().orc_split_scaled(flat.size, _ptr(flat), _ptr(out[0]), _ptr(out[1]), _ptr(out[2]))
+    return tuple(o.reshape(x.shape) for o in out)
+
+
+def split_scaled_patterns(first: int, count: int):
+    """Scaled split (R29) of every FP32 bit pattern in [first, first+count)."""
+    out = [np.empty(count, dtype=np.uint16) for _ in range(3)]
+    lib().orc_split_scaled_patterns(first, count, _ptr(out[0]), _ptr(out[1]), _ptr(out[2]))
+    return tuple(out)
+
+
 def widen(p: np.ndarray) -> np.ndarray:
     """Exact BF16 pattern -> FP32 values (bits << 16); plain numpy bit view."""
     return (np.asarray(p, dtype=np.uint16).astype(np.uint32) << 16).view(np.float32)
@@ -134,10 +157,12 @@ def partials(A, B, cols=None) -> np.ndarray:
     return Z.reshape(3, 3, nc, m).transpose(0, 1, 3, 2)
 
 
-def gemm(A, B, C=None, alpha=1.0, beta=0.0, variant=6, cols=None) -> np.ndarray:
+def gemm(A, B, C=None, alpha=1.0, beta=0.0, variant=6, cols=None, scaled=False, fp64_combine=False) -> np.ndarray:
     """Split GEMM C_out = alpha*A*B + beta*C (BLAS scaling R19).
 
-    variant in {1, 3, 5, 6, 7, 8, 9}.  Returns the m x len(cols) FP32 result."""
+    variant in {1, 3, 5, 6, 7, 8, 9}.  scaled: N2 power-of-two scaled pieces (R29);
+    fp64_combine: the paper's "d" variants, bins collected in FP64 and rounded once
+    (R30).  Returns the m x len(cols) FP32 result."""
     A = _colmajor_f32(A)
     B = _colmajor_f32(B)
     m, k = A.shape
@@ -154,8 +179,9 @@ def gemm(A, B, C=None, alpha=1.0, beta=0.0, variant=6, cols=None) -> np.ndarray:
     else:
         Cin = _colmajor_f32(C)
         ldc = max(1, m)
-    rc = lib().orc_gemm_split_cols(m, n, k, float(alpha), _ptr(A), max(1, m), _ptr(B), max(1, k), float(beta),
-                                   _ptr(Cin), ldc, int(variant), _ptr(cols_arr), nc, _ptr(out))
+    mode = (1 if scaled else 0) | (2 if fp64_combine else 0)
+    rc = lib().orc_gemm_split_ex_cols(m, n, k, float(alpha), _ptr(A), max(1, m), _ptr(B), max(1, k), float(beta),
+                                      _ptr(Cin), ldc, int(variant), mode, _ptr(cols_arr), nc, _ptr(out))
     if rc != 0:
         raise ValueError(f"oracle gemm returned {rc}")
     return out

@@ -22,6 +22,12 @@
  *   orc_gemm_split_cols   bins Z^(0..4) P:257-265, Z_2 (x6) P:269-272,
  *                         x3 P:378-380, x9 reading R9 ("smallest to
  *                         largest"), x8 = Z_3 P:274-277; alpha/beta R19
+ *   orc_split_scaled      N2 power-of-two scaled pieces (SURVEY 8(f) N2 on
+ *                         P:344-351; reading R29): b1, b2 stored times 2^8, 2^16
+ *   orc_gemm_split_ex_cols  the split GEMM with options: scaled pieces (R29)
+ *                         and/or the final combine in FP64 ("d", P:420,
+ *                         P:425 caption "collect the final answer with d";
+ *                         reading R30)
  *   orc_sgemm_fma_cols    FP32 FMA reference dot product, §II-C
  *   orc_dgemm_cols        FP64 reference ("DGEMM")
  *   orc_getrf_split       blocked right-looking LU with partial pivoting
@@ -132,22 +138,77 @@ void orc_split_patterns(uint64_t first, int64_t count, uint16_t *b0, uint16_t *b
 }
 
 /* ------------------------------------------------------------------------ */
+/* N2 scaled pieces (reading R29).  P:344-351 (§II-F) explains that the split
+ * loses bits when the pieces b1, b2 fall below the BF16 normal range (exponent
+ * "no smaller than -110").  The scaled split keeps each residual at the
+ * magnitude of x by multiplying it by 2^8 before it is rounded:
+ *    b0  = (B16) a
+ *    s1  = (F32)(a - (F32)b0) * 2^8        (one subtraction, one multiply)
+ *    b1' = (B16) s1
+ *    s2  = (F32)(s1 - (F32)b1') * 2^8
+ *    b2' = (B16) s2
+ * so that a = b0 + 2^-8 b1' + 2^-16 b2' (exactly, for every finite a; pinned
+ * in tests/test_oracle_scaled.py).  Multiplying by 2^8 is exact in FP32 here
+ * (no overflow: |a - b0| <= 2^119).  Non-finite a: (bf16(a), +0, +0) (R4).
+ * ------------------------------------------------------------------------ */
+static void split_scalar_scaled(float a, uint16_t *b0, uint16_t *b1, uint16_t *b2)
+{
+    uint16_t p0 = orc_bf16_round(a);
+    if (!isfinite(a)) { *b0 = p0; *b1 = 0; *b2 = 0; return; }
+    float s1 = (a - orc_bf16_widen(p0)) * 256.0f;
+    uint16_t p1 = orc_bf16_round(s1);
+    float s2 = (s1 - orc_bf16_widen(p1)) * 256.0f;
+    uint16_t p2 = orc_bf16_round(s2);
+    *b0 = p0; *b1 = p1; *b2 = p2;
+}
+
+void orc_split_scaled(int64_t n, const float *x, uint16_t *b0, uint16_t *b1, uint16_t *b2)
+{
+    int64_t i;
+#pragma omp parallel for schedule(static)
+    for (i = 0; i < n; ++i) {
+        uint16_t p0, p1, p2;
+        split_scalar_scaled(x[i], &p0, &p1, &p2);
+        b0[i] = p0;
+        if (b1) b1[i] = p1;
+        if (b2) b2[i] = p2;
+    }
+}
+
+void orc_split_scaled_patterns(uint64_t first, int64_t count, uint16_t *b0, uint16_t *b1, uint16_t *b2)
+{
+    int64_t i;
+#pragma omp parallel for schedule(static)
+    for (i = 0; i < count; ++i) {
+        uint16_t p0, p1, p2;
+        split_scalar_scaled(float_of((uint32_t)(first + (uint64_t)i)), &p0, &p1, &p2);
+        b0[i] = p0; b1[i] = p1; b2[i] = p2;
+    }
+}
+
+/* ------------------------------------------------------------------------ */
 /* Split an FP32 column-major matrix into 3 FP32 planes holding the (exactly
  * widened) BF16 pieces, packed with leading dimension `rows`. */
-static void split_matrix_widened(int rows, int cols, const float *X, int ldx, float *P[3])
+static void split_matrix_widened_opt(int rows, int cols, const float *X, int ldx, float *P[3], int scaled)
 {
     int64_t j;
 #pragma omp parallel for schedule(static)
     for (j = 0; j < cols; ++j) {
         for (int i = 0; i < rows; ++i) {
             uint16_t p0, p1, p2;
-            split_scalar(X[i + j * (int64_t)ldx], &p0, &p1, &p2);
+            if (scaled) split_scalar_scaled(X[i + j * (int64_t)ldx], &p0, &p1, &p2);
+            else split_scalar(X[i + j * (int64_t)ldx], &p0, &p1, &p2);
             int64_t o = i + j * (int64_t)rows;
             P[0][o] = orc_bf16_widen(p0);
             P[1][o] = orc_bf16_widen(p1);
             P[2][o] = orc_bf16_widen(p2);
         }
     }
+}
+
+static void split_matrix_widened(int rows, int cols, const float *X, int ldx, float *P[3])
+{
+    split_matrix_widened_opt(rows, cols, X, ldx, P, 0);
 }
 
 /* ------------------------------------------------------------------------ */
@@ -242,6 +303,65 @@ static float combine_bins(int variant, const float Z[3][3])
     return NAN;
 }
 
+/* N2 scaled pieces (R29): Z'^(i,j) are the partial sums of the scaled pieces,
+ * so bin s is held at 2^(8s) times its unscaled value.  Bins are still added
+ * smallest first, each partial result brought down one bin with
+ * an FP32 multiply by q = 2^-8 (Horner form; exact unless it underflows):
+ *    x6: Z'0 + (Z'1 + Z'2*q)*q,  x9: Z'0 + (Z'1 + (Z'2 + (Z'3 + Z'4*q)*q)*q)*q
+ * When no scaling underflows this equals combine_bins on the unscaled pieces
+ * bit for bit (power-of-two scaling commutes with round-to-nearest). */
+static float combine_bins_scaled(int variant, const float Z[3][3])
+{
+    const float q = 0x1p-8f;
+    float Z0 = Z[0][0];
+    float Z1 = Z[0][1] + Z[1][0];
+    float Z2 = Z[0][2] + (Z[1][1] + Z[2][0]);
+    float Z3 = Z[1][2] + Z[2][1];
+    float Z4 = Z[2][2];
+    switch (variant) {
+    case 1: return Z0;
+    case 3: return Z0 + Z1 * q;
+    case 5: return Z0 + (Z1 + (Z[0][2] + Z[1][1]) * q) * q;
+    case 6: return Z0 + (Z1 + Z2 * q) * q;
+    case 7: return Z0 + (Z1 + (Z2 + Z[1][2] * q) * q) * q;
+    case 8: return Z0 + (Z1 + (Z2 + Z3 * q) * q) * q;
+    case 9: return Z0 + (Z1 + (Z2 + (Z3 + Z4 * q) * q) * q) * q;
+    }
+    return NAN;
+}
+
+/* "d" variants (R30): "the same as the last but adding the final
+ * results together in FP64"; P:425 caption "Optionally, collect the final
+ * answer with d (double precision)".  The FP32 partial sums Z^(i,j) of O-3
+ * are widened (exactly) and every addition of the combine -- inside the bins
+ * and between them, in the order of combine_bins -- is one FP64 operation;
+ * the result is rounded once to FP32.  scaled: the Z' of R29, brought down by
+ * exact FP64 multiplies by 2^-8. */
+static float combine_bins_f64(int variant, const float Zf[3][3], int scaled)
+{
+    const double q = scaled ? 0x1p-8 : 1.0;
+    double Z[3][3];
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) Z[i][j] = (double)Zf[i][j];
+    double Z0 = Z[0][0];
+    double Z1 = Z[0][1] + Z[1][0];
+    double Z2 = Z[0][2] + (Z[1][1] + Z[2][0]);
+    double Z3 = Z[1][2] + Z[2][1];
+    double Z4 = Z[2][2];
+    double r;
+    switch (variant) {
+    case 1: r = Z0; break;
+    case 3: r = Z0 + Z1 * q; break;
+    case 5: r = Z0 + (Z1 + (Z[0][2] + Z[1][1]) * q) * q; break;
+    case 6: r = Z0 + (Z1 + Z2 * q) * q; break;
+    case 7: r = Z0 + (Z1 + (Z2 + Z[1][2] * q) * q) * q; break;
+    case 8: r = Z0 + (Z1 + (Z2 + Z3 * q) * q) * q; break;
+    case 9: r = Z0 + (Z1 + (Z2 + (Z3 + Z4 * q) * q) * q) * q; break;
+    default: return NAN;
+    }
+    return (float)r;
+}
+
 static int product_needed(int variant, int i, int j)
 {
     switch (variant) {
@@ -266,10 +386,13 @@ static float scale_output(float alpha, float z, float beta, float c_old)
  *   C_out (m x ncols, ld m) receives alpha*A*B[:,cols] + beta*C_in[:,cols];
  *   C_in (m x n, ldc) may be NULL when beta == 0.
  * Quick returns (R19): alpha == 0 or k == 0 -> beta*C. */
-int orc_gemm_split_cols(int m, int n, int k, float alpha, const float *A, int lda,
-                        const float *B, int ldb, float beta, const float *C_in, int ldc,
-                        int variant, const int *cols, int ncols, float *C_out)
+/* mode bits: 1 = scaled pieces (R29), 2 = FP64 final combine (R30). */
+int orc_gemm_split_ex_cols(int m, int n, int k, float alpha, const float *A, int lda,
+                           const float *B, int ldb, float beta, const float *C_in, int ldc,
+                           int variant, int mode, const int *cols, int ncols, float *C_out)
 {
+    const int scaled = (mode & 1) != 0, f64 = (mode & 2) != 0;
+    if (mode & ~3) return -13;
     if (variant_pieces(variant) == 0) return -12;
     if (m <= 0 || ncols <= 0) return 0;
     int64_t t;
@@ -288,8 +411,8 @@ int orc_gemm_split_cols(int m, int n, int k, float alpha, const float *A, int ld
         Ap[p] = (float *)malloc(sizeof(float) * (size_t)m * (size_t)k);
         Bp[p] = (float *)malloc(sizeof(float) * (size_t)k * (size_t)n);
     }
-    split_matrix_widened(m, k, A, lda, Ap);
-    split_matrix_widened(k, n, B, ldb, Bp);
+    split_matrix_widened_opt(m, k, A, lda, Ap, scaled);
+    split_matrix_widened_opt(k, n, B, ldb, Bp, scaled);
 #pragma omp parallel
     {
         float *Zcol[3][3];
@@ -310,7 +433,8 @@ int orc_gemm_split_cols(int m, int n, int k, float alpha, const float *A, int ld
                 float Z[3][3];
                 for (int i = 0; i < 3; ++i)
                     for (int j = 0; j < 3; ++j) Z[i][j] = Zcol[i][j][r];
-                float z = combine_bins(variant, Z);
+                float z = f64 ? combine_bins_f64(variant, Z, scaled)
+                              : (scaled ? combine_bins_scaled(variant, Z) : combine_bins(variant, Z));
                 float cold = (beta == 0.0f) ? 0.0f : C_in[r + (int64_t)c * ldc];
                 C_out[r + t * (int64_t)m] = scale_output(alpha, z, beta, cold);
             }
@@ -320,6 +444,14 @@ int orc_gemm_split_cols(int m, int n, int k, float alpha, const float *A, int ld
     }
     for (int p = 0; p < 3; ++p) { free(Ap[p]); free(Bp[p]); }
     return 0;
+}
+
+int orc_gemm_split_cols(int m, int n, int k, float alpha, const float *A, int lda,
+                        const float *B, int ldb, float beta, const float *C_in, int ldc,
+                        int variant, const int *cols, int ncols, float *C_out)
+{
+    return orc_gemm_split_ex_cols(m, n, k, alpha, A, lda, B, ldb, beta, C_in, ldc, variant, 0,
+                                  cols, ncols, C_out);
 }
 
 /* Full split GEMM in place, BLAS sgemm('N','N') semantics. */
