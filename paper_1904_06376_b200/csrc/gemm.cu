@@ -20,563 +20,10 @@
 //     register accumulator G (the B200 form of the paper's FP32-accumulated bins); TMEM
 //     is double buffered so the tensor core fills one buffer while the other drains.
 //     After the last interval: C = fmaf(alpha, G, beta*C) (beta == 0: C is not read).
-#include <algorithm>
-#include <mutex>
-
-#include "common.cuh"
-#include "kernels.cuh"
+#include "gemm_impl.cuh"
 
 namespace bf16x {
 
-constexpr int kBM = 128;              // accumulator lanes (rows) per CTA
-constexpr int kBK = 32;               // k per stage = promotion interval
-constexpr int kUK = 16;               // k per tcgen05.mma kind::f16
-constexpr int kRowBytes = kBK * 2;    // 64 B rows -> SWIZZLE_64B
-constexpr int kSwizzleAtom = 8 * kRowBytes;  // 8 rows x 64 B: stride between row groups (SBO)
-constexpr int kNumEpiWarps = 8;       // 2 per TMEM lane quadrant, BN/2 columns each
-constexpr int kThreads = (4 + kNumEpiWarps) * 32;
-constexpr int kNumXfWarps = 8;        // fused split: warps 12..19 convert FP32 tiles to pieces
-constexpr int kThreadsFused = kThreads + kNumXfWarps * 32;
-constexpr int kF32Tile = kBM * kBK * 4;   // one FP32 operand tile per CTA per stage (16 KB)
-constexpr int kTmemCols = 512;        // two accumulator buffers at column 0 and 256
-constexpr int kTmemBufStride = 256;
-constexpr int kGroupM = 8;            // tile raster: 8 m-tiles per group for L2 reuse
-constexpr int kDefaultCtaGroup = 2;   // 2-CTA pairs, 64-k promotion interval
-constexpr int kSmemBudget = 224 * 1024;
-
-// pieces per operand: x1 1; x3 2; x5 A 2, B 3; x6 / x7 / x8 / x9 3
-__host__ __device__ constexpr int variant_pieces_a(int v) { return v == 1 ? 1 : ((v == 3 || v == 5) ? 2 : 3); }
-__host__ __device__ constexpr int variant_pieces_b(int v) { return v == 1 ? 1 : (v == 3 ? 2 : 3); }
-
-template <int CG, int V, int BN>
-struct Cfg {
-    static constexpr int PA = variant_pieces_a(V), PB = variant_pieces_b(V);
-    static constexpr int TILE_M = kBM * CG;
-    static constexpr int BN_LOCAL = BN / CG;          // B rows (output columns) loaded per CTA
-    static constexpr int EPI_COLS = BN / 2;           // accumulator columns per epilogue warp
-    static constexpr int A_PIECE = kBM * kRowBytes;
-    static constexpr int B_PIECE = BN_LOCAL * kRowBytes;
-    static constexpr int A_STAGE = PA * A_PIECE;
-    static constexpr int B_STAGE = PB * B_PIECE;
-    static constexpr int STAGE = A_STAGE + B_STAGE;
-    static constexpr int BAR_BYTES = 256;
-    static constexpr int STAGES_RAW = (kSmemBudget - BAR_BYTES - 1024) / STAGE;
-    static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
-    static constexpr int SMEM = STAGES * STAGE + BAR_BYTES + 1024;
-    static_assert(STAGES >= 2, "need at least two pipeline stages");
-    static_assert(BN % (16 * CG) == 0 && BN <= 256 && EPI_COLS % 32 == 0, "invalid tile N");
-};
-
-// Fused-split configuration (2-CTA pairs, tile N 256, one stage per promotion interval): a ring
-// of FSTAGES FP32 stages (TMA destination: A rows x 32 k and B rows x 32 k per CTA) feeding a
-// ring of STAGES piece stages (MMA source), converted by the transform warps.
-template <int V>
-struct CfgF {
-    using Cf = Cfg<2, V, 256>;
-    static constexpr int FSTAGES = 2;
-    static constexpr int F32_STAGE = 2 * kF32Tile;
-    static constexpr int STAGES_RAW = (kSmemBudget - 256 - 1024 - FSTAGES * F32_STAGE) / Cf::STAGE;
-    static constexpr int STAGES = STAGES_RAW > 6 ? 6 : STAGES_RAW;
-    static constexpr int SMEM = STAGES * Cf::STAGE + FSTAGES * F32_STAGE + 256 + 1024;
-    static_assert(STAGES >= 2, "fused split needs two piece stages");
-};
-
-struct KParams {
-    int m, n, k;
-    float alpha, beta;
-    float *C;
-    int ldc;
-    unsigned flags;
-    float *acc;
-    int tiles_m, tiles_n, nkb;
-    // schedule: tiles [0, dp_tiles) data-parallel (one cluster per tile); tiles
-    // [dp_tiles, dp_tiles + sk_tiles) stream-K: their sk_tiles * n_int promotion intervals are
-    // split evenly over the clusters; a tile cut in two is finished by the cluster holding its
-    // first intervals ("owner"), which adds the other part's raw FP32 accumulator (sk_ws,
-    // published with sk_flags = epoch) before the epilogue.
-    int dp_tiles, sk_tiles, n_int;
-    float *sk_ws;
-    unsigned int *sk_flags;
-    unsigned int epoch;
-};
-
-struct Work {
-    int tile, i0, i1;      // promotion intervals [i0, i1) of `tile`
-    int role;              // 0 complete tile, 1 owner of a split tile, 2 contributor
-    int sk_slot;           // stream-K tile index (sk workspace slot)
-};
-
-// Identical on every role of a cluster: data-parallel tiles first, then this cluster's
-// contiguous range of stream-K intervals.
-struct WorkIter {
-    int cid, ncl, dp_next, u, u_end;
-    __device__ __forceinline__ WorkIter(const KParams &p, int cid_, int ncl_) : cid(cid_), ncl(ncl_), dp_next(cid_) {
-        const int64_t U = (int64_t)p.sk_tiles * p.n_int;
-        u = (int)(U * cid / ncl);
-        u_end = (int)(U * (cid + 1) / ncl);
-    }
-    __device__ __forceinline__ bool next(const KParams &p, Work &w) {
-        if (dp_next < p.dp_tiles) {
-            w.tile = dp_next;
-            w.i0 = 0;
-            w.i1 = p.n_int;
-            w.role = 0;
-            w.sk_slot = -1;
-            dp_next += ncl;
-            return true;
-        }
-        if (u >= u_end) return false;
-        const int t = u / p.n_int, j0 = u - t * p.n_int;
-        const int j1 = min(p.n_int, j0 + (u_end - u));
-        w.tile = p.dp_tiles + t;
-        w.i0 = j0;
-        w.i1 = j1;
-        w.role = (j0 == 0) ? ((j1 == p.n_int) ? 0 : 1) : 2;
-        w.sk_slot = t;
-        u += j1 - j0;
-        return true;
-    }
-};
-
-__device__ __forceinline__ void tile_coords(int tile, int tiles_m, int tiles_n, int &tm, int &tn) {
-    const int per_group = kGroupM * tiles_n;
-    const int group = tile / per_group;
-    const int first_m = group * kGroupM;
-    const int gm = min(kGroupM, tiles_m - first_m);
-    const int r = tile - group * per_group;
-    tm = first_m + r % gm;
-    tn = r / gm;
-}
-
-// Issue one promotion interval's MMAs, smallest bin first: every band is
-// issued over all K=16 halves of the interval's ns stages (ns <= S) before the next,
-// larger band.  SA = false: one TMEM accumulator for all bands.  SA = true ("split
-// accumulators"): bins >= 1 go to d_small and bin 0 to d_big, so the tensor core's
-// alignment truncation of each MMA step (K3 probe) never cuts the small bins against the
-// bin-0 products; the epilogue combines them as (small + big) in FP32 round-to-nearest.
-// Each accumulator's first MMA of the interval overwrites it.
-template <int CG, int V, int BN, int S, bool SA>
-__device__ __forceinline__ void issue_interval(uint32_t d_big, uint32_t d_small, const uint64_t (&a_desc)[S],
-                                               const uint64_t (&b_desc)[S], int ns, uint32_t idesc) {
-    using Cf = Cfg<CG, V, BN>;
-    constexpr int H = S * (kBK / kUK);     // K=16 halves per interval (max)
-    const int nh = ns * (kBK / kUK);
-    bool first_small = true, first_big = true;
-    // descriptor start-address field is in 16-byte units: piece / K-half offsets add directly
-    auto mma = [&](int i, int j, int h) {
-        const int st = h / (kBK / kUK), kk = h % (kBK / kUK);
-        const uint64_t ad = a_desc[st] + (uint64_t)((i * Cf::A_PIECE + kk * (kUK * 2)) >> 4);
-        const uint64_t bd = b_desc[st] + (uint64_t)((j * Cf::B_PIECE + kk * (kUK * 2)) >> 4);
-        const bool big = SA && (i + j == 0);
-        bool &first = (SA && !big) ? first_small : first_big;
-        umma_bf16_elect<CG>(big || !SA ? d_big : d_small, ad, bd, idesc, first ? 0u : 1u);
-        first = false;
-        if constexpr (!SA) first_small = false;
-    };
-    if constexpr (V == 9) {
-#pragma unroll
-        for (int h = 0; h < H; ++h) if (h < nh) mma(2, 2, h);                              // bin 4: 2^-32
-    }
-    if constexpr (V >= 8) {   // x8 = the paper's Z_3: bins 0..3
-#pragma unroll
-        for (int h = 0; h < H; ++h) if (h < nh) { mma(1, 2, h); mma(2, 1, h); }           // bin 3: 2^-24
-    }
-    if constexpr (V == 7) {   // x7: x6 + the a1*b2 term ("at least 7 products"; R27)
-#pragma unroll
-        for (int h = 0; h < H; ++h) if (h < nh) mma(1, 2, h);
-    }
-    if constexpr (V >= 6) {
-#pragma unroll
-        for (int h = 0; h < H; ++h) if (h < nh) { mma(0, 2, h); mma(1, 1, h); mma(2, 0, h); }  // bin 2: 2^-16
-    }
-    if constexpr (V == 5) {   // x5: A in two pieces, bin 2 = {02, 11} (R27)
-#pragma unroll
-        for (int h = 0; h < H; ++h) if (h < nh) { mma(0, 2, h); mma(1, 1, h); }
-    }
-    if constexpr (V >= 3) {
-#pragma unroll
-        for (int h = 0; h < H; ++h) if (h < nh) { mma(0, 1, h); mma(1, 0, h); }           // bin 1: 2^-8
-    }
-#pragma unroll
-    for (int h = 0; h < H; ++h) if (h < nh) mma(0, 0, h);                                  // bin 0
-}
-
-// MC = number of CTA pairs per cluster sharing the B tile (1, or 2: two vertically adjacent
-// 256 x BN tiles; each pair loads half of every B slice and multicasts it to both pairs).
-// FU (fused split): tmA / tmB are FP32 maps of A and B; warp 0 loads FP32 tiles, warps
-// 12..15 convert them into the piece ring (the MMA reads exactly what the pre-pass + TMA path
-// would have placed there), and the piece-ring "full" barrier counts the converters' arrivals.
-template <int CG, int V, int BN, int S, int MC, bool SA, bool FU = false>
-__global__ void __launch_bounds__(FU ? kThreadsFused : kThreads, 1)
-    gemm_split_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                      const KParams p) {
-    using Cf = Cfg<CG, V, BN>;
-    constexpr int NST = FU ? CfgF<V>::STAGES : Cf::STAGES;     // piece ring stages
-    constexpr int NF = FU ? CfgF<V>::FSTAGES : 0;              // FP32 ring stages
-    static_assert(!FU || (CG == 2 && BN == 256 && S == 1 && MC == 1 && !SA), "fused split: 2-CTA, N 256, S 1");
-    constexpr int CL = CG * MC;   // cluster size
-    static_assert(MC == 1 || CG == 2, "multicast needs 2-CTA pairs");
-    static_assert(!SA || 2 * BN <= kTmemBufStride, "split accumulators need 4 x BN TMEM columns");
-    extern __shared__ uint8_t smem_raw[];
-    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint8_t *sA = smem;
-    uint8_t *sB = smem + NST * Cf::A_STAGE;
-    uint8_t *f32 = smem + NST * Cf::STAGE;                      // FU: [NF][A tile | B tile]
-    uint64_t *full = reinterpret_cast<uint64_t *>(smem + NST * Cf::STAGE + NF * 2 * kF32Tile);
-    uint64_t *empty = full + NST;
-    uint64_t *acc_full = empty + NST;
-    uint64_t *acc_empty = acc_full + 2;
-    uint64_t *f32_full = acc_empty + 2;
-    uint64_t *f32_empty = f32_full + 2;
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(f32_empty + 2);
-
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t crank = (CL > 1) ? cluster_ctarank() : 0u;   // rank in the cluster
-    const uint32_t rank = crank % CG;                            // rank in the CTA pair
-    const uint32_t pair = crank / CG;                            // which pair of the cluster
-
-    if (warp == 0 && lane == 0) {
-        prefetch_tmap(&tmA);
-        prefetch_tmap(&tmB);
-    }
-    if (warp == 1 && lane == 0) {
-        for (int s = 0; s < NST; ++s) {
-            mbar_init(&full[s], FU ? kNumXfWarps * CG : 1);
-            mbar_init(&empty[s], MC);     // one commit per pair reading the (shared) stage
-        }
-        for (int b = 0; b < 2; ++b) {
-            mbar_init(&acc_full[b], 1);
-            mbar_init(&acc_empty[b], kNumEpiWarps * CG);
-        }
-        if constexpr (FU)
-            for (int b = 0; b < NF; ++b) {
-                mbar_init(&f32_full[b], 1);
-                mbar_init(&f32_empty[b], kNumXfWarps);
-            }
-        fence_barrier_init();
-    }
-    if (warp == 2) tmem_alloc<CG>(tmem_slot, kTmemCols);
-    tc_fence_before();
-    if constexpr (CL > 1) cluster_sync(); else __syncthreads();
-    tc_fence_after();
-    const uint32_t tmem_base = *tmem_slot;
-    // Programmatic dependent launch: everything above overlapped the previous kernel's tail;
-    // from here on we read its outputs (the pieces) and may overwrite what it read.
-    asm volatile("griddepcontrol.wait;" ::: "memory");
-    // FU register split (per warpgroup, at the top of each role): the epilogue warpgroups hold
-    // G (160 registers), producer / MMA and the two transform warpgroups need few (48); the sum
-    // must not exceed the launch allocation (96 x 640), or the increase waits forever
-
-    const int cid = blockIdx.x / CL, ncl = gridDim.x / CL;
-
-    if (warp < 4) {
-        if constexpr (FU) asm volatile("setmaxnreg.dec.sync.aligned.u32 48;" ::: "memory");
-        if (warp == 0) {
-            // ------------------------------ TMA producer ------------------------------
-            if (lane == 0) {
-                int stage = 0;
-                uint32_t phase = 0;
-                WorkIter it(p, cid, ncl);
-                Work w;
-                while (it.next(p, w)) {
-                    int tm, tn;
-                    tile_coords(w.tile, p.tiles_m, p.tiles_n, tm, tn);
-                    tm = tm * MC + (int)pair;
-                    const int a_row = tm * Cf::TILE_M + (int)rank * kBM;
-                    const int b_row = tn * BN + (int)rank * Cf::BN_LOCAL;
-                    const int kb_end = min(p.nkb, w.i1 * S);
-                    if constexpr (FU) {
-                        // FP32 tiles of this CTA's 128 A rows and 128 B rows, local completion
-                        for (int kb = w.i0 * S; kb < kb_end; ++kb) {
-                            mbar_wait(&f32_empty[stage], phase ^ 1u);
-                            mbar_arrive_expect_tx(&f32_full[stage], 2 * kF32Tile);
-                            uint8_t *dst = f32 + stage * 2 * kF32Tile;
-                            tma_load_2d(dst, &tmA, &f32_full[stage], a_row, kb * kBK);
-                            tma_load_2d(dst + kF32Tile, &tmB, &f32_full[stage], kb * kBK, b_row);
-                            if (++stage == NF) { stage = 0; phase ^= 1u; }
-                        }
-                        continue;
-                    }
-                    for (int kb = w.i0 * S; kb < kb_end; ++kb) {
-                        mbar_wait(&empty[stage], phase ^ 1u);
-                        uint8_t *a_dst = sA + stage * Cf::A_STAGE;
-                        uint8_t *b_dst = sB + stage * Cf::B_STAGE;
-                        if constexpr (CG == 1) {
-                            mbar_arrive_expect_tx(&full[stage], Cf::STAGE);
-                            tma_load_3d(a_dst, &tmA, &full[stage], kb * kBK, a_row, 0);
-                            tma_load_3d(b_dst, &tmB, &full[stage], kb * kBK, b_row, 0);
-                        } else {
-                            if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * Cf::STAGE);
-                            tma_load_3d_2sm(a_dst, &tmA, &full[stage], kb * kBK, a_row, 0);
-                            if constexpr (MC == 1) {
-                                tma_load_3d_2sm(b_dst, &tmB, &full[stage], kb * kBK, b_row, 0);
-                            } else {
-                                // this pair's half of the B slice, piece by piece, to both pairs
-                                constexpr int HB = Cf::BN_LOCAL / MC;
-                                const uint16_t mask = (uint16_t)((1u << rank) | (1u << (CG + rank)));
-#pragma unroll
-                                for (int q = 0; q < Cf::PB; ++q)
-                                    tma_load_3d_2sm_mc(b_dst + q * Cf::B_PIECE + (int)pair * HB * kRowBytes, &tmB,
-                                                       &full[stage], kb * kBK, b_row + (int)pair * HB, q, mask);
-                            }
-                        }
-                        if (++stage == NST) { stage = 0; phase ^= 1u; }
-                    }
-                }
-            }
-        } else if (warp == 1) {
-            // ------------------------------ MMA issuer --------------------------------
-            if (rank == 0) {   // warp-uniform loop; one elected lane issues (umma_*_elect)
-                const uint32_t idesc = idesc_bf16_f32(kBM * CG, BN);
-                int stage = 0;
-                uint32_t phase = 0, acc_it = 0;
-                WorkIter it(p, cid, ncl);
-                Work w;
-                while (it.next(p, w)) {
-                    const int kb_end = min(p.nkb, w.i1 * S);
-                    for (int kb = w.i0 * S; kb < kb_end; kb += S, ++acc_it) {
-                        const int ns = min(S, kb_end - kb);
-                        const uint32_t buf = acc_it & 1u, apar = (acc_it >> 1) & 1u;
-                        mbar_wait(&acc_empty[buf], apar ^ 1u);
-                        uint64_t a_desc[S], b_desc[S];
-                        int stages[S];
-#pragma unroll
-                        for (int q = 0; q < S; ++q) {
-                            stages[q] = stage;
-                            if (q < ns) {
-                                mbar_wait(&full[stage], phase);
-                                a_desc[q] = smem_desc_kmajor(smem_u32(sA + stage * Cf::A_STAGE), kSwizzleAtom, 4);
-                                b_desc[q] = smem_desc_kmajor(smem_u32(sB + stage * Cf::B_STAGE), kSwizzleAtom, 4);
-                                if (++stage == NST) { stage = 0; phase ^= 1u; }
-                            } else {
-                                a_desc[q] = a_desc[0];
-                                b_desc[q] = b_desc[0];
-                            }
-                        }
-                        tc_fence_after();
-                        // buffer layout: SA -> small at buf*BN, big at 256 + buf*BN; else one at buf*256
-                        const uint32_t d_big = SA ? tmem_base + kTmemBufStride + buf * BN : tmem_base + buf * kTmemBufStride;
-                        const uint32_t d_small = SA ? tmem_base + buf * BN : d_big;
-                        issue_interval<CG, V, BN, S, SA>(d_big, d_small, a_desc, b_desc, ns, idesc);
-#pragma unroll
-                        for (int q = 0; q < S; ++q)
-                            if (q < ns) {
-                                if constexpr (MC == 1) umma_commit_elect<CG>(&empty[stages[q]]);
-                                else umma_commit2_mask_elect(&empty[stages[q]], (uint16_t)((1u << CL) - 1));
-                            }
-                        if constexpr (MC == 1) umma_commit_elect<CG>(&acc_full[buf]);
-                        else umma_commit2_mask_elect(&acc_full[buf], (uint16_t)(3u << (CG * pair)));
-                    }
-                }
-            }
-        }
-    } else if (warp < 4 + kNumEpiWarps) {
-        if constexpr (FU) asm volatile("setmaxnreg.inc.sync.aligned.u32 160;" ::: "memory");
-        // ------------------------- promotion + epilogue ---------------------------
-        constexpr int EC = Cf::EPI_COLS;
-        const int ew = warp - 4;
-        const int quad = warp & 3;                // TMEM lane quadrant this warp may access
-        const int half = ew >> 2;                 // which half of the accumulator columns
-        const uint32_t tm_lane = tmem_base + ((uint32_t)(quad * 32) << 16) + half * EC;
-        uint32_t acc_it = 0;
-        WorkIter it(p, cid, ncl);
-        Work w;
-        while (it.next(p, w)) {
-            int tm, tn;
-            tile_coords(w.tile, p.tiles_m, p.tiles_n, tm, tn);
-            tm = tm * MC + (int)pair;
-            const int row = tm * Cf::TILE_M + (int)rank * kBM + quad * 32 + lane;
-            const int col0 = tn * BN + half * EC;
-            float G[EC];
-            if ((p.flags & BF16X_ACC_IN) && w.i0 == 0) {
-#pragma unroll
-                for (int j = 0; j < EC; ++j)
-                    G[j] = (row < p.m && col0 + j < p.n) ? p.acc[(int64_t)(col0 + j) * p.ldc + row] : 0.f;
-            } else {
-#pragma unroll
-                for (int j = 0; j < EC; ++j) G[j] = 0.f;
-            }
-            const int kb_end = min(p.nkb, w.i1 * S);
-            for (int kb = w.i0 * S; kb < kb_end; kb += S, ++acc_it) {
-                const uint32_t buf = acc_it & 1u, apar = (acc_it >> 1) & 1u;
-                mbar_wait(&acc_full[buf], apar);
-                tc_fence_after();
-                if constexpr (!SA) {
-                    const uint32_t taddr = tm_lane + buf * kTmemBufStride;
-#pragma unroll
-                    for (int c = 0; c < EC / 16; ++c) {
-                        float v[16];
-                        tmem_ld16(taddr + c * 16, v);
-                        tmem_ld_wait();
-#pragma unroll
-                        for (int j = 0; j < 16; ++j) G[c * 16 + j] = __fadd_rn(G[c * 16 + j], v[j]);
-                    }
-                } else {
-                    // interval total = small bins + bin 0 (RN), then into G (RN)
-                    const uint32_t ts = tm_lane + buf * BN, tb = tm_lane + kTmemBufStride + buf * BN;
-#pragma unroll
-                    for (int c = 0; c < EC / 16; ++c) {
-                        float vs[16], vb[16];
-                        tmem_ld16(ts + c * 16, vs);
-                        tmem_ld16(tb + c * 16, vb);
-                        tmem_ld_wait();
-#pragma unroll
-                        for (int j = 0; j < 16; ++j) G[c * 16 + j] = __fadd_rn(G[c * 16 + j], __fadd_rn(vs[j], vb[j]));
-                    }
-                }
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) {
-                    if (CG == 1 || rank == 0) mbar_arrive(&acc_empty[buf]);
-                    else mbar_arrive_cluster(&acc_empty[buf], pair * CG);
-                }
-            }
-            if (w.role != 0) {
-                // stream-K fix-up: slot layout [sk tile][cta rank][column 0..BN)[row 0..127]
-                float *slot = p.sk_ws + ((size_t)w.sk_slot * CL + crank) * (size_t)BN * kBM;
-                const int lrow = quad * 32 + lane;
-                unsigned int *flag = p.sk_flags + (size_t)w.sk_slot * CL + crank;
-                if (w.role == 2) {
-#pragma unroll
-                    for (int j = 0; j < EC; ++j) __stcg(slot + (size_t)(half * EC + j) * kBM + lrow, G[j]);
-                    __threadfence();
-                    asm volatile("bar.sync 1, %0;" ::"n"(kNumEpiWarps * 32));
-                    if (ew == 0 && lane == 0) st_release_u32(flag, p.epoch);
-                    continue;
-                }
-                if (lane == 0)
-                    while (ld_acquire_u32(flag) != p.epoch) __nanosleep(64);
-                __syncwarp();
-#pragma unroll
-                for (int j = 0; j < EC; ++j) G[j] = __fadd_rn(G[j], __ldcg(slot + (size_t)(half * EC + j) * kBM + lrow));
-            }
-            if (row < p.m) {
-                float *crow = p.C + row;
-                if (p.flags & BF16X_ACC_OUT) {
-#pragma unroll
-                    for (int j = 0; j < EC; ++j)
-                        if (col0 + j < p.n) p.acc[(int64_t)(col0 + j) * p.ldc + row] = G[j];
-                } else if (p.beta == 0.f) {
-#pragma unroll
-                    for (int j = 0; j < EC; ++j)
-                        if (col0 + j < p.n) __stcs(crow + (int64_t)(col0 + j) * p.ldc, fmaf(p.alpha, G[j], 0.f));
-                } else {
-                    // beta != 0: batch 8 independent loads of C before the FMAs and stores, so
-                    // the old values stream in parallel instead of one round trip per column
-#pragma unroll
-                    for (int j0 = 0; j0 < EC; j0 += 8) {
-                        float cold[8];
-#pragma unroll
-                        for (int j = 0; j < 8; ++j)
-                            cold[j] = (col0 + j0 + j < p.n) ? __ldcs(crow + (int64_t)(col0 + j0 + j) * p.ldc) : 0.f;
-#pragma unroll
-                        for (int j = 0; j < 8; ++j)
-                            if (col0 + j0 + j < p.n)
-                                __stcs(crow + (int64_t)(col0 + j0 + j) * p.ldc, fmaf(p.alpha, G[j0 + j], p.beta * cold[j]));
-                    }
-                }
-            }
-        }
-    } else if constexpr (FU) {
-        asm volatile("setmaxnreg.dec.sync.aligned.u32 48;" ::: "memory");
-        // ----------------------- fused split: FP32 tiles -> pieces ----------------------
-        // Threads 0..127 of the transform warps convert row t of the A tile ([k][128 rows] FP32,
-        // no swizzle), threads 128..255 row t of the B tile ([128 rows][32 k] FP32, 128-byte
-        // swizzle), 8 values of k at a time, into the K-major piece planes with the 64-byte
-        // swizzle the MMA descriptors expect (16-byte chunk c of row r at chunk
-        // c ^ ((r >> 1) & 3)): exactly the bytes the pre-pass + TMA would have written.
-        const int tx = threadIdx.x - (4 + kNumEpiWarps) * 32;
-        const bool isA = tx < kBM;
-        const int t = isA ? tx : tx - kBM;
-        const uint32_t swz = (uint32_t)((t >> 1) & 3);
-        const uint32_t f32_s = smem_u32(f32), sA_s = smem_u32(sA), sB_s = smem_u32(sB);
-        int fs = 0, ps = 0;
-        uint32_t fph = 0, pph = 0;
-        WorkIter it(p, cid, ncl);
-        Work w;
-        while (it.next(p, w)) {
-            const int kb_end = min(p.nkb, w.i1 * S);
-            for (int kb = w.i0 * S; kb < kb_end; ++kb) {
-                mbar_wait(&f32_full[fs], fph);
-                mbar_wait(&empty[ps], pph ^ 1u);
-                const uint32_t fbase = f32_s + (uint32_t)(fs * 2 * kF32Tile);
-                if (isA) {
-                    const uint32_t fa = fbase + (uint32_t)t * 4u;           // element (t, k) at k*512 + 4t
-                    const uint32_t pa = sA_s + (uint32_t)(ps * Cf::A_STAGE) + (uint32_t)t * kRowBytes;
-#pragma unroll
-                    for (int hh = 0; hh < 4; ++hh) {
-                        float x[8];
-#pragma unroll
-                        for (int j = 0; j < 8; ++j) x[j] = lds_f32(fa + (uint32_t)((hh * 8 + j) * kBM * 4));
-                        uint32_t q[4][3];
-                        bool ok = true;                     // one branch per 8 values
-#pragma unroll
-                        for (int j = 0; j < 8; ++j) ok = ok && regular(x[j]);
-                        if (ok) {
-#pragma unroll
-                            for (int j = 0; j < 4; ++j) split_pair_fast<Cf::PA>(x[2 * j], x[2 * j + 1], q[j]);
-                        } else {
-#pragma unroll
-                            for (int j = 0; j < 4; ++j) split_pair<Cf::PA>(x[2 * j], x[2 * j + 1], q[j]);
-                        }
-#pragma unroll
-                        for (int pc = 0; pc < Cf::PA; ++pc)
-                            sts_u32x4(pa + (uint32_t)(pc * Cf::A_PIECE) + (((uint32_t)hh ^ swz) << 4), q[0][pc], q[1][pc],
-                                      q[2][pc], q[3][pc]);
-                    }
-                } else {
-                    const uint32_t fb = fbase + (uint32_t)kF32Tile + (uint32_t)t * (kBK * 4);
-                    const uint32_t pb = sB_s + (uint32_t)(ps * Cf::B_STAGE) + (uint32_t)t * kRowBytes;
-#pragma unroll
-                    for (int hh = 0; hh < 4; ++hh) {
-                        float x[8];
-#pragma unroll
-                        for (int c2 = 0; c2 < 2; ++c2) {
-                            const uint32_t c = (uint32_t)(hh * 2 + c2);
-                            const float4 v = lds_f32x4(fb + ((c ^ (uint32_t)(t & 7)) << 4));
-                            x[4 * c2] = v.x; x[4 * c2 + 1] = v.y; x[4 * c2 + 2] = v.z; x[4 * c2 + 3] = v.w;
-                        }
-                        uint32_t q[4][3];
-                        bool ok = true;
-#pragma unroll
-                        for (int j = 0; j < 8; ++j) ok = ok && regular(x[j]);
-                        if (ok) {
-#pragma unroll
-                            for (int j = 0; j < 4; ++j) split_pair_fast<Cf::PB>(x[2 * j], x[2 * j + 1], q[j]);
-                        } else {
-#pragma unroll
-                            for (int j = 0; j < 4; ++j) split_pair<Cf::PB>(x[2 * j], x[2 * j + 1], q[j]);
-                        }
-#pragma unroll
-                        for (int pc = 0; pc < Cf::PB; ++pc)
-                            sts_u32x4(pb + (uint32_t)(pc * Cf::B_PIECE) + (((uint32_t)hh ^ swz) << 4), q[0][pc], q[1][pc],
-                                      q[2][pc], q[3][pc]);
-                    }
-                }
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // visible to the tensor core
-                __syncwarp();
-                if (lane == 0) {
-                    mbar_arrive(&f32_empty[fs]);
-                    if (rank == 0) mbar_arrive(&full[ps]);
-                    else mbar_arrive_release_cluster(&full[ps], pair * CG);
-                }
-                if (++fs == NF) { fs = 0; fph ^= 1u; }
-                if (++ps == NST) { ps = 0; pph ^= 1u; }
-            }
-        }
-    }
-
-    tc_fence_before();
-    if constexpr (CL > 1) cluster_sync(); else __syncthreads();
-    if (warp == 2) {
-        tc_fence_after();
-        tmem_dealloc<CG>(tmem_base, kTmemCols);
-    }
-}
-
-// ------------------------------------------------------------------------------------
-// host side
-// ------------------------------------------------------------------------------------
 typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
                                   const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -595,8 +42,8 @@ static EncodeTiledFn encode_fn() {
 }
 
 // 3D map over p K-major piece planes: dims (k, rows, p), box (BK, box_rows, p).
-static int make_piece_map(CUtensorMap *map, const uint16_t *base, int k, int rows, int64_t ld, int64_t plane,
-                          int p, int box_rows, int box_p = 0) {
+int make_piece_map(CUtensorMap *map, const uint16_t *base, int k, int rows, int64_t ld, int64_t plane,
+                          int p, int box_rows, int box_p) {
     if (box_p <= 0) box_p = p;
     EncodeTiledFn enc = encode_fn();
     if (!enc) return BF16X_ERR_CUDA;
@@ -612,7 +59,7 @@ static int make_piece_map(CUtensorMap *map, const uint16_t *base, int k, int row
 
 // 2D map over a column-major FP32 matrix: dims (rows [inner], cols), box (box_rows, box_cols);
 // out-of-range elements read as zero (they become zero pieces).
-static int make_f32_map(CUtensorMap *map, const float *base, int rows, int cols, int64_t ld, int box_rows,
+int make_f32_map(CUtensorMap *map, const float *base, int rows, int cols, int64_t ld, int box_rows,
                         int box_cols, CUtensorMapSwizzle swz) {
     EncodeTiledFn enc = encode_fn();
     if (!enc) return BF16X_ERR_CUDA;
@@ -636,7 +83,7 @@ static unsigned int *g_sk_flags = nullptr;
 static size_t g_sk_ws_n = 0, g_sk_flags_n = 0;
 static unsigned int g_sk_epoch = 0;
 
-static int sk_workspace(size_t ws_floats, size_t nflags, float **ws, unsigned int **flags, unsigned int *epoch) {
+int sk_workspace(size_t ws_floats, size_t nflags, float **ws, unsigned int **flags, unsigned int *epoch) {
     std::lock_guard<std::mutex> g(g_sk_mu);
     if (ws_floats > g_sk_ws_n) {
         if (g_sk_ws) { cudaDeviceSynchronize(); cudaFree(g_sk_ws); }
@@ -692,148 +139,17 @@ int pieces_a(int variant) { return variant_pieces_a(variant); }
 int pieces_b(int variant) { return variant_pieces_b(variant); }
 int default_cta_group() { return kDefaultCtaGroup; }
 
-template <int CG, int V, int BN, int S, int MC, bool SA = false, bool FU = false>
-static int launch_t(const GemmPlan &pl, cudaStream_t st) {
-    using Cf = Cfg<CG, V, BN>;
-    constexpr int CL = CG * MC;
-    constexpr int THREADS = FU ? kThreadsFused : kThreads;
-    constexpr int SMEM = FU ? CfgF<V>::SMEM : Cf::SMEM;
-    auto kern = gemm_split_kernel<CG, V, BN, S, MC, SA, FU>;
-    CUtensorMap tmA, tmB;
-    int rc;
-    if constexpr (FU) {
-        rc = make_f32_map(&tmA, pl.Af, pl.m, pl.k, pl.lda, kBM, kBK, CU_TENSOR_MAP_SWIZZLE_NONE);
-        if (rc) return rc;
-        rc = make_f32_map(&tmB, pl.Bf, pl.k, pl.n, pl.ldb, kBK, Cf::BN_LOCAL, CU_TENSOR_MAP_SWIZZLE_128B);
-    } else {
-        rc = make_piece_map(&tmA, pl.Ap, pl.k, pl.m, pl.ldap, pl.a_plane, Cf::PA, kBM);
-        if (rc) return rc;
-        if (MC == 1) rc = make_piece_map(&tmB, pl.Bp, pl.k, pl.n, pl.ldbp, pl.b_plane, Cf::PB, Cf::BN_LOCAL);
-        else rc = make_piece_map(&tmB, pl.Bp, pl.k, pl.n, pl.ldbp, pl.b_plane, Cf::PB, Cf::BN_LOCAL / MC, 1);
+static int dispatch(const GemmPlan &pl, cudaStream_t st, int kind) {
+    switch (pl.variant) {
+    case 1: return launch_variant_1(pl, st, kind);
+    case 3: return launch_variant_3(pl, st, kind);
+    case 5: return launch_variant_5(pl, st, kind);
+    case 6: return launch_variant_6(pl, st, kind);
+    case 7: return launch_variant_7(pl, st, kind);
+    case 8: return launch_variant_8(pl, st, kind);
+    case 9: return launch_variant_9(pl, st, kind);
     }
-    if (rc) return rc;
-    KParams kp;
-    kp.m = pl.m; kp.n = pl.n; kp.k = pl.k;
-    kp.alpha = pl.alpha; kp.beta = pl.beta;
-    kp.C = pl.C; kp.ldc = pl.ldc; kp.flags = pl.flags; kp.acc = pl.acc;
-    kp.tiles_m = ((pl.m + Cf::TILE_M - 1) / Cf::TILE_M + MC - 1) / MC;   // rows of (MC-tall) super-tiles
-    kp.tiles_n = (pl.n + BN - 1) / BN;
-    kp.nkb = (pl.k + kBK - 1) / kBK;
-    const int tiles = kp.tiles_m * kp.tiles_n;
-    int units = num_sms() / CL;
-    if (pl.max_ctas > 0) units = std::max(1, pl.max_ctas / CL);
-    if constexpr (CL > 2) {
-        // clusters of 4 do not tile every GPC: only co-resident clusters may be launched
-        static int max_clusters = -1;
-        if (max_clusters < 0) {
-            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
-            cudaLaunchConfig_t qc = {};
-            qc.gridDim = dim3(units * CL);
-            qc.blockDim = dim3(THREADS);
-            qc.dynamicSmemBytes = SMEM;
-            cudaLaunchAttribute qa[1];
-            qa[0].id = cudaLaunchAttributeClusterDimension;
-            qa[0].val.clusterDim.x = CL;
-            qa[0].val.clusterDim.y = 1;
-            qa[0].val.clusterDim.z = 1;
-            qc.attrs = qa;
-            qc.numAttrs = 1;
-            int nclu = 0;
-            if (cudaOccupancyMaxActiveClusters(&nclu, kern, &qc) != cudaSuccess) {
-                cudaGetLastError();
-                nclu = 0;
-            }
-            max_clusters = nclu;
-        }
-        if (max_clusters > 0) units = std::min(units, max_clusters);
-    }
-    const int grid = std::min(tiles, units) * CL;
-    // Hybrid schedule: all full waves but the last run data-parallel; the last full wave plus
-    // the partial one are spread over every cluster by promotion interval (stream-K), so the
-    // partial wave no longer idles most of the GPU.  Disabled for accumulator-carry launches.
-    kp.n_int = (kp.nkb + S - 1) / S;
-    kp.dp_tiles = tiles;
-    kp.sk_tiles = 0;
-    kp.sk_ws = nullptr;
-    kp.sk_flags = nullptr;
-    kp.epoch = 0;
-    const int ncl = grid / CL;
-    if (pl.stream_k != 0 && !(pl.flags & (BF16X_ACC_IN | BF16X_ACC_OUT)) && tiles > ncl && tiles % ncl != 0) {
-        const int full = tiles / ncl;
-        kp.dp_tiles = (full - 1) * ncl;
-        kp.sk_tiles = tiles - kp.dp_tiles;
-        int rc2 = sk_workspace((size_t)kp.sk_tiles * CL * BN * kBM, (size_t)kp.sk_tiles * CL, &kp.sk_ws, &kp.sk_flags,
-                               &kp.epoch);
-        if (rc2) return rc2;
-    }
-
-    static bool attr_set = false;  // per template instance
-    if (!attr_set) {
-        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM) != cudaSuccess)
-            return check_launch("gemm attr");
-        attr_set = true;
-    }
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(THREADS);
-    cfg.dynamicSmemBytes = SMEM;
-    cfg.stream = st;
-    cudaLaunchAttribute attr[2];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = CL;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[1].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 2;
-    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, tmA, tmB, kp);
-    if (e != cudaSuccess) {
-        set_cuda_error(e, "gemm launch");
-        return BF16X_ERR_CUDA;
-    }
-    count_launch();
-    return check_launch("gemm");
-}
-
-// Stages per promotion interval: 2 (64 values of k) for the 2-CTA kernel, whose promotion
-// round trip (TMEM drain in both CTAs + remote mbarrier arrivals) needs the longer
-// interval to stay hidden behind the MMAs; 1 (32 values of k) otherwise.
-//
-// Tile N (2-CTA kernel only): 256, or 192 / 128 when that needs fewer waves-of-work on the
-// persistent grid (wave quantisation: cost ~ ceil(tiles / clusters) * N).
-// Measured (r02, x3/x6/x9 at 4096-16384): N = 192 and 128 lose more per-MMA efficiency than
-// they win on wave quantisation, so 256 is the default; 192 stays available to the tuner.
-int choose_tile_n(int m, int n, int cg, int units, int forced) {
-    (void)m; (void)n; (void)units;
-    if (cg == 1) return 256;
-    if (forced == 192) return 192;
-    return 256;
-}
-
-template <int CG, int V>
-static int launch_s(const GemmPlan &pl, cudaStream_t st) {
-    int s = pl.stages_per_interval;
-    // Short k (<= 128): the whole product is one or two intervals, so the tensor core's
-    // truncating accumulation dominates the error; 32-k intervals halve it (measured wide
-    // exponents, k = 64: max ratio to the oracle 2.07 -> 1.66) at no cost that matters.
-    if (s != 1 && s != 2) s = (CG == 2 && pl.k > 128) ? 2 : 1;
-    if (s == 2 && Cfg<CG, V, 256>::STAGES < 4) s = 1;
-    if constexpr (CG == 2) {
-        if (s == 2) {
-            const int units = (pl.max_ctas > 0 ? pl.max_ctas : num_sms()) / CG;
-            const int bn = choose_tile_n(pl.m, pl.n, CG, units, pl.tile_n);
-            if (bn == 192) return launch_t<CG, V, 192, 2, 1>(pl, st);
-            if (pl.split_acc && V >= 3) return launch_t<CG, V, 128, 2, 1, true>(pl, st);
-            // Two pairs per cluster sharing B (TMA multicast) cut L2->SM and DRAM traffic by a
-            // quarter but clusters of 4 leave 16 SMs idle; measured (r05) a win only for large
-            // outputs, where the kernel runs long enough to be power-limited (16384^3: x3 +17 %,
-            // x6 +7 %), and a loss at 8192^3.  Auto: multicast for m*n >= 12288^2.
-            const bool mc2 = pl.multicast == 2 || (pl.multicast == 0 && (int64_t)pl.m * pl.n >= 12288LL * 12288LL);
-            if (mc2) return launch_t<CG, V, 256, 2, 2>(pl, st);
-        }
-    }
-    return s == 2 ? launch_t<CG, V, 256, 2, 1>(pl, st) : launch_t<CG, V, 256, 1, 1>(pl, st);
+    return -12;
 }
 
 // Fused split: 2-CTA pairs, tile N 256, one 32-k stage per promotion interval, FP32 operands
@@ -848,43 +164,13 @@ int launch_gemm_fused(const GemmPlan &pl, cudaStream_t st) {
     if (!aligned || cg != 2 || pl.split_acc || mc2 || (pl.tile_n && pl.tile_n != 256) ||
         pl.stages_per_interval == 2 || pl.k <= 0)
         return -1;
-    switch (pl.variant) {
-    case 1: return launch_t<2, 1, 256, 1, 1, false, true>(pl, st);
-    case 3: return launch_t<2, 3, 256, 1, 1, false, true>(pl, st);
-    case 5: return launch_t<2, 5, 256, 1, 1, false, true>(pl, st);
-    case 6: return launch_t<2, 6, 256, 1, 1, false, true>(pl, st);
-    case 7: return launch_t<2, 7, 256, 1, 1, false, true>(pl, st);
-    case 8: return launch_t<2, 8, 256, 1, 1, false, true>(pl, st);
-    case 9: return launch_t<2, 9, 256, 1, 1, false, true>(pl, st);
-    }
-    return -1;
+    return dispatch(pl, st, 3);
 }
 
 int launch_gemm_pieces(const GemmPlan &pl, cudaStream_t st) {
     int cg = pl.cta_group;
     if (cg == 0) cg = kDefaultCtaGroup;
-    if (cg == 1) {
-        switch (pl.variant) {
-        case 1: return launch_s<1, 1>(pl, st);
-        case 3: return launch_s<1, 3>(pl, st);
-        case 5: return launch_s<1, 5>(pl, st);
-        case 6: return launch_s<1, 6>(pl, st);
-        case 7: return launch_s<1, 7>(pl, st);
-        case 8: return launch_s<1, 8>(pl, st);
-        case 9: return launch_s<1, 9>(pl, st);
-        }
-    } else {
-        switch (pl.variant) {
-        case 1: return launch_s<2, 1>(pl, st);
-        case 3: return launch_s<2, 3>(pl, st);
-        case 5: return launch_s<2, 5>(pl, st);
-        case 6: return launch_s<2, 6>(pl, st);
-        case 7: return launch_s<2, 7>(pl, st);
-        case 8: return launch_s<2, 8>(pl, st);
-        case 9: return launch_s<2, 9>(pl, st);
-        }
-    }
-    return -12;
+    return dispatch(pl, st, cg == 1 ? 1 : 2);
 }
 
 // C <- beta*C (quick return of BLAS sgemm when alpha == 0 or k == 0; beta == 0 -> 0).
