@@ -45,6 +45,21 @@ enum {
 /* gemm_ex flags: FP32 promoted-accumulator carry between k-chunks (multi-GPU overlap). */
 #define BF16X_ACC_IN  1u  /* the promoted accumulator starts from acc_carry instead of 0 */
 #define BF16X_ACC_OUT 2u  /* store the raw accumulator to acc_carry; skip alpha/beta/C  */
+/* N2 options, gemm_ex and split_ex flags:
+ * BF16X_SCALED_PIECES: power-of-two scaled pieces (R29; the loss the paper notes
+ *   below exponent -110, removed): b1' = (B16)(2^8 (x - b0)), b2' = (B16)(2^8 (2^8
+ *   (x - b0) - b1')), so x = b0 + 2^-8 b1' + 2^-16 b2' for every finite x.  The GEMM scales its
+ *   tensor-memory accumulator by 2^-8 (tcgen05.mma scale-input-d) on each move to the next
+ *   larger bin, so bins are still added smallest first.  Pre-split pieces passed to
+ *   bf16x_gemm_ex with this flag must come from bf16x_split_ex(.., BF16X_SCALED_PIECES, ..).
+ * BF16X_FP64_COMBINE (gemm_ex only): the paper's "d" variants ("adding the final results
+ *   together in FP64"; R30): bins >= 1 and bin 0 accumulate in separate FP32 tensor-memory
+ *   accumulators per 64-k interval and are collected in an FP64 accumulator, rounded once to
+ *   FP32 before alpha/beta.  Variants 3, 5, 6, 7, 8, 9; not with BF16X_ACC_IN / _OUT.
+ * BF16X_SPLIT_TRANSPOSED (split_ex only): write the pieces transposed, as bf16x_split_t. */
+#define BF16X_SCALED_PIECES    4u
+#define BF16X_FP64_COMBINE     8u
+#define BF16X_SPLIT_TRANSPOSED 16u
 
 /* ------------------------------------------------------------------------------------
  * bf16x_split -- the 3-way decomposition of P:180-184 (section II-A):
@@ -68,6 +83,12 @@ int bf16x_split(int64_t rows, int64_t cols, const float *X, int64_t ldx,
  * Errors as bf16x_split, with -8 for ldp < max(1, cols). */
 int bf16x_split_t(int64_t rows, int64_t cols, const float *X, int64_t ldx,
                   uint16_t *P0, uint16_t *P1, uint16_t *P2, int64_t ldp, bf16x_stream_t stream);
+
+/* Split with options (flags: BF16X_SCALED_PIECES, BF16X_SPLIT_TRANSPOSED; see above).  With
+ * BF16X_SCALED_PIECES the pieces are (b0, b1', b2') of reading R29.  Arguments and errors as
+ * bf16x_split (bf16x_split_t when transposed), plus -9 for unknown flags. */
+int bf16x_split_ex(int64_t rows, int64_t cols, const float *X, int64_t ldx,
+                   uint16_t *P0, uint16_t *P1, uint16_t *P2, int64_t ldp, unsigned flags, bf16x_stream_t stream);
 
 /* Both GEMM operands in one launch (the pre-pass bf16x_gemm runs): A (m x k, lda) is split
  * transposed into K-major pieces (element (i,l) of piece q at Ap[q*a_plane + l + i*ldap]),
@@ -113,7 +134,9 @@ size_t bf16x_gemm_workspace_size(int m, int n, int k, int variant);
  *              element (l,j) of piece q at B_pieces[q*b_plane + l + j*ldbp], ldbp >= k,
  *              ldbp % 8 == 0, b_plane % 8 == 0; then B may be NULL.
  *   acc_carry: m x n FP32 (ld = ldc) used by BF16X_ACC_IN / BF16X_ACC_OUT.
- * Errors: as bf16x_gemm, plus -13 flags, -14 A_pieces layout, -16 B_pieces layout,
+ *   flags    : BF16X_ACC_IN | BF16X_ACC_OUT | BF16X_SCALED_PIECES | BF16X_FP64_COMBINE (above).
+ * Errors: as bf16x_gemm, plus -13 flags (unknown bits, FP64_COMBINE with ACC_* or with
+ * variant 1), -14 A_pieces layout, -16 B_pieces layout,
  * -19 acc_carry NULL with ACC flags, -21 ws_bytes too small. */
 int bf16x_gemm_ex(int m, int n, int k, float alpha, const float *A, int lda,
                   const float *B, int ldb, float beta, float *C, int ldc, int variant,

@@ -19,6 +19,7 @@ HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "bf16x.h")
 
 SUCCESS, ERR_CUDA, ERR_ALLOC, ERR_ARCH, ERR_SINGULAR, NOT_CONVERGED = 0, 1, 2, 3, 4, 5
 ACC_IN, ACC_OUT = 1, 2
+SCALED_PIECES, FP64_COMBINE, SPLIT_TRANSPOSED = 4, 8, 16   # N2 options (bf16x.h; R29, R30)
 VARIANTS = (1, 3, 5, 6, 7, 8, 9)
 PIECES = {1: 1, 3: 2, 6: 3, 8: 3, 9: 3}
 
@@ -49,6 +50,7 @@ def lib() -> ctypes.CDLL:
         L = ctypes.CDLL(LIB_PATH)
         L.bf16x_split.argtypes = [_i64, _i64, _vp, _i64, _vp, _vp, _vp, _i64, _vp]
         L.bf16x_split_t.argtypes = [_i64, _i64, _vp, _i64, _vp, _vp, _vp, _i64, _vp]
+        L.bf16x_split_ex.argtypes = [_i64, _i64, _vp, _i64, _vp, _vp, _vp, _i64, _u, _vp]
         L.bf16x_split_operands.argtypes = [_i, _i, _i, _vp, _i64, _vp, _i64, _i, _vp, _i64, _i64, _vp, _i64, _i64, _vp]
         L.bf16x_gemm.argtypes = [_i, _i, _i, _f, _vp, _i, _vp, _i, _f, _vp, _i, _i]
         L.bf16x_gemm_workspace_size.argtypes = [_i, _i, _i, _i]
@@ -135,9 +137,10 @@ def _rowmajor(t):
 # ------------------------------------------------------------------------------------
 # K1: split
 # ------------------------------------------------------------------------------------
-def split(x, pieces: int = 3, stream=None):
+def split(x, pieces: int = 3, stream=None, scaled: bool = False):
     """b0, b1, b2 = (B16) pieces of an FP32 CUDA tensor (any 2-D strided layout with a unit
-    stride, or 1-D contiguous).  Returns `pieces` uint16 tensors with x's shape and layout."""
+    stride, or 1-D contiguous).  Returns `pieces` uint16 tensors with x's shape and layout.
+    scaled: the N2 power-of-two scaled pieces (b0, b1', b2') of DESIGN.md R29."""
     import torch
     if x.dtype != torch.float32 or not x.is_cuda:
         raise TypeError("split expects a float32 CUDA tensor")
@@ -162,8 +165,12 @@ def split(x, pieces: int = 3, stream=None):
                 for _ in range(pieces)]
         ldp = max(1, rows)
     p = [_ptr(o) for o in outs] + [0] * (3 - pieces)
-    _check(lib().bf16x_split(rows, cols, ptr, ld, p[0], p[1] or None, p[2] or None, ldp, _stream(stream)),
-           "bf16x_split")
+    if scaled:
+        _check(lib().bf16x_split_ex(rows, cols, ptr, ld, p[0], p[1] or None, p[2] or None, ldp, SCALED_PIECES,
+                                    _stream(stream)), "bf16x_split_ex")
+    else:
+        _check(lib().bf16x_split(rows, cols, ptr, ld, p[0], p[1] or None, p[2] or None, ldp, _stream(stream)),
+               "bf16x_split")
     return tuple(o.reshape(x.shape) for o in outs)
 
 
@@ -184,9 +191,11 @@ def gemm_raw(m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, variant=6, flags=0, A
            "bf16x_gemm_ex")
 
 
-def gemm(A, B, C=None, alpha: float = 1.0, beta: float = 0.0, variant: int = 6, stream=None, cta_group: int = 0):
+def gemm(A, B, C=None, alpha: float = 1.0, beta: float = 0.0, variant: int = 6, stream=None, cta_group: int = 0,
+         scaled: bool = False, fp64_combine: bool = False):
     """C = alpha * A @ B + beta * C for FP32 CUDA tensors, computed with the bf16x`variant`
-    split GEMM.  Column-major (Fortran) and row-major inputs are both used in place."""
+    split GEMM.  Column-major (Fortran) and row-major inputs are both used in place.
+    scaled: N2 power-of-two scaled pieces (R29); fp64_combine: the paper's "d" variants (R30)."""
     import torch
     if variant not in VARIANTS:
         raise ValueError(f"variant must be one of {VARIANTS}")
@@ -214,10 +223,11 @@ def gemm(A, B, C=None, alpha: float = 1.0, beta: float = 0.0, variant: int = 6, 
             raise ValueError("A, B, C must share one layout (all row-major or all column-major)")
         # row-major C = A B  <=>  column-major C^T = B^T A^T
         args = (n, m, k, alpha, b[0], b[3], a[0], a[3], beta, c[0], c[3], variant)
-    if cta_group:
+    flags = (SCALED_PIECES if scaled else 0) | (FP64_COMBINE if fp64_combine else 0)
+    if cta_group and not flags:
         _check(lib().bf16x_gemm_cg(*args, cta_group, st), "bf16x_gemm_cg")
     else:
-        _check(lib().bf16x_gemm_ex(*args, 0, None, 0, 0, None, 0, 0, None, None, 0, st), "bf16x_gemm_ex")
+        _check(lib().bf16x_gemm_ex(*args, flags, None, 0, 0, None, 0, 0, None, None, 0, st), "bf16x_gemm_ex")
     return C
 
 

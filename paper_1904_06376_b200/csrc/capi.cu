@@ -122,8 +122,11 @@ int gemm_core(int m, int n, int k, float alpha, const float *A, int lda, const f
     pl.stream_k = g_stream_k;
     pl.multicast = g_multicast;
     pl.split_acc = g_split_acc;
+    pl.scaled = (flags & BF16X_SCALED_PIECES) ? 1 : 0;
+    pl.fp64 = (flags & BF16X_FP64_COMBINE) ? 1 : 0;
+    const bool sc = pl.scaled != 0;
     pl.Af = A; pl.Bf = B; pl.lda = lda; pl.ldb = ldb;
-    if (!Ap && !Bp && g_fused) {   // split inside the GEMM when the plan qualifies
+    if (!Ap && !Bp && g_fused && !sc && !pl.fp64) {   // split inside the GEMM when the plan qualifies
         pl.Ap = nullptr; pl.Bp = nullptr;
         const int frc = launch_gemm_fused(pl, st);
         if (frc != -1) return frc;
@@ -135,7 +138,7 @@ int gemm_core(int m, int n, int k, float alpha, const float *A, int lda, const f
         uint16_t *b = a + pa * a_plane;
         b_plane = (int64_t)n * kp;
         ldbp = kp;
-        rc = launch_split_ab(m, n, k, A, lda, a, ldap, a_plane, B, ldb, b, ldbp, b_plane, pa, pb, st);
+        rc = launch_split_ab(m, n, k, A, lda, a, ldap, a_plane, B, ldb, b, ldbp, b_plane, pa, pb, st, sc);
         if (rc) return rc;
         Ap = a;
         Bp = b;
@@ -145,7 +148,7 @@ int gemm_core(int m, int n, int k, float alpha, const float *A, int lda, const f
         a_plane = (int64_t)m * kp;
         ldap = kp;
         rc = launch_split(m, k, A, lda, a, pa > 1 ? a + a_plane : nullptr, pa > 2 ? a + 2 * a_plane : nullptr, ldap,
-                          true, st);
+                          true, st, sc);
         if (rc) return rc;
         Ap = a;
         w += 2ull * pa * (size_t)a_plane;
@@ -155,7 +158,7 @@ int gemm_core(int m, int n, int k, float alpha, const float *A, int lda, const f
         b_plane = (int64_t)n * kp;
         ldbp = kp;
         rc = launch_split(k, n, B, ldb, b, pb > 1 ? b + b_plane : nullptr, pb > 2 ? b + 2 * b_plane : nullptr, ldbp,
-                          false, st);
+                          false, st, sc);
         if (rc) return rc;
         Bp = b;
     }
@@ -190,7 +193,8 @@ int bf16x_gemm_ex(int m, int n, int k, float alpha, const float *A, int lda, con
                   void *workspace_ptr, size_t ws_bytes, bf16x_stream_t stream) {
     int a = gemm_args(m, n, k, A_pieces ? (m > 1 ? m : 1) : lda, B_pieces ? (k > 1 ? k : 1) : ldb, ldc, variant);
     if (a) return a;
-    if (flags & ~(BF16X_ACC_IN | BF16X_ACC_OUT)) return -13;
+    if (flags & ~(BF16X_ACC_IN | BF16X_ACC_OUT | BF16X_SCALED_PIECES | BF16X_FP64_COMBINE)) return -13;
+    if ((flags & BF16X_FP64_COMBINE) && ((flags & (BF16X_ACC_IN | BF16X_ACC_OUT)) || variant == 1)) return -13;
     if (A_pieces && (ldap < k || ldap % 8 || a_plane % 8 || a_plane < ldap * (int64_t)m ||
                      (reinterpret_cast<uintptr_t>(A_pieces) & 15u)))
         return -14;

@@ -54,6 +54,32 @@ __device__ __forceinline__ Split3 split3(float x) {
     return s;
 }
 
+// N2 scaled pieces (R29): the residuals are multiplied by 2^8 (exact) before each
+// rounding, b1' = (B16)(2^8 (x - b0)), b2' = (B16)(2^8 (2^8 (x - b0) - b1')), so every piece
+// stays at the magnitude of x and x = b0 + 2^-8 b1' + 2^-16 b2' for every finite x.
+__device__ __forceinline__ Split3 split3_scaled(float x) {
+    Split3 s;
+    s.b0 = rne_sat_bf16(x);
+    if (!isfinite(x)) { s.b1 = 0u; s.b2 = 0u; return s; }
+    float s1 = __fmul_rn(__fsub_rn(x, bf16_bits_to_float(s.b0)), 256.f);
+    s.b1 = rne_sat_bf16(s1);
+    float s2 = __fmul_rn(__fsub_rn(s1, bf16_bits_to_float(s.b1)), 256.f);
+    s.b2 = rne_sat_bf16(s2);
+    return s;
+}
+template <bool SC>
+__device__ __forceinline__ Split3 split3_t(float x) {
+    if constexpr (SC) return split3_scaled(x);
+    else return split3(x);
+}
+// residual scaling of the fast path: 2^8 for scaled pieces (exact: |residual| <= 2^119 below
+// the b0-overflow band), identity otherwise
+template <bool SC>
+__device__ __forceinline__ float res_scale(float r) {
+    if constexpr (SC) return __fmul_rn(r, 256.f);
+    else return r;
+}
+
 // Hardware fast path of the split for two values below the b0-overflow band (shared by the
 // split pre-pass and the GEMM's in-kernel transform): cvt.rn.bf16x2.f32 is IEEE RNE on two
 // values, the FP32 residual subtractions are exact; anything else takes split3.
@@ -67,42 +93,30 @@ __device__ __forceinline__ bool regular(float x) { return (__float_as_uint(x) & 
 
 // Fast path only (both values known to be below the b0-overflow band): branch-free, so many
 // pairs' dependency chains interleave.
-template <int NP>
+template <int NP, bool SC = false>
 __device__ __forceinline__ void split_pair_fast(float lo, float hi, uint32_t (&p)[3]) {
     const uint32_t a = cvt_bf16x2(hi, lo);
     p[0] = a;
     if constexpr (NP >= 2) {
-        const float r1lo = __fsub_rn(lo, __uint_as_float(a << 16));
-        const float r1hi = __fsub_rn(hi, __uint_as_float(a & 0xFFFF0000u));
+        const float r1lo = res_scale<SC>(__fsub_rn(lo, __uint_as_float(a << 16)));
+        const float r1hi = res_scale<SC>(__fsub_rn(hi, __uint_as_float(a & 0xFFFF0000u)));
         const uint32_t b = cvt_bf16x2(r1hi, r1lo);
         p[1] = b;
         if constexpr (NP >= 3) {
-            const float r2lo = __fsub_rn(r1lo, __uint_as_float(b << 16));
-            const float r2hi = __fsub_rn(r1hi, __uint_as_float(b & 0xFFFF0000u));
+            const float r2lo = res_scale<SC>(__fsub_rn(r1lo, __uint_as_float(b << 16)));
+            const float r2hi = res_scale<SC>(__fsub_rn(r1hi, __uint_as_float(b & 0xFFFF0000u)));
             p[2] = cvt_bf16x2(r2hi, r2lo);
         }
     }
 }
 
 // Split two values; packs piece q of (lo, hi) as (hi << 16) | lo in p[q].
-template <int NP>
+template <int NP, bool SC = false>
 __device__ __forceinline__ void split_pair(float lo, float hi, uint32_t (&p)[3]) {
     if (regular(lo) && regular(hi)) {
-        const uint32_t a = cvt_bf16x2(hi, lo);
-        p[0] = a;
-        if constexpr (NP >= 2) {
-            const float r1lo = __fsub_rn(lo, __uint_as_float(a << 16));
-            const float r1hi = __fsub_rn(hi, __uint_as_float(a & 0xFFFF0000u));
-            const uint32_t b = cvt_bf16x2(r1hi, r1lo);
-            p[1] = b;
-            if constexpr (NP >= 3) {
-                const float r2lo = __fsub_rn(r1lo, __uint_as_float(b << 16));
-                const float r2hi = __fsub_rn(r1hi, __uint_as_float(b & 0xFFFF0000u));
-                p[2] = cvt_bf16x2(r2hi, r2lo);
-            }
-        }
+        split_pair_fast<NP, SC>(lo, hi, p);
     } else {
-        const Split3 a = split3(lo), b = split3(hi);
+        const Split3 a = split3_t<SC>(lo), b = split3_t<SC>(hi);
         p[0] = a.b0 | (b.b0 << 16);
         p[1] = a.b1 | (b.b1 << 16);
         p[2] = a.b2 | (b.b2 << 16);
@@ -295,6 +309,21 @@ __device__ __forceinline__ void umma_bf16_elect(uint32_t d_tmem, uint64_t adesc,
             "{\n\t.reg .pred p, e;\n\telect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\t"
             "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
             "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+// Accumulating MMA that first scales the accumulator by 2^-8 (tcgen05.mma scale-input-d = 8:
+// D = A*B + D * 2^-8), used on the move to the next larger bin with scaled pieces (R29).
+template <int CG>
+__device__ __forceinline__ void umma_bf16_elect_sc8(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc) {
+    if constexpr (CG == 1)
+        asm volatile(
+            "{\n\t.reg .pred p, e;\n\telect.sync _|e, 0xffffffff;\n\tsetp.eq.u32 p, 1, 1;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p, 8;\n\t}" ::"r"(d_tmem),
+            "l"(adesc), "l"(bdesc), "r"(idesc));
+    else
+        asm volatile(
+            "{\n\t.reg .pred p, e;\n\telect.sync _|e, 0xffffffff;\n\tsetp.eq.u32 p, 1, 1;\n\t"
+            "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p, 8;\n\t}" ::"r"(d_tmem),
+            "l"(adesc), "l"(bdesc), "r"(idesc));
 }
 template <int CG>
 __device__ __forceinline__ void umma_commit_elect(uint64_t *bar) {

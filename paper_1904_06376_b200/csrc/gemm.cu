@@ -161,7 +161,7 @@ int launch_gemm_fused(const GemmPlan &pl, cudaStream_t st) {
     const bool aligned = pl.Af && pl.Bf && ((reinterpret_cast<uintptr_t>(pl.Af) | reinterpret_cast<uintptr_t>(pl.Bf)) & 15u) == 0 &&
                          pl.lda % 4 == 0 && pl.ldb % 4 == 0;
     const bool mc2 = pl.multicast == 2 || (pl.multicast == 0 && (int64_t)pl.m * pl.n >= 12288LL * 12288LL);
-    if (!aligned || cg != 2 || pl.split_acc || mc2 || (pl.tile_n && pl.tile_n != 256) ||
+    if (!aligned || cg != 2 || pl.split_acc || pl.scaled || pl.fp64 || mc2 || (pl.tile_n && pl.tile_n != 256) ||
         pl.stages_per_interval == 2 || pl.k <= 0)
         return -1;
     return dispatch(pl, st, 3);

@@ -4,6 +4,7 @@
 #pragma once
 #include <algorithm>
 #include <mutex>
+#include <type_traits>
 
 #include "common.cuh"
 #include "kernels.cuh"
@@ -80,6 +81,7 @@ struct KParams {
     float *sk_ws;
     unsigned int *sk_flags;
     unsigned int epoch;
+    int scaled;            // N2 scaled pieces (R29): scale the accumulator by 2^-8 per bin step
 };
 
 struct Work {
@@ -137,13 +139,17 @@ __device__ __forceinline__ void tile_coords(int tile, int tiles_m, int tiles_n, 
 // alignment truncation of each MMA step (K3 probe) never cuts the small bins against the
 // bin-0 products; the epilogue combines them as (small + big) in FP32 round-to-nearest.
 // Each accumulator's first MMA of the interval overwrites it.
+// scaled (R29): the pieces of bin s are scaled by 2^(8s), so the first MMA of each band that
+// adds into an already-started accumulator scales it by 2^-8 (scale-input-d): the accumulator
+// always holds the current band's scale and ends at bin 0's (bin 1's for SA's small one).
 template <int CG, int V, int BN, int S, bool SA>
 __device__ __forceinline__ void issue_interval(uint32_t d_big, uint32_t d_small, const uint64_t (&a_desc)[S],
-                                               const uint64_t (&b_desc)[S], int ns, uint32_t idesc) {
+                                               const uint64_t (&b_desc)[S], int ns, uint32_t idesc, bool scaled) {
     using Cf = Cfg<CG, V, BN>;
     constexpr int H = S * (kBK / kUK);     // K=16 halves per interval (max)
     const int nh = ns * (kBK / kUK);
     bool first_small = true, first_big = true;
+    bool band_start = false;   // next MMA is the first of a band
     // descriptor start-address field is in 16-byte units: piece / K-half offsets add directly
     auto mma = [&](int i, int j, int h) {
         const int st = h / (kBK / kUK), kk = h % (kBK / kUK);
@@ -151,34 +157,44 @@ __device__ __forceinline__ void issue_interval(uint32_t d_big, uint32_t d_small,
         const uint64_t bd = b_desc[st] + (uint64_t)((j * Cf::B_PIECE + kk * (kUK * 2)) >> 4);
         const bool big = SA && (i + j == 0);
         bool &first = (SA && !big) ? first_small : first_big;
-        umma_bf16_elect<CG>(big || !SA ? d_big : d_small, ad, bd, idesc, first ? 0u : 1u);
+        const uint32_t d = (big || !SA) ? d_big : d_small;
+        if (scaled && band_start && !first) umma_bf16_elect_sc8<CG>(d, ad, bd, idesc);
+        else umma_bf16_elect<CG>(d, ad, bd, idesc, first ? 0u : 1u);
+        band_start = false;
         first = false;
         if constexpr (!SA) first_small = false;
     };
     if constexpr (V == 9) {
+        band_start = true;
 #pragma unroll
         for (int h = 0; h < H; ++h) if (h < nh) mma(2, 2, h);                              // bin 4: 2^-32
     }
     if constexpr (V >= 8) {   // x8 = the paper's Z_3: bins 0..3
+        band_start = true;
 #pragma unroll
         for (int h = 0; h < H; ++h) if (h < nh) { mma(1, 2, h); mma(2, 1, h); }           // bin 3: 2^-24
     }
     if constexpr (V == 7) {   // x7: x6 + the a1*b2 term ("at least 7 products"; R27)
+        band_start = true;
 #pragma unroll
         for (int h = 0; h < H; ++h) if (h < nh) mma(1, 2, h);
     }
     if constexpr (V >= 6) {
+        band_start = true;
 #pragma unroll
         for (int h = 0; h < H; ++h) if (h < nh) { mma(0, 2, h); mma(1, 1, h); mma(2, 0, h); }  // bin 2: 2^-16
     }
     if constexpr (V == 5) {   // x5: A in two pieces, bin 2 = {02, 11} (R27)
+        band_start = true;
 #pragma unroll
         for (int h = 0; h < H; ++h) if (h < nh) { mma(0, 2, h); mma(1, 1, h); }
     }
     if constexpr (V >= 3) {
+        band_start = true;
 #pragma unroll
         for (int h = 0; h < H; ++h) if (h < nh) { mma(0, 1, h); mma(1, 0, h); }           // bin 1: 2^-8
     }
+    band_start = true;
 #pragma unroll
     for (int h = 0; h < H; ++h) if (h < nh) mma(0, 0, h);                                  // bin 0
 }
@@ -188,7 +204,11 @@ __device__ __forceinline__ void issue_interval(uint32_t d_big, uint32_t d_small,
 // FU (fused split): tmA / tmB are FP32 maps of A and B; warp 0 loads FP32 tiles, warps
 // 12..15 convert them into the piece ring (the MMA reads exactly what the pre-pass + TMA path
 // would have placed there), and the piece-ring "full" barrier counts the converters' arrivals.
-template <int CG, int V, int BN, int S, int MC, bool SA, bool FU = false>
+// GD ("d" variants, R30; requires SA): the bins >= 1 and bin 0 are promoted into two separate
+// FP32 register accumulators (G[0, EC) = bin 0, G[EC, 2 EC) = bins >= 1: the paper's FP32
+// partial sums Z^(i,j), pooled per accumulator) and only their final collection is
+// FP64, rounded once to FP32 ("adding the final results together in FP64").
+template <int CG, int V, int BN, int S, int MC, bool SA, bool FU = false, bool GD = false>
 __global__ void __launch_bounds__(FU ? kThreadsFused : kThreads, 1)
     gemm_split_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                       const KParams p) {
@@ -199,6 +219,8 @@ __global__ void __launch_bounds__(FU ? kThreadsFused : kThreads, 1)
     constexpr int CL = CG * MC;   // cluster size
     static_assert(MC == 1 || CG == 2, "multicast needs 2-CTA pairs");
     static_assert(!SA || 2 * BN <= kTmemBufStride, "split accumulators need 4 x BN TMEM columns");
+    static_assert(!GD || (SA && !FU), "FP64 collection needs split accumulators");
+    constexpr int NG = GD ? 2 : 1;     // promoted accumulators per output element
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t *sA = smem;
@@ -339,7 +361,7 @@ __global__ void __launch_bounds__(FU ? kThreadsFused : kThreads, 1)
                         // buffer layout: SA -> small at buf*BN, big at 256 + buf*BN; else one at buf*256
                         const uint32_t d_big = SA ? tmem_base + kTmemBufStride + buf * BN : tmem_base + buf * kTmemBufStride;
                         const uint32_t d_small = SA ? tmem_base + buf * BN : d_big;
-                        issue_interval<CG, V, BN, S, SA>(d_big, d_small, a_desc, b_desc, ns, idesc);
+                        issue_interval<CG, V, BN, S, SA>(d_big, d_small, a_desc, b_desc, ns, idesc, p.scaled != 0);
 #pragma unroll
                         for (int q = 0; q < S; ++q)
                             if (q < ns) {
@@ -369,14 +391,14 @@ __global__ void __launch_bounds__(FU ? kThreadsFused : kThreads, 1)
             tm = tm * MC + (int)pair;
             const int row = tm * Cf::TILE_M + (int)rank * kBM + quad * 32 + lane;
             const int col0 = tn * BN + half * EC;
-            float G[EC];
-            if ((p.flags & BF16X_ACC_IN) && w.i0 == 0) {
+            float G[NG * EC];
+            if ((p.flags & BF16X_ACC_IN) && w.i0 == 0) {   // (never with GD)
 #pragma unroll
                 for (int j = 0; j < EC; ++j)
                     G[j] = (row < p.m && col0 + j < p.n) ? p.acc[(int64_t)(col0 + j) * p.ldc + row] : 0.f;
             } else {
 #pragma unroll
-                for (int j = 0; j < EC; ++j) G[j] = 0.f;
+                for (int j = 0; j < NG * EC; ++j) G[j] = 0.f;
             }
             const int kb_end = min(p.nkb, w.i1 * S);
             for (int kb = w.i0 * S; kb < kb_end; kb += S, ++acc_it) {
@@ -394,8 +416,20 @@ __global__ void __launch_bounds__(FU ? kThreadsFused : kThreads, 1)
                         for (int j = 0; j < 16; ++j) G[c * 16 + j] = __fadd_rn(G[c * 16 + j], v[j]);
                     }
                 } else {
-                    // interval total = small bins + bin 0 (RN), then into G (RN)
+                    // interval total = small bins + bin 0 (RN), then into G (RN); GD: each into
+                    // its own accumulator.  Scaled pieces: the small one is at bin 1's scale, 2^8.
                     const uint32_t ts = tm_lane + buf * BN, tb = tm_lane + kTmemBufStride + buf * BN;
+                    const float qs = p.scaled ? 0x1p-8f : 1.f;
+                    if constexpr (GD) {   // one accumulator at a time: 16 live temporaries
+#pragma unroll
+                        for (int c = 0; c < 2 * EC / 16; ++c) {
+                            float v[16];
+                            tmem_ld16((c < EC / 16 ? tb : ts) + (c % (EC / 16)) * 16, v);
+                            tmem_ld_wait();
+#pragma unroll
+                            for (int j = 0; j < 16; ++j) G[c * 16 + j] = __fadd_rn(G[c * 16 + j], v[j]);
+                        }
+                    } else
 #pragma unroll
                     for (int c = 0; c < EC / 16; ++c) {
                         float vs[16], vb[16];
@@ -403,7 +437,9 @@ __global__ void __launch_bounds__(FU ? kThreadsFused : kThreads, 1)
                         tmem_ld16(tb + c * 16, vb);
                         tmem_ld_wait();
 #pragma unroll
-                        for (int j = 0; j < 16; ++j) G[c * 16 + j] = __fadd_rn(G[c * 16 + j], __fadd_rn(vs[j], vb[j]));
+                        for (int j = 0; j < 16; ++j) {
+                            G[c * 16 + j] = __fadd_rn(G[c * 16 + j], __fadd_rn(__fmul_rn(vs[j], qs), vb[j]));
+                        }
                     }
                 }
                 tc_fence_before();
@@ -415,12 +451,12 @@ __global__ void __launch_bounds__(FU ? kThreadsFused : kThreads, 1)
             }
             if (w.role != 0) {
                 // stream-K fix-up: slot layout [sk tile][cta rank][column 0..BN)[row 0..127]
-                float *slot = p.sk_ws + ((size_t)w.sk_slot * CL + crank) * (size_t)BN * kBM;
+                float *slot = p.sk_ws + ((size_t)w.sk_slot * CL + crank) * (size_t)NG * BN * kBM;
                 const int lrow = quad * 32 + lane;
                 unsigned int *flag = p.sk_flags + (size_t)w.sk_slot * CL + crank;
                 if (w.role == 2) {
 #pragma unroll
-                    for (int j = 0; j < EC; ++j) __stcg(slot + (size_t)(half * EC + j) * kBM + lrow, G[j]);
+                    for (int j = 0; j < NG * EC; ++j) __stcg(slot + (size_t)(half * NG * EC + j) * kBM + lrow, G[j]);
                     __threadfence();
                     asm volatile("bar.sync 1, %0;" ::"n"(kNumEpiWarps * 32));
                     if (ew == 0 && lane == 0) st_release_u32(flag, p.epoch);
@@ -430,8 +466,14 @@ __global__ void __launch_bounds__(FU ? kThreadsFused : kThreads, 1)
                     while (ld_acquire_u32(flag) != p.epoch) __nanosleep(64);
                 __syncwarp();
 #pragma unroll
-                for (int j = 0; j < EC; ++j) G[j] = __fadd_rn(G[j], __ldcg(slot + (size_t)(half * EC + j) * kBM + lrow));
+                for (int j = 0; j < NG * EC; ++j) G[j] = __fadd_rn(G[j], __ldcg(slot + (size_t)(half * NG * EC + j) * kBM + lrow));
             }
+            // GD: final collection in FP64, rounded once (R30)
+            const double qd = p.scaled ? 0x1p-8 : 1.0;
+            auto zval = [&](int j) -> float {
+                if constexpr (GD) return __double2float_rn(__dadd_rn((double)G[EC + j] * qd, (double)G[j]));
+                else return G[j];
+            };
             if (row < p.m) {
                 float *crow = p.C + row;
                 if (p.flags & BF16X_ACC_OUT) {
@@ -441,7 +483,7 @@ __global__ void __launch_bounds__(FU ? kThreadsFused : kThreads, 1)
                 } else if (p.beta == 0.f) {
 #pragma unroll
                     for (int j = 0; j < EC; ++j)
-                        if (col0 + j < p.n) __stcs(crow + (int64_t)(col0 + j) * p.ldc, fmaf(p.alpha, G[j], 0.f));
+                        if (col0 + j < p.n) __stcs(crow + (int64_t)(col0 + j) * p.ldc, fmaf(p.alpha, zval(j), 0.f));
                 } else {
                     // beta != 0: batch 8 independent loads of C before the FMAs and stores, so
                     // the old values stream in parallel instead of one round trip per column
@@ -454,7 +496,7 @@ __global__ void __launch_bounds__(FU ? kThreadsFused : kThreads, 1)
 #pragma unroll
                         for (int j = 0; j < 8; ++j)
                             if (col0 + j0 + j < p.n)
-                                __stcs(crow + (int64_t)(col0 + j0 + j) * p.ldc, fmaf(p.alpha, G[j0 + j], p.beta * cold[j]));
+                                __stcs(crow + (int64_t)(col0 + j0 + j) * p.ldc, fmaf(p.alpha, zval(j0 + j), p.beta * cold[j]));
                     }
                 }
             }
@@ -565,13 +607,13 @@ int make_f32_map(CUtensorMap *map, const float *base, int rows, int cols, int64_
                  CUtensorMapSwizzle swz);
 int sk_workspace(size_t ws_floats, size_t nflags, float **ws, unsigned int **flags, unsigned int *epoch);
 
-template <int CG, int V, int BN, int S, int MC, bool SA = false, bool FU = false>
+template <int CG, int V, int BN, int S, int MC, bool SA = false, bool FU = false, bool GD = false>
 int launch_t(const GemmPlan &pl, cudaStream_t st) {
     using Cf = Cfg<CG, V, BN>;
     constexpr int CL = CG * MC;
     constexpr int THREADS = FU ? kThreadsFused : kThreads;
     constexpr int SMEM = FU ? CfgF<V>::SMEM : Cf::SMEM;
-    auto kern = gemm_split_kernel<CG, V, BN, S, MC, SA, FU>;
+    auto kern = gemm_split_kernel<CG, V, BN, S, MC, SA, FU, GD>;
     CUtensorMap tmA, tmB;
     int rc;
     if constexpr (FU) {
@@ -630,12 +672,13 @@ int launch_t(const GemmPlan &pl, cudaStream_t st) {
     kp.sk_ws = nullptr;
     kp.sk_flags = nullptr;
     kp.epoch = 0;
+    kp.scaled = pl.scaled;
     const int ncl = grid / CL;
     if (pl.stream_k != 0 && !(pl.flags & (BF16X_ACC_IN | BF16X_ACC_OUT)) && tiles > ncl && tiles % ncl != 0) {
         const int full = tiles / ncl;
         kp.dp_tiles = (full - 1) * ncl;
         kp.sk_tiles = tiles - kp.dp_tiles;
-        int rc2 = sk_workspace((size_t)kp.sk_tiles * CL * BN * kBM, (size_t)kp.sk_tiles * CL, &kp.sk_ws, &kp.sk_flags,
+        int rc2 = sk_workspace((size_t)kp.sk_tiles * CL * BN * kBM * (GD ? 2 : 1), (size_t)kp.sk_tiles * CL, &kp.sk_ws, &kp.sk_flags,
                                &kp.epoch);
         if (rc2) return rc2;
     }
@@ -692,6 +735,10 @@ int launch_s(const GemmPlan &pl, cudaStream_t st) {
     // exponents, k = 64: max ratio to the oracle 2.07 -> 1.66) at no cost that matters.
     if (s != 1 && s != 2) s = (CG == 2 && pl.k > 128) ? 2 : 1;
     if (s == 2 && Cfg<CG, V, 256>::STAGES < 4) s = 1;
+    // "d" variants (R30): 2-CTA pairs, tile N 128, split accumulators, FP64 collection, 64-k
+    // intervals (one instance per variant)
+    if constexpr (V >= 3)
+        if (pl.fp64) return launch_t<2, V, 128, 2, 1, true, false, true>(pl, st);
     if constexpr (CG == 2) {
         if (s == 2) {
             const int units = (pl.max_ctas > 0 ? pl.max_ctas : num_sms()) / CG;

@@ -6,11 +6,11 @@
 namespace bf16x {
 
 int launch_split(int64_t rows, int64_t cols, const float *X, int64_t ldx, uint16_t *P0, uint16_t *P1,
-                 uint16_t *P2, int64_t ldp, bool transpose, cudaStream_t st);
+                 uint16_t *P2, int64_t ldp, bool transpose, cudaStream_t st, bool scaled = false);
 
 int launch_split_ab(int m, int n, int k, const float *A, int64_t lda, uint16_t *Ap, int64_t ldap, int64_t a_plane,
                     const float *B, int64_t ldb, uint16_t *Bp, int64_t ldbp, int64_t b_plane, int npa, int npb,
-                    cudaStream_t st);
+                    cudaStream_t st, bool scaled = false);
 
 struct GemmPlan {
     int m, n, k;
@@ -31,6 +31,8 @@ struct GemmPlan {
     int stream_k;        // 0 = data-parallel only, else hybrid stream-K for the last waves
     int multicast;       // 2 = two CTA pairs per cluster share B tiles (TMA multicast), else 1
     int split_acc;       // 1 = separate TMEM accumulators for bin 0 and bins >= 1 (tile N 128)
+    int scaled;          // 1 = N2 scaled pieces (R29): band transitions scale the accumulator by 2^-8
+    int fp64;            // 1 = FP64 collection of the bins ("d" variants, R30; implies split_acc)
     // fused split (Ap == Bp == nullptr): the FP32 operands, converted to pieces inside the GEMM
     const float *Af, *Bf;   // A (m x k, lda), B (k x n, ldb), column-major, 16-byte aligned
     int64_t lda, ldb;

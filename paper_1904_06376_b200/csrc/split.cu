@@ -20,7 +20,7 @@ namespace bf16x {
 // same layout: each thread splits 8 consecutive rows of one column per iteration;
 // 16-byte vector loads/stores when the whole matrix is 16-byte aligned (vec != 0).
 // ---------------------------------------------------------------------------------
-template <int NP>
+template <int NP, bool SC>
 __device__ __forceinline__ void split_same_body(int64_t rows, int64_t cols, const float *__restrict__ X, int64_t ldx,
                                                 uint16_t *__restrict__ P0, uint16_t *__restrict__ P1,
                                                 uint16_t *__restrict__ P2, int64_t ldp, int vec, int64_t vblock,
@@ -36,10 +36,10 @@ __device__ __forceinline__ void split_same_body(int64_t rows, int64_t cols, cons
             const float4 u = __ldcs(reinterpret_cast<const float4 *>(x + r0));
             const float4 w = __ldcs(reinterpret_cast<const float4 *>(x + r0 + 4));
             uint32_t q[4][3];
-            split_pair<NP>(u.x, u.y, q[0]);
-            split_pair<NP>(u.z, u.w, q[1]);
-            split_pair<NP>(w.x, w.y, q[2]);
-            split_pair<NP>(w.z, w.w, q[3]);
+            split_pair<NP, SC>(u.x, u.y, q[0]);
+            split_pair<NP, SC>(u.z, u.w, q[1]);
+            split_pair<NP, SC>(w.x, w.y, q[2]);
+            split_pair<NP, SC>(w.z, w.w, q[3]);
             __stcs(reinterpret_cast<uint4 *>(P0 + o + r0), make_uint4(q[0][0], q[1][0], q[2][0], q[3][0]));
             if constexpr (NP >= 2)
                 __stcs(reinterpret_cast<uint4 *>(P1 + o + r0), make_uint4(q[0][1], q[1][1], q[2][1], q[3][1]));
@@ -47,7 +47,7 @@ __device__ __forceinline__ void split_same_body(int64_t rows, int64_t cols, cons
                 __stcs(reinterpret_cast<uint4 *>(P2 + o + r0), make_uint4(q[0][2], q[1][2], q[2][2], q[3][2]));
         } else {
             for (int64_t r = r0; r < rows && r < r0 + 8; ++r) {
-                Split3 s = split3(x[r]);
+                Split3 s = split3_t<SC>(x[r]);
                 P0[o + r] = (uint16_t)s.b0;
                 if constexpr (NP >= 2) P1[o + r] = (uint16_t)s.b1;
                 if constexpr (NP >= 3) P2[o + r] = (uint16_t)s.b2;
@@ -56,13 +56,13 @@ __device__ __forceinline__ void split_same_body(int64_t rows, int64_t cols, cons
     }
 }
 
-template <int NP>
+template <int NP, bool SC>
 __global__ void __launch_bounds__(256) split_same_kernel(int64_t rows, int64_t cols, const float *__restrict__ X,
                                                          int64_t ldx, uint16_t *__restrict__ P0,
                                                          uint16_t *__restrict__ P1, uint16_t *__restrict__ P2,
                                                          int64_t ldp, int vec) {
     asm volatile("griddepcontrol.launch_dependents;");
-    split_same_body<NP>(rows, cols, X, ldx, P0, P1, P2, ldp, vec, blockIdx.x, gridDim.x);
+    split_same_body<NP, SC>(rows, cols, X, ldx, P0, P1, P2, ldp, vec, blockIdx.x, gridDim.x);
 }
 
 // ---------------------------------------------------------------------------------
@@ -74,7 +74,7 @@ __global__ void __launch_bounds__(256) split_same_kernel(int64_t rows, int64_t c
 // ---------------------------------------------------------------------------------
 constexpr int TT = 64;
 constexpr int TW = TT / 2 + 1;   // words per smem row (+1 pad)
-template <int NP>
+template <int NP, bool SC>
 __device__ __forceinline__ void split_trans_body(int64_t rows, int64_t cols, const float *__restrict__ X, int64_t ldx,
                                                  uint16_t *__restrict__ P0, uint16_t *__restrict__ P1,
                                                  uint16_t *__restrict__ P2, int64_t ldp, int vec, int64_t vblock,
@@ -110,7 +110,7 @@ __device__ __forceinline__ void split_trans_body(int64_t rows, int64_t cols, con
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
                 uint32_t q[3];
-                split_pair<NP>(a[i], b[i], q);     // lo = column c, hi = column c+1
+                split_pair<NP, SC>(a[i], b[i], q);     // lo = column c, hi = column c+1
 #pragma unroll
                 for (int p = 0; p < NP; ++p) s[p][4 * mq + i][cp] = q[p];
             }
@@ -139,14 +139,14 @@ __device__ __forceinline__ void split_trans_body(int64_t rows, int64_t cols, con
     }
 }
 
-template <int NP>
+template <int NP, bool SC>
 __global__ void __launch_bounds__(256) split_trans_kernel(int64_t rows, int64_t cols, const float *__restrict__ X,
                                                           int64_t ldx, uint16_t *__restrict__ P0,
                                                           uint16_t *__restrict__ P1, uint16_t *__restrict__ P2,
                                                           int64_t ldp, int vec) {
     __shared__ uint32_t s[3][TT][TW];
     asm volatile("griddepcontrol.launch_dependents;");
-    split_trans_body<NP>(rows, cols, X, ldx, P0, P1, P2, ldp, vec, blockIdx.x, gridDim.x, s);
+    split_trans_body<NP, SC>(rows, cols, X, ldx, P0, P1, P2, ldp, vec, blockIdx.x, gridDim.x, s);
 }
 
 // Both GEMM operands in one launch: blocks [0, gA) split A transposed (K-major pieces),
@@ -157,15 +157,24 @@ struct SplitArgs {
     uint16_t *P0, *P1, *P2;
     int vec;
 };
-template <int NPA, int NPB>
+template <int NPA, int NPB, bool SC>
 __global__ void __launch_bounds__(256) split_ab_kernel(SplitArgs a, SplitArgs b, int gA) {
     __shared__ uint32_t s[3][TT][TW];
     asm volatile("griddepcontrol.launch_dependents;");   // let the GEMM's prologue start early
     if ((int)blockIdx.x < gA)
-        split_trans_body<NPA>(a.rows, a.cols, a.X, a.ldx, a.P0, a.P1, a.P2, a.ldp, a.vec, blockIdx.x, gA, s);
+        split_trans_body<NPA, SC>(a.rows, a.cols, a.X, a.ldx, a.P0, a.P1, a.P2, a.ldp, a.vec, blockIdx.x, gA, s);
     else
-        split_same_body<NPB>(b.rows, b.cols, b.X, b.ldx, b.P0, b.P1, b.P2, b.ldp, b.vec, blockIdx.x - gA,
+        split_same_body<NPB, SC>(b.rows, b.cols, b.X, b.ldx, b.P0, b.P1, b.P2, b.ldp, b.vec, blockIdx.x - gA,
                              gridDim.x - gA);
+}
+
+template <bool SC>
+static void split_ab_launch(const SplitArgs &a, const SplitArgs &b, int gA, unsigned grid, int npa, int npb,
+                            cudaStream_t st) {
+    if (npa == 1 && npb == 1) split_ab_kernel<1, 1, SC><<<grid, 256, 0, st>>>(a, b, gA);
+    else if (npa == 2 && npb == 2) split_ab_kernel<2, 2, SC><<<grid, 256, 0, st>>>(a, b, gA);
+    else if (npa == 2 && npb == 3) split_ab_kernel<2, 3, SC><<<grid, 256, 0, st>>>(a, b, gA);
+    else split_ab_kernel<3, 3, SC><<<grid, 256, 0, st>>>(a, b, gA);
 }
 
 static int sm_count() {
@@ -179,9 +188,9 @@ static int sm_count() {
     return n;
 }
 
-int launch_split(int64_t rows, int64_t cols, const float *X, int64_t ldx, uint16_t *P0, uint16_t *P1, uint16_t *P2,
-                 int64_t ldp, bool transpose, cudaStream_t st) {
-    if (rows == 0 || cols == 0) return BF16X_SUCCESS;
+template <bool SC>
+static void split_launch(int64_t rows, int64_t cols, const float *X, int64_t ldx, uint16_t *P0, uint16_t *P1,
+                         uint16_t *P2, int64_t ldp, bool transpose, cudaStream_t st) {
     const int np = P2 ? 3 : (P1 ? 2 : 1);
     if (!transpose) {
         const bool vec = ((reinterpret_cast<uintptr_t>(X) & 15u) == 0) && ldx % 4 == 0 &&
@@ -192,26 +201,33 @@ int launch_split(int64_t rows, int64_t cols, const float *X, int64_t ldx, uint16
         int64_t g = (total + 255) / 256;
         const int64_t cap = (int64_t)sm_count() * 8 * 8;
         if (g > cap) g = cap;
-        if (np == 1) split_same_kernel<1><<<(unsigned)g, 256, 0, st>>>(rows, cols, X, ldx, P0, P1, P2, ldp, vec);
-        else if (np == 2) split_same_kernel<2><<<(unsigned)g, 256, 0, st>>>(rows, cols, X, ldx, P0, P1, P2, ldp, vec);
-        else split_same_kernel<3><<<(unsigned)g, 256, 0, st>>>(rows, cols, X, ldx, P0, P1, P2, ldp, vec);
+        if (np == 1) split_same_kernel<1, SC><<<(unsigned)g, 256, 0, st>>>(rows, cols, X, ldx, P0, P1, P2, ldp, vec);
+        else if (np == 2) split_same_kernel<2, SC><<<(unsigned)g, 256, 0, st>>>(rows, cols, X, ldx, P0, P1, P2, ldp, vec);
+        else split_same_kernel<3, SC><<<(unsigned)g, 256, 0, st>>>(rows, cols, X, ldx, P0, P1, P2, ldp, vec);
     } else {
         const bool vec = ((reinterpret_cast<uintptr_t>(X) & 15u) == 0) && ldx % 4 == 0;
         const int64_t tiles = ((rows + TT - 1) / TT) * ((cols + TT - 1) / TT);
         int64_t g = tiles;
         const int64_t cap = (int64_t)sm_count() * 8;
         if (g > cap) g = cap;
-        if (np == 1) split_trans_kernel<1><<<(unsigned)g, 256, 0, st>>>(rows, cols, X, ldx, P0, P1, P2, ldp, vec);
-        else if (np == 2) split_trans_kernel<2><<<(unsigned)g, 256, 0, st>>>(rows, cols, X, ldx, P0, P1, P2, ldp, vec);
-        else split_trans_kernel<3><<<(unsigned)g, 256, 0, st>>>(rows, cols, X, ldx, P0, P1, P2, ldp, vec);
+        if (np == 1) split_trans_kernel<1, SC><<<(unsigned)g, 256, 0, st>>>(rows, cols, X, ldx, P0, P1, P2, ldp, vec);
+        else if (np == 2) split_trans_kernel<2, SC><<<(unsigned)g, 256, 0, st>>>(rows, cols, X, ldx, P0, P1, P2, ldp, vec);
+        else split_trans_kernel<3, SC><<<(unsigned)g, 256, 0, st>>>(rows, cols, X, ldx, P0, P1, P2, ldp, vec);
     }
+}
+
+int launch_split(int64_t rows, int64_t cols, const float *X, int64_t ldx, uint16_t *P0, uint16_t *P1, uint16_t *P2,
+                 int64_t ldp, bool transpose, cudaStream_t st, bool scaled) {
+    if (rows == 0 || cols == 0) return BF16X_SUCCESS;
+    if (scaled) split_launch<true>(rows, cols, X, ldx, P0, P1, P2, ldp, transpose, st);
+    else split_launch<false>(rows, cols, X, ldx, P0, P1, P2, ldp, transpose, st);
     count_launch();
     return check_launch("split");
 }
 
 int launch_split_ab(int m, int n, int k, const float *A, int64_t lda, uint16_t *Ap, int64_t ldap, int64_t a_plane,
                     const float *B, int64_t ldb, uint16_t *Bp, int64_t ldbp, int64_t b_plane, int npa, int npb,
-                    cudaStream_t st) {
+                    cudaStream_t st, bool scaled) {
     if (m == 0 || n == 0 || k == 0) return BF16X_SUCCESS;
     SplitArgs a{m, k, lda, ldap, A, Ap, npa > 1 ? Ap + a_plane : nullptr, npa > 2 ? Ap + 2 * a_plane : nullptr, 0};
     SplitArgs b{k, n, ldb, ldbp, B, Bp, npb > 1 ? Bp + b_plane : nullptr, npb > 2 ? Bp + 2 * b_plane : nullptr, 0};
@@ -222,10 +238,8 @@ int launch_split_ab(int m, int n, int k, const float *A, int64_t lda, uint16_t *
     const double wa = (double)m * k, wb = (double)k * n;
     int gA = (int)(grid * wa / (wa + wb));
     gA = gA < 1 ? 1 : (gA > grid - 1 ? (int)grid - 1 : gA);
-    if (npa == 1 && npb == 1) split_ab_kernel<1, 1><<<(unsigned)grid, 256, 0, st>>>(a, b, gA);
-    else if (npa == 2 && npb == 2) split_ab_kernel<2, 2><<<(unsigned)grid, 256, 0, st>>>(a, b, gA);
-    else if (npa == 2 && npb == 3) split_ab_kernel<2, 3><<<(unsigned)grid, 256, 0, st>>>(a, b, gA);
-    else split_ab_kernel<3, 3><<<(unsigned)grid, 256, 0, st>>>(a, b, gA);
+    if (scaled) split_ab_launch<true>(a, b, gA, (unsigned)grid, npa, npb, st);
+    else split_ab_launch<false>(a, b, gA, (unsigned)grid, npa, npb, st);
     count_launch();
     return check_launch("split_ab");
 }
@@ -251,7 +265,7 @@ extern "C" int bf16x_split(int64_t rows, int64_t cols, const float *X, int64_t l
     if (a) return a;
     int ok = arch_ok();
     if (ok) return ok;
-    return launch_split(rows, cols, X, ldx, P0, P1, P2, ldp, false, (cudaStream_t)stream);
+    return launch_split(rows, cols, X, ldx, P0, P1, P2, ldp, false, (cudaStream_t)stream, false);
 }
 
 extern "C" int bf16x_split_operands(int m, int n, int k, const float *A, int64_t lda, const float *B, int64_t ldb,
@@ -268,7 +282,7 @@ extern "C" int bf16x_split_operands(int m, int n, int k, const float *A, int64_t
     int ok = arch_ok();
     if (ok) return ok;
     return launch_split_ab(m, n, k, A, lda, Ap, ldap, a_plane, B, ldb, Bp, ldbp, b_plane, pieces, pieces,
-                           (cudaStream_t)stream);
+                           (cudaStream_t)stream, false);
 }
 
 extern "C" int bf16x_split_t(int64_t rows, int64_t cols, const float *X, int64_t ldx, uint16_t *P0, uint16_t *P1,
@@ -277,5 +291,19 @@ extern "C" int bf16x_split_t(int64_t rows, int64_t cols, const float *X, int64_t
     if (a) return a;
     int ok = arch_ok();
     if (ok) return ok;
-    return launch_split(rows, cols, X, ldx, P0, P1, P2, ldp, true, (cudaStream_t)stream);
+    return launch_split(rows, cols, X, ldx, P0, P1, P2, ldp, true, (cudaStream_t)stream, false);
+}
+
+// N2 scaled pieces (R29), either layout: flags BF16X_SCALED_PIECES (required, documents the
+// piece format) | BF16X_SPLIT_TRANSPOSED (K-major output as bf16x_split_t).
+extern "C" int bf16x_split_ex(int64_t rows, int64_t cols, const float *X, int64_t ldx, uint16_t *P0, uint16_t *P1,
+                              uint16_t *P2, int64_t ldp, unsigned flags, bf16x_stream_t stream) {
+    const bool tr = (flags & BF16X_SPLIT_TRANSPOSED) != 0;
+    int a = split_args(rows, cols, ldx, P0, P1, P2, ldp, tr ? cols : rows);
+    if (a) return a;
+    if (flags & ~(BF16X_SCALED_PIECES | BF16X_SPLIT_TRANSPOSED)) return -9;
+    int ok = arch_ok();
+    if (ok) return ok;
+    return launch_split(rows, cols, X, ldx, P0, P1, P2, ldp, tr, (cudaStream_t)stream,
+                        (flags & BF16X_SCALED_PIECES) != 0);
 }

@@ -36,7 +36,10 @@ def test_gemm_argument_errors():
     assert f(4, 4, 4, 1.0, None, 4, None, 4, 0.0, None, 3, 6) == -11
     assert f(4, 4, 4, 1.0, None, 4, None, 4, 0.0, None, 4, 4) == -12
     ex = L.bf16x_gemm_ex
-    assert ex(4, 4, 4, 1.0, None, 4, None, 4, 0.0, None, 4, 6, 8, None, 0, 0, None, 0, 0, None, None, 0, None) == -13
+    assert ex(4, 4, 4, 1.0, None, 4, None, 4, 0.0, None, 4, 6, 32, None, 0, 0, None, 0, 0, None, None, 0, None) == -13
+    # FP64 combine (R30) excludes the accumulator carry and the one-product variant
+    assert ex(4, 4, 4, 1.0, None, 4, None, 4, 0.0, None, 4, 6, 9, None, 0, 0, None, 0, 0, 16, None, 0, None) == -13
+    assert ex(4, 4, 4, 1.0, None, 4, None, 4, 0.0, None, 4, 1, 8, None, 0, 0, None, 0, 0, None, None, 0, None) == -13
     assert ex(4, 4, 4, 1.0, None, 4, None, 4, 0.0, None, 4, 6, 0, 16, 3, 32, None, 0, 0, None, None, 0, None) == -14
     assert ex(4, 4, 4, 1.0, None, 4, None, 4, 0.0, None, 4, 6, 0, None, 0, 0, 16, 8, 4, None, None, 0, None) == -16
     assert ex(4, 4, 4, 1.0, None, 4, None, 4, 0.0, None, 4, 6, 1, None, 0, 0, None, 0, 0, None, None, 0, None) == -19
@@ -52,6 +55,11 @@ def test_split_argument_errors():
     assert s(4, 2, None, 4, 16, None, 32, 4, None) == -7
     assert s(4, 2, None, 4, 16, None, None, 3, None) == -8
     assert L.bf16x_split_t(4, 6, None, 4, 16, None, None, 5, None) == -8
+    se = L.bf16x_split_ex
+    se.argtypes = [ctypes.c_int64] * 2 + [ctypes.c_void_p, ctypes.c_int64] + [ctypes.c_void_p] * 3 + \
+        [ctypes.c_int64, ctypes.c_uint, ctypes.c_void_p]
+    assert se(4, 2, None, 4, 16, None, None, 4, 64, None) == -9          # unknown flag
+    assert se(4, 6, None, 4, 16, None, None, 5, 4 | 16, None) == -8      # transposed: ldp >= cols
 
 
 def test_workspace_size_formula():
