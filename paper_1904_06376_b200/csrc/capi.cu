@@ -90,7 +90,7 @@ static int gemm_args(int m, int n, int k, int lda, int ldb, int ldc, int variant
 int gemm_core(int m, int n, int k, float alpha, const float *A, int lda, const float *B, int ldb, float beta,
               float *C, int ldc, int variant, unsigned flags, const uint16_t *Ap, int64_t ldap, int64_t a_plane,
               const uint16_t *Bp, int64_t ldbp, int64_t b_plane, float *acc, void *ws, size_t ws_bytes,
-              cudaStream_t st, int cta_group) {
+              cudaStream_t st, int cta_group, bool allow_stream_k) {
     int rc = arch_ok();
     if (rc) return rc;
     if (m == 0 || n == 0) return BF16X_SUCCESS;
@@ -119,7 +119,7 @@ int gemm_core(int m, int n, int k, float alpha, const float *A, int lda, const f
     pl.max_ctas = 0;
     pl.tile_n = g_force_bn;
     pl.stages_per_interval = g_force_spi;
-    pl.stream_k = g_stream_k;
+    pl.stream_k = allow_stream_k ? g_stream_k : 0;   // (its workspace is shared: one stream at a time)
     pl.multicast = g_multicast;
     pl.split_acc = g_split_acc;
     pl.scaled = (flags & BF16X_SCALED_PIECES) ? 1 : 0;
@@ -178,7 +178,7 @@ int bf16x_gemm(int m, int n, int k, float alpha, const float *A, int lda, const 
     int a = gemm_args(m, n, k, lda, ldb, ldc, variant);
     if (a) return a;
     return gemm_core(m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, variant, 0u, nullptr, 0, 0, nullptr, 0, 0,
-                     nullptr, nullptr, 0, g_stream, 0);
+                     nullptr, nullptr, 0, g_stream, 0, true);
 }
 
 size_t bf16x_gemm_workspace_size(int m, int n, int k, int variant) {
@@ -203,7 +203,7 @@ int bf16x_gemm_ex(int m, int n, int k, float alpha, const float *A, int lda, con
         return -16;
     if ((flags & (BF16X_ACC_IN | BF16X_ACC_OUT)) && !acc_carry) return -19;
     return gemm_core(m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, variant, flags, A_pieces, ldap, a_plane,
-                     B_pieces, ldbp, b_plane, acc_carry, workspace_ptr, ws_bytes, (cudaStream_t)stream, 0);
+                     B_pieces, ldbp, b_plane, acc_carry, workspace_ptr, ws_bytes, (cudaStream_t)stream, 0, true);
 }
 
 // testing hook (not in the public header): force cta_group 1 or 2
@@ -212,15 +212,30 @@ int bf16x_gemm_cg(int m, int n, int k, float alpha, const float *A, int lda, con
     int a = gemm_args(m, n, k, lda, ldb, ldc, variant);
     if (a) return a;
     return gemm_core(m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, variant, 0u, nullptr, 0, 0, nullptr, 0, 0,
-                     nullptr, nullptr, 0, (cudaStream_t)stream, cta_group);
+                     nullptr, nullptr, 0, (cudaStream_t)stream, cta_group, true);
 }
 
 static std::mutex g_host_mu;
 static float *g_hA = nullptr, *g_hB = nullptr, *g_hC = nullptr, *g_hAp = nullptr;   // g_hAp: A's pieces
 static size_t g_hA_n = 0, g_hB_n = 0, g_hC_n = 0, g_hAp_n = 0;
 // host-path pipeline: copy-in / copy-out streams and per-chunk events (created once)
-constexpr int kHostChunks = 8;
-static cudaStream_t g_s_in = nullptr, g_s_out = nullptr;
+constexpr int kHostChunks = 16;     // event slots; the chunk count is min(g_host_chunks, n / 256)
+constexpr int kHostStreams = 4;     // compute streams: consecutive chunk GEMMs run concurrently
+static int g_host_chunks = 12;
+static cudaStream_t g_s_in = nullptr, g_s_out = nullptr, g_s_comp[kHostStreams] = {};
+static float *g_hBp = nullptr;      // per-compute-stream B piece slices
+static size_t g_hBp_n = 0;
+static cudaEvent_t g_ev_asplit = nullptr, g_ev_end[kHostStreams] = {};
+// optional timeline of the last pipelined call (bf16x_host_timeline): events with timing
+static bool g_tl_on = false;
+static cudaEvent_t g_tl_ev[4 + 3 * kHostChunks] = {};
+static int g_tl_n = 0;
+static int tl_record(int slot, cudaStream_t s) {
+    if (!g_tl_on) return 0;
+    if (!g_tl_ev[slot] && cudaEventCreate(&g_tl_ev[slot]) != cudaSuccess) return 1;
+    if (slot + 1 > g_tl_n) g_tl_n = slot + 1;
+    return cudaEventRecord(g_tl_ev[slot], s) != cudaSuccess;
+}
 static cudaEvent_t g_ev_a = nullptr, g_ev_b[kHostChunks], g_ev_c[kHostChunks], g_ev_done = nullptr;
 
 static int ensure(float **p, size_t *cap, size_t n) {
@@ -242,6 +257,11 @@ static int host_pipeline_init() {
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&g_s_out, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&g_ev_a, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&g_ev_done, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&g_ev_asplit, cudaEventDisableTiming);
+    for (int q = 0; q < kHostStreams && e == cudaSuccess; ++q) {
+        e = cudaStreamCreateWithFlags(&g_s_comp[q], cudaStreamNonBlocking);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&g_ev_end[q], cudaEventDisableTiming);
+    }
     for (int j = 0; j < kHostChunks && e == cudaSuccess; ++j) {
         e = cudaEventCreateWithFlags(&g_ev_b[j], cudaEventDisableTiming);
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&g_ev_c[j], cudaEventDisableTiming);
@@ -256,11 +276,15 @@ static int host_pipeline_init() {
 // Host-buffer GEMM.  Small problems: copy in, GEMM, copy out on the library stream.  Large ones
 // are pipelined over column chunks of B and C so the PCIe transfers overlap the device work:
 //   copy-in stream : A, then B chunk 0, 1, ... (and C chunks when beta != 0)
-//   library stream : split A once (K-major pieces); per chunk, once its B has landed: split the
-//                    chunk and run the GEMM on the pre-split A
+//   library stream : split A once (K-major pieces)
+//   compute streams: chunk j on stream j % 4, once its B has landed: split the chunk (own piece
+//                    slice) and run the GEMM on the pre-split A.  A narrow chunk fills only part
+//                    of the GPU, so consecutive chunks' GEMMs run side by side and keep up with
+//                    the PCIe stream; the tail after the last byte lands is one chunk's GEMM
 //   copy-out stream: C chunk j as soon as its GEMM is done (overlaps the next chunks' copy-in)
-// Each chunk is an independent GEMM: its columns equal bf16x_gemm on that column block (chunk
-// width: n / min(8, n / 512) rounded up to 256 columns when m*k >= 2^20 and n >= 1024).
+// Each chunk is an independent GEMM: its columns equal bf16x_gemm on that column block without
+// the stream-K schedule (chunk width: n / min(12, n / 256) rounded up to 256 columns when
+// m*k >= 2^20 and n >= 1024).
 int bf16x_gemm_host(int m, int n, int k, float alpha, const float *A_host, int lda, const float *B_host, int ldb,
                     float beta, float *C_host, int ldc, int variant) {
     int a = gemm_args(m, n, k, lda, ldb, ldc, variant);
@@ -275,10 +299,10 @@ int bf16x_gemm_host(int m, int n, int k, float alpha, const float *A_host, int l
         return rc;
     const int p = pieces_a(variant);
     const int64_t kp = round_up8(k);
-    // chunk width: a multiple of 256 columns, >= 512, at most kHostChunks chunks
+    // chunk width: a multiple of 256 columns, at most g_host_chunks chunks
     int nchunk = 1;
     if (k > 0 && alpha != 0.f && (int64_t)m * k >= (1 << 20) && n >= 1024)
-        nchunk = std::min(kHostChunks, n / 512);
+        nchunk = std::max(1, std::min(std::min(g_host_chunks, kHostChunks), n / 256));
     if (nchunk > 1) {
         if ((rc = host_pipeline_init())) return rc;
         if ((rc = ensure(&g_hAp, &g_hAp_n, ((size_t)p * m * kp + 1) / 2))) return rc;
@@ -300,7 +324,7 @@ int bf16x_gemm_host(int m, int n, int k, float alpha, const float *A_host, int l
             return BF16X_ERR_CUDA;
         }
         rc = gemm_core(m, n, k, alpha, g_hA, m, g_hB, k > 0 ? k : 1, beta, g_hC, m, variant, 0u, nullptr, 0, 0,
-                       nullptr, 0, 0, nullptr, nullptr, 0, st, 0);
+                       nullptr, 0, 0, nullptr, nullptr, 0, st, 0, true);
         if (rc) return rc;
         e = cudaMemcpy2DAsync(C_host, (size_t)ldc * 4, g_hC, (size_t)m * 4, (size_t)m * 4, n, cudaMemcpyDeviceToHost,
                               st);
@@ -318,10 +342,13 @@ int bf16x_gemm_host(int m, int n, int k, float alpha, const float *A_host, int l
     // the caller's stream may still be using the device buffers / host arrays
     e = cudaEventRecord(g_ev_done, st);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(g_s_in, g_ev_done, 0);
+    g_tl_n = 0;
+    tl_record(0, g_s_in);                                     // timeline: start
     if (e == cudaSuccess)
         e = cudaMemcpy2DAsync(g_hA, (size_t)m * 4, A_host, (size_t)lda * 4, (size_t)m * 4, k, cudaMemcpyHostToDevice,
                               g_s_in);
     if (e == cudaSuccess) e = cudaEventRecord(g_ev_a, g_s_in);
+    tl_record(1, g_s_in);                                     // A landed
     for (int j = 0; j < nchunk && e == cudaSuccess; ++j) {
         const int c0 = j * cw, nj = std::min(cw, n - c0);
         e = cudaMemcpy2DAsync(g_hB + (size_t)c0 * k, (size_t)k * 4, B_host + (size_t)c0 * ldb, (size_t)ldb * 4,
@@ -330,6 +357,7 @@ int bf16x_gemm_host(int m, int n, int k, float alpha, const float *A_host, int l
             e = cudaMemcpy2DAsync(g_hC + (size_t)c0 * m, (size_t)m * 4, C_host + (size_t)c0 * ldc, (size_t)ldc * 4,
                                   (size_t)m * 4, nj, cudaMemcpyHostToDevice, g_s_in);
         if (e == cudaSuccess) e = cudaEventRecord(g_ev_b[j], g_s_in);
+        tl_record(4 + 3 * j, g_s_in);                         // B chunk j landed
     }
     if (e == cudaSuccess) e = cudaStreamWaitEvent(st, g_ev_a, 0);
     if (e != cudaSuccess) {
@@ -338,19 +366,35 @@ int bf16x_gemm_host(int m, int n, int k, float alpha, const float *A_host, int l
     }
     rc = launch_split(m, k, g_hA, m, ap, p > 1 ? ap + a_plane : nullptr, p > 2 ? ap + 2 * a_plane : nullptr, kp, true,
                       st);
-    for (int j = 0; j < nchunk && rc == BF16X_SUCCESS; ++j) {
+    if (rc == BF16X_SUCCESS) e = cudaEventRecord(g_ev_asplit, st);
+    tl_record(2, st);                                         // A split
+    const int pb = pieces_b(variant);
+    const size_t slice = 2ull * pb * (size_t)cw * (size_t)kp;   // bytes of one chunk's B pieces
+    if (rc == BF16X_SUCCESS && e == cudaSuccess)
+        rc = ensure(&g_hBp, &g_hBp_n, (kHostStreams * slice + 3) / 4);
+    for (int q = 0; q < kHostStreams && rc == BF16X_SUCCESS && e == cudaSuccess; ++q)
+        e = cudaStreamWaitEvent(g_s_comp[q], g_ev_asplit, 0);
+    for (int j = 0; j < nchunk && rc == BF16X_SUCCESS && e == cudaSuccess; ++j) {
         const int c0 = j * cw, nj = std::min(cw, n - c0);
-        e = cudaStreamWaitEvent(st, g_ev_b[j], 0);
+        cudaStream_t cs = g_s_comp[j % kHostStreams];
+        e = cudaStreamWaitEvent(cs, g_ev_b[j], 0);
         if (e != cudaSuccess) break;
         rc = gemm_core(m, nj, k, alpha, nullptr, m, g_hB + (size_t)c0 * k, k, beta, g_hC + (size_t)c0 * m, m, variant,
-                       0u, ap, kp, a_plane, nullptr, 0, 0, nullptr, nullptr, 0, st, 0);
+                       0u, ap, kp, a_plane, nullptr, 0, 0, nullptr,
+                       reinterpret_cast<uint8_t *>(g_hBp) + (j % kHostStreams) * slice, slice, cs, 0, false);
         if (rc) break;
-        e = cudaEventRecord(g_ev_c[j], st);
+        e = cudaEventRecord(g_ev_c[j], cs);
+        tl_record(5 + 3 * j, cs);                             // GEMM j done
         if (e == cudaSuccess) e = cudaStreamWaitEvent(g_s_out, g_ev_c[j], 0);
         if (e == cudaSuccess)
             e = cudaMemcpy2DAsync(C_host + (size_t)c0 * ldc, (size_t)ldc * 4, g_hC + (size_t)c0 * m, (size_t)m * 4,
                                   (size_t)m * 4, nj, cudaMemcpyDeviceToHost, g_s_out);
+        tl_record(6 + 3 * j, g_s_out);                        // C chunk j back on the host
         if (e != cudaSuccess) break;
+    }
+    for (int q = 0; q < kHostStreams && e == cudaSuccess; ++q) {   // the library stream joins the
+        e = cudaEventRecord(g_ev_end[q], g_s_comp[q]);               // compute streams (error paths too)
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(st, g_ev_end[q], 0);
     }
     if (rc) return rc;
     if (e == cudaSuccess) e = cudaStreamSynchronize(g_s_out);
@@ -380,8 +424,9 @@ void bf16x_release(void) {
     if (g_hB) cudaFree(g_hB);
     if (g_hC) cudaFree(g_hC);
     if (g_hAp) cudaFree(g_hAp);
-    g_hA = g_hB = g_hC = g_hAp = nullptr;
-    g_hA_n = g_hB_n = g_hC_n = g_hAp_n = 0;
+    if (g_hBp) cudaFree(g_hBp);
+    g_hA = g_hB = g_hC = g_hAp = g_hBp = nullptr;
+    g_hA_n = g_hB_n = g_hC_n = g_hAp_n = g_hBp_n = 0;
 }
 
 const char *bf16x_status_string(int status) {
@@ -412,6 +457,23 @@ uint64_t bf16x_launch_count(void) { return g_launches.load(); }
 int bf16x_default_cta_group(void) { return default_cta_group(); }
 void bf16x_stream_k(int on) { g_stream_k = on; }
 void bf16x_split_acc(int on) { g_split_acc = on; }
+// Timeline of the last pipelined bf16x_gemm_host call, ms since its start: [0] start, [1] A
+// landed, [2] A split, [3] unused, then per chunk j: [4+3j] B_j landed, [5+3j] GEMM_j done,
+// [6+3j] C_j copied back (-1 = not recorded).  on: enable recording for later calls.
+int bf16x_host_timeline(int on, float *ms, int cap) {
+    g_tl_on = on != 0;
+    int n = 0;
+    for (int i = 0; i < g_tl_n && i < cap; ++i, ++n) {
+        float t = -1.f;
+        if (g_tl_ev[i] && g_tl_ev[0] && cudaEventElapsedTime(&t, g_tl_ev[0], g_tl_ev[i]) != cudaSuccess) {
+            cudaGetLastError();
+            t = -1.f;
+        }
+        ms[i] = t;
+    }
+    return n;
+}
+void bf16x_host_chunks(int n) { g_host_chunks = n > 0 ? n : 12; }   // bf16x_gemm_host pipeline depth
 void bf16x_fused_split(int on) { g_fused = on; }   // 1: split inside the GEMM when eligible (default 0)
 void bf16x_multicast(int pairs) { g_multicast = pairs; }   // 0 = auto, 1 = off, 2 = on
 void bf16x_tune(int cta_group, int tile_n, int stages_per_interval) {

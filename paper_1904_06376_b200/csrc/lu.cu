@@ -29,7 +29,7 @@ namespace bf16x {
 int gemm_core(int m, int n, int k, float alpha, const float *A, int lda, const float *B, int ldb, float beta,
               float *C, int ldc, int variant, unsigned flags, const uint16_t *Ap, int64_t ldap, int64_t a_plane,
               const uint16_t *Bp, int64_t ldbp, int64_t b_plane, float *acc, void *ws, size_t ws_bytes,
-              cudaStream_t st, int cta_group);
+              cudaStream_t st, int cta_group, bool allow_stream_k = true);
 
 constexpr int kLuThreads = 256;
 

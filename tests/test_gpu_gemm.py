@@ -156,16 +156,22 @@ def test_row_major_torch_and_host_api(orc):
     assert orc.normwise_error(Cr.cpu().numpy(), C64, A, B) <= RATIO * eo
 
 
+@pytest.mark.parametrize("depth", [4, 12, 16])
 @pytest.mark.parametrize("beta", [0.0, 0.75])
-def test_host_api_pipelined_chunks(orc, beta):
-    """bf16x_gemm_host's chunked pipeline (m*k >= 2^20, n >= 1024): every column chunk equals
-    the device GEMM on that column block bit for bit; sampled columns meet the oracle bar."""
+def test_host_api_pipelined_chunks(orc, beta, depth):
+    """bf16x_gemm_host's chunked pipeline (m*k >= 2^20, n >= 1024; chunk GEMMs on 4 concurrent
+    compute streams, each with its own piece slice): every column chunk equals the device GEMM
+    on that column block bit for bit; sampled columns meet the oracle bar."""
     m, k, n = 1024, 1100, 2600
     A = synthetic.uniform(m, k, seed=21)
     B = synthetic.uniform(k, n, seed=22)
     C0 = synthetic.uniform(m, n, seed=23)
-    Gh = bx.gemm_host(A, B, C=np.asfortranarray(C0.copy()), alpha=1.25, beta=beta, variant=6)
-    nchunk = min(8, n // 512)
+    bx.lib().bf16x_host_chunks(depth)
+    try:
+        Gh = bx.gemm_host(A, B, C=np.asfortranarray(C0.copy()), alpha=1.25, beta=beta, variant=6)
+    finally:
+        bx.lib().bf16x_host_chunks(0)
+    nchunk = min(depth, n // 256)
     cw = ((n + nchunk - 1) // nchunk + 255) // 256 * 256
     Ad = torch.from_numpy(np.asfortranarray(A)).cuda()
     for c0 in range(0, n, cw):
