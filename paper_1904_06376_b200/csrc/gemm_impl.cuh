@@ -23,7 +23,7 @@ constexpr int kThreadsFused = kThreads + kNumXfWarps * 32;
 constexpr int kF32Tile = kBM * kBK * 4;   // one FP32 operand tile per CTA per stage (16 KB)
 constexpr int kTmemCols = 512;        // two accumulator buffers at column 0 and 256
 constexpr int kTmemBufStride = 256;
-constexpr int kGroupM = 8;            // tile raster: 8 m-tiles per group for L2 reuse
+constexpr int kGroupM = 8;            // tile raster: 8 m-tiles per group for L2 reuse (default)
 constexpr int kDefaultCtaGroup = 2;   // 2-CTA pairs, 64-k promotion interval
 constexpr int kSmemBudget = 224 * 1024;
 
@@ -82,6 +82,7 @@ struct KParams {
     unsigned int *sk_flags;
     unsigned int epoch;
     int scaled;            // N2 scaled pieces (R29): scale the accumulator by 2^-8 per bin step
+    int group_m;           // tile raster: m-tiles per group
 };
 
 struct Work {
@@ -122,11 +123,11 @@ struct WorkIter {
     }
 };
 
-__device__ __forceinline__ void tile_coords(int tile, int tiles_m, int tiles_n, int &tm, int &tn) {
-    const int per_group = kGroupM * tiles_n;
+__device__ __forceinline__ void tile_coords(int tile, int tiles_m, int tiles_n, int group_m, int &tm, int &tn) {
+    const int per_group = group_m * tiles_n;
     const int group = tile / per_group;
-    const int first_m = group * kGroupM;
-    const int gm = min(kGroupM, tiles_m - first_m);
+    const int first_m = group * group_m;
+    const int gm = min(group_m, tiles_m - first_m);
     const int r = tile - group * per_group;
     tm = first_m + r % gm;
     tn = r / gm;
@@ -284,7 +285,7 @@ __global__ void __launch_bounds__(FU ? kThreadsFused : kThreads, 1)
                 Work w;
                 while (it.next(p, w)) {
                     int tm, tn;
-                    tile_coords(w.tile, p.tiles_m, p.tiles_n, tm, tn);
+                    tile_coords(w.tile, p.tiles_m, p.tiles_n, p.group_m, tm, tn);
                     tm = tm * MC + (int)pair;
                     const int a_row = tm * Cf::TILE_M + (int)rank * kBM;
                     const int b_row = tn * BN + (int)rank * Cf::BN_LOCAL;
@@ -387,7 +388,7 @@ __global__ void __launch_bounds__(FU ? kThreadsFused : kThreads, 1)
         Work w;
         while (it.next(p, w)) {
             int tm, tn;
-            tile_coords(w.tile, p.tiles_m, p.tiles_n, tm, tn);
+            tile_coords(w.tile, p.tiles_m, p.tiles_n, p.group_m, tm, tn);
             tm = tm * MC + (int)pair;
             const int row = tm * Cf::TILE_M + (int)rank * kBM + quad * 32 + lane;
             const int col0 = tn * BN + half * EC;
@@ -673,6 +674,10 @@ int launch_t(const GemmPlan &pl, cudaStream_t st) {
     kp.sk_flags = nullptr;
     kp.epoch = 0;
     kp.scaled = pl.scaled;
+    // raster group height: row-major raster (1) while a wave spans whole rows of at most 16
+    // tiles (measured r06, tools/raster_probe.py: 4096^3 x6 +1.5 %, GEMM DRAM reads 830 -> 630
+    // MB), 8-tall groups for wider outputs (8192^3: 8 beats 1 by 3-5 %)
+    kp.group_m = pl.group_m > 0 ? pl.group_m : (kp.tiles_n <= 16 ? 1 : kGroupM);
     const int ncl = grid / CL;
     if (pl.stream_k != 0 && !(pl.flags & (BF16X_ACC_IN | BF16X_ACC_OUT)) && tiles > ncl && tiles % ncl != 0) {
         const int full = tiles / ncl;

@@ -33,6 +33,7 @@ struct GemmPlan {
     int split_acc;       // 1 = separate TMEM accumulators for bin 0 and bins >= 1 (tile N 128)
     int scaled;          // 1 = N2 scaled pieces (R29): band transitions scale the accumulator by 2^-8
     int fp64;            // 1 = FP64 collection of the bins ("d" variants, R30; implies split_acc)
+    int group_m;         // tile raster group height in m-tiles (0 = default 8)
     // fused split (Ap == Bp == nullptr): the FP32 operands, converted to pieces inside the GEMM
     const float *Af, *Bf;   // A (m x k, lda), B (k x n, ldb), column-major, 16-byte aligned
     int64_t lda, ldb;
