@@ -17,6 +17,7 @@ static std::mutex g_ws_mu;
 static void *g_ws = nullptr;
 static size_t g_ws_bytes = 0;
 static int g_group_m = 0;   // tile raster group (bf16x_group_m hook; 0 = default)
+static int g_split_ahead = 0;   // split inside the GEMM (split-ahead warps; opt-in, not faster)
 static int g_force_cg = 0, g_force_bn = 0, g_force_spi = 0, g_stream_k = 1, g_multicast = 0, g_split_acc = 0, g_fused = 0;  // tuning overrides (bf16x_tune; not in the public ABI)
 
 void set_cuda_error(cudaError_t e, const char *where) {
@@ -126,12 +127,24 @@ int gemm_core(int m, int n, int k, float alpha, const float *A, int lda, const f
     pl.scaled = (flags & BF16X_SCALED_PIECES) ? 1 : 0;
     pl.fp64 = (flags & BF16X_FP64_COMBINE) ? 1 : 0;
     pl.group_m = g_group_m;
+    pl.split_ahead = 0;
     const bool sc = pl.scaled != 0;
     pl.Af = A; pl.Bf = B; pl.lda = lda; pl.ldb = ldb;
     if (!Ap && !Bp && g_fused && !sc && !pl.fp64) {   // split inside the GEMM when the plan qualifies
         pl.Ap = nullptr; pl.Bp = nullptr;
         const int frc = launch_gemm_fused(pl, st);
         if (frc != -1) return frc;
+    }
+    if (!Ap && !Bp && g_split_ahead && allow_stream_k && split_ahead_ok(pl)) {
+        // the GEMM's split-ahead warps write the pieces into the workspace (pre-pass layout)
+        pl.Ap = (uint16_t *)w;
+        pl.ldap = kp;
+        pl.a_plane = (int64_t)m * kp;
+        pl.Bp = (uint16_t *)w + pa * pl.a_plane;
+        pl.ldbp = kp;
+        pl.b_plane = (int64_t)n * kp;
+        pl.split_ahead = 1;
+        return launch_gemm_pieces(pl, st);
     }
     if (!Ap && !Bp) {   // both operands: one pre-pass launch
         uint16_t *a = (uint16_t *)w;
@@ -460,6 +473,7 @@ int bf16x_default_cta_group(void) { return default_cta_group(); }
 void bf16x_stream_k(int on) { g_stream_k = on; }
 void bf16x_split_acc(int on) { g_split_acc = on; }
 void bf16x_group_m(int g) { g_group_m = g; }   // tile raster group height (0 = default)
+void bf16x_split_ahead(int on) { g_split_ahead = on; }   // split inside the GEMM (split-ahead warps)
 // Timeline of the last pipelined bf16x_gemm_host call, ms since its start: [0] start, [1] A
 // landed, [2] A split, [3] unused, then per chunk j: [4+3j] B_j landed, [5+3j] GEMM_j done,
 // [6+3j] C_j copied back (-1 = not recorded).  on: enable recording for later calls.

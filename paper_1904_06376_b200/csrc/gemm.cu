@@ -115,8 +115,16 @@ int sk_workspace(size_t ws_floats, size_t nflags, float **ws, unsigned int **fla
     return BF16X_SUCCESS;
 }
 
+// Split-ahead slab counters: nslab ready counters + one completion counter, zero between
+// launches (the last CTA of each launch resets them).  Grown with a device sync.
+static unsigned int *g_sp_ctr = nullptr;
+static size_t g_sp_ctr_n = 0;
+
 void release_gemm_workspace() {
     std::lock_guard<std::mutex> g(g_sk_mu);
+    if (g_sp_ctr) cudaFree(g_sp_ctr);
+    g_sp_ctr = nullptr;
+    g_sp_ctr_n = 0;
     if (g_sk_ws) cudaFree(g_sk_ws);
     if (g_sk_flags) cudaFree(g_sk_flags);
     g_sk_ws = nullptr;
@@ -138,6 +146,35 @@ int num_sms() {
 int pieces_a(int variant) { return variant_pieces_a(variant); }
 int pieces_b(int variant) { return variant_pieces_b(variant); }
 int default_cta_group() { return kDefaultCtaGroup; }
+
+
+int sp_counters(int nslab, unsigned int **ctr) {
+    std::lock_guard<std::mutex> g(g_sk_mu);
+    const size_t need = (size_t)nslab + 1;
+    if (need > g_sp_ctr_n) {
+        const size_t cap = std::max<size_t>(need, 1024);
+        if (g_sp_ctr) { cudaDeviceSynchronize(); cudaFree(g_sp_ctr); }
+        g_sp_ctr = nullptr;
+        g_sp_ctr_n = 0;
+        if (cudaMalloc(&g_sp_ctr, cap * sizeof(unsigned int)) != cudaSuccess ||
+            cudaMemset(g_sp_ctr, 0, cap * sizeof(unsigned int)) != cudaSuccess) {
+            cudaGetLastError();
+            set_error_msg("split-ahead counters: allocation failed");
+            return BF16X_ERR_ALLOC;
+        }
+        g_sp_ctr_n = cap;
+    }
+    *ctr = g_sp_ctr;
+    return BF16X_SUCCESS;
+}
+
+bool split_ahead_ok(const GemmPlan &pl) {
+    const int cg = pl.cta_group ? pl.cta_group : kDefaultCtaGroup;
+    if (cg != 2 || pl.fp64 || pl.split_acc || pl.k <= 128 || pl.stages_per_interval == 1 || pl.tile_n == 192)
+        return false;
+    const bool mc2 = pl.multicast == 2 || (pl.multicast == 0 && (int64_t)pl.m * pl.n >= 12288LL * 12288LL);
+    return !mc2 && pl.Af && pl.Bf;
+}
 
 static int dispatch(const GemmPlan &pl, cudaStream_t st, int kind) {
     switch (pl.variant) {

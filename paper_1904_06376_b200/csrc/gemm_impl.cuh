@@ -20,6 +20,13 @@ constexpr int kNumEpiWarps = 8;       // 2 per TMEM lane quadrant, BN/2 columns 
 constexpr int kThreads = (4 + kNumEpiWarps) * 32;
 constexpr int kNumXfWarps = 8;        // fused split: warps 12..19 convert FP32 tiles to pieces
 constexpr int kThreadsFused = kThreads + kNumXfWarps * 32;
+// split-ahead (SP): warps 12..15 of every CTA split a static share of A and B into the global
+// piece workspace, slab by slab (kSlab values of k), while the TMA producers wait per slab on
+// a global counter -- the split hides behind the first wave's MMAs ("the splitting
+// can be hidden behind the computations") instead of running as a separate pre-pass.
+constexpr int kNumSpWarps = 4;
+constexpr int kThreadsSp = kThreads + kNumSpWarps * 32;
+constexpr int kSlab = 128;
 constexpr int kF32Tile = kBM * kBK * 4;   // one FP32 operand tile per CTA per stage (16 KB)
 constexpr int kTmemCols = 512;        // two accumulator buffers at column 0 and 256
 constexpr int kTmemBufStride = 256;
@@ -83,6 +90,14 @@ struct KParams {
     unsigned int epoch;
     int scaled;            // N2 scaled pieces (R29): scale the accumulator by 2^-8 per bin step
     int group_m;           // tile raster: m-tiles per group
+    // split-ahead (SP): FP32 operands in, piece workspace out (the layout the tensor maps read),
+    // per-slab ready counters (reset by the last CTA to finish)
+    const float *Af, *Bf;
+    int64_t lda, ldb;
+    uint16_t *Apw, *Bpw;
+    int64_t ldap, a_plane, ldbp, b_plane;
+    unsigned int *slab_ctr, *done_ctr;
+    int nslab;
 };
 
 struct Work {
@@ -200,6 +215,126 @@ __device__ __forceinline__ void issue_interval(uint32_t d_big, uint32_t d_small,
     for (int h = 0; h < H; ++h) if (h < nh) mma(0, 0, h);                                  // bin 0
 }
 
+// Split-ahead warps (SP): this CTA's contiguous share of every slab's work list (below)
+// converted into the piece workspace in the K-major layout of bf16x_split_t (A) / bf16x_split
+// (B), bit for bit the pre-pass's split (same split_pair arithmetic).  After a slab: proxy
+// fence, named barrier of the 4 warps, one release increment of the slab's counter.
+// Measured (r06, tools/sp_probe.py): correct and bit-identical, but not faster than the
+// pre-pass at 4096^3 / 8192^3 -- the transposed A pieces are written as 32-byte fragments per
+// lane (one row each), which the 4 warps cannot issue fast enough to stay ahead of the first
+// wave's MMAs (without the stores the kernel would be 3 % faster).  Opt-in (bf16x_split_ahead).
+template <int PA, int PB>
+__device__ __forceinline__ void store_piece16(uint16_t *dst, const uint32_t (&w)[8], int64_t kleft) {
+    // 16 values at dst (32-byte aligned); the piece row ends at a multiple of 8 (kp): write
+    // the second half only if it starts inside the row
+    if (kleft > 0) *reinterpret_cast<uint4 *>(dst) = make_uint4(w[0], w[1], w[2], w[3]);
+    if (kleft > 8) *reinterpret_cast<uint4 *>(dst + 8) = make_uint4(w[4], w[5], w[6], w[7]);
+}
+
+template <int NP>
+__device__ __forceinline__ void split16(const float (&x)[16], uint32_t (&q)[3][8], bool scaled) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        uint32_t t[3];
+        if (scaled) split_pair<NP, true>(x[2 * j], x[2 * j + 1], t);
+        else split_pair<NP, false>(x[2 * j], x[2 * j + 1], t);
+#pragma unroll
+        for (int pc = 0; pc < 3; ++pc) q[pc][j] = t[pc];
+    }
+}
+
+
+template <int PA, int PB>
+__device__ __forceinline__ void split_ahead_warps(const KParams &p, int t) {
+    // Per slab the work is a list of items of 16 values of k: first A's (m * 8 items, ordered
+    // (block of 256 rows, 16-k part, row) so that a run of consecutive items reads 1 KB runs of
+    // one column of the column-major A), then B's (n * 8 items, (column, part): 8 consecutive
+    // items = one column's 512-byte slab).  Every CTA takes one contiguous share of the list.
+    constexpr int NPART = kSlab / 16;
+    constexpr int RB = 256;                 // rows per A block
+    constexpr int NT = kNumSpWarps * 32;
+    const int G = gridDim.x;
+    const int64_t IA = (int64_t)p.m * NPART, I = IA + (int64_t)p.n * NPART;
+    const int64_t i0 = I * blockIdx.x / G, i1 = I * (blockIdx.x + 1) / G;
+    const int64_t kp_a = p.ldap, kp_b = p.ldbp;
+    const bool scaled = p.scaled != 0;
+    const bool bvec = ((reinterpret_cast<uintptr_t>(p.Bf) & 15u) == 0) && (p.ldb % 4 == 0);
+    for (int slab = 0; slab < p.nslab; ++slab) {
+        const int k0 = slab * kSlab;
+        for (int64_t it0 = i0 + t; it0 < i1; it0 += 2 * NT) {
+            float x[2][16];
+            int64_t dst[2];      // element offset of the 16-value run in piece plane 0, or -1
+            int isb[2], kcv[2];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int64_t it = it0 + h * NT;
+                dst[h] = -1;
+                isb[h] = 0;
+                kcv[h] = 0;
+                if (it >= i1) {
+#pragma unroll
+                    for (int q = 0; q < 16; ++q) x[h][q] = 0.f;
+                    continue;
+                }
+                if (it < IA) {
+                    const int64_t blk = it / (RB * NPART);
+                    const int64_t rem = it - blk * (RB * NPART);
+                    const int rows_in = (int)min((int64_t)RB, (int64_t)p.m - blk * RB);   // last block may be short
+                    // within a block: part-major over its rows
+                    const int part = (int)(rem / rows_in), r = (int)(rem - (int64_t)part * rows_in);
+                    const int64_t row = blk * RB + r;
+                    const int kc = k0 + part * 16;
+                    kcv[h] = kc;
+                    if (kc < p.k) dst[h] = row * kp_a + kc;
+#pragma unroll
+                    for (int q = 0; q < 16; ++q)
+                        x[h][q] = (kc + q < p.k) ? __ldcs(p.Af + (int64_t)(kc + q) * p.lda + row) : 0.f;
+                } else {
+                    const int64_t j = it - IA;
+                    const int64_t col = j / NPART;
+                    const int part = (int)(j - col * NPART);
+                    const int kc = k0 + part * 16;
+                    kcv[h] = kc;
+                    isb[h] = 1;
+                    if (kc < p.k) dst[h] = col * kp_b + kc;
+                    const float *src = p.Bf + col * p.ldb + kc;
+                    if (bvec && kc + 16 <= p.k) {
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            const float4 v = __ldcs(reinterpret_cast<const float4 *>(src) + q);
+                            x[h][4 * q] = v.x; x[h][4 * q + 1] = v.y; x[h][4 * q + 2] = v.z; x[h][4 * q + 3] = v.w;
+                        }
+                    } else {
+#pragma unroll
+                        for (int q = 0; q < 16; ++q) x[h][q] = (kc + q < p.k) ? src[q] : 0.f;
+                    }
+                }
+            }
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                if (dst[h] < 0) continue;
+                uint32_t w[3][8];
+                if (isb[h]) {
+                    split16<PB>(x[h], w, scaled);
+#pragma unroll
+                    for (int pc = 0; pc < PB; ++pc)
+                        store_piece16<PA, PB>(p.Bpw + pc * p.b_plane + dst[h], w[pc], kp_b - kcv[h]);
+                } else {
+                    split16<PA>(x[h], w, scaled);
+#pragma unroll
+                    for (int pc = 0; pc < PA; ++pc)
+                        store_piece16<PA, PB>(p.Apw + pc * p.a_plane + dst[h], w[pc], kp_a - kcv[h]);
+                }
+            }
+        }
+        // publish the slab: stores -> async proxy (TMA readers), then one release increment
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        __threadfence();
+        asm volatile("bar.sync 2, %0;" ::"n"(NT));
+        if (t == 0) asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(p.slab_ctr + slab) : "memory");
+    }
+}
+
 // MC = number of CTA pairs per cluster sharing the B tile (1, or 2: two vertically adjacent
 // 256 x BN tiles; each pair loads half of every B slice and multicasts it to both pairs).
 // FU (fused split): tmA / tmB are FP32 maps of A and B; warp 0 loads FP32 tiles, warps
@@ -209,8 +344,9 @@ __device__ __forceinline__ void issue_interval(uint32_t d_big, uint32_t d_small,
 // FP32 register accumulators (G[0, EC) = bin 0, G[EC, 2 EC) = bins >= 1: the paper's FP32
 // partial sums Z^(i,j), pooled per accumulator) and only their final collection is
 // FP64, rounded once to FP32 ("adding the final results together in FP64").
-template <int CG, int V, int BN, int S, int MC, bool SA, bool FU = false, bool GD = false>
-__global__ void __launch_bounds__(FU ? kThreadsFused : kThreads, 1)
+// SP (split-ahead): see kNumSpWarps.
+template <int CG, int V, int BN, int S, int MC, bool SA, bool FU = false, bool GD = false, bool SP = false>
+__global__ void __launch_bounds__(FU ? kThreadsFused : (SP ? kThreadsSp : kThreads), 1)
     gemm_split_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                       const KParams p) {
     using Cf = Cfg<CG, V, BN>;
@@ -221,6 +357,7 @@ __global__ void __launch_bounds__(FU ? kThreadsFused : kThreads, 1)
     static_assert(MC == 1 || CG == 2, "multicast needs 2-CTA pairs");
     static_assert(!SA || 2 * BN <= kTmemBufStride, "split accumulators need 4 x BN TMEM columns");
     static_assert(!GD || (SA && !FU), "FP64 collection needs split accumulators");
+    static_assert(!SP || (!FU && !GD && !SA && MC == 1), "split-ahead: plain pre-split layout");
     constexpr int NG = GD ? 2 : 1;     // promoted accumulators per output element
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -276,11 +413,13 @@ __global__ void __launch_bounds__(FU ? kThreadsFused : kThreads, 1)
 
     if (warp < 4) {
         if constexpr (FU) asm volatile("setmaxnreg.dec.sync.aligned.u32 48;" ::: "memory");
+        if constexpr (SP) asm volatile("setmaxnreg.dec.sync.aligned.u32 56;" ::: "memory");
         if (warp == 0) {
             // ------------------------------ TMA producer ------------------------------
             if (lane == 0) {
                 int stage = 0;
                 uint32_t phase = 0;
+                int slab_ready = -1;   // SP: highest slab known to be split by every CTA
                 WorkIter it(p, cid, ncl);
                 Work w;
                 while (it.next(p, w)) {
@@ -303,6 +442,15 @@ __global__ void __launch_bounds__(FU ? kThreadsFused : kThreads, 1)
                         continue;
                     }
                     for (int kb = w.i0 * S; kb < kb_end; ++kb) {
+                        if constexpr (SP) {
+                            const int slab = kb * kBK / kSlab;
+                            if (slab > slab_ready) {
+                                while (ld_acquire_u32(p.slab_ctr + slab) < gridDim.x) __nanosleep(32);
+                                // generic-proxy stores of other CTAs -> this CTA's TMA reads
+                                asm volatile("fence.proxy.async.global;" ::: "memory");
+                                slab_ready = slab;
+                            }
+                        }
                         mbar_wait(&empty[stage], phase ^ 1u);
                         uint8_t *a_dst = sA + stage * Cf::A_STAGE;
                         uint8_t *b_dst = sB + stage * Cf::B_STAGE;
@@ -377,6 +525,7 @@ __global__ void __launch_bounds__(FU ? kThreadsFused : kThreads, 1)
         }
     } else if (warp < 4 + kNumEpiWarps) {
         if constexpr (FU) asm volatile("setmaxnreg.inc.sync.aligned.u32 160;" ::: "memory");
+        if constexpr (SP) asm volatile("setmaxnreg.inc.sync.aligned.u32 168;" ::: "memory");
         // ------------------------- promotion + epilogue ---------------------------
         constexpr int EC = Cf::EPI_COLS;
         const int ew = warp - 4;
@@ -502,6 +651,9 @@ __global__ void __launch_bounds__(FU ? kThreadsFused : kThreads, 1)
                 }
             }
         }
+    } else if constexpr (SP) {
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 112;" ::: "memory");
+        split_ahead_warps<Cf::PA, Cf::PB>(p, threadIdx.x - kThreads);
     } else if constexpr (FU) {
         asm volatile("setmaxnreg.dec.sync.aligned.u32 48;" ::: "memory");
         // ----------------------- fused split: FP32 tiles -> pieces ----------------------
@@ -597,6 +749,18 @@ __global__ void __launch_bounds__(FU ? kThreadsFused : kThreads, 1)
         tc_fence_after();
         tmem_dealloc<CG>(tmem_base, kTmemCols);
     }
+    if constexpr (SP) {
+        // the last CTA to get here resets the slab counters for the next launch (every CTA's
+        // producer has passed its last wait and every split warp its last increment)
+        if (threadIdx.x == 0) {
+            __threadfence();
+            if (atomicAdd(p.done_ctr, 1u) == gridDim.x - 1) {
+                for (int s2 = 0; s2 < p.nslab; ++s2) p.slab_ctr[s2] = 0u;
+                *p.done_ctr = 0u;
+                __threadfence();
+            }
+        }
+    }
 }
 
 // ------------------------------------------------------------------------------------
@@ -607,14 +771,16 @@ int make_piece_map(CUtensorMap *map, const uint16_t *base, int k, int rows, int6
 int make_f32_map(CUtensorMap *map, const float *base, int rows, int cols, int64_t ld, int box_rows, int box_cols,
                  CUtensorMapSwizzle swz);
 int sk_workspace(size_t ws_floats, size_t nflags, float **ws, unsigned int **flags, unsigned int *epoch);
+// split-ahead slab counters (nslab + 1 words, zero between launches; one stream at a time)
+int sp_counters(int nslab, unsigned int **ctr);
 
-template <int CG, int V, int BN, int S, int MC, bool SA = false, bool FU = false, bool GD = false>
+template <int CG, int V, int BN, int S, int MC, bool SA = false, bool FU = false, bool GD = false, bool SP = false>
 int launch_t(const GemmPlan &pl, cudaStream_t st) {
     using Cf = Cfg<CG, V, BN>;
     constexpr int CL = CG * MC;
-    constexpr int THREADS = FU ? kThreadsFused : kThreads;
+    constexpr int THREADS = FU ? kThreadsFused : (SP ? kThreadsSp : kThreads);
     constexpr int SMEM = FU ? CfgF<V>::SMEM : Cf::SMEM;
-    auto kern = gemm_split_kernel<CG, V, BN, S, MC, SA, FU, GD>;
+    auto kern = gemm_split_kernel<CG, V, BN, S, MC, SA, FU, GD, SP>;
     CUtensorMap tmA, tmB;
     int rc;
     if constexpr (FU) {
@@ -678,6 +844,18 @@ int launch_t(const GemmPlan &pl, cudaStream_t st) {
     // tiles (measured r06, tools/raster_probe.py: 4096^3 x6 +1.5 %, GEMM DRAM reads 830 -> 630
     // MB), 8-tall groups for wider outputs (8192^3: 8 beats 1 by 3-5 %)
     kp.group_m = pl.group_m > 0 ? pl.group_m : (kp.tiles_n <= 16 ? 1 : kGroupM);
+    kp.Af = pl.Af; kp.Bf = pl.Bf; kp.lda = pl.lda; kp.ldb = pl.ldb;
+    kp.Apw = const_cast<uint16_t *>(pl.Ap); kp.Bpw = const_cast<uint16_t *>(pl.Bp);
+    kp.ldap = pl.ldap; kp.a_plane = pl.a_plane; kp.ldbp = pl.ldbp; kp.b_plane = pl.b_plane;
+    kp.slab_ctr = nullptr; kp.done_ctr = nullptr;
+    kp.nslab = (pl.k + kSlab - 1) / kSlab;
+    if constexpr (SP) {
+        unsigned int *ctr = nullptr;
+        const int rc3 = sp_counters(kp.nslab, &ctr);
+        if (rc3) return rc3;
+        kp.slab_ctr = ctr;
+        kp.done_ctr = ctr + kp.nslab;
+    }
     const int ncl = grid / CL;
     if (pl.stream_k != 0 && !(pl.flags & (BF16X_ACC_IN | BF16X_ACC_OUT)) && tiles > ncl && tiles % ncl != 0) {
         const int full = tiles / ncl;
@@ -744,6 +922,13 @@ int launch_s(const GemmPlan &pl, cudaStream_t st) {
     // intervals (one instance per variant)
     if constexpr (V >= 3)
         if (pl.fp64) return launch_t<2, V, 128, 2, 1, true, false, true>(pl, st);
+    // split-ahead: the caller (gemm_core) chose it with split_ahead_ok(), which mirrors the
+    // conditions below; the pieces are written by this launch only
+    if (pl.split_ahead) {
+        if (CG == 2 && s == 2) return launch_t<2, V, 256, 2, 1, false, false, false, true>(pl, st);
+        set_error_msg("split-ahead plan not launchable");
+        return BF16X_ERR_CUDA;
+    }
     if constexpr (CG == 2) {
         if (s == 2) {
             const int units = (pl.max_ctas > 0 ? pl.max_ctas : num_sms()) / CG;

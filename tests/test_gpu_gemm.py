@@ -383,3 +383,32 @@ def test_fused_split_nonfinite_and_ragged(orc, fused_on):
     Aw[7, 8] = np.float32(2.0 ** -140)
     I = np.eye(48, dtype=np.float32)
     assert np.array_equal(_gpu(Aw, I, variant=6), orc.gemm(Aw, I, variant=6))
+
+
+@pytest.fixture
+def split_ahead_on():
+    L = bx.lib()
+    L.bf16x_split_ahead(1)
+    yield L
+    L.bf16x_split_ahead(0)
+
+
+@pytest.mark.parametrize("scaled", [False, True])
+@pytest.mark.parametrize("variant", [1, 3, 5, 6, 7, 8, 9])
+@pytest.mark.parametrize("shape", [(256, 256, 200), (300, 700, 333), (1024, 2048, 1000), (130, 260, 1037), (4096, 1024, 2048)])
+def test_split_ahead_matches_prepass(orc, split_ahead_on, shape, variant, scaled):
+    """The opt-in split-ahead GEMM (the split done by 4 extra warps per CTA, slab by slab,
+    producers waiting on per-slab global counters) writes the pre-pass's pieces and so returns
+    the pre-pass result bit for bit, ragged k and rows included; back-to-back launches reuse the
+    self-resetting counters."""
+    m, n, k = shape
+    A = synthetic.wide(m, k, seed=m + k, E=20)
+    B = synthetic.wide(k, n, seed=n + k, E=20)
+    Ad = torch.from_numpy(np.asfortranarray(A)).cuda()
+    Bd = torch.from_numpy(np.asfortranarray(B)).cuda()
+    outs = []
+    for on in (1, 0, 1, 1):
+        split_ahead_on.bf16x_split_ahead(on)
+        outs.append(bx.gemm(Ad, Bd, variant=variant, scaled=scaled).cpu().numpy())
+    for o in outs[1:]:
+        assert np.array_equal(o.view(np.uint32), outs[0].view(np.uint32))
