@@ -913,6 +913,10 @@ inline int choose_tile_n(int m, int n, int cg, int units, int forced) {
 template <int CG, int V>
 int launch_s(const GemmPlan &pl, cudaStream_t st) {
     int s = pl.stages_per_interval;
+    // 128-k promotion intervals (4 stages) for the one-product variant (tuning hook; r06
+    // tools/spi_probe.py: x1 +13 %, but x3 -14 %: its 6-stage ring then stalls between intervals)
+    if constexpr (CG == 2 && V == 1)
+        if (s == 4 && !pl.fp64 && !pl.split_ahead && !pl.split_acc) return launch_t<2, V, 256, 4, 1>(pl, st);
     // Short k (<= 128): the whole product is one or two intervals, so the tensor core's
     // truncating accumulation dominates the error; 32-k intervals halve it (measured wide
     // exponents, k = 64: max ratio to the oracle 2.07 -> 1.66) at no cost that matters.
