@@ -16,6 +16,7 @@ static std::atomic<uint64_t> g_launches{0};
 static std::mutex g_ws_mu;
 static void *g_ws = nullptr;
 static size_t g_ws_bytes = 0;
+static int g_max_ctas = 0;  // cap on the GEMM's persistent grid (bf16x_max_ctas hook; 0 = all SMs)
 static int g_group_m = 0;   // tile raster group (bf16x_group_m hook; 0 = default)
 static int g_split_ahead = 0;   // split inside the GEMM (split-ahead warps; opt-in, not faster)
 static int g_force_cg = 0, g_force_bn = 0, g_force_spi = 0, g_stream_k = 1, g_multicast = 0, g_split_acc = 0, g_fused = 0;  // tuning overrides (bf16x_tune; not in the public ABI)
@@ -118,7 +119,7 @@ int gemm_core(int m, int n, int k, float alpha, const float *A, int lda, const f
     pl.variant = variant; pl.flags = flags;
     pl.acc = acc;
     pl.cta_group = cta_group ? cta_group : g_force_cg;
-    pl.max_ctas = 0;
+    pl.max_ctas = g_max_ctas;
     pl.tile_n = g_force_bn;
     pl.stages_per_interval = g_force_spi;
     pl.stream_k = allow_stream_k ? g_stream_k : 0;   // (its workspace is shared: one stream at a time)
@@ -472,7 +473,8 @@ uint64_t bf16x_launch_count(void) { return g_launches.load(); }
 int bf16x_default_cta_group(void) { return default_cta_group(); }
 void bf16x_stream_k(int on) { g_stream_k = on; }
 void bf16x_split_acc(int on) { g_split_acc = on; }
-void bf16x_group_m(int g) { g_group_m = g; }   // tile raster group height (0 = default)
+void bf16x_group_m(int g) { g_group_m = g; }
+void bf16x_max_ctas(int c) { g_max_ctas = c; }   // tile raster group height (0 = default)
 void bf16x_split_ahead(int on) { g_split_ahead = on; }   // split inside the GEMM (split-ahead warps)
 // Timeline of the last pipelined bf16x_gemm_host call, ms since its start: [0] start, [1] A
 // landed, [2] A split, [3] unused, then per chunk j: [4+3j] B_j landed, [5+3j] GEMM_j done,
