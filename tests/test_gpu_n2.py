@@ -73,9 +73,17 @@ def test_scaled_split_transposed_layout(orc, rows, cols, ld):
 # ---------------------------------------------------------------------------------------
 # GEMM with scaled pieces (R29)
 # ---------------------------------------------------------------------------------------
+@pytest.fixture(params=[0, 2], ids=["mc_auto", "mc2"])
+def mc(request):
+    """0: library default (no multicast at these sizes); 2: two CTA pairs per cluster sharing B."""
+    bx.lib().bf16x_multicast(request.param)
+    yield request.param
+    bx.lib().bf16x_multicast(0)
+
+
 @pytest.mark.parametrize("variant", [1, 3, 5, 6, 7, 8, 9])
 @pytest.mark.parametrize("shape", [(129, 257, 33), (333, 517, 77), (512, 384, 1000), (700, 300, 200)])
-def test_scaled_equals_unscaled_on_normal_range_inputs(shape, variant):
+def test_scaled_equals_unscaled_on_normal_range_inputs(shape, variant, mc):
     """U[-1,1] inputs: nothing leaves the normal range, so scaling each band's accumulator by
     2^-8 (scale-input-d) on the tensor core reproduces the unscaled GEMM bit for bit (both
     promotion-interval lengths, alpha/beta included) -- the hardware check that the scale is
