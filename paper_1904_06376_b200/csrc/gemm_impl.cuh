@@ -842,8 +842,10 @@ int launch_t(const GemmPlan &pl, cudaStream_t st) {
     kp.scaled = pl.scaled;
     // raster group height: row-major raster (1) while a wave spans whole rows of at most 16
     // tiles (measured r06, tools/raster_probe.py: 4096^3 x6 +1.5 %, GEMM DRAM reads 830 -> 630
-    // MB), 8-tall groups for wider outputs (8192^3: 8 beats 1 by 3-5 %)
-    kp.group_m = pl.group_m > 0 ? pl.group_m : (kp.tiles_n <= 16 ? 1 : kGroupM);
+    // MB), 8-tall groups for wider outputs (8192^3: 8 beats 1 and 2 by 3-5 %), and groups of 2
+    // super-rows on the multicast schedule of the largest outputs (16384^3 x6: 228 vs 215
+    // TFLOPS, DRAM reads ~50 vs ~85 GB per launch -- power-limited, so traffic costs clock)
+    kp.group_m = pl.group_m > 0 ? pl.group_m : (MC == 2 ? 2 : (kp.tiles_n <= 16 ? 1 : kGroupM));
     kp.Af = pl.Af; kp.Bf = pl.Bf; kp.lda = pl.lda; kp.ldb = pl.ldb;
     kp.Apw = const_cast<uint16_t *>(pl.Ap); kp.Bpw = const_cast<uint16_t *>(pl.Bp);
     kp.ldap = pl.ldap; kp.a_plane = pl.a_plane; kp.ldbp = pl.ldbp; kp.b_plane = pl.b_plane;
