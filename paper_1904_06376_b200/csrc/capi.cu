@@ -93,7 +93,7 @@ static int gemm_args(int m, int n, int k, int lda, int ldb, int ldc, int variant
 int gemm_core(int m, int n, int k, float alpha, const float *A, int lda, const float *B, int ldb, float beta,
               float *C, int ldc, int variant, unsigned flags, const uint16_t *Ap, int64_t ldap, int64_t a_plane,
               const uint16_t *Bp, int64_t ldbp, int64_t b_plane, float *acc, void *ws, size_t ws_bytes,
-              cudaStream_t st, int cta_group, bool allow_stream_k) {
+              cudaStream_t st, int cta_group, bool allow_stream_k, int max_ctas) {
     int rc = arch_ok();
     if (rc) return rc;
     if (m == 0 || n == 0) return BF16X_SUCCESS;
@@ -119,7 +119,7 @@ int gemm_core(int m, int n, int k, float alpha, const float *A, int lda, const f
     pl.variant = variant; pl.flags = flags;
     pl.acc = acc;
     pl.cta_group = cta_group ? cta_group : g_force_cg;
-    pl.max_ctas = g_max_ctas;
+    pl.max_ctas = max_ctas > 0 ? max_ctas : g_max_ctas;
     pl.tile_n = g_force_bn;
     pl.stages_per_interval = g_force_spi;
     pl.stream_k = allow_stream_k ? g_stream_k : 0;   // (its workspace is shared: one stream at a time)
@@ -194,7 +194,7 @@ int bf16x_gemm(int m, int n, int k, float alpha, const float *A, int lda, const 
     int a = gemm_args(m, n, k, lda, ldb, ldc, variant);
     if (a) return a;
     return gemm_core(m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, variant, 0u, nullptr, 0, 0, nullptr, 0, 0,
-                     nullptr, nullptr, 0, g_stream, 0, true);
+                     nullptr, nullptr, 0, g_stream, 0, true, 0);
 }
 
 size_t bf16x_gemm_workspace_size(int m, int n, int k, int variant) {
@@ -219,7 +219,7 @@ int bf16x_gemm_ex(int m, int n, int k, float alpha, const float *A, int lda, con
         return -16;
     if ((flags & (BF16X_ACC_IN | BF16X_ACC_OUT)) && !acc_carry) return -19;
     return gemm_core(m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, variant, flags, A_pieces, ldap, a_plane,
-                     B_pieces, ldbp, b_plane, acc_carry, workspace_ptr, ws_bytes, (cudaStream_t)stream, 0, true);
+                     B_pieces, ldbp, b_plane, acc_carry, workspace_ptr, ws_bytes, (cudaStream_t)stream, 0, true, 0);
 }
 
 // testing hook (not in the public header): force cta_group 1 or 2
@@ -228,7 +228,7 @@ int bf16x_gemm_cg(int m, int n, int k, float alpha, const float *A, int lda, con
     int a = gemm_args(m, n, k, lda, ldb, ldc, variant);
     if (a) return a;
     return gemm_core(m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, variant, 0u, nullptr, 0, 0, nullptr, 0, 0,
-                     nullptr, nullptr, 0, (cudaStream_t)stream, cta_group, true);
+                     nullptr, nullptr, 0, (cudaStream_t)stream, cta_group, true, 0);
 }
 
 static std::mutex g_host_mu;
@@ -340,7 +340,7 @@ int bf16x_gemm_host(int m, int n, int k, float alpha, const float *A_host, int l
             return BF16X_ERR_CUDA;
         }
         rc = gemm_core(m, n, k, alpha, g_hA, m, g_hB, k > 0 ? k : 1, beta, g_hC, m, variant, 0u, nullptr, 0, 0,
-                       nullptr, 0, 0, nullptr, nullptr, 0, st, 0, true);
+                       nullptr, 0, 0, nullptr, nullptr, 0, st, 0, true, 0);
         if (rc) return rc;
         e = cudaMemcpy2DAsync(C_host, (size_t)ldc * 4, g_hC, (size_t)m * 4, (size_t)m * 4, n, cudaMemcpyDeviceToHost,
                               st);
@@ -397,7 +397,7 @@ int bf16x_gemm_host(int m, int n, int k, float alpha, const float *A_host, int l
         if (e != cudaSuccess) break;
         rc = gemm_core(m, nj, k, alpha, nullptr, m, g_hB + (size_t)c0 * k, k, beta, g_hC + (size_t)c0 * m, m, variant,
                        0u, ap, kp, a_plane, nullptr, 0, 0, nullptr,
-                       reinterpret_cast<uint8_t *>(g_hBp) + (j % kHostStreams) * slice, slice, cs, 0, false);
+                       reinterpret_cast<uint8_t *>(g_hBp) + (j % kHostStreams) * slice, slice, cs, 0, false, 0);
         if (rc) break;
         e = cudaEventRecord(g_ev_c[j], cs);
         tl_record(5 + 3 * j, cs);                             // GEMM j done

@@ -13,6 +13,7 @@
 //   refine (FP64, factors widened exactly):
 //     K6 residual       r = b - A x, deterministic two-phase row sums
 //        trsv_kernel    cooperative blocked forward / backward substitution
+#include <chrono>
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
@@ -29,7 +30,7 @@ namespace bf16x {
 int gemm_core(int m, int n, int k, float alpha, const float *A, int lda, const float *B, int ldb, float beta,
               float *C, int ldc, int variant, unsigned flags, const uint16_t *Ap, int64_t ldap, int64_t a_plane,
               const uint16_t *Bp, int64_t ldbp, int64_t b_plane, float *acc, void *ws, size_t ws_bytes,
-              cudaStream_t st, int cta_group, bool allow_stream_k = true);
+              cudaStream_t st, int cta_group, bool allow_stream_k = true, int max_ctas = 0);
 
 constexpr int kLuThreads = 256;
 
@@ -447,6 +448,25 @@ __global__ void __launch_bounds__(256) laswp_kernel(float *LU, int ld, int c0, i
     for (int e = lane; e < np; e += 32) col[pairs[e].x] = buf[e];
 }
 
+// K5a': a whole panel's interchanges (nmaps sub-panel gather maps of <= 64 pairs each, applied
+// in order) on the columns outside the panel, deferred from the sub-panels (lookahead schedule).
+__global__ void __launch_bounds__(256) laswp_multi_kernel(float *LU, int ld, int c0, int c1, const int2 *pairs,
+                                                          const int *npairs, int nmaps) {
+    __shared__ float sv[8][2 * 32];
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int c = c0 + blockIdx.x * 8 + wid;
+    if (c >= c1) return;
+    float *col = LU + (int64_t)c * ld;
+    for (int s = 0; s < nmaps; ++s) {
+        const int np = npairs[s];
+        const int2 *pr = pairs + 64 * s;
+        for (int e = lane; e < np; e += 32) sv[wid][e] = col[pr[e].y];
+        __syncwarp();
+        for (int e = lane; e < np; e += 32) col[pr[e].x] = sv[wid][e];
+        __syncwarp();
+    }
+}
+
 // K5b: U12 = L11^-1 A12 with L11 = unit lower jb x jb at (j0, j0), A12 = rows j0..j0+jb of
 // columns [c0, c0 + ncols).  One CTA per 32 columns held in shared memory; L11 is staged in
 // 32-column chunks.  Per chunk: the 32 x 32 diagonal triangle is solved by warp shuffles
@@ -855,7 +875,7 @@ static int sub_rpt(int n, int cl) {
     return 0;
 }
 
-static cudaError_t launch_subpanel(const LuWork &w, int s0, int sw, cudaStream_t st) {
+static cudaError_t launch_subpanel(const LuWork &w, int s0, int sw, cudaStream_t st, int2 *pairs, int *npairs) {
     const int rpt = sub_rpt(w.n, w.cl);
     if (rpt == 0) return cudaErrorInvalidValue;
     cudaLaunchConfig_t cfg = {};
@@ -870,9 +890,9 @@ static cudaError_t launch_subpanel(const LuWork &w, int s0, int sw, cudaStream_t
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    if (rpt == 1) return cudaLaunchKernelEx(&cfg, subpanel_kernel<1>, w.LU, w.ld, w.n, s0, sw, w.ipiv, w.pairs, w.npairs, w.info);
-    if (rpt == 2) return cudaLaunchKernelEx(&cfg, subpanel_kernel<2>, w.LU, w.ld, w.n, s0, sw, w.ipiv, w.pairs, w.npairs, w.info);
-    return cudaLaunchKernelEx(&cfg, subpanel_kernel<4>, w.LU, w.ld, w.n, s0, sw, w.ipiv, w.pairs, w.npairs, w.info);
+    if (rpt == 1) return cudaLaunchKernelEx(&cfg, subpanel_kernel<1>, w.LU, w.ld, w.n, s0, sw, w.ipiv, pairs, npairs, w.info);
+    if (rpt == 2) return cudaLaunchKernelEx(&cfg, subpanel_kernel<2>, w.LU, w.ld, w.n, s0, sw, w.ipiv, pairs, npairs, w.info);
+    return cudaLaunchKernelEx(&cfg, subpanel_kernel<4>, w.LU, w.ld, w.n, s0, sw, w.ipiv, pairs, npairs, w.info);
 }
 
 static int coop_launch(const void *fn, int grid, int threads, void **args, size_t smem, cudaStream_t st) {
@@ -945,8 +965,9 @@ static int lu_prepare(LuWork &w, int n, int nb, float *LU, int ld, int *ipiv, bo
     const int nchunk = (n + kResChunk - 1) / kResChunk;
     alloc((void **)&w.perm, sizeof(int) * n);
     alloc((void **)&w.info, sizeof(int));
-    alloc((void **)&w.npairs, sizeof(int));
-    alloc((void **)&w.pairs, sizeof(int2) * 2 * (size_t)w.nb);
+    const int nmap = (w.nb + kSubW - 1) / kSubW;
+    alloc((void **)&w.npairs, sizeof(int) * (size_t)nmap);            // one gather map per sub-panel
+    alloc((void **)&w.pairs, sizeof(int2) * (size_t)nmap * 64);
     alloc((void **)&w.bar, sizeof(unsigned int) * ((size_t)w.coop_grid + 1));
     alloc((void **)&w.r, sizeof(double) * n);
     alloc((void **)&w.d, sizeof(double) * n);
@@ -968,27 +989,37 @@ static int lu_prepare(LuWork &w, int n, int nb, float *LU, int ld, int *ipiv, bo
 
 // Factor w.LU (order w.n, ld w.ld) in place: P A = L U, ipiv 0-based, perm for the solves.
 // Enqueued on st; the zero-pivot column lands in w.info (device).
+static double g_lu_host_ms = 0.0;   // host time to enqueue the last factorisation (diagnostic)
 static int lu_factor(LuWork &w, int variant, cudaStream_t st) {
+    const auto t_host0 = std::chrono::steady_clock::now();
+    // Right-looking blocked LU.  Each sub-panel's interchanges are applied at once only inside
+    // the panel (the sub-panels and the in-panel updates need them); the whole panel's gather
+    // maps are then applied to the columns outside it in one pass (laswp_multi), before the
+    // TRSM of U12 and the trailing GEMM.  (A lookahead schedule -- panel p+1 factored while
+    // panel p's wide update runs on a second stream -- was measured at equal time: the
+    // sub-panel's 16-CTA cluster cannot be placed beside the persistent GEMM, r06.)
     const int n = w.n, nb = w.nb, ld = w.ld;
     int rc = BF16X_SUCCESS;
-    auto laswp = [&](int c0, int c1, int pair_cap) {
+    auto laswp_multi = [&](int nm, int c0, int c1) {
         if (c1 <= c0) return;
-        laswp_kernel<<<(c1 - c0 + 7) / 8, 256, 8 * (size_t)pair_cap * sizeof(float), st>>>(w.LU, ld, c0, c1, w.pairs,
-                                                                                          w.npairs, w.perm);
+        laswp_multi_kernel<<<(c1 - c0 + 7) / 8, 256, 0, st>>>(w.LU, ld, c0, c1, w.pairs, w.npairs, nm);
         count_launch();
     };
     iota_kernel<<<(n + 255) / 256, 256, 0, st>>>(n, w.perm);
     count_launch();
     for (int j0 = 0; j0 < n && !rc; j0 += nb) {
-        const int jb = std::min(nb, n - j0);
-        for (int s0 = j0; s0 < j0 + jb && !rc; s0 += kSubW) {
-            const int sw = std::min(kSubW, j0 + jb - s0);
+        const int jb = std::min(nb, n - j0), j1 = j0 + jb;
+        int nm = 0;
+        for (int s0 = j0; s0 < j1 && !rc; s0 += kSubW, ++nm) {
+            const int sw = std::min(kSubW, j1 - s0);
+            int2 *pr = w.pairs + 64 * nm;
+            int *np = w.npairs + nm;
             // (1) sub-panel factorisation on one cluster (rows in registers, RPT per thread)
-            cudaError_t e = launch_subpanel(w, s0, sw, st);
+            cudaError_t e = launch_subpanel(w, s0, sw, st, pr, np);
             if (e != cudaSuccess && w.cl == 16) {    // 16-CTA clusters unavailable: use 8
                 cudaGetLastError();
                 w.cl = 8;
-                e = launch_subpanel(w, s0, sw, st);
+                e = launch_subpanel(w, s0, sw, st, pr, np);
             }
             if (e != cudaSuccess) {
                 set_cuda_error(e, "subpanel launch");
@@ -996,23 +1027,26 @@ static int lu_factor(LuWork &w, int variant, cudaStream_t st) {
                 break;
             }
             count_launch();
-            // (2) its interchanges (emitted by the sub-panel kernel), applied to all n columns
-            laswp(0, n, 2 * sw);
+            // (2) its interchanges inside the panel (and on the row permutation)
+            laswp_kernel<<<(jb + 7) / 8, 256, 8 * (size_t)(2 * sw) * sizeof(float), st>>>(w.LU, ld, j0, j1, pr, np,
+                                                                                          w.perm);
+            count_launch();
             // (3) TRSM + rank-sw update of the rest of the panel
-            const int c1 = s0 + sw, c2 = j0 + jb;
-            if (c1 < c2) {
-                const size_t smem = panel_update_smem(c2 - c1);
-                panel_update_kernel<<<(n - c1 + kUpdRows - 1) / kUpdRows, 256, smem, st>>>(w.LU, ld, n, s0, sw, c1,
-                                                                                            c2);
+            const int c1 = s0 + sw;
+            if (c1 < j1) {
+                const size_t smem = panel_update_smem(j1 - c1);
+                panel_update_kernel<<<(n - c1 + kUpdRows - 1) / kUpdRows, 256, smem, st>>>(w.LU, ld, n, s0, sw, c1, j1);
                 count_launch();
             }
             rc = check_launch("panel");
         }
         if (rc) break;
-        const int j1 = j0 + jb, rest = n - j1;
+        // the panel's interchanges on the columns outside it
+        laswp_multi(nm, 0, j0);
+        laswp_multi(nm, j1, n);
+        const int rest = n - j1;
         if (rest > 0) {
-            trsm_kernel<<<(rest + kTrsmCols - 1) / kTrsmCols, 256, trsm_smem(jb), st>>>(
-                w.LU, ld, j0, jb, j1, rest);
+            trsm_kernel<<<(rest + kTrsmCols - 1) / kTrsmCols, 256, trsm_smem(jb), st>>>(w.LU, ld, j0, jb, j1, rest);
             count_launch();
             rc = check_launch("trsm");
             if (rc) break;
@@ -1030,6 +1064,7 @@ static int lu_factor(LuWork &w, int variant, cudaStream_t st) {
         }
         rc = check_launch("lu");
     }
+    g_lu_host_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_host0).count();
     return rc;
 }
 
@@ -1361,3 +1396,5 @@ extern "C" int bf16x_gesv_gmres_ir(int n, const float *A, int lda, const double 
     lu_free(w);
     return rc;
 }
+
+extern "C" double bf16x_lu_host_ms(void) { return g_lu_host_ms; }   // diagnostic hook
