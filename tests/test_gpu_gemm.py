@@ -187,6 +187,28 @@ def test_host_api_pipelined_chunks(orc, beta, depth):
     assert orc.normwise_error(Gh[:, cols], C64, A, B[:, cols]) <= RATIO * eo
 
 
+def test_bench_launch_sequence_matches_gemm():
+    """bench.py's timed step (bf16x_split_operands of both operands into caller buffers, then
+    bf16x_gemm_ex on the pre-split pieces) is the same computation as bf16x_gemm: bit-identical
+    C at configs[1]'s size, so the parity tests of bx.gemm cover the benchmarked launches."""
+    n = 4096
+    A = torch.from_numpy(np.asfortranarray(synthetic.uniform(n, n, seed=1))).cuda()
+    B = torch.from_numpy(np.asfortranarray(synthetic.uniform(n, n, seed=2))).cuda()
+    want = bx.gemm(A, B, variant=6)
+    L = bx.lib()
+    kp = n
+    Ap = torch.empty(3 * n * kp, dtype=torch.uint16, device="cuda")
+    Bp = torch.empty(3 * n * kp, dtype=torch.uint16, device="cuda")
+    C = torch.empty_strided((n, n), (1, n), dtype=torch.float32, device="cuda")
+    st = torch.cuda.current_stream().cuda_stream
+    assert L.bf16x_split_operands(n, n, n, A.data_ptr(), n, B.data_ptr(), n, 3, Ap.data_ptr(), kp, n * kp,
+                                  Bp.data_ptr(), kp, n * kp, st) == 0
+    assert L.bf16x_gemm_ex(n, n, n, 1.0, None, n, None, n, 0.0, C.data_ptr(), n, 6, 0, Ap.data_ptr(), kp, n * kp,
+                           Bp.data_ptr(), kp, n * kp, None, None, 0, st) == 0
+    torch.cuda.synchronize()
+    assert torch.equal(C.view(torch.int32), want.view(torch.int32))
+
+
 def test_config2_4096_sampled(orc):
     """configs[1]: 4096^3 bf16x6, U[-1,1], in the launch configuration bench.py times
     (2-CTA persistent).  The oracle computes 24 sampled output columns one by one; the whole

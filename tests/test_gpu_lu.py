@@ -67,3 +67,23 @@ def test_singular_reports_column():
     b = np.ones(n)
     x, rep, _ = _solve(A, b)
     assert rep.info == 11 and rep.converged == 0
+
+
+@pytest.mark.parametrize("kappa", [1e1, 1e4])
+def test_config5_full_size(kappa):
+    """configs[4] at its full size, n = 8192, nb = 256, bf16x3 trailing updates (the launch
+    configuration of tools/config5.py): the oracle's LU is too slow at this size, so the checks
+    are the properties the method guarantees -- convergence to the LAPACK-dsgesv test (R14),
+    backward error within the stopping test's sqrt(n) 2^-53, forward error within the
+    conditioning bound.  The matrix
+    is U diag(sigma) V^T with geometric singular values (R15)."""
+    n = 8192
+    A, _ = synthetic.conditioned(n, kappa, seed=500 + int(np.log10(kappa)))
+    x_true = synthetic.rhs(n, seed=501)
+    b = A.astype(np.float64) @ x_true
+    x, rep, hist = _solve(A, b, variant=3, nb=256)
+    assert rep.converged == 1 and rep.info == 0
+    assert rep.backward_error <= np.sqrt(n) * 2.0 ** -53 * 1.01      # the R14 stopping test
+    fe = np.linalg.norm(x - x_true) / np.linalg.norm(x_true)
+    assert fe < 100 * kappa * 2.0 ** -53 * n ** 0.5
+    assert len(hist) == rep.iterations + 1 and hist[-1] <= rep.tol
