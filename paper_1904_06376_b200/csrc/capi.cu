@@ -18,6 +18,7 @@ static void *g_ws = nullptr;
 static size_t g_ws_bytes = 0;
 static int g_max_ctas = 0;  // cap on the GEMM's persistent grid (bf16x_max_ctas hook; 0 = all SMs)
 static int g_group_m = 0;   // tile raster group (bf16x_group_m hook; 0 = default)
+static int g_fused_a = 0;       // convert A inside the GEMM, split only B (bf16x_fused_a hook)
 static int g_split_ahead = 0;   // split inside the GEMM (split-ahead warps; opt-in, not faster)
 static int g_force_cg = 0, g_force_bn = 0, g_force_spi = 0, g_stream_k = 1, g_multicast = 0, g_split_acc = 0, g_fused = 0;  // tuning overrides (bf16x_tune; not in the public ABI)
 
@@ -129,12 +130,26 @@ int gemm_core(int m, int n, int k, float alpha, const float *A, int lda, const f
     pl.fp64 = (flags & BF16X_FP64_COMBINE) ? 1 : 0;
     pl.group_m = g_group_m;
     pl.split_ahead = 0;
+    pl.fused_a = 0;
     const bool sc = pl.scaled != 0;
     pl.Af = A; pl.Bf = B; pl.lda = lda; pl.ldb = ldb;
     if (!Ap && !Bp && g_fused && !sc && !pl.fp64) {   // split inside the GEMM when the plan qualifies
         pl.Ap = nullptr; pl.Bp = nullptr;
         const int frc = launch_gemm_fused(pl, st);
         if (frc != -1) return frc;
+    }
+    if (!Ap && !Bp && g_fused_a && fused_a_ok(pl)) {
+        // only B is split in the pre-pass; the GEMM converts A from FP32 tiles
+        uint16_t *b = (uint16_t *)w;
+        b_plane = (int64_t)n * kp;
+        ldbp = kp;
+        rc = launch_split(k, n, B, ldb, b, pb > 1 ? b + b_plane : nullptr, pb > 2 ? b + 2 * b_plane : nullptr, ldbp,
+                          false, st, false);
+        if (rc) return rc;
+        pl.Ap = nullptr;
+        pl.Bp = b; pl.ldbp = ldbp; pl.b_plane = b_plane;
+        pl.fused_a = 1;
+        return launch_gemm_pieces(pl, st);
     }
     if (!Ap && !Bp && g_split_ahead && allow_stream_k && split_ahead_ok(pl)) {
         // the GEMM's split-ahead warps write the pieces into the workspace (pre-pass layout)
@@ -475,6 +490,7 @@ void bf16x_stream_k(int on) { g_stream_k = on; }
 void bf16x_split_acc(int on) { g_split_acc = on; }
 void bf16x_group_m(int g) { g_group_m = g; }
 void bf16x_max_ctas(int c) { g_max_ctas = c; }   // tile raster group height (0 = default)
+void bf16x_fused_a(int on) { g_fused_a = on; }   // convert A inside the GEMM (fused-A warps)
 void bf16x_split_ahead(int on) { g_split_ahead = on; }   // split inside the GEMM (split-ahead warps)
 // Timeline of the last pipelined bf16x_gemm_host call, ms since its start: [0] start, [1] A
 // landed, [2] A split, [3] unused, then per chunk j: [4+3j] B_j landed, [5+3j] GEMM_j done,

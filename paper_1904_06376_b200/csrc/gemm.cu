@@ -176,6 +176,14 @@ bool split_ahead_ok(const GemmPlan &pl) {
     return !mc2 && pl.Af && pl.Bf;
 }
 
+bool fused_a_ok(const GemmPlan &pl) {
+    const int cg = pl.cta_group ? pl.cta_group : kDefaultCtaGroup;
+    if (cg != 2 || pl.fp64 || pl.split_acc || pl.scaled || pl.k <= 0 || pl.tile_n == 192 || !pl.Af) return false;
+    if ((reinterpret_cast<uintptr_t>(pl.Af) & 15u) || pl.lda % 4) return false;
+    const bool mc2 = pl.multicast == 2 || (pl.multicast == 0 && (int64_t)pl.m * pl.n >= 12288LL * 12288LL);
+    return !mc2;
+}
+
 static int dispatch(const GemmPlan &pl, cudaStream_t st, int kind) {
     switch (pl.variant) {
     case 1: return launch_variant_1(pl, st, kind);

@@ -71,6 +71,21 @@ struct CfgF {
     static_assert(STAGES >= 2, "fused split needs two piece stages");
 };
 
+// Fused-A configuration (FA: A converted inside the GEMM from FP32 tiles, B pre-split): a ring of
+// FSTAGES FP32 A tiles (128 rows x 32 k per CTA, 16 KB) beside the piece ring, 227 KB in all.
+#ifndef FA_FST
+#define FA_FST 2
+#endif
+template <int V>
+struct CfgFA {
+    using Cf = Cfg<2, V, 256>;
+    static constexpr int FSTAGES = FA_FST;
+    static constexpr int STAGES_RAW = (232448 - 1280 - FSTAGES * kF32Tile) / Cf::STAGE;
+    static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
+    static constexpr int SMEM = STAGES * Cf::STAGE + FSTAGES * kF32Tile + 256 + 1024;
+    static_assert(STAGES >= 3, "fused A needs three piece stages");
+};
+
 struct KParams {
     int m, n, k;
     float alpha, beta;
@@ -345,13 +360,20 @@ __device__ __forceinline__ void split_ahead_warps(const KParams &p, int t) {
 // partial sums Z^(i,j), pooled per accumulator) and only their final collection is
 // FP64, rounded once to FP32 ("adding the final results together in FP64").
 // SP (split-ahead): see kNumSpWarps.
-template <int CG, int V, int BN, int S, int MC, bool SA, bool FU = false, bool GD = false, bool SP = false>
-__global__ void __launch_bounds__(FU ? kThreadsFused : (SP ? kThreadsSp : kThreads), 1)
+// FA (fused A): A is read as FP32 tiles by TMA and converted by 4 extra warps (warps 12..15,
+// thread t = row t of the CTA's 128 A rows) into the A half of the piece ring; B's pieces come
+// from the pre-pass by TMA as usual.  The piece-ring "full" barrier counts the leader's
+// expect-tx arrival (B bytes) plus the converters' arrivals of both CTAs.
+template <int CG, int V, int BN, int S, int MC, bool SA, bool FU = false, bool GD = false, bool SP = false,
+          bool FA = false>
+__global__ void __launch_bounds__((FU || FA) ? kThreadsFused : (SP ? kThreadsSp : kThreads), 1)
     gemm_split_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                       const KParams p) {
     using Cf = Cfg<CG, V, BN>;
-    constexpr int NST = FU ? CfgF<V>::STAGES : Cf::STAGES;     // piece ring stages
-    constexpr int NF = FU ? CfgF<V>::FSTAGES : 0;              // FP32 ring stages
+    constexpr int NST = FU ? CfgF<V>::STAGES : (FA ? CfgFA<V>::STAGES : Cf::STAGES);   // piece ring stages
+    constexpr int NF = FU ? CfgF<V>::FSTAGES : (FA ? CfgFA<V>::FSTAGES : 0);         // FP32 ring stages
+    constexpr int F32_STAGE = FA ? kF32Tile : 2 * kF32Tile;                          // FP32 ring stage bytes
+    static_assert(!FA || (CG == 2 && BN == 256 && MC == 1 && !SA && !FU && !SP && !GD), "fused A: 2-CTA, N 256");
     static_assert(!FU || (CG == 2 && BN == 256 && S == 1 && MC == 1 && !SA), "fused split: 2-CTA, N 256, S 1");
     constexpr int CL = CG * MC;   // cluster size
     static_assert(MC == 1 || CG == 2, "multicast needs 2-CTA pairs");
@@ -364,13 +386,13 @@ __global__ void __launch_bounds__(FU ? kThreadsFused : (SP ? kThreadsSp : kThrea
     uint8_t *sA = smem;
     uint8_t *sB = smem + NST * Cf::A_STAGE;
     uint8_t *f32 = smem + NST * Cf::STAGE;                      // FU: [NF][A tile | B tile]
-    uint64_t *full = reinterpret_cast<uint64_t *>(smem + NST * Cf::STAGE + NF * 2 * kF32Tile);
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem + NST * Cf::STAGE + NF * F32_STAGE);
     uint64_t *empty = full + NST;
     uint64_t *acc_full = empty + NST;
     uint64_t *acc_empty = acc_full + 2;
     uint64_t *f32_full = acc_empty + 2;
-    uint64_t *f32_empty = f32_full + 2;
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(f32_empty + 2);
+    uint64_t *f32_empty = f32_full + (NF > 2 ? NF : 2);
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(f32_empty + (NF > 2 ? NF : 2));
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t crank = (CL > 1) ? cluster_ctarank() : 0u;   // rank in the cluster
@@ -383,14 +405,14 @@ __global__ void __launch_bounds__(FU ? kThreadsFused : (SP ? kThreadsSp : kThrea
     }
     if (warp == 1 && lane == 0) {
         for (int s = 0; s < NST; ++s) {
-            mbar_init(&full[s], FU ? kNumXfWarps * CG : 1);
+            mbar_init(&full[s], FU ? kNumXfWarps * CG : (FA ? 1 + kNumXfWarps * CG : 1));
             mbar_init(&empty[s], MC);     // one commit per pair reading the (shared) stage
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(&acc_full[b], 1);
             mbar_init(&acc_empty[b], kNumEpiWarps * CG);
         }
-        if constexpr (FU)
+        if constexpr (FU || FA)
             for (int b = 0; b < NF; ++b) {
                 mbar_init(&f32_full[b], 1);
                 mbar_init(&f32_empty[b], kNumXfWarps);
@@ -414,12 +436,15 @@ __global__ void __launch_bounds__(FU ? kThreadsFused : (SP ? kThreadsSp : kThrea
     if (warp < 4) {
         if constexpr (FU) asm volatile("setmaxnreg.dec.sync.aligned.u32 48;" ::: "memory");
         if constexpr (SP) asm volatile("setmaxnreg.dec.sync.aligned.u32 56;" ::: "memory");
+        if constexpr (FA) asm volatile("setmaxnreg.dec.sync.aligned.u32 48;" ::: "memory");
         if (warp == 0) {
             // ------------------------------ TMA producer ------------------------------
             if (lane == 0) {
                 int stage = 0;
                 uint32_t phase = 0;
                 int slab_ready = -1;   // SP: highest slab known to be split by every CTA
+                int fstage = 0;        // FA: FP32 ring
+                uint32_t fphase = 0;
                 WorkIter it(p, cid, ncl);
                 Work w;
                 while (it.next(p, w)) {
@@ -429,6 +454,21 @@ __global__ void __launch_bounds__(FU ? kThreadsFused : (SP ? kThreadsSp : kThrea
                     const int a_row = tm * Cf::TILE_M + (int)rank * kBM;
                     const int b_row = tn * BN + (int)rank * Cf::BN_LOCAL;
                     const int kb_end = min(p.nkb, w.i1 * S);
+                    if constexpr (FA) {
+                        // FP32 tile of this CTA's 128 A rows (local completion, converted by
+                        // warps 12..15) and the B pieces of the pair (TMA to the leader's barrier)
+                        for (int kb = w.i0 * S; kb < kb_end; ++kb) {
+                            mbar_wait(&f32_empty[fstage], fphase ^ 1u);
+                            mbar_arrive_expect_tx(&f32_full[fstage], kF32Tile);
+                            tma_load_2d(f32 + fstage * kF32Tile, &tmA, &f32_full[fstage], a_row, kb * kBK);
+                            if (++fstage == NF) { fstage = 0; fphase ^= 1u; }
+                            mbar_wait(&empty[stage], phase ^ 1u);
+                            if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * Cf::B_STAGE);
+                            tma_load_3d_2sm(sB + stage * Cf::B_STAGE, &tmB, &full[stage], kb * kBK, b_row, 0);
+                            if (++stage == NST) { stage = 0; phase ^= 1u; }
+                        }
+                        continue;
+                    }
                     if constexpr (FU) {
                         // FP32 tiles of this CTA's 128 A rows and 128 B rows, local completion
                         for (int kb = w.i0 * S; kb < kb_end; ++kb) {
@@ -524,7 +564,7 @@ __global__ void __launch_bounds__(FU ? kThreadsFused : (SP ? kThreadsSp : kThrea
             }
         }
     } else if (warp < 4 + kNumEpiWarps) {
-        if constexpr (FU) asm volatile("setmaxnreg.inc.sync.aligned.u32 160;" ::: "memory");
+        if constexpr (FU || FA) asm volatile("setmaxnreg.inc.sync.aligned.u32 160;" ::: "memory");
         if constexpr (SP) asm volatile("setmaxnreg.inc.sync.aligned.u32 168;" ::: "memory");
         // ------------------------- promotion + epilogue ---------------------------
         constexpr int EC = Cf::EPI_COLS;
@@ -654,6 +694,63 @@ __global__ void __launch_bounds__(FU ? kThreadsFused : (SP ? kThreadsSp : kThrea
     } else if constexpr (SP) {
         asm volatile("setmaxnreg.dec.sync.aligned.u32 112;" ::: "memory");
         split_ahead_warps<Cf::PA, Cf::PB>(p, threadIdx.x - kThreads);
+    } else if constexpr (FA) {
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 48;" ::: "memory");
+        // ------------------- fused A: FP32 A tiles -> A pieces -------------------
+        // 8 warps: thread tx converts half (16 values of k) of row t = tx % 128 of the A tile,
+        // which is [k][128 rows] FP32 (no swizzle): element (t, k) at k*512 + 4t, so the 32
+        // lanes of a warp read 32 consecutive words per k.  The 16 values are loaded first,
+        // then split in pairs (same arithmetic as the pre-pass) and stored as two 16-byte chunks
+        // of the row's 64-byte K-major piece rows, with the 64-byte swizzle of the descriptors.
+        const int tx = threadIdx.x - kThreads;
+        const int t = tx & (kBM - 1), hk = tx >> 7;
+        const uint32_t swz = (uint32_t)((t >> 1) & 3);
+        const uint32_t f32_s = smem_u32(f32), sA_s = smem_u32(sA);
+        int fs = 0, ps = 0;
+        uint32_t fph = 0, pph = 0;
+        WorkIter it(p, cid, ncl);
+        Work w;
+        while (it.next(p, w)) {
+            const int kb_end = min(p.nkb, w.i1 * S);
+            for (int kb = w.i0 * S; kb < kb_end; ++kb) {
+                mbar_wait(&f32_full[fs], fph);
+                const uint32_t fa = f32_s + (uint32_t)(fs * kF32Tile) + (uint32_t)t * 4u;
+                float x[kBK / 2];
+#pragma unroll
+                for (int j = 0; j < kBK / 2; ++j) x[j] = lds_f32(fa + (uint32_t)((hk * 16 + j) * kBM * 4));
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&f32_empty[fs]);      // the FP32 tile is in registers
+                if (++fs == NF) { fs = 0; fph ^= 1u; }
+                mbar_wait(&empty[ps], pph ^ 1u);
+                const uint32_t pa = sA_s + (uint32_t)(ps * Cf::A_STAGE) + (uint32_t)t * kRowBytes;
+#pragma unroll
+                for (int h2 = 0; h2 < 2; ++h2) {
+                    const uint32_t hh = (uint32_t)(2 * hk + h2);     // 16-byte chunk of the row
+                    uint32_t q[4][3];
+                    bool ok = true;
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) ok = ok && regular(x[h2 * 8 + j]);
+                    if (ok) {
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) split_pair_fast<Cf::PA>(x[h2 * 8 + 2 * j], x[h2 * 8 + 2 * j + 1], q[j]);
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) split_pair<Cf::PA>(x[h2 * 8 + 2 * j], x[h2 * 8 + 2 * j + 1], q[j]);
+                    }
+#pragma unroll
+                    for (int pc = 0; pc < Cf::PA; ++pc)
+                        sts_u32x4(pa + (uint32_t)(pc * Cf::A_PIECE) + ((hh ^ swz) << 4), q[0][pc], q[1][pc], q[2][pc],
+                                  q[3][pc]);
+                }
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // visible to the tensor core
+                __syncwarp();
+                if (lane == 0) {
+                    if (rank == 0) mbar_arrive(&full[ps]);
+                    else mbar_arrive_release_cluster(&full[ps], pair * CG);
+                }
+                if (++ps == NST) { ps = 0; pph ^= 1u; }
+            }
+        }
     } else if constexpr (FU) {
         asm volatile("setmaxnreg.dec.sync.aligned.u32 48;" ::: "memory");
         // ----------------------- fused split: FP32 tiles -> pieces ----------------------
@@ -774,16 +871,21 @@ int sk_workspace(size_t ws_floats, size_t nflags, float **ws, unsigned int **fla
 // split-ahead slab counters (nslab + 1 words, zero between launches; one stream at a time)
 int sp_counters(int nslab, unsigned int **ctr);
 
-template <int CG, int V, int BN, int S, int MC, bool SA = false, bool FU = false, bool GD = false, bool SP = false>
+template <int CG, int V, int BN, int S, int MC, bool SA = false, bool FU = false, bool GD = false, bool SP = false,
+          bool FA = false>
 int launch_t(const GemmPlan &pl, cudaStream_t st) {
     using Cf = Cfg<CG, V, BN>;
     constexpr int CL = CG * MC;
-    constexpr int THREADS = FU ? kThreadsFused : (SP ? kThreadsSp : kThreads);
-    constexpr int SMEM = FU ? CfgF<V>::SMEM : Cf::SMEM;
-    auto kern = gemm_split_kernel<CG, V, BN, S, MC, SA, FU, GD, SP>;
+    constexpr int THREADS = (FU || FA) ? kThreadsFused : (SP ? kThreadsSp : kThreads);
+    constexpr int SMEM = FU ? CfgF<V>::SMEM : (FA ? CfgFA<V>::SMEM : Cf::SMEM);
+    auto kern = gemm_split_kernel<CG, V, BN, S, MC, SA, FU, GD, SP, FA>;
     CUtensorMap tmA, tmB;
     int rc;
-    if constexpr (FU) {
+    if constexpr (FA) {
+        rc = make_f32_map(&tmA, pl.Af, pl.m, pl.k, pl.lda, kBM, kBK, CU_TENSOR_MAP_SWIZZLE_NONE);
+        if (rc) return rc;
+        rc = make_piece_map(&tmB, pl.Bp, pl.k, pl.n, pl.ldbp, pl.b_plane, Cf::PB, Cf::BN_LOCAL);
+    } else if constexpr (FU) {
         rc = make_f32_map(&tmA, pl.Af, pl.m, pl.k, pl.lda, kBM, kBK, CU_TENSOR_MAP_SWIZZLE_NONE);
         if (rc) return rc;
         rc = make_f32_map(&tmB, pl.Bf, pl.k, pl.n, pl.ldb, kBK, Cf::BN_LOCAL, CU_TENSOR_MAP_SWIZZLE_128B);
@@ -928,6 +1030,13 @@ int launch_s(const GemmPlan &pl, cudaStream_t st) {
     // intervals (one instance per variant)
     if constexpr (V >= 3)
         if (pl.fp64) return launch_t<2, V, 128, 2, 1, true, false, true>(pl, st);
+    // fused A: the caller (gemm_core) chose it with fused_a_ok() and split only B
+    if (pl.fused_a) {
+        if (CG == 2) return s == 2 ? launch_t<2, V, 256, 2, 1, false, false, false, false, true>(pl, st)
+                                   : launch_t<2, V, 256, 1, 1, false, false, false, false, true>(pl, st);
+        set_error_msg("fused-A plan not launchable");
+        return BF16X_ERR_CUDA;
+    }
     // split-ahead: the caller (gemm_core) chose it with split_ahead_ok(), which mirrors the
     // conditions below; the pieces are written by this launch only
     if (pl.split_ahead) {

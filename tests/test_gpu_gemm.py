@@ -434,3 +434,53 @@ def test_split_ahead_matches_prepass(orc, split_ahead_on, shape, variant, scaled
         outs.append(bx.gemm(Ad, Bd, variant=variant, scaled=scaled).cpu().numpy())
     for o in outs[1:]:
         assert np.array_equal(o.view(np.uint32), outs[0].view(np.uint32))
+
+
+@pytest.fixture
+def fused_a_on():
+    L = bx.lib()
+    L.bf16x_fused_a(1)
+    yield L
+    L.bf16x_fused_a(0)
+
+
+@pytest.mark.parametrize("variant", [1, 3, 5, 6, 7, 8, 9])
+@pytest.mark.parametrize("shape", [(256, 256, 200), (300, 700, 333), (1024, 2048, 1000), (130, 260, 1037),
+                                   (4096, 1024, 2048), (200, 300, 96)])
+def test_fused_a_matches_prepass(orc, fused_a_on, shape, variant):
+    """Fused A (A's FP32 tiles converted by 4 extra warps inside the GEMM, only B split in the
+    pre-pass) places exactly the pre-pass's A pieces in shared memory, so C is bit-identical,
+    ragged rows / k and both promotion intervals (k <= 128 uses 32-k intervals) included."""
+    m, n, k = shape
+    A = synthetic.wide(m, k, seed=m + 3 * k, E=20)
+    B = synthetic.wide(k, n, seed=n + 5 * k, E=20)
+    Ad = torch.from_numpy(np.asfortranarray(A)).cuda()
+    Bd = torch.from_numpy(np.asfortranarray(B)).cuda()
+    outs = []
+    for on in (1, 0, 1):
+        fused_a_on.bf16x_fused_a(on)
+        outs.append(bx.gemm(Ad, Bd, variant=variant).cpu().numpy())
+    for o in outs[1:]:
+        assert np.array_equal(o.view(np.uint32), outs[0].view(np.uint32))
+
+
+def test_fused_a_nonfinite_and_ld(orc, fused_a_on):
+    """NaN / Inf / the b0-overflow band in A take the integer path of the in-kernel split; a
+    leading dimension > m (multiple of 4) and beta != 0 as well."""
+    m, n, k = 300, 260, 150
+    lda = 304
+    Abig = synthetic.uniform(lda, k, seed=9)
+    Abig[5, 7] = np.nan
+    Abig[17, 3] = np.inf
+    Abig[40, 100] = -np.inf
+    Abig[99, 33] = np.float32(3.4e38)
+    B = synthetic.uniform(k, n, seed=10)
+    C0 = synthetic.uniform(m, n, seed=11)
+    Ad = torch.from_numpy(np.asfortranarray(Abig)).cuda()[:m]
+    Bd = torch.from_numpy(np.asfortranarray(B)).cuda()
+    res = []
+    for on in (1, 0):
+        fused_a_on.bf16x_fused_a(on)
+        Cd = torch.from_numpy(np.asfortranarray(C0)).cuda()
+        res.append(bx.gemm(Ad, Bd, C=Cd, alpha=0.5, beta=2.0, variant=6).cpu().numpy())
+    assert np.array_equal(res[0].view(np.uint32), res[1].view(np.uint32))
