@@ -1029,7 +1029,14 @@ int launch_s(const GemmPlan &pl, cudaStream_t st) {
     // "d" variants (R30): 2-CTA pairs, tile N 128, split accumulators, FP64 collection, 64-k
     // intervals (one instance per variant)
     if constexpr (V >= 3)
-        if (pl.fp64) return launch_t<2, V, 128, 2, 1, true, false, true>(pl, st);
+        if (pl.fp64) {
+            // x3d: 128-k intervals (fewer promotions of the two accumulators; +12 % at 4096^3,
+            // r06 tools/gd_probe.py); the longer-product variants keep 64-k intervals (x6d -4 %,
+            // x9d -15 % with 128-k ones: their 6-stage ring then stalls between intervals)
+            if (pl.stages_per_interval == 4 || (V <= 3 && pl.stages_per_interval == 0))
+                return launch_t<2, V, 128, 4, 1, true, false, true>(pl, st);
+            return launch_t<2, V, 128, 2, 1, true, false, true>(pl, st);
+        }
     // fused A: the caller (gemm_core) chose it with fused_a_ok() and split only B
     if (pl.fused_a) {
         if (CG == 2) return s == 2 ? launch_t<2, V, 256, 2, 1, false, false, false, false, true>(pl, st)
