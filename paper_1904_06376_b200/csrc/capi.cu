@@ -18,7 +18,9 @@ static void *g_ws = nullptr;
 static size_t g_ws_bytes = 0;
 static int g_max_ctas = 0;  // cap on the GEMM's persistent grid (bf16x_max_ctas hook; 0 = all SMs)
 static int g_group_m = 0;   // tile raster group (bf16x_group_m hook; 0 = default)
-static int g_fused_a = 0;       // convert A inside the GEMM, split only B (bf16x_fused_a hook)
+// convert A inside the GEMM, split only B (bf16x_fused_a hook: 1 on, 0 off, -1 auto = bf16x9
+// only, the variant where it measured faster: +1..6 % for 2048^3..8192^3, r06 tools/fa9_probe.py)
+static int g_fused_a = -1;
 static int g_split_ahead = 0;   // split inside the GEMM (split-ahead warps; opt-in, not faster)
 static int g_force_cg = 0, g_force_bn = 0, g_force_spi = 0, g_stream_k = 1, g_multicast = 0, g_split_acc = 0, g_fused = 0;  // tuning overrides (bf16x_tune; not in the public ABI)
 
@@ -138,7 +140,7 @@ int gemm_core(int m, int n, int k, float alpha, const float *A, int lda, const f
         const int frc = launch_gemm_fused(pl, st);
         if (frc != -1) return frc;
     }
-    if (!Ap && !Bp && g_fused_a && fused_a_ok(pl)) {
+    if (!Ap && !Bp && (g_fused_a == 1 || (g_fused_a < 0 && variant == 9)) && fused_a_ok(pl)) {
         // only B is split in the pre-pass; the GEMM converts A from FP32 tiles
         uint16_t *b = (uint16_t *)w;
         b_plane = (int64_t)n * kp;
@@ -490,7 +492,7 @@ void bf16x_stream_k(int on) { g_stream_k = on; }
 void bf16x_split_acc(int on) { g_split_acc = on; }
 void bf16x_group_m(int g) { g_group_m = g; }
 void bf16x_max_ctas(int c) { g_max_ctas = c; }   // tile raster group height (0 = default)
-void bf16x_fused_a(int on) { g_fused_a = on; }   // convert A inside the GEMM (fused-A warps)
+void bf16x_fused_a(int on) { g_fused_a = on; }   // 1 on, 0 off, -1 auto (fused-A warps)
 void bf16x_split_ahead(int on) { g_split_ahead = on; }   // split inside the GEMM (split-ahead warps)
 // Timeline of the last pipelined bf16x_gemm_host call, ms since its start: [0] start, [1] A
 // landed, [2] A split, [3] unused, then per chunk j: [4+3j] B_j landed, [5+3j] GEMM_j done,

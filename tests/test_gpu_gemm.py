@@ -441,7 +441,7 @@ def fused_a_on():
     L = bx.lib()
     L.bf16x_fused_a(1)
     yield L
-    L.bf16x_fused_a(0)
+    L.bf16x_fused_a(-1)
 
 
 @pytest.mark.parametrize("variant", [1, 3, 5, 6, 7, 8, 9])
@@ -457,7 +457,7 @@ def test_fused_a_matches_prepass(orc, fused_a_on, shape, variant):
     Ad = torch.from_numpy(np.asfortranarray(A)).cuda()
     Bd = torch.from_numpy(np.asfortranarray(B)).cuda()
     outs = []
-    for on in (1, 0, 1):
+    for on in (1, 0, 1, -1):
         fused_a_on.bf16x_fused_a(on)
         outs.append(bx.gemm(Ad, Bd, variant=variant).cpu().numpy())
     for o in outs[1:]:
