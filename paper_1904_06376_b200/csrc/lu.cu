@@ -99,11 +99,13 @@ __device__ __forceinline__ void async_wait_all() {
 // c = s0+t), per owned unpivoted row:
 //   (a) apply step t-1: l = a[i,c-1] / p[c-1] stored in place (the L multiplier),
 //       a[i,c'] -= l * p[c'] for c' >= c (p = pivot row of step t-1);
-//   (b) candidate |a[i,c]| (ties -> lowest row, LAPACK isamax on the unswapped order); warp
-//       0 reduces the warps' candidates and PUSHES the CTA's (|a|, row, row entries) into
-//       every peer's receive slot with st.async, completing bytes on the peer's mbarrier;
-//   (c) warp 0 waits on its own mbarrier for all peers' records (no cluster barrier, no
-//       GPU-scope fence per column), picks the same winner everywhere and stores its row as p.
+//   (b) candidate |a[i,c]| (ties -> lowest row, LAPACK isamax on the unswapped order): each
+//       warp's best key into its shared slot (its best row into its record); warp 0 reduces
+//       the 16 warp keys and PUSHES the CTA's key (|a|, row) into every peer's receive slot
+//       with st.async, completing bytes on the peer's mbarrier;
+//   (c) warp 0 waits on its own mbarrier for all peers' keys (no cluster barrier, no
+//       GPU-scope fence per column), picks the same winner everywhere and reads the winning
+//       row from the winner CTA's record (DSMEM load) as p.
 // Rows are not moved inside the sub-panel: at the end CTA 0 turns the chosen rows into the
 // LAPACK interchange sequence (ipiv) and the equivalent gather pairs, which laswp_kernel
 // then applies to all n columns.  All panel arithmetic is FP32.
@@ -127,6 +129,39 @@ __device__ __forceinline__ void st_async_v4(uint32_t raddr, uint32_t a, uint32_t
                  : "memory");
 }
 
+// One bulk DSMEM copy (async proxy) of `bytes` (multiple of 16) from this CTA's shared memory
+// into a peer's, completing the bytes on the peer's mbarrier: one transaction-count update per
+// record at the receiver instead of one per 16-byte st.async.
+__device__ __forceinline__ void bulk_to_peer(uint32_t dst_cluster, uint32_t src_cta, uint32_t bytes,
+                                             uint32_t mbar_cluster) {
+    asm volatile("cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     dst_cluster),
+                 "r"(src_cta), "r"(bytes), "r"(mbar_cluster)
+                 : "memory");
+}
+
+__device__ __forceinline__ void st_async_v2(uint32_t raddr, uint32_t a, uint32_t b, uint32_t rbar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.b32 [%0], {%1, %2}, [%3];" ::"r"(raddr),
+                 "r"(a), "r"(b), "r"(rbar)
+                 : "memory");
+}
+__device__ __forceinline__ void st_cluster_v4(uint32_t caddr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+    asm volatile("st.shared::cluster.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(caddr), "r"(a), "r"(b), "r"(c), "r"(d)
+                 : "memory");
+}
+__device__ __forceinline__ uint4 ld_volatile_v4(uint32_t saddr) {
+    uint4 v;
+    asm volatile("ld.volatile.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "r"(saddr)
+                 : "memory");
+    return v;
+}
+__device__ __forceinline__ float ld_cluster_f32(uint32_t caddr) {
+    float v;
+    asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(caddr) : "memory");
+    return v;
+}
+
 // Candidate key: |a| (non-negative float bits, monotone as unsigned) in the high word, the
 // complemented row index in the low word, so the largest key is the largest |a| with ties
 // going to the lowest row (LAPACK isamax on the unswapped order).  0 = no candidate.
@@ -140,19 +175,34 @@ __device__ __forceinline__ uint64_t warp_max_key(uint32_t hi, uint32_t lo) {
     return ((uint64_t)mh << 32) | ml;
 }
 
-template <int RPT>
+__device__ unsigned long long g_sp_trace[kSubMaxCl * 32];   // [cta][0..7 phases, 8..23 warp work, 24..31 max-warp hist]
+extern "C" int bf16x_lu_subpanel_trace(unsigned long long *host, int clear) {   // diagnostic hook
+    if (clear) {
+        static const unsigned long long z[kSubMaxCl * 32] = {};
+        return cudaMemcpyToSymbol(g_sp_trace, z, sizeof(z)) == cudaSuccess ? 0 : 1;
+    }
+    return cudaMemcpyFromSymbol(host, g_sp_trace, sizeof(unsigned long long) * kSubMaxCl * 32) == cudaSuccess ? 0 : 1;
+}
+
+template <int RPT, bool TRACE>
 __global__ void __launch_bounds__(kSubThreads) subpanel_kernel(float *LU, int ld, int n, int s0, int w, int *ipiv,
-                                                              int2 *pairs, int *npairs, int *info) {
+                                                              int2 *pairs, int *npairs, int *info, int bulk) {
     namespace cg = cooperative_groups;
     cg::cluster_group cl = cg::this_cluster();
     const int ncta = (int)cl.num_blocks(), rank = (int)cl.block_rank();
     __shared__ __align__(16) uint64_t rbar[2];                   // receive barriers
     __shared__ __align__(16) float rbuf[2 * kSubMaxCl * kSubRec];  // [2][cluster][record]
-    __shared__ __align__(16) float wslot[kSubWarps * kSubW];      // each warp's candidate row
+    // each warp's candidate record (header: key lo, key hi, 2 pad; then the row), double-buffered
+    // by step parity: a bulk copy of step t may still read its source while step t+1 runs, never
+    // at step t+2 (every peer's step-(t+1) record, which needs ours of step t, has arrived)
+    __shared__ __align__(16) float wrec[2 * kSubWarps * kSubRec];
     __shared__ __align__(16) float prow[kSubW];                   // pivot row, columns t.. (shifted)
-    __shared__ unsigned long long s_key[2];                       // CTA candidate (atomicMax)
+    __shared__ unsigned long long s_wkey[kSubWarps];              // each warp's candidate key
+    __shared__ __align__(16) uint4 rk[2 * kSubMaxCl];             // mode 3: [parity][cta] (key lo, hi, seq)
     __shared__ int s_rows[kSubW];                                 // chosen rows, step order
+    __shared__ int s_r0[kSubMaxCl];                               // first row of every CTA
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const long long tc_start = clock64();
     const int R = n - s0;
     const int r0 = s0 + (int)(((int64_t)R * rank) / ncta), r1 = s0 + (int)(((int64_t)R * (rank + 1)) / ncta);
     const int rl = r1 - r0;
@@ -173,9 +223,9 @@ __global__ void __launch_bounds__(kSubThreads) subpanel_kernel(float *LU, int ld
         mbar_init(&rbar[0], 1);
         mbar_init(&rbar[1], 1);
         fence_barrier_init();
-        s_key[0] = 0ull;
-        s_key[1] = 0ull;
     }
+    if (tid < 2 * kSubMaxCl) rk[tid] = make_uint4(0u, 0u, 0u, 0u);   // mode 3 sequence numbers start at 1
+    if (tid < ncta) s_r0[tid] = s0 + (int)(((int64_t)R * tid) / ncta);
     cl.sync();                                       // barriers initialised cluster-wide
     const uint32_t rbar_s = smem_u32(rbar), rbuf_s = smem_u32(rbuf);
     // interchange bookkeeping (CTA 0, warp 1, overlapped with the exchange): rows are at their
@@ -211,7 +261,15 @@ __global__ void __launch_bounds__(kSubThreads) subpanel_kernel(float *LU, int ld
         set(q, other);
         set(here, r);
     };
+    // diagnostic trace (mode bit 4): thread 0's cycles per phase, summed over the steps, and
+    // CTA 0 warp 1's bookkeeping cycles; slots [rank][0..7] of g_sp_trace
+    constexpr bool trace = TRACE;
+    bulk &= 3;
+    long long tc0 = clock64(), tc1 = 0, tc2 = 0, tc3 = 0, tc4 = 0;
+    long long acc[6] = {0, 0, 0, 0, 0, 0};
+    long long wstart = clock64(), wwork = 0;   // this warp's cycles from sync2 to its arrival at sync1
     for (int t = 0; t <= w; ++t) {
+        if (trace && tid == 0) { tc0 = clock64(); if (t > 0) acc[4] += tc0 - tc4; }
         if (t > 0) {
             // apply step t-1: l = a[i,c-1] / p[c-1] (stored), a[i,c'] -= l * p[c'], shift by one
             const float piv = prow[0];
@@ -234,6 +292,7 @@ __global__ void __launch_bounds__(kSubThreads) subpanel_kernel(float *LU, int ld
             }
         }
         if (t == w) break;
+        if (trace && tid == 0) { tc1 = clock64(); acc[0] += tc1 - tc0; }
         // this thread's best live row, then the warp's (two redux), then the CTA's (smem atomic)
         uint32_t bh = 0u, bl = 0u;
         int bk = -1;
@@ -247,68 +306,120 @@ __global__ void __launch_bounds__(kSubThreads) subpanel_kernel(float *LU, int ld
         }
         const uint64_t wk = warp_max_key(bh, bk >= 0 ? bl : 0u);
         if (bk >= 0 && wk == (((uint64_t)bh << 32) | bl)) {   // this lane holds the warp's best row
+            float *wrow = wrec + ((t & 1) * kSubWarps + wid) * kSubRec + 4;
 #pragma unroll
             for (int k = 0; k < RPT; ++k)
                 if (k == bk) {
 #pragma unroll
                     for (int c4 = 0; c4 < kSubW / 4; ++c4)
-                        reinterpret_cast<float4 *>(wslot + wid * kSubW)[c4] =
+                        reinterpret_cast<float4 *>(wrow)[c4] =
                             make_float4(a[k][4 * c4], a[k][4 * c4 + 1], a[k][4 * c4 + 2], a[k][4 * c4 + 3]);
                 }
+            if (bulk == 1) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // read by the bulk copy
         }
-        if (lane == 0 && (uint32_t)wk != 0u) atomicMax(&s_key[t & 1], (unsigned long long)wk);
+        if (lane == 0) s_wkey[wid] = wk;                   // 0: no live row in this warp
+        if (trace) wwork += clock64() - wstart;
         __syncthreads();
+        if (trace && tid == 0) { tc2 = clock64(); acc[1] += tc2 - tc1; }
         if (wid == 0) {
             const int buf = t & 1;
-            const uint64_t ck = s_key[buf];
-            const int crow = (int)(0xFFFFFFFFu - (uint32_t)ck);
-            const int cw = ((uint32_t)ck != 0u) ? ((crow - r0) % kSubThreads) / 32 : 0;   // winner warp
-            if (lane == 0) mbar_arrive_expect_tx(&rbar[buf], (uint32_t)(ncta * kSubRec * 4));
-            // lane q pushes the whole record (key, row entries; 9 x 16 B) into slot `rank` of
-            // CTA q's receive buffer
-            if (lane < ncta) {
-                const uint32_t slot = rbuf_s + (uint32_t)((buf * kSubMaxCl + rank) * kSubRec) * 4u;
-                const uint32_t rs = mapa_u32(slot, lane), rb = mapa_u32(rbar_s + (uint32_t)buf * 8u, lane);
-                st_async_v4(rs, (uint32_t)ck, (uint32_t)(ck >> 32), 0u, 0u, rb);
-                const float4 *src = reinterpret_cast<const float4 *>(wslot + cw * kSubW);
-#pragma unroll
-                for (int c4 = 0; c4 < kSubW / 4; ++c4) {
-                    const float4 r4 = src[c4];
-                    st_async_v4(rs + 16u + 16u * c4, __float_as_uint(r4.x), __float_as_uint(r4.y),
-                                __float_as_uint(r4.z), __float_as_uint(r4.w), rb);
+            // the CTA's candidate: maximum of the warps' keys (no shared atomics)
+            const uint64_t kq = (lane < kSubWarps) ? s_wkey[lane] : 0ull;
+            const uint64_t ck = warp_max_key((uint32_t)(kq >> 32), (uint32_t)kq);
+            const unsigned wh = __ballot_sync(0xffffffffu, lane < kSubWarps && kq == ck && ck != 0ull);
+            const int cw = wh ? __ffs(wh) - 1 : 0;                   // winner warp
+            float *crec = wrec + (buf * kSubWarps + cw) * kSubRec;   // the CTA's record
+            // exchange modes: 3 keys by plain remote stores + local polling, 2 keys by st.async,
+            // 1 whole records by bulk copy, 0 whole records by 9 st.async; 2 and 3 read the
+            // winning row from its CTA afterwards (pull)
+            const bool pull = bulk >= 2;
+            uint32_t ql = 0u, qh = 0u;
+            const float *rec = rbuf + buf * kSubMaxCl * (pull ? 2 : kSubRec);
+            const int rs = pull ? 2 : kSubRec;
+            if (bulk == 3) {
+                const uint32_t seq = (uint32_t)t + 1u;
+                if (lane < ncta)
+                    st_cluster_v4(mapa_u32(smem_u32(&rk[buf * kSubMaxCl + rank]), (uint32_t)lane), (uint32_t)ck,
+                                  (uint32_t)(ck >> 32), seq, 0u);
+                if (lane < ncta) {
+                    uint4 v;
+                    do { v = ld_volatile_v4(smem_u32(&rk[buf * kSubMaxCl + lane])); } while (v.z != seq);
+                    ql = v.x;
+                    qh = v.y;
                 }
+                __syncwarp();
+                if (trace && tid == 0) { tc3 = clock64(); acc[2] += tc3 - tc2; }
+            } else {
+                if (bulk == 1 && lane == 0) {
+                    reinterpret_cast<uint4 *>(crec)[0] = make_uint4((uint32_t)ck, (uint32_t)(ck >> 32), 0u, 0u);
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                }
+                if (lane == 0) mbar_arrive_expect_tx(&rbar[buf], (uint32_t)(ncta * (pull ? 8 : kSubRec * 4)));
+                if (bulk == 1) __syncwarp();
+                // lane q pushes into slot `rank` of CTA q's receive buffer
+                if (pull) {
+                    if (lane < ncta)
+                        st_async_v2(mapa_u32(rbuf_s + (uint32_t)((buf * kSubMaxCl + rank) * 2) * 4u, lane),
+                                    (uint32_t)ck, (uint32_t)(ck >> 32), mapa_u32(rbar_s + (uint32_t)buf * 8u, lane));
+                } else if (bulk == 1 && lane < ncta) {
+                    const uint32_t slot = rbuf_s + (uint32_t)((buf * kSubMaxCl + rank) * kSubRec) * 4u;
+                    bulk_to_peer(mapa_u32(slot, lane), smem_u32(crec), (uint32_t)(kSubRec * 4),
+                                 mapa_u32(rbar_s + (uint32_t)buf * 8u, lane));
+                } else if (lane < ncta) {
+                    const uint32_t slot = rbuf_s + (uint32_t)((buf * kSubMaxCl + rank) * kSubRec) * 4u;
+                    const uint32_t rsl = mapa_u32(slot, lane), rb = mapa_u32(rbar_s + (uint32_t)buf * 8u, lane);
+                    st_async_v4(rsl, (uint32_t)ck, (uint32_t)(ck >> 32), 0u, 0u, rb);
+                    const float4 *src = reinterpret_cast<const float4 *>(crec + 4);
+#pragma unroll
+                    for (int c4 = 0; c4 < kSubW / 4; ++c4) {
+                        const float4 r4 = src[c4];
+                        st_async_v4(rsl + 16u + 16u * c4, __float_as_uint(r4.x), __float_as_uint(r4.y),
+                                    __float_as_uint(r4.z), __float_as_uint(r4.w), rb);
+                    }
+                }
+                {   // spin (no suspend): this wait is on the factorisation's critical path
+                    const uint32_t par = (uint32_t)((t >> 1) & 1);
+                    uint32_t done = 0;
+                    while (!done)
+                        asm volatile(
+                            "{\n\t.reg .pred p;\n\t"
+                            "mbarrier.test_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+                            "selp.u32 %0, 1, 0, p;\n\t}"
+                            : "=r"(done)
+                            : "r"(rbar_s + (uint32_t)buf * 8u), "r"(par)
+                            : "memory");
+                }
+                if (trace && tid == 0) { tc3 = clock64(); acc[2] += tc3 - tc2; }
+                ql = (lane < ncta) ? __float_as_uint(rec[lane * rs]) : 0u;
+                qh = (lane < ncta) ? __float_as_uint(rec[lane * rs + 1]) : 0u;
             }
-            if (lane == 0) s_key[buf ^ 1] = 0ull;   // next step's accumulator (all atomics of
-                                                    // step t - 1 finished before this step's sync)
-            {   // spin (no suspend): this wait is on the factorisation's critical path
-                const uint32_t par = (uint32_t)((t >> 1) & 1);
-                uint32_t done = 0;
-                while (!done)
-                    asm volatile(
-                        "{\n\t.reg .pred p;\n\t"
-                        "mbarrier.test_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
-                        "selp.u32 %0, 1, 0, p;\n\t}"
-                        : "=r"(done)
-                        : "r"(rbar_s + (uint32_t)buf * 8u), "r"(par)
-                        : "memory");
-            }
-            // the cluster's winner, identical in every CTA: lane q holds record q
-            const float *rec = rbuf + buf * kSubMaxCl * kSubRec;
-            const uint32_t ql = (lane < ncta) ? __float_as_uint(rec[lane * kSubRec]) : 0u;
-            const uint32_t qh = (lane < ncta) ? __float_as_uint(rec[lane * kSubRec + 1]) : 0u;
+            // the cluster's winner, identical in every CTA: lane q holds CTA q's key
             const uint64_t gk = warp_max_key(qh, ql);
             const unsigned hit = __ballot_sync(0xffffffffu, lane < ncta && qh == (uint32_t)(gk >> 32) &&
                                                                 ql == (uint32_t)gk);
             const int gq = __ffs(hit) - 1;
-            prow[lane] = rec[gq * kSubRec + 4 + lane];
+            if (pull) {
+                // the winning row sits in CTA gq's record of its winning warp (same step parity)
+                const int grow = (int)(0xFFFFFFFFu - (uint32_t)gk);
+                const int r0q = s_r0[gq];
+                const int cwq = ((uint32_t)gk != 0u) ? ((grow - r0q) % kSubThreads) / 32 : 0;
+                const uint32_t src = smem_u32(wrec + (buf * kSubWarps + cwq) * kSubRec + 4 + lane);
+                prow[lane] = ld_cluster_f32(mapa_u32(src, (uint32_t)gq));
+            } else {
+                prow[lane] = rec[gq * kSubRec + 4 + lane];
+            }
             if (lane == 0) {
                 s_rows[t] = (int)(0xFFFFFFFFu - (uint32_t)gk);
                 if (rank == 0 && (uint32_t)(gk >> 32) == 0u && *info == 0) *info = s0 + t + 1;
             }
         } else if (book && t > 0) {
+            const long long b0 = clock64();
             book_step(t - 1);
+            if (trace && lane == 0) acc[5] += clock64() - b0;
         }
         __syncthreads();
+        if (trace && tid == 0) { tc4 = clock64(); acc[3] += tc4 - tc3; }
+        if (trace) wstart = clock64();
         const int gi = s_rows[t];                    // the owner retires its pivot row: U part
 #pragma unroll
         for (int k = 0; k < RPT; ++k)
@@ -331,6 +442,17 @@ __global__ void __launch_bounds__(kSubThreads) subpanel_kernel(float *LU, int ld
         if (lane == 0) *npairs = np;
     }
     cl.sync();   // no CTA exits while a peer may still push into it
+    if (trace && lane == 0) atomicAdd(g_sp_trace + rank * 32 + 8 + wid, (unsigned long long)wwork);
+    if (trace && (tid == 0 || (book && lane == 0))) {
+        unsigned long long *tr = g_sp_trace + rank * 32;
+        if (tid == 0) {
+            for (int q = 0; q < 5; ++q) atomicAdd(tr + q, (unsigned long long)acc[q]);
+            atomicAdd(tr + 6, (unsigned long long)(clock64() - tc_start));
+            atomicAdd(tr + 7, 1ull);
+        } else {
+            atomicAdd(tr + 5, (unsigned long long)acc[5]);
+        }
+    }
 }
 
 // After sub-panel [s0, s0+w) (rows already interchanged): remaining panel columns [c1, c2)
@@ -875,6 +997,15 @@ static int sub_rpt(int n, int cl) {
     return 0;
 }
 
+// sub-panel exchange mode (diagnostic hook bf16x_lu_subpanel_bulk; bit 4 = clock64 trace):
+// 2 = keys by st.async + winning row read from its CTA (default), 0 = whole records by 9 st.async
+// per peer, 1 = whole records by one bulk copy per peer, 3 = keys by plain remote stores polled
+// locally.  All four are bit-identical; measured (r06, tools/lu_bulk_probe.py / lu_time.py) the
+// factorisation device time is the same within 1 % (26.4 ms at n = 8192): the exchange is not
+// what bounds the ~1.9 us per column.
+static int g_sub_bulk = 2;
+extern "C" void bf16x_lu_subpanel_bulk(int mode) { g_sub_bulk = mode & 7; }   // bit 4: trace
+
 static cudaError_t launch_subpanel(const LuWork &w, int s0, int sw, cudaStream_t st, int2 *pairs, int *npairs) {
     const int rpt = sub_rpt(w.n, w.cl);
     if (rpt == 0) return cudaErrorInvalidValue;
@@ -890,9 +1021,18 @@ static cudaError_t launch_subpanel(const LuWork &w, int s0, int sw, cudaStream_t
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    if (rpt == 1) return cudaLaunchKernelEx(&cfg, subpanel_kernel<1>, w.LU, w.ld, w.n, s0, sw, w.ipiv, pairs, npairs, w.info);
-    if (rpt == 2) return cudaLaunchKernelEx(&cfg, subpanel_kernel<2>, w.LU, w.ld, w.n, s0, sw, w.ipiv, pairs, npairs, w.info);
-    return cudaLaunchKernelEx(&cfg, subpanel_kernel<4>, w.LU, w.ld, w.n, s0, sw, w.ipiv, pairs, npairs, w.info);
+    const int bulk = g_sub_bulk;
+#define SUBPANEL_LAUNCH(R_, T_) \
+    cudaLaunchKernelEx(&cfg, subpanel_kernel<R_, T_>, w.LU, w.ld, w.n, s0, sw, w.ipiv, pairs, npairs, w.info, bulk)
+    if (bulk & 4) {
+        if (rpt == 1) return SUBPANEL_LAUNCH(1, true);
+        if (rpt == 2) return SUBPANEL_LAUNCH(2, true);
+        return SUBPANEL_LAUNCH(4, true);
+    }
+    if (rpt == 1) return SUBPANEL_LAUNCH(1, false);
+    if (rpt == 2) return SUBPANEL_LAUNCH(2, false);
+    return SUBPANEL_LAUNCH(4, false);
+#undef SUBPANEL_LAUNCH
 }
 
 static int coop_launch(const void *fn, int grid, int threads, void **args, size_t smem, cudaStream_t st) {
@@ -938,9 +1078,12 @@ static int lu_prepare(LuWork &w, int n, int nb, float *LU, int ld, int *ipiv, bo
     }
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(subpanel_kernel<1>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-        cudaFuncSetAttribute(subpanel_kernel<2>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-        cudaFuncSetAttribute(subpanel_kernel<4>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        cudaFuncSetAttribute(subpanel_kernel<1, false>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        cudaFuncSetAttribute(subpanel_kernel<2, false>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        cudaFuncSetAttribute(subpanel_kernel<4, false>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        cudaFuncSetAttribute(subpanel_kernel<1, true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        cudaFuncSetAttribute(subpanel_kernel<2, true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        cudaFuncSetAttribute(subpanel_kernel<4, true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         cudaFuncSetAttribute(trsm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024 + 1024);
         cudaFuncSetAttribute(panel_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024 + 1024);
         cudaFuncSetAttribute(trsv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTrsvSmem);
