@@ -238,3 +238,7 @@ int launch_scale(int m, int n, float beta, float *C, int ldc, cudaStream_t st) {
 }
 
 }  // namespace bf16x
+
+// testing hook (not in the public header): lazy stage waits in the MMA issuer (1, default) or
+// all of an interval's stages waited for before its first MMA (0)
+extern "C" void bf16x_lazy_full(int on) { bf16x::g_lazy_full = on ? 1 : 0; }

@@ -32,7 +32,8 @@ constexpr int kTmemCols = 512;        // two accumulator buffers at column 0 and
 constexpr int kTmemBufStride = 256;
 constexpr int kGroupM = 8;            // tile raster: 8 m-tiles per group for L2 reuse (default)
 constexpr int kDefaultCtaGroup = 2;   // 2-CTA pairs, 64-k promotion interval
-constexpr int kSmemBudget = 224 * 1024;
+constexpr int kSmemBudget = 232448 - 1024;   // 227 KB opt-in maximum (x3: 7 stages of 32 KB)
+inline int g_lazy_full = 1;           // lazy stage waits in the MMA issuer (bf16x_lazy_full hook)
 
 // pieces per operand: x1 1; x3 2; x5 A 2, B 3; x6 / x7 / x8 / x9 3
 __host__ __device__ constexpr int variant_pieces_a(int v) { return v == 1 ? 1 : ((v == 3 || v == 5) ? 2 : 3); }
@@ -105,6 +106,7 @@ struct KParams {
     unsigned int epoch;
     int scaled;            // N2 scaled pieces (R29): scale the accumulator by 2^-8 per bin step
     int group_m;           // tile raster: m-tiles per group
+    int lazy_full;         // issuer waits for each stage just before its first MMA (issue_interval)
     // split-ahead (SP): FP32 operands in, piece workspace out (the layout the tensor maps read),
     // per-slab ready counters (reset by the last CTA to finish)
     const float *Af, *Bf;
@@ -173,17 +175,27 @@ __device__ __forceinline__ void tile_coords(int tile, int tiles_m, int tiles_n, 
 // scaled (R29): the pieces of bin s are scaled by 2^(8s), so the first MMA of each band that
 // adds into an already-started accumulator scales it by 2^-8 (scale-input-d): the accumulator
 // always holds the current band's scale and ends at bin 0's (bin 1's for SA's small one).
+// Lazy stage waits (fullw != nullptr): the interval's stage q is waited for just before its
+// first MMA (in the first band), so the first band starts as soon as stage 0 has landed
+// instead of after all S stages; the MMAs and their order are unchanged.
 template <int CG, int V, int BN, int S, bool SA>
 __device__ __forceinline__ void issue_interval(uint32_t d_big, uint32_t d_small, const uint64_t (&a_desc)[S],
-                                               const uint64_t (&b_desc)[S], int ns, uint32_t idesc, bool scaled) {
+                                               const uint64_t (&b_desc)[S], int ns, uint32_t idesc, bool scaled,
+                                               uint64_t *fullw, const int (&stg)[S], const uint32_t (&phs)[S]) {
     using Cf = Cfg<CG, V, BN>;
     constexpr int H = S * (kBK / kUK);     // K=16 halves per interval (max)
     const int nh = ns * (kBK / kUK);
     bool first_small = true, first_big = true;
     bool band_start = false;   // next MMA is the first of a band
+    uint32_t waited = 0u;
     // descriptor start-address field is in 16-byte units: piece / K-half offsets add directly
     auto mma = [&](int i, int j, int h) {
         const int st = h / (kBK / kUK), kk = h % (kBK / kUK);
+        if (fullw && !((waited >> st) & 1u)) {
+            mbar_wait(&fullw[stg[st]], phs[st]);
+            tc_fence_after();
+            waited |= 1u << st;
+        }
         const uint64_t ad = a_desc[st] + (uint64_t)((i * Cf::A_PIECE + kk * (kUK * 2)) >> 4);
         const uint64_t bd = b_desc[st] + (uint64_t)((j * Cf::B_PIECE + kk * (kUK * 2)) >> 4);
         const bool big = SA && (i + j == 0);
@@ -533,11 +545,13 @@ __global__ void __launch_bounds__((FU || FA) ? kThreadsFused : (SP ? kThreadsSp 
                         mbar_wait(&acc_empty[buf], apar ^ 1u);
                         uint64_t a_desc[S], b_desc[S];
                         int stages[S];
+                        uint32_t phs[S];
 #pragma unroll
                         for (int q = 0; q < S; ++q) {
                             stages[q] = stage;
+                            phs[q] = phase;
                             if (q < ns) {
-                                mbar_wait(&full[stage], phase);
+                                if (!p.lazy_full) mbar_wait(&full[stage], phase);
                                 a_desc[q] = smem_desc_kmajor(smem_u32(sA + stage * Cf::A_STAGE), kSwizzleAtom, 4);
                                 b_desc[q] = smem_desc_kmajor(smem_u32(sB + stage * Cf::B_STAGE), kSwizzleAtom, 4);
                                 if (++stage == NST) { stage = 0; phase ^= 1u; }
@@ -550,7 +564,8 @@ __global__ void __launch_bounds__((FU || FA) ? kThreadsFused : (SP ? kThreadsSp 
                         // buffer layout: SA -> small at buf*BN, big at 256 + buf*BN; else one at buf*256
                         const uint32_t d_big = SA ? tmem_base + kTmemBufStride + buf * BN : tmem_base + buf * kTmemBufStride;
                         const uint32_t d_small = SA ? tmem_base + buf * BN : d_big;
-                        issue_interval<CG, V, BN, S, SA>(d_big, d_small, a_desc, b_desc, ns, idesc, p.scaled != 0);
+                        issue_interval<CG, V, BN, S, SA>(d_big, d_small, a_desc, b_desc, ns, idesc, p.scaled != 0,
+                                                         p.lazy_full ? full : nullptr, stages, phs);
 #pragma unroll
                         for (int q = 0; q < S; ++q)
                             if (q < ns) {
@@ -947,6 +962,7 @@ int launch_t(const GemmPlan &pl, cudaStream_t st) {
     // MB), 8-tall groups for wider outputs (8192^3: 8 beats 1 and 2 by 3-5 %), and groups of 2
     // super-rows on the multicast schedule of the largest outputs (16384^3 x6: 228 vs 215
     // TFLOPS, DRAM reads ~50 vs ~85 GB per launch -- power-limited, so traffic costs clock)
+    kp.lazy_full = g_lazy_full;
     kp.group_m = pl.group_m > 0 ? pl.group_m : (MC == 2 ? 2 : (kp.tiles_n <= 16 ? 1 : kGroupM));
     kp.Af = pl.Af; kp.Bf = pl.Bf; kp.lda = pl.lda; kp.ldb = pl.ldb;
     kp.Apw = const_cast<uint16_t *>(pl.Ap); kp.Bpw = const_cast<uint16_t *>(pl.Bp);
@@ -1017,14 +1033,30 @@ inline int choose_tile_n(int m, int n, int cg, int units, int forced) {
 template <int CG, int V>
 int launch_s(const GemmPlan &pl, cudaStream_t st) {
     int s = pl.stages_per_interval;
-    // 128-k promotion intervals (4 stages) for the one-product variant (tuning hook; r06
-    // tools/spi_probe.py: x1 +13 %, but x3 -14 %: its 6-stage ring then stalls between intervals)
+    // A carried accumulator (k-chunked calls) keeps the interval of the unchunked problem, so
+    // chunks whose widths are multiples of 128 reproduce it bit for bit (distributed.py).
+    const bool carry = (pl.flags & (BF16X_ACC_IN | BF16X_ACC_OUT)) != 0;
+    // 128-k promotion intervals (4 stages): x1 as a tuning hook (r06 tools/spi_probe.py +13 %);
+    // x3 by default since the issuer waits for each stage lazily and the x3 ring has 7 stages
+    // (r06 tools/lazy_probe.py, burst clocks: 4096^3 -3..5 %, 8192^3 -4 % step time; before,
+    // with all 4 stages awaited up front and a 6-stage ring, it was 14 % slower)
+    // (the opt-in fused-A and split-ahead kernels follow, so they stay bit-identical to it)
+    if constexpr (CG == 2 && V == 3)
+        if (s == 0 && (pl.k > 128 || carry) && !pl.fp64 && !pl.split_acc) s = 4;
+    if constexpr (CG == 2 && V == 3)
+        if (s == 4 && !pl.fp64 && !pl.split_acc) {
+            if (pl.fused_a) return launch_t<2, V, 256, 4, 1, false, false, false, false, true>(pl, st);
+            if (pl.split_ahead) return launch_t<2, V, 256, 4, 1, false, false, false, true>(pl, st);
+            if (pl.multicast == 2 || (pl.multicast == 0 && (int64_t)pl.m * pl.n >= 12288LL * 12288LL))
+                return launch_t<2, V, 256, 4, 2>(pl, st);
+            return launch_t<2, V, 256, 4, 1>(pl, st);
+        }
     if constexpr (CG == 2 && V == 1)
-        if (s == 4 && !pl.fp64 && !pl.split_ahead && !pl.split_acc) return launch_t<2, V, 256, 4, 1>(pl, st);
+        if (s == 4 && !pl.fp64 && !pl.split_ahead && !pl.split_acc && !pl.fused_a) return launch_t<2, V, 256, 4, 1>(pl, st);
     // Short k (<= 128): the whole product is one or two intervals, so the tensor core's
     // truncating accumulation dominates the error; 32-k intervals halve it (measured wide
     // exponents, k = 64: max ratio to the oracle 2.07 -> 1.66) at no cost that matters.
-    if (s != 1 && s != 2) s = (CG == 2 && pl.k > 128) ? 2 : 1;
+    if (s != 1 && s != 2) s = (CG == 2 && (pl.k > 128 || carry)) ? 2 : 1;
     if (s == 2 && Cfg<CG, V, 256>::STAGES < 4) s = 1;
     // "d" variants (R30): 2-CTA pairs, tile N 128, split accumulators, FP64 collection, 64-k
     // intervals (one instance per variant)

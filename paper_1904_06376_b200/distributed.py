@@ -9,7 +9,7 @@ are independent, so the only exchanges are
     A[:, Kc] (contiguous in column-major storage) so the first sub-block's GEMM can start on
     chunk c while chunk c+1 is in flight; the FP32 promoted accumulator is carried between
     chunks (bf16x_gemm_ex ACC_IN/ACC_OUT), which makes the chunked result bit-identical to a
-    one-pass GEMM when chunk widths are multiples of the 64-wide promotion interval;
+    one-pass GEMM when chunk widths are multiples of the promotion interval (64, or 128 for x3);
   * one all-gather per sub-round of C's column blocks.  Ownership is block-cyclic: with P
     ranks and S sub-blocks of width w = n / (P*S), rank q owns blocks s*P + q, so sub-round s
     covers the contiguous column range [s*P*w, (s+1)*P*w) of C and the all-gather of C^T
@@ -74,7 +74,7 @@ def gemm_colsharded(A: torch.Tensor, B_local: torch.Tensor, C: torch.Tensor, var
     # --- A broadcast in contiguous k-chunks; sub-block 0 consumes chunks as they land ---
     kc_edges = [(k * c) // max(1, k_chunks) for c in range(max(1, k_chunks) + 1)]
     if k_chunks > 1:
-        kc_edges = [min(k, (e + 63) // 64 * 64) for e in kc_edges]   # promotion-interval aligned
+        kc_edges = [min(k, (e + 127) // 128 * 128) for e in kc_edges]   # promotion-interval aligned
         kc_edges[0] = 0
     chunk_events = []
     for c in range(len(kc_edges) - 1):
