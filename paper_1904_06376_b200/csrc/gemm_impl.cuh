@@ -175,10 +175,12 @@ __device__ __forceinline__ void tile_coords(int tile, int tiles_m, int tiles_n, 
 // scaled (R29): the pieces of bin s are scaled by 2^(8s), so the first MMA of each band that
 // adds into an already-started accumulator scales it by 2^-8 (scale-input-d): the accumulator
 // always holds the current band's scale and ends at bin 0's (bin 1's for SA's small one).
-// Lazy stage waits (fullw != nullptr): the interval's stage q is waited for just before its
-// first MMA (in the first band), so the first band starts as soon as stage 0 has landed
-// instead of after all S stages; the MMAs and their order are unchanged.
-template <int CG, int V, int BN, int S, bool SA>
+// Lazy stage waits (LZ and fullw != nullptr): the interval's stage q is waited for just before
+// its first MMA (in the first band), so the first band starts as soon as stage 0 has landed
+// instead of after all S stages; the MMAs and their order are unchanged.  Compiled in only
+// where it measured faster (x3, 128-k intervals): the runtime check in every other kernel's
+// issuer cost x6 10 % at 4096^3 (r07, profiles/r07/old_vs_head.txt).
+template <int CG, int V, int BN, int S, bool SA, bool LZ>
 __device__ __forceinline__ void issue_interval(uint32_t d_big, uint32_t d_small, const uint64_t (&a_desc)[S],
                                                const uint64_t (&b_desc)[S], int ns, uint32_t idesc, bool scaled,
                                                uint64_t *fullw, const int (&stg)[S], const uint32_t (&phs)[S]) {
@@ -191,7 +193,7 @@ __device__ __forceinline__ void issue_interval(uint32_t d_big, uint32_t d_small,
     // descriptor start-address field is in 16-byte units: piece / K-half offsets add directly
     auto mma = [&](int i, int j, int h) {
         const int st = h / (kBK / kUK), kk = h % (kBK / kUK);
-        if (fullw && !((waited >> st) & 1u)) {
+        if (LZ && fullw && !((waited >> st) & 1u)) {
             mbar_wait(&fullw[stg[st]], phs[st]);
             tc_fence_after();
             waited |= 1u << st;
@@ -546,12 +548,14 @@ __global__ void __launch_bounds__((FU || FA) ? kThreadsFused : (SP ? kThreadsSp 
                         uint64_t a_desc[S], b_desc[S];
                         int stages[S];
                         uint32_t phs[S];
+                        constexpr bool kLazy = (V == 3 && S == 4 && !SA);
+                        const bool lz = kLazy && p.lazy_full;
 #pragma unroll
                         for (int q = 0; q < S; ++q) {
                             stages[q] = stage;
                             phs[q] = phase;
                             if (q < ns) {
-                                if (!p.lazy_full) mbar_wait(&full[stage], phase);
+                                if (!lz) mbar_wait(&full[stage], phase);
                                 a_desc[q] = smem_desc_kmajor(smem_u32(sA + stage * Cf::A_STAGE), kSwizzleAtom, 4);
                                 b_desc[q] = smem_desc_kmajor(smem_u32(sB + stage * Cf::B_STAGE), kSwizzleAtom, 4);
                                 if (++stage == NST) { stage = 0; phase ^= 1u; }
@@ -564,8 +568,8 @@ __global__ void __launch_bounds__((FU || FA) ? kThreadsFused : (SP ? kThreadsSp 
                         // buffer layout: SA -> small at buf*BN, big at 256 + buf*BN; else one at buf*256
                         const uint32_t d_big = SA ? tmem_base + kTmemBufStride + buf * BN : tmem_base + buf * kTmemBufStride;
                         const uint32_t d_small = SA ? tmem_base + buf * BN : d_big;
-                        issue_interval<CG, V, BN, S, SA>(d_big, d_small, a_desc, b_desc, ns, idesc, p.scaled != 0,
-                                                         p.lazy_full ? full : nullptr, stages, phs);
+                        issue_interval<CG, V, BN, S, SA, kLazy>(d_big, d_small, a_desc, b_desc, ns, idesc, p.scaled != 0,
+                                                                lz ? full : nullptr, stages, phs);
 #pragma unroll
                         for (int q = 0; q < S; ++q)
                             if (q < ns) {
@@ -1036,13 +1040,11 @@ int launch_s(const GemmPlan &pl, cudaStream_t st) {
     // A carried accumulator (k-chunked calls) keeps the interval of the unchunked problem, so
     // chunks whose widths are multiples of 128 reproduce it bit for bit (distributed.py).
     const bool carry = (pl.flags & (BF16X_ACC_IN | BF16X_ACC_OUT)) != 0;
-    // 128-k promotion intervals (4 stages): x1 as a tuning hook (r06 tools/spi_probe.py +13 %);
-    // x3 by default since the issuer waits for each stage lazily and the x3 ring has 7 stages
-    // (r06 tools/lazy_probe.py, burst clocks: 4096^3 -3..5 %, 8192^3 -4 % step time; before,
-    // with all 4 stages awaited up front and a 6-stage ring, it was 14 % slower)
-    // (the opt-in fused-A and split-ahead kernels follow, so they stay bit-identical to it)
-    if constexpr (CG == 2 && V == 3)
-        if (s == 0 && (pl.k > 128 || carry) && !pl.fp64 && !pl.split_acc) s = 4;
+    // 128-k promotion intervals (4 stages) as a tuning hook: x1 (r06 tools/spi_probe.py +13 %)
+    // and x3 (issuer with lazy stage waits, 7-stage ring).  x3 keeps 64-k intervals by default:
+    // r07 tools/lazy_probe.py, burst clocks, 64-k vs 128-k step time 353.6 vs 386.6 us at
+    // 4096^3 and 2.60 vs 2.82 ms at 8192^3 (profiles/r07/old_vs_fix.txt).  The opt-in fused-A
+    // and split-ahead x3 kernels follow the hook, so they stay bit-identical to the pre-pass path.
     if constexpr (CG == 2 && V == 3)
         if (s == 4 && !pl.fp64 && !pl.split_acc) {
             if (pl.fused_a) return launch_t<2, V, 256, 4, 1, false, false, false, false, true>(pl, st);

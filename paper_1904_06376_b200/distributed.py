@@ -9,7 +9,8 @@ are independent, so the only exchanges are
     A[:, Kc] (contiguous in column-major storage) so the first sub-block's GEMM can start on
     chunk c while chunk c+1 is in flight; the FP32 promoted accumulator is carried between
     chunks (bf16x_gemm_ex ACC_IN/ACC_OUT), which makes the chunked result bit-identical to a
-    one-pass GEMM when chunk widths are multiples of the promotion interval (64, or 128 for x3);
+    one-pass GEMM when chunk widths are multiples of the promotion interval (64 k by default, 128 k
+    for the x1/x3 128-k tuning hook; chunk edges are aligned to 128);
   * one all-gather per sub-round of C's column blocks.  Ownership is block-cyclic: with P
     ranks and S sub-blocks of width w = n / (P*S), rank q owns blocks s*P + q, so sub-round s
     covers the contiguous column range [s*P*w, (s+1)*P*w) of C and the all-gather of C^T

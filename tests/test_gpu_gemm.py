@@ -484,3 +484,27 @@ def test_fused_a_nonfinite_and_ld(orc, fused_a_on):
         Cd = torch.from_numpy(np.asfortranarray(C0)).cuda()
         res.append(bx.gemm(Ad, Bd, C=Cd, alpha=0.5, beta=2.0, variant=6).cpu().numpy())
     assert np.array_equal(res[0].view(np.uint32), res[1].view(np.uint32))
+
+
+@pytest.mark.parametrize("mc", [1, 2])
+@pytest.mark.parametrize("variant", [1, 3])
+@pytest.mark.parametrize("dist", ["uniform", "wide"])
+def test_128k_interval_hook(orc, dist, variant, mc):
+    """The 128-k promotion-interval hook (bf16x_tune spi = 4; x3's issuer waits for each stage
+    lazily): within 2x of the oracle on a ragged shape spanning several tiles and intervals,
+    and bit-identical with the lazy waits on and off (the MMAs and their order are the same)."""
+    A = synthetic.by_name(dist, 333, 1000, seed=41)
+    B = synthetic.by_name(dist, 1000, 517, seed=42)
+    bx.lib().bf16x_tune(0, 0, 4)
+    bx.lib().bf16x_multicast(mc)
+    try:
+        eg, _ = _check_ratio(orc, A, B, variant, 2)
+        outs = []
+        for lazy in (0, 1):
+            bx.lib().bf16x_lazy_full(lazy)
+            outs.append(_gpu(A, B, variant=variant, cg=2))
+    finally:
+        bx.lib().bf16x_lazy_full(1)
+        bx.lib().bf16x_multicast(0)
+        bx.lib().bf16x_tune(0, 0, 0)
+    assert np.array_equal(outs[0].view(np.uint32), outs[1].view(np.uint32))
