@@ -600,6 +600,17 @@ __global__ void __launch_bounds__((FU || FA) ? kThreadsFused : (SP ? kThreadsSp 
             tm = tm * MC + (int)pair;
             const int row = tm * Cf::TILE_M + (int)rank * kBM + quad * 32 + lane;
             const int col0 = tn * BN + half * EC;
+            // beta != 0: the old C values this thread will read (its row, its EC columns; one
+            // 128-byte line per warp and column) are prefetched into L2 when the tile starts,
+            // so all of them are in flight at once instead of one batch of 8 loads at a time
+            // (r07 tools/shortk_probe.py: the LU's k = 256 trailing updates ran at 1.2-1.6 TB/s
+            // of C traffic with beta = 1, 2.3x the beta = 0 time)
+            if (p.beta != 0.f && !(p.flags & BF16X_ACC_OUT) && w.role != 2 && row < p.m) {
+                const float *pc = p.C + row;
+#pragma unroll 8
+                for (int j = 0; j < EC; ++j)
+                    if (col0 + j < p.n) asm volatile("prefetch.global.L2 [%0];" ::"l"(pc + (int64_t)(col0 + j) * p.ldc));
+            }
             float G[NG * EC];
             if ((p.flags & BF16X_ACC_IN) && w.i0 == 0) {   // (never with GD)
 #pragma unroll
