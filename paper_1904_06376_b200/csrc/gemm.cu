@@ -242,3 +242,6 @@ int launch_scale(int m, int n, float beta, float *C, int ldc, cudaStream_t st) {
 // testing hook (not in the public header): lazy stage waits in the MMA issuer (1, default) or
 // all of an interval's stages waited for before its first MMA (0)
 extern "C" void bf16x_lazy_full(int on) { bf16x::g_lazy_full = on ? 1 : 0; }
+// testing hook (not in the public header): red.global.add epilogue for C += +-Z (alpha = +-1,
+// beta = 1): -1 where the caller asks for it (the LU's trailing update), 0 never, 1 always
+extern "C" void bf16x_red_add(int mode) { bf16x::g_red_add = mode; }

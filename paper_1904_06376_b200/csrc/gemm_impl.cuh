@@ -34,6 +34,11 @@ constexpr int kGroupM = 8;            // tile raster: 8 m-tiles per group for L2
 constexpr int kDefaultCtaGroup = 2;   // 2-CTA pairs, 64-k promotion interval
 constexpr int kSmemBudget = 232448 - 1024;   // 227 KB opt-in maximum (x3: 7 stages of 32 KB)
 inline int g_lazy_full = 1;           // lazy stage waits in the MMA issuer (bf16x_lazy_full hook)
+// Internal flag (not in the public header): C += alpha * Z with alpha = +-1, beta = 1 written as
+// red.global.add.f32 -- RN(C + (+-Z)) is exactly fmaf(+-1, Z, C) -- so the epilogue never waits
+// for the old C (the LU's trailing update, csrc/lu.cu).  g_red_add: -1 as requested (default),
+// 0 never, 1 for every eligible call (bf16x_red_add hook, tests).
+inline int g_red_add = -1;            // kFlagRedAdd (kernels.cuh) override: bf16x_red_add hook
 
 // pieces per operand: x1 1; x3 2; x5 A 2, B 3; x6 / x7 / x8 / x9 3
 __host__ __device__ constexpr int variant_pieces_a(int v) { return v == 1 ? 1 : ((v == 3 || v == 5) ? 2 : 3); }
@@ -605,7 +610,11 @@ __global__ void __launch_bounds__((FU || FA) ? kThreadsFused : (SP ? kThreadsSp 
             // so all of them are in flight at once instead of one batch of 8 loads at a time
             // (r07 tools/shortk_probe.py: the LU's k = 256 trailing updates ran at 1.2-1.6 TB/s
             // of C traffic with beta = 1, 2.3x the beta = 0 time)
-            if (p.beta != 0.f && !(p.flags & BF16X_ACC_OUT) && w.role != 2 && row < p.m) {
+            // (compiled into the default 2-CTA, N = 256 kernels only: the others, tuner options,
+            // keep the fmaf epilogue, which gives the same bits, and their register allocation)
+            const bool red_add = (CG == 2 && BN == 256 && !GD) && (p.flags & kFlagRedAdd) && p.beta == 1.f &&
+                                 (p.alpha == 1.f || p.alpha == -1.f);
+            if (p.beta != 0.f && !red_add && !(p.flags & BF16X_ACC_OUT) && w.role != 2 && row < p.m) {
                 const float *pc = p.C + row;
 #pragma unroll 8
                 for (int j = 0; j < EC; ++j)
@@ -704,6 +713,13 @@ __global__ void __launch_bounds__((FU || FA) ? kThreadsFused : (SP ? kThreadsSp 
 #pragma unroll
                     for (int j = 0; j < EC; ++j)
                         if (col0 + j < p.n) __stcs(crow + (int64_t)(col0 + j) * p.ldc, fmaf(p.alpha, zval(j), 0.f));
+                } else if (CG == 2 && BN == 256 && !GD && red_add) {
+                    // alpha * Z is exact (alpha = +-1): the L2 adds it to C with one RN rounding
+#pragma unroll
+                    for (int j = 0; j < EC; ++j)
+                        if (col0 + j < p.n)
+                            asm volatile("red.global.add.f32 [%0], %1;" ::"l"(crow + (int64_t)(col0 + j) * p.ldc),
+                                         "f"(p.alpha * zval(j)) : "memory");
                 } else {
                     // beta != 0: batch 8 independent loads of C before the FMAs and stores, so
                     // the old values stream in parallel instead of one round trip per column
@@ -929,7 +945,8 @@ int launch_t(const GemmPlan &pl, cudaStream_t st) {
     KParams kp;
     kp.m = pl.m; kp.n = pl.n; kp.k = pl.k;
     kp.alpha = pl.alpha; kp.beta = pl.beta;
-    kp.C = pl.C; kp.ldc = pl.ldc; kp.flags = pl.flags; kp.acc = pl.acc;
+    kp.C = pl.C; kp.ldc = pl.ldc; kp.acc = pl.acc;
+    kp.flags = g_red_add == 0 ? (pl.flags & ~kFlagRedAdd) : (g_red_add == 1 ? (pl.flags | kFlagRedAdd) : pl.flags);
     kp.tiles_m = ((pl.m + Cf::TILE_M - 1) / Cf::TILE_M + MC - 1) / MC;   // rows of (MC-tall) super-tiles
     kp.tiles_n = (pl.n + BN - 1) / BN;
     kp.nkb = (pl.k + kBK - 1) / kBK;

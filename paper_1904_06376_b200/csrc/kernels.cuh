@@ -5,6 +5,10 @@
 
 namespace bf16x {
 
+// internal gemm_core flag (not in the public header): red.global.add epilogue for C += +-Z
+// (alpha = +-1, beta = 1), see gemm_impl.cuh
+constexpr unsigned kFlagRedAdd = 1u << 30;
+
 int launch_split(int64_t rows, int64_t cols, const float *X, int64_t ldx, uint16_t *P0, uint16_t *P1,
                  uint16_t *P2, int64_t ldp, bool transpose, cudaStream_t st, bool scaled = false);
 

@@ -1195,7 +1195,7 @@ static int lu_factor(LuWork &w, int variant, cudaStream_t st) {
             if (rc) break;
             // A22 <- -L21 U12 + A22 : the cubic work, in the split GEMM
             rc = gemm_core(rest, rest, jb, -1.0f, w.LU + (int64_t)j0 * ld + j1, ld, w.LU + (int64_t)j1 * ld + j0, ld,
-                           1.0f, w.LU + (int64_t)j1 * ld + j1, ld, variant, 0u, nullptr, 0, 0, nullptr, 0, 0, nullptr,
+                           1.0f, w.LU + (int64_t)j1 * ld + j1, ld, variant, kFlagRedAdd, nullptr, 0, 0, nullptr, 0, 0, nullptr,
                            nullptr, 0, st, 0);
         }
     }

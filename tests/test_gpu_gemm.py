@@ -508,3 +508,38 @@ def test_128k_interval_hook(orc, dist, variant, mc):
         bx.lib().bf16x_multicast(0)
         bx.lib().bf16x_tune(0, 0, 0)
     assert np.array_equal(outs[0].view(np.uint32), outs[1].view(np.uint32))
+
+
+@pytest.mark.parametrize("alpha", [1.0, -1.0])
+@pytest.mark.parametrize("variant", [3, 6])
+@pytest.mark.parametrize("shape", [(333, 517, 256), (1100, 900, 96), (2304, 2304, 256)])
+def test_red_add_epilogue_bit_identical(shape, variant, alpha):
+    """C += +-Z through red.global.add.f32 (the LU's trailing update) is bit-identical to the
+    fmaf(alpha, Z, beta * C) epilogue for alpha = +-1, beta = 1 -- including subnormal C values,
+    results that cancel to zero or land in the subnormal range, and stream-K tiles (2304^2 has
+    a partial last wave)."""
+    m, n, k = shape
+    A = synthetic.uniform(m, k, seed=m + 13 * k)
+    B = synthetic.uniform(k, n, seed=n + 17 * k)
+    C = synthetic.uniform(m, n, seed=7)
+    C[::7, ::5] = np.float32(3e-39) * np.sign(C[::7, ::5])           # subnormal old C
+    C[1::11, :] = np.float32(1e-30)
+    outs = []
+    for mode in (0, 1):
+        bx.lib().bf16x_red_add(mode)
+        try:
+            outs.append(_gpu(A, B, C, alpha=alpha, beta=1.0, variant=variant))
+        finally:
+            bx.lib().bf16x_red_add(-1)
+    # exact cancellation: C = -(+-Z) read back from the fmaf path, then C + (+-Z) must be +0 / the
+    # same bits in both modes
+    C2 = (-outs[0] + C).astype(np.float32)
+    outs2 = []
+    for mode in (0, 1):
+        bx.lib().bf16x_red_add(mode)
+        try:
+            outs2.append(_gpu(A, B, C2, alpha=alpha, beta=1.0, variant=variant))
+        finally:
+            bx.lib().bf16x_red_add(-1)
+    assert np.array_equal(outs[0].view(np.uint32), outs[1].view(np.uint32))
+    assert np.array_equal(outs2[0].view(np.uint32), outs2[1].view(np.uint32))

@@ -19,10 +19,12 @@ f = []
 hms = []
 import ctypes
 bx.lib().bf16x_lu_host_ms.restype = ctypes.c_double
+if os.environ.get("BF16X_RED_ADD"):   # trailing-update epilogue: 0 fmaf (load C), -1 red.add (default)
+    bx.lib().bf16x_red_add(int(os.environ["BF16X_RED_ADD"]))
 for _ in range(reps):
     x, rep, hist = bx.gesv_ir(A, b, variant=v)
     f.append(rep.factor_ms)
     hms.append(bx.lib().bf16x_lu_host_ms())
 print(f"host enqueue ms: {[round(t, 2) for t in hms]}", flush=True)
 f.sort()
-print(f"n={n} x{v}: factor_ms min {f[0]:.2f} median {f[len(f) // 2]:.2f} (all {[round(t, 2) for t in f]})", flush=True)
+print(f"n={n} x{v} red_add={os.environ.get('BF16X_RED_ADD', '-1')}: factor_ms min {f[0]:.2f} median {f[len(f) // 2]:.2f} (all {[round(t, 2) for t in f]})", flush=True)

@@ -37,8 +37,12 @@ for j in (256, 2048, 4096, 6144, 7680):
     res = {}
     for beta in (1.0, 0.0):
         res[beta] = tm(lambda: bx.gemm_raw(mn, mn, KB, -1.0 if beta else 1.0, a, ld, b, ld, beta, c, ld, variant=3))
+    L = bx.lib()
+    L.bf16x_red_add(1)
+    t_red = tm(lambda: bx.gemm_raw(mn, mn, KB, -1.0, a, ld, b, ld, 1.0, c, ld, variant=3))
+    L.bf16x_red_add(-1)
     view = M[j:, j:]
     t_copy = tm(lambda: view.mul_(1.0))
     mnk = 2 * mn * mn * KB
-    print(f"j={j} mn={mn}: beta=1 {res[1.0]:.1f} us  beta=0 {res[0.0]:.1f} us  C rd+wr (torch) {t_copy:.1f} us  "
+    print(f"j={j} mn={mn}: beta=1 {res[1.0]:.1f} us  beta=1 red.add {t_red:.1f} us  beta=0 {res[0.0]:.1f} us  C rd+wr (torch) {t_copy:.1f} us  "
           f"C bytes/beta1 time {8 * mn * mn / res[1.0] / 1e3:.0f} GB/s  MMA {3 * mnk / res[1.0] / 1e6:.0f} TF/s", flush=True)
