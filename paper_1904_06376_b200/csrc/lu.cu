@@ -488,6 +488,21 @@ __global__ void __launch_bounds__(256) panel_update_kernel(float *LU, int ld, in
         if (r < nr && t < w) async_copy_f32(sL21 + t * kUpdRows + r, LU + (int64_t)(s0 + t) * ld + rb + r);
         else sL21[t * kUpdRows + r] = 0.f;
     }
+    // this thread's first 4 x 4 block of the update target, loaded now so its latency overlaps
+    // the staging copies and the forward substitution (rows rb.. are disjoint from the U rows
+    // s0..s0+w that block 0 writes below)
+    const int ty = tid >> 4, tx = tid & 15;
+    float old[4][4];
+    auto load_old = [&](int cq) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int r = 4 * ty + i;
+                old[j][i] = (cq + j < nc && r < nr) ? LU[(int64_t)(c1 + cq + j) * ld + rb + r] : 0.f;
+            }
+    };
+    load_old(4 * tx);
     async_wait_all();
     __syncthreads();
     for (int c = tid; c < nc; c += blockDim.x) {      // forward substitution, column in registers
@@ -507,16 +522,8 @@ __global__ void __launch_bounds__(256) panel_update_kernel(float *LU, int ld, in
     }
     __syncthreads();
     // A[rb + 4ty + i, c1 + cq + j] -= sum_t L21[., t] U[t, .]
-    const int ty = tid >> 4, tx = tid & 15;
     for (int cq = 4 * tx; cq < nc; cq += 64) {
-        float old[4][4];
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                const int r = 4 * ty + i;
-                old[j][i] = (cq + j < nc && r < nr) ? LU[(int64_t)(c1 + cq + j) * ld + rb + r] : 0.f;
-            }
+        if (cq != 4 * tx) load_old(cq);
         float acc[4][4] = {};
 #pragma unroll 8
         for (int t = 0; t < kSubW; ++t) {
