@@ -212,12 +212,15 @@ static void split_matrix_widened(int rows, int cols, const float *X, int ldx, fl
 }
 
 /* ------------------------------------------------------------------------ */
-/* O-3  one partial inner-product column.  P:247-255 (§II-D):
+/* O-3  one partial inner-product column.  P:247-255 (§II-D), P:253 literally:
  *    Z^(i,j) <- 0;  for l = 1..n:  Z^(i,j) <- FMA(x_l^(i), y_l^(j), Z^(i,j))
- * The BF16 x BF16 product is exact in FP32 (<= 16 significant bits), so the
- * FMA equals one product followed by one FP32 round-to-nearest add (R10).
- * For every output row r the sum runs over l strictly in increasing order;
- * the loop over r is only a vectorisable sweep across independent outputs.
+ * one fused multiply-add (one rounding) per term (R10).  A BF16 x BF16 product
+ * has <= 16 significant bits, so the FMA equals a multiply followed by an add
+ * wherever the product is a normal FP32 number; where it is subnormal in FP32
+ * (|product| < 2^-126) the separate multiply would round it first, so the FMA
+ * is spelled out.  For every output row r the sum runs over l strictly in
+ * increasing order; the loop over r is only a vectorisable sweep across
+ * independent outputs.
  *   Ai: m x k piece plane (ld m), bj: column c of a k x n piece plane.
  * ------------------------------------------------------------------------ */
 static void partial_column(int m, int k, const float *Ai, const float *bj, float *Z)
@@ -226,10 +229,7 @@ static void partial_column(int m, int k, const float *Ai, const float *bj, float
     for (int l = 0; l < k; ++l) {
         const float y = bj[l];
         const float *a = Ai + (int64_t)l * m;
-        for (int r = 0; r < m; ++r) {
-            float prod = a[r] * y;          /* exact */
-            Z[r] = Z[r] + prod;             /* one rounding */
-        }
+        for (int r = 0; r < m; ++r) Z[r] = fmaf(a[r], y, Z[r]);   /* one rounding */
     }
 }
 
@@ -406,13 +406,22 @@ int orc_gemm_split_ex_cols(int m, int n, int k, float alpha, const float *A, int
         }
         return 0;
     }
+    /* A is split whole (every output column needs every row); of B only the requested
+     * columns are gathered (k x ncols, ld k) and split, so a column-sampled call costs the
+     * sample, not the whole of B */
     float *Ap[3], *Bp[3];
+    float *Bsel = (float *)malloc(sizeof(float) * (size_t)k * (size_t)ncols);
     for (int p = 0; p < 3; ++p) {
         Ap[p] = (float *)malloc(sizeof(float) * (size_t)m * (size_t)k);
-        Bp[p] = (float *)malloc(sizeof(float) * (size_t)k * (size_t)n);
+        Bp[p] = (float *)malloc(sizeof(float) * (size_t)k * (size_t)ncols);
+    }
+    for (t = 0; t < ncols; ++t) {
+        const int c = cols ? cols[t] : (int)t;
+        memcpy(Bsel + (size_t)t * k, B + (int64_t)c * ldb, sizeof(float) * (size_t)k);
     }
     split_matrix_widened_opt(m, k, A, lda, Ap, scaled);
-    split_matrix_widened_opt(k, n, B, ldb, Bp, scaled);
+    split_matrix_widened_opt(k, ncols, Bsel, k, Bp, scaled);
+    free(Bsel);
 #pragma omp parallel
     {
         float *Zcol[3][3];
@@ -425,7 +434,7 @@ int orc_gemm_split_ex_cols(int m, int n, int k, float alpha, const float *A, int
             for (int i = 0; i < 3; ++i)
                 for (int j = 0; j < 3; ++j) {
                     if (product_needed(variant, i, j))
-                        partial_column(m, k, Ap[i], Bp[j] + (int64_t)c * k, Zcol[i][j]);
+                        partial_column(m, k, Ap[i], Bp[j] + (int64_t)t * k, Zcol[i][j]);
                     else
                         for (int r = 0; r < m; ++r) Zcol[i][j][r] = 0.0f;
                 }

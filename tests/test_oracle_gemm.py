@@ -93,6 +93,49 @@ def test_variant_product_sets_by_value(orc):
     assert float(orc.gemm(A, B2, variant=6)[0, 0]) == 2 ** -8 + 2 * 2 ** -18
 
 
+def test_x9_product_set_and_order_by_value(orc):
+    """x9 = Z0 + (Z1 + (Z2 + (Z3 + Z4))) ("bins should be added from smallest to
+    largest"; reading R9), pinned by value: Z^(2,2) must be present and the bins must be
+    added smallest first.  u = 1 + 2^-8 + 2^-17 splits into (1 + 2^-7, -2^-8, 2^-17); with
+    k = 6, A = (u, -u0, u, u0, 1, 2^-23), B = (u, u, -u0, u0, 1, 1) every Z^(0,j) and Z^(i,0)
+    cancels exactly except Z00 = 1 + 2^-23 (each FP32 step exact), and Z11 = u1^2 = 2^-16,
+    Z12 = Z21 = u1 u2 = -2^-25, Z22 = u2^2 = 2^-34.  Hence
+      x9 (smallest first): 1 + 2^-23 + (2^-16 - 2^-24 + 2^-34) -> 1 + 2^-16 + 2^-23
+          (the exact sum is 1 + 2^-16 + 2^-24 + 2^-34: above the half-ulp, rounds up);
+      x8 (no Z22): 1 + 2^-16 + 2^-24 is a tie -> even -> 1 + 2^-16;
+      largest first ((((Z0 + Z1) + Z2) + Z3) + Z4): the tie is met before Z22 -> 1 + 2^-16."""
+    u = 1 + 2 ** -8 + 2 ** -17
+    p = [float(orc.widen(q)[0, 0]) for q in orc.split(np.array([[u]], dtype=np.float32))]
+    assert p == [1 + 2 ** -7, -2 ** -8, 2 ** -17]
+    u0 = p[0]
+    A = np.array([[u, -u0, u, u0, 1.0, 2 ** -23]], dtype=np.float32)
+    B = np.array([[u], [u], [-u0], [u0], [1.0], [1.0]], dtype=np.float32)
+    Z = orc.partials(A, B)[:, :, 0, 0].astype(np.float64)
+    want_z = np.zeros((3, 3))
+    want_z[0, 0], want_z[1, 1], want_z[1, 2], want_z[2, 1], want_z[2, 2] = 1 + 2 ** -23, 2 ** -16, -2 ** -25, -2 ** -25, 2 ** -34
+    assert np.array_equal(Z, want_z)
+    assert float(orc.gemm(A, B, variant=9)[0, 0]) == 1 + 2 ** -16 + 2 ** -23
+    assert float(orc.gemm(A, B, variant=8)[0, 0]) == 1 + 2 ** -16
+    f = np.float32
+    largest_first = f(f(f(f(f(Z[0, 0]) + f(0)) + f(Z[1, 1])) + f(f(Z[1, 2]) + f(Z[2, 1]))) + f(Z[2, 2]))
+    assert float(largest_first) == 1 + 2 ** -16          # the order is what the pin detects
+
+
+def test_partial_sums_are_fused_multiply_adds(orc):
+    """Z <- FMA(x_l, y_l, Z), one rounding per term.  A BF16 x BF16 product is exact
+    in FP32 unless it is subnormal; there a multiply-then-add rounds twice.  With
+    A = (2^-125, 2^-74, (1 + 2^-7) 2^-75) and B = (1, 2^-74, 2^-75) (all BF16), Z reaches
+    2^-125 + 2^-148 (odd at its quantum 2^-148) and the third product is (1 + 2^-7) 2^-150:
+    FMA: RN(Z + 0.252 quantum) = Z;  multiply first: RN(p) = 2^-149 = half a quantum, a tie
+    that rounds Z up to 2^-125 + 2^-147."""
+    A = np.array([[2.0 ** -125, 2.0 ** -74, (1 + 2 ** -7) * 2.0 ** -75]], dtype=np.float32)
+    B = np.array([[1.0], [2.0 ** -74], [2.0 ** -75]], dtype=np.float32)
+    for v in (1, 3, 6, 9):
+        assert float(orc.gemm(A, B, variant=v)[0, 0]) == 2.0 ** -125 + 2.0 ** -148, v
+    mul_add = np.float32(np.float32(2.0 ** -125 + 2.0 ** -148) + np.float32(A[0, 2] * B[2, 0]))
+    assert float(mul_add) == 2.0 ** -125 + 2.0 ** -147
+
+
 def test_x5_x7_identity_closed_forms(orc):
     """A*I under x5 (A in two pieces) is fl32(a0 + a1) -- the third piece is dropped -- and
     under x7 it is A exactly; I*B is B exactly under both (B keeps three pieces).  x5 equals
