@@ -13,7 +13,9 @@
  *    done, cuBLAS-style.  Buffers must stay valid until the stream reaches the work.
  *    bf16x_gemm_host and bf16x_gesv_ir are synchronous.
  *  - The caller owns every buffer it passes.  The library owns a cached device
- *    workspace (pieces of A and B), released by bf16x_release().
+ *    workspace PER STREAM (pieces of A and B, stream-K fix-up buffers), released by
+ *    bf16x_release(): calls on different streams never share library memory and may run
+ *    concurrently; calls on one stream are ordered by the stream.
  *  - Return value: BF16X_SUCCESS (0), a positive BF16X_* status, or -i when argument
  *    i (1-based) is invalid (LAPACK xerbla convention).  NaN/Inf inputs are never
  *    rejected; they propagate (reading R4).
@@ -56,10 +58,18 @@ enum {
  *   together in FP64"; R30): bins >= 1 and bin 0 accumulate in separate FP32 tensor-memory
  *   accumulators per 64-k interval and are collected in an FP64 accumulator, rounded once to
  *   FP32 before alpha/beta.  Variants 3, 5, 6, 7, 8, 9; not with BF16X_ACC_IN / _OUT.
- * BF16X_SPLIT_TRANSPOSED (split_ex only): write the pieces transposed, as bf16x_split_t. */
+ * BF16X_SPLIT_TRANSPOSED (split_ex only): write the pieces transposed, as bf16x_split_t.
+ * BF16X_NO_STREAM_K (gemm_ex only): every output tile's k-range runs in one CTA pair, so each
+ *   element's value depends only on its row of A, its column of B, k and the variant -- not
+ *   on m, n or the SM count.  Without it the last waves of tiles may be split in k between two
+ *   CTA pairs (stream-K), whose two FP32 partial sums are then added with one extra
+ *   round-to-nearest: still within the accuracy contract, but a sub-matrix computed alone
+ *   (e.g. one rank's column block, distributed.py) can differ in the last bit from the same
+ *   columns of a larger call. */
 #define BF16X_SCALED_PIECES    4u
 #define BF16X_FP64_COMBINE     8u
 #define BF16X_SPLIT_TRANSPOSED 16u
+#define BF16X_NO_STREAM_K      32u
 
 /* ------------------------------------------------------------------------------------
  * bf16x_split -- the 3-way decomposition of P:180-184 (section II-A):
@@ -134,7 +144,10 @@ size_t bf16x_gemm_workspace_size(int m, int n, int k, int variant);
  *              element (l,j) of piece q at B_pieces[q*b_plane + l + j*ldbp], ldbp >= k,
  *              ldbp % 8 == 0, b_plane % 8 == 0; then B may be NULL.
  *   acc_carry: m x n FP32 (ld = ldc) used by BF16X_ACC_IN / BF16X_ACC_OUT.
- *   flags    : BF16X_ACC_IN | BF16X_ACC_OUT | BF16X_SCALED_PIECES | BF16X_FP64_COMBINE (above).
+ *   flags    : BF16X_ACC_IN | BF16X_ACC_OUT | BF16X_SCALED_PIECES | BF16X_FP64_COMBINE |
+ *              BF16X_NO_STREAM_K (above).
+ *   workspace: NULL (the library's cache for `stream`), or ws_bytes >= bf16x_gemm_workspace_size
+ *              bytes of device memory owned by the caller, not used by other work meanwhile.
  * Errors: as bf16x_gemm, plus -13 flags (unknown bits, FP64_COMBINE with ACC_* or with
  * variant 1), -14 A_pieces layout, -16 B_pieces layout,
  * -19 acc_carry NULL with ACC flags, -21 ws_bytes too small. */
@@ -161,16 +174,20 @@ int bf16x_gemm_host(int m, int n, int k, float alpha, const float *A_host, int l
  * r = A*x - b, and use the results from the lower precision solver to solve the updated
  * system Ay = r ... and then update x with x + y").  Panel factorisation and U12 solves
  * are FP32; residuals and triangular solves are FP64 (the factors widened exactly).
- * Stopping rule (R14): ||r||_inf <= sqrt(n)*||x||_inf*||A||_inf*2^-53 (LAPACK dsgesv);
- * stagnation = residual not halved over 3 iterations.  Synchronous.
+ * Stopping rule: with tol > 0, ||r||_inf <= tol * ||b||_inf -- the paper's "residual
+ * tolerance of cond(A)*eps" is tol = cond(A) * 2^-53; with tol <= 0 the default
+ * (R14) ||r||_inf <= sqrt(n)*||x||_inf*||A||_inf*2^-53 (LAPACK dsgesv).  Stagnation =
+ * residual not halved over 3 iterations.  Synchronous.
  *   n         : order (>= 0);  A: n x n FP32 device, lda >= max(1,n), NOT modified
  *   b, x      : FP64 device vectors of length n (x is output)
  *   variant   : 3, 6 or 9;  nb: panel width (<= 0: 256)
+ *   tol       : relative residual tolerance (above; NaN: error -8)
  *   max_iter  : refinement iterations (<= 0: 30)
  *   residual_history : HOST, nullable, max_iter+1 doubles (||r||_inf per iteration)
  *   report    : HOST, required; always filled.
  * Returns BF16X_SUCCESS, BF16X_ERR_SINGULAR (report->info = 1-based column),
- * BF16X_NOT_CONVERGED (x = last iterate), or an error. */
+ * BF16X_NOT_CONVERGED (x = last iterate), or an error: -1 n, -3 lda, -6 variant, -8 tol,
+ * -11 report NULL. */
 typedef struct {
     int converged;           /* 1 if the stopping test was met */
     int iterations;          /* refinement corrections applied */
@@ -184,7 +201,7 @@ typedef struct {
 } bf16x_ir_report;
 
 int bf16x_gesv_ir(int n, const float *A, int lda, const double *b, double *x, int variant,
-                  int nb, int max_iter, double *residual_history, bf16x_ir_report *report);
+                  int nb, double tol, int max_iter, double *residual_history, bf16x_ir_report *report);
 
 /* ------------------------------------------------------------------------------------
  * bf16x_gesv_gmres_ir -- GMRES-IR (section III: "combining Iterative Refinement with
@@ -196,15 +213,15 @@ int bf16x_gesv_ir(int n, const float *A, int lda, const double *b, double *x, in
  * Arnoldi by classical Gram-Schmidt applied twice, Givens rotations, cycle ends after
  * `restart` steps, on breakdown, or when the rotated residual <= inner_tol * ||M^-1 r||_2
  * (reading R25).  Synchronous.
- *   n, A, lda, b, x, variant, nb, max_iter, residual_history, report: as bf16x_gesv_ir
+ *   n, A, lda, b, x, variant, nb, tol, max_iter, residual_history, report: as bf16x_gesv_ir
  *     (report->iterations = outer corrections, report->inner_iterations = Arnoldi steps)
  *   restart   : Arnoldi steps per correction (<= 0: 200; capped at n and at 8190)
  *   inner_tol : relative tolerance of each GMRES cycle (0: 1e-10; < 0 or NaN: error -9)
  * Device workspace: n*(restart+1) doubles for the Krylov basis on top of bf16x_gesv_ir's.
- * Returns as bf16x_gesv_ir; errors -1 n, -3 lda, -6 variant, -9 inner_tol,
- * -12 report NULL. */
+ * Returns as bf16x_gesv_ir; errors -1 n, -3 lda, -6 variant, -9 inner_tol, -10 tol,
+ * -13 report NULL. */
 int bf16x_gesv_gmres_ir(int n, const float *A, int lda, const double *b, double *x, int variant,
-                        int nb, int restart, double inner_tol, int max_iter,
+                        int nb, int restart, double inner_tol, double tol, int max_iter,
                         double *residual_history, bf16x_ir_report *report);
 
 /* ------------------------------------------------------------------------------------

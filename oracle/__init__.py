@@ -262,13 +262,14 @@ def residual_f64(A, b, x) -> np.ndarray:
     return r
 
 
-def gesv_ir(A, b, variant=3, nb=64, max_iter=30):
+def gesv_ir(A, b, variant=3, nb=64, max_iter=30, tol=0.0):
     """LU + iterative refinement: factor in low precision; loop { r = b - A x
     in FP64; solve A d = r with the factors in FP64; x += d }.
 
-    Stopping rule (reading R14): converged when
-    ||r||_inf <= sqrt(n) * ||x||_inf * ||A||_inf * 2^-53 (LAPACK dsgesv's rule);
-    stagnation = residual not halved over 3 consecutive iterations.
+    Stopping rule (reading R14): with tol > 0 converged when
+    ||r||_inf <= tol * ||b||_inf (P:469 "a residual tolerance of cond(A)*eps": tol =
+    cond(A) * 2^-53); otherwise when ||r||_inf <= sqrt(n) * ||x||_inf * ||A||_inf * 2^-53
+    (LAPACK dsgesv's rule); stagnation = residual not halved over 3 consecutive iterations.
     Returns dict(x, converged, iterations, info, history)."""
     A = _colmajor_f32(A)
     n = A.shape[0]
@@ -276,6 +277,7 @@ def gesv_ir(A, b, variant=3, nb=64, max_iter=30):
     if info != 0:
         return dict(x=np.zeros(n), converged=False, iterations=0, info=info, history=[])
     anrm = float(np.max(np.sum(np.abs(A.astype(np.float64)), axis=1)))
+    bnrm = float(np.max(np.abs(np.asarray(b, dtype=np.float64)))) if n else 0.0
     eps = 2.0 ** -53
     x = lu_solve_f64(LU, ipiv, b)
     hist = []
@@ -285,7 +287,8 @@ def gesv_ir(A, b, variant=3, nb=64, max_iter=30):
         r = residual_f64(A, b, x)
         rn = float(np.max(np.abs(r)))
         hist.append(rn)
-        if rn <= np.sqrt(n) * float(np.max(np.abs(x))) * anrm * eps:
+        thr = tol * bnrm if tol > 0 else np.sqrt(n) * float(np.max(np.abs(x))) * anrm * eps
+        if rn <= thr:
             converged = True
             break
         if it == max_iter:
@@ -370,7 +373,7 @@ def gmres(matvec, psolve, b, x0=None, restart=None, tol=1e-10, max_cycles=1):
     return dict(x=x, iterations=steps, history=hist, converged=converged)
 
 
-def gmres_ir(A, b, variant=3, nb=64, restart=200, inner_tol=1e-10, max_iter=30):
+def gmres_ir(A, b, variant=3, nb=64, restart=200, inner_tol=1e-10, max_iter=30, tol=0.0):
     """GMRES-IR: factor once in low precision (getrf, the split-GEMM trailing updates of
     P:406); outer loop as gesv_ir (r = b - A x in FP64, same stopping and stagnation rules,
     R14), but the correction equation A d = r is solved by one cycle of FP64 GMRES left-
@@ -383,6 +386,7 @@ def gmres_ir(A, b, variant=3, nb=64, restart=200, inner_tol=1e-10, max_iter=30):
     if info != 0:
         return dict(x=np.zeros(n), converged=False, iterations=0, inner_iterations=0, info=info, history=[])
     anrm = float(np.max(np.sum(np.abs(A.astype(np.float64)), axis=1)))
+    bnrm = float(np.max(np.abs(np.asarray(b, dtype=np.float64)))) if n else 0.0
     eps = 2.0 ** -53
     zero = np.zeros(n)
     matvec = lambda v: -residual_f64(A, zero, v)          # A v, FP64 sums of FP32 A
@@ -396,7 +400,8 @@ def gmres_ir(A, b, variant=3, nb=64, restart=200, inner_tol=1e-10, max_iter=30):
         r = residual_f64(A, b, x)
         rn = float(np.max(np.abs(r)))
         hist.append(rn)
-        if rn <= np.sqrt(n) * float(np.max(np.abs(x))) * anrm * eps:
+        thr = tol * bnrm if tol > 0 else np.sqrt(n) * float(np.max(np.abs(x))) * anrm * eps
+        if rn <= thr:
             converged = True
             break
         if it == max_iter:

@@ -19,7 +19,7 @@ HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "bf16x.h")
 
 SUCCESS, ERR_CUDA, ERR_ALLOC, ERR_ARCH, ERR_SINGULAR, NOT_CONVERGED = 0, 1, 2, 3, 4, 5
 ACC_IN, ACC_OUT = 1, 2
-SCALED_PIECES, FP64_COMBINE, SPLIT_TRANSPOSED = 4, 8, 16   # N2 options (bf16x.h; R29, R30)
+SCALED_PIECES, FP64_COMBINE, SPLIT_TRANSPOSED, NO_STREAM_K = 4, 8, 16, 32   # bf16x.h flags (R29, R30)
 VARIANTS = (1, 3, 5, 6, 7, 8, 9)
 PIECES = {1: 1, 3: 2, 6: 3, 8: 3, 9: 3}
 
@@ -59,8 +59,8 @@ def lib() -> ctypes.CDLL:
                                     _vp, _i64, _i64, _vp, _i64, _i64, _vp, _vp, ctypes.c_size_t, _vp]
         L.bf16x_gemm_cg.argtypes = [_i, _i, _i, _f, _vp, _i, _vp, _i, _f, _vp, _i, _i, _i, _vp]
         L.bf16x_gemm_host.argtypes = [_i, _i, _i, _f, _vp, _i, _vp, _i, _f, _vp, _i, _i]
-        L.bf16x_gesv_ir.argtypes = [_i, _vp, _i, _vp, _vp, _i, _i, _i, _vp, ctypes.POINTER(IRReport)]
-        L.bf16x_gesv_gmres_ir.argtypes = [_i, _vp, _i, _vp, _vp, _i, _i, _i, ctypes.c_double, _i, _vp,
+        L.bf16x_gesv_ir.argtypes = [_i, _vp, _i, _vp, _vp, _i, _i, _d, _i, _vp, ctypes.POINTER(IRReport)]
+        L.bf16x_gesv_gmres_ir.argtypes = [_i, _vp, _i, _vp, _vp, _i, _i, _i, _d, _d, _i, _vp,
                                           ctypes.POINTER(IRReport)]
         L.bf16x_getrf.argtypes = [_i, _vp, _i, _vp, _i, _i, ctypes.POINTER(ctypes.c_int)]
         L.bf16x_gesv16_batched.argtypes = [_i, _i, _vp, _i, _i64, _vp, _i64, _vp, _i64, _i, _i, _i, _vp, _vp, _vp,
@@ -192,10 +192,11 @@ def gemm_raw(m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, variant=6, flags=0, A
 
 
 def gemm(A, B, C=None, alpha: float = 1.0, beta: float = 0.0, variant: int = 6, stream=None, cta_group: int = 0,
-         scaled: bool = False, fp64_combine: bool = False):
+         scaled: bool = False, fp64_combine: bool = False, no_stream_k: bool = False):
     """C = alpha * A @ B + beta * C for FP32 CUDA tensors, computed with the bf16x`variant`
     split GEMM.  Column-major (Fortran) and row-major inputs are both used in place.
-    scaled: N2 power-of-two scaled pieces (R29); fp64_combine: the paper's "d" variants (R30)."""
+    scaled: N2 power-of-two scaled pieces (R29); fp64_combine: the paper's "d" variants (R30);
+    no_stream_k: BF16X_NO_STREAM_K (each element independent of the problem's shape)."""
     import torch
     if variant not in VARIANTS:
         raise ValueError(f"variant must be one of {VARIANTS}")
@@ -223,7 +224,7 @@ def gemm(A, B, C=None, alpha: float = 1.0, beta: float = 0.0, variant: int = 6, 
             raise ValueError("A, B, C must share one layout (all row-major or all column-major)")
         # row-major C = A B  <=>  column-major C^T = B^T A^T
         args = (n, m, k, alpha, b[0], b[3], a[0], a[3], beta, c[0], c[3], variant)
-    flags = (SCALED_PIECES if scaled else 0) | (FP64_COMBINE if fp64_combine else 0)
+    flags = (SCALED_PIECES if scaled else 0) | (FP64_COMBINE if fp64_combine else 0) | (NO_STREAM_K if no_stream_k else 0)
     if cta_group and not flags:
         _check(lib().bf16x_gemm_cg(*args, cta_group, st), "bf16x_gemm_cg")
     else:
@@ -259,9 +260,11 @@ def workspace_size(m, n, k, variant) -> int:
 # ------------------------------------------------------------------------------------
 # LU + iterative refinement
 # ------------------------------------------------------------------------------------
-def gesv_ir(A, b, variant: int = 3, nb: int = 256, max_iter: int = 30):
+def gesv_ir(A, b, variant: int = 3, nb: int = 256, max_iter: int = 30, tol: float = 0.0):
     """Solve A x = b (A: n x n float32 CUDA, column-major or row-major -- row-major is
-    transposed on the device first; b: float64 CUDA vector).  Returns (x, report, history)."""
+    transposed on the device first; b: float64 CUDA vector).  tol > 0: stop when
+    ||r||_inf <= tol ||b||_inf (the paper's cond(A)*eps); 0: the R14 default.
+    Returns (x, report, history)."""
     import torch
     n = A.shape[0]
     cm = _colmajor(A)
@@ -272,7 +275,7 @@ def gesv_ir(A, b, variant: int = 3, nb: int = 256, max_iter: int = 30):
     b = b.to(torch.float64).contiguous()
     hist = np.zeros(max(1, max_iter) + 1, dtype=np.float64)
     rep = IRReport()
-    rc = lib().bf16x_gesv_ir(n, cm[0], cm[3], _ptr(b), _ptr(x), variant, nb, max_iter, hist.ctypes.data,
+    rc = lib().bf16x_gesv_ir(n, cm[0], cm[3], _ptr(b), _ptr(x), variant, nb, float(tol), max_iter, hist.ctypes.data,
                              ctypes.byref(rep))
     if rc not in (SUCCESS, NOT_CONVERGED, ERR_SINGULAR):
         _check(rc, "bf16x_gesv_ir")
@@ -288,7 +291,7 @@ def _square_colmajor(A):
 
 
 def gesv_gmres_ir(A, b, variant: int = 3, nb: int = 256, restart: int = 200, inner_tol: float = 1e-10,
-                  max_iter: int = 30):
+                  max_iter: int = 30, tol: float = 0.0):
     """GMRES-IR (bf16x_gesv_gmres_ir): LU with bf16x trailing updates as the preconditioner of
     FP64 GMRES corrections.  Arguments as gesv_ir plus restart / inner_tol.
     Returns (x, report, history); report.inner_iterations = total Arnoldi steps."""
@@ -299,7 +302,7 @@ def gesv_gmres_ir(A, b, variant: int = 3, nb: int = 256, restart: int = 200, inn
     b = b.to(torch.float64).contiguous()
     hist = np.zeros(max(1, max_iter) + 1, dtype=np.float64)
     rep = IRReport()
-    rc = lib().bf16x_gesv_gmres_ir(n, cm[0], cm[3], _ptr(b), _ptr(x), variant, nb, restart, float(inner_tol),
+    rc = lib().bf16x_gesv_gmres_ir(n, cm[0], cm[3], _ptr(b), _ptr(x), variant, nb, restart, float(inner_tol), float(tol),
                                    max_iter, hist.ctypes.data, ctypes.byref(rep))
     if rc not in (SUCCESS, NOT_CONVERGED, ERR_SINGULAR):
         _check(rc, "bf16x_gesv_gmres_ir")

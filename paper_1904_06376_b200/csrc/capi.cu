@@ -4,6 +4,7 @@
 #include <cstdio>
 #include <cstring>
 #include <mutex>
+#include <unordered_map>
 
 #include "common.cuh"
 #include "kernels.cuh"
@@ -13,16 +14,13 @@ namespace bf16x {
 static thread_local char g_err[256] = "";
 static cudaStream_t g_stream = nullptr;
 static std::atomic<uint64_t> g_launches{0};
-static std::mutex g_ws_mu;
-static void *g_ws = nullptr;
-static size_t g_ws_bytes = 0;
 static int g_max_ctas = 0;  // cap on the GEMM's persistent grid (bf16x_max_ctas hook; 0 = all SMs)
 static int g_group_m = 0;   // tile raster group (bf16x_group_m hook; 0 = default)
-// convert A inside the GEMM, split only B (bf16x_fused_a hook: 1 on, 0 off, -1 auto = bf16x9
-// only, the variant where it measured faster: +1..6 % for 2048^3..8192^3, r06 tools/fa9_probe.py)
+// bf16x9 converts A inside the GEMM and splits only B (bf16x_fused_a hook: 0 off, else on; the
+// variant where it measured faster: +1..6 % for 2048^3..8192^3, r06 tools/fa9_probe.py; slower
+// for x3 / x6, so not compiled for them)
 static int g_fused_a = -1;
-static int g_split_ahead = 0;   // split inside the GEMM (split-ahead warps; opt-in, not faster)
-static int g_force_cg = 0, g_force_bn = 0, g_force_spi = 0, g_stream_k = 1, g_multicast = 0, g_split_acc = 0, g_fused = 0;  // tuning overrides (bf16x_tune; not in the public ABI)
+static int g_force_cg = 0, g_force_bn = 0, g_force_spi = 0, g_stream_k = 1, g_multicast = 0, g_split_acc = 0;  // tuning overrides (bf16x_tune; not in the public ABI)
 
 void set_cuda_error(cudaError_t e, const char *where) {
     snprintf(g_err, sizeof(g_err), "%s: %s", where, cudaGetErrorString(e));
@@ -58,26 +56,89 @@ int arch_ok() {
 
 static int64_t round_up8(int64_t v) { return (v + 7) / 8 * 8; }
 
-// cached library workspace (grown on demand, never shrunk until bf16x_release)
-static void *workspace(size_t bytes, int *rc) {
-    std::lock_guard<std::mutex> g(g_ws_mu);
-    *rc = BF16X_SUCCESS;
-    if (bytes <= g_ws_bytes) return g_ws;
-    if (g_ws) {
-        cudaDeviceSynchronize();
-        cudaFree(g_ws);
-        g_ws = nullptr;
-        g_ws_bytes = 0;
-    }
-    if (cudaMalloc(&g_ws, bytes) != cudaSuccess) {
+// Per-stream library resources (bf16x.h: "the library owns a cached workspace per stream"):
+// the piece workspace of calls without a caller workspace, and the stream-K fix-up buffers
+// (partial accumulators + ready flags compared against a per-stream launch epoch).  Keyed by
+// cudaStreamGetId, which is unique for the lifetime of the process (a destroyed stream's
+// handle reused by a new stream gets a new id), so calls on different streams never share a
+// buffer and may run concurrently.  A buffer grows after a synchronisation of its own stream
+// (its earlier work may still read it); bf16x_release frees everything.
+struct StreamRes {
+    void *ws = nullptr;
+    size_t ws_bytes = 0;
+    float *sk = nullptr;
+    size_t sk_n = 0;
+    unsigned int *flags = nullptr;
+    size_t flags_n = 0;
+    unsigned int epoch = 0;
+};
+static std::mutex g_res_mu;
+static std::unordered_map<unsigned long long, StreamRes> g_res;
+
+static unsigned long long stream_key(cudaStream_t st) {
+    unsigned long long id = 0;
+    if (cudaStreamGetId(st, &id) != cudaSuccess) {
         cudaGetLastError();
-        snprintf(g_err, sizeof(g_err), "workspace: cannot allocate %zu bytes", bytes);
-        g_ws = nullptr;
-        *rc = BF16X_ERR_ALLOC;
-        return nullptr;
+        id = (unsigned long long)(uintptr_t)st;
     }
-    g_ws_bytes = bytes;
-    return g_ws;
+    return id;
+}
+
+static int grow(cudaStream_t st, void **buf, size_t *have, size_t bytes, bool zero, const char *what) {
+    if (bytes <= *have) return BF16X_SUCCESS;
+    if (*buf) {
+        cudaStreamSynchronize(st);
+        cudaFree(*buf);
+    }
+    *buf = nullptr;
+    *have = 0;
+    if (cudaMalloc(buf, bytes) != cudaSuccess || (zero && cudaMemset(*buf, 0, bytes) != cudaSuccess)) {
+        cudaGetLastError();
+        if (*buf) cudaFree(*buf);
+        *buf = nullptr;
+        snprintf(g_err, sizeof(g_err), "%s: cannot allocate %zu bytes", what, bytes);
+        return BF16X_ERR_ALLOC;
+    }
+    *have = bytes;
+    return BF16X_SUCCESS;
+}
+
+static void *workspace(cudaStream_t st, size_t bytes, int *rc) {
+    std::lock_guard<std::mutex> g(g_res_mu);
+    StreamRes &r = g_res[stream_key(st)];
+    *rc = grow(st, &r.ws, &r.ws_bytes, bytes, false, "workspace");
+    return *rc ? nullptr : r.ws;
+}
+
+int sk_workspace(cudaStream_t st, size_t ws_floats, size_t nflags, float **ws, unsigned int **flags,
+                 unsigned int *epoch) {
+    std::lock_guard<std::mutex> g(g_res_mu);
+    StreamRes &r = g_res[stream_key(st)];
+    size_t skb = r.sk_n * sizeof(float), flb = r.flags_n * sizeof(unsigned int);
+    int rc = grow(st, reinterpret_cast<void **>(&r.sk), &skb, ws_floats * sizeof(float), false, "stream-K workspace");
+    r.sk_n = skb / sizeof(float);
+    if (rc) return rc;
+    const bool fresh = nflags > r.flags_n;
+    rc = grow(st, reinterpret_cast<void **>(&r.flags), &flb, nflags * sizeof(unsigned int), true, "stream-K flags");
+    r.flags_n = flb / sizeof(unsigned int);
+    if (rc) return rc;
+    if (fresh) r.epoch = 0;                  // new flags are zero: any epoch > 0 is unseen
+    if (++r.epoch == 0) ++r.epoch;           // never 0 (the reset value)
+    *ws = r.sk;
+    *flags = r.flags;
+    *epoch = r.epoch;
+    return BF16X_SUCCESS;
+}
+
+static void release_all_streams() {
+    std::lock_guard<std::mutex> g(g_res_mu);
+    cudaDeviceSynchronize();
+    for (auto &kv : g_res) {
+        if (kv.second.ws) cudaFree(kv.second.ws);
+        if (kv.second.sk) cudaFree(kv.second.sk);
+        if (kv.second.flags) cudaFree(kv.second.flags);
+    }
+    g_res.clear();
 }
 
 static bool variant_ok(int v) { return v == 1 || v == 3 || v == 5 || v == 6 || v == 7 || v == 8 || v == 9; }
@@ -111,7 +172,7 @@ int gemm_core(int m, int n, int k, float alpha, const float *A, int lda, const f
             if (ws_bytes < need) return -21;
             w = (uint8_t *)ws;
         } else {
-            w = (uint8_t *)workspace(need, &rc);
+            w = (uint8_t *)workspace(st, need, &rc);
             if (rc) return rc;
         }
     }
@@ -125,22 +186,16 @@ int gemm_core(int m, int n, int k, float alpha, const float *A, int lda, const f
     pl.max_ctas = max_ctas > 0 ? max_ctas : g_max_ctas;
     pl.tile_n = g_force_bn;
     pl.stages_per_interval = g_force_spi;
-    pl.stream_k = allow_stream_k ? g_stream_k : 0;   // (its workspace is shared: one stream at a time)
+    pl.stream_k = (allow_stream_k && !(flags & BF16X_NO_STREAM_K)) ? g_stream_k : 0;
     pl.multicast = g_multicast;
     pl.split_acc = g_split_acc;
     pl.scaled = (flags & BF16X_SCALED_PIECES) ? 1 : 0;
     pl.fp64 = (flags & BF16X_FP64_COMBINE) ? 1 : 0;
     pl.group_m = g_group_m;
-    pl.split_ahead = 0;
     pl.fused_a = 0;
     const bool sc = pl.scaled != 0;
     pl.Af = A; pl.Bf = B; pl.lda = lda; pl.ldb = ldb;
-    if (!Ap && !Bp && g_fused && !sc && !pl.fp64) {   // split inside the GEMM when the plan qualifies
-        pl.Ap = nullptr; pl.Bp = nullptr;
-        const int frc = launch_gemm_fused(pl, st);
-        if (frc != -1) return frc;
-    }
-    if (!Ap && !Bp && (g_fused_a == 1 || (g_fused_a < 0 && variant == 9)) && fused_a_ok(pl)) {
+    if (!Ap && !Bp && g_fused_a != 0 && variant == 9 && fused_a_ok(pl)) {
         // only B is split in the pre-pass; the GEMM converts A from FP32 tiles
         uint16_t *b = (uint16_t *)w;
         b_plane = (int64_t)n * kp;
@@ -151,17 +206,6 @@ int gemm_core(int m, int n, int k, float alpha, const float *A, int lda, const f
         pl.Ap = nullptr;
         pl.Bp = b; pl.ldbp = ldbp; pl.b_plane = b_plane;
         pl.fused_a = 1;
-        return launch_gemm_pieces(pl, st);
-    }
-    if (!Ap && !Bp && g_split_ahead && allow_stream_k && split_ahead_ok(pl)) {
-        // the GEMM's split-ahead warps write the pieces into the workspace (pre-pass layout)
-        pl.Ap = (uint16_t *)w;
-        pl.ldap = kp;
-        pl.a_plane = (int64_t)m * kp;
-        pl.Bp = (uint16_t *)w + pa * pl.a_plane;
-        pl.ldbp = kp;
-        pl.b_plane = (int64_t)n * kp;
-        pl.split_ahead = 1;
         return launch_gemm_pieces(pl, st);
     }
     if (!Ap && !Bp) {   // both operands: one pre-pass launch
@@ -226,7 +270,8 @@ int bf16x_gemm_ex(int m, int n, int k, float alpha, const float *A, int lda, con
                   void *workspace_ptr, size_t ws_bytes, bf16x_stream_t stream) {
     int a = gemm_args(m, n, k, A_pieces ? (m > 1 ? m : 1) : lda, B_pieces ? (k > 1 ? k : 1) : ldb, ldc, variant);
     if (a) return a;
-    if (flags & ~(BF16X_ACC_IN | BF16X_ACC_OUT | BF16X_SCALED_PIECES | BF16X_FP64_COMBINE)) return -13;
+    if (flags & ~(BF16X_ACC_IN | BF16X_ACC_OUT | BF16X_SCALED_PIECES | BF16X_FP64_COMBINE | BF16X_NO_STREAM_K))
+        return -13;
     if ((flags & BF16X_FP64_COMBINE) && ((flags & (BF16X_ACC_IN | BF16X_ACC_OUT)) || variant == 1)) return -13;
     if (A_pieces && (ldap < k || ldap % 8 || a_plane % 8 || a_plane < ldap * (int64_t)m ||
                      (reinterpret_cast<uintptr_t>(A_pieces) & 15u)))
@@ -446,12 +491,7 @@ int bf16x_set_stream(bf16x_stream_t stream) {
 bf16x_stream_t bf16x_get_stream(void) { return (bf16x_stream_t)g_stream; }
 
 void bf16x_release(void) {
-    release_gemm_workspace();
-    std::lock_guard<std::mutex> g(g_ws_mu);
-    cudaDeviceSynchronize();
-    if (g_ws) cudaFree(g_ws);
-    g_ws = nullptr;
-    g_ws_bytes = 0;
+    release_all_streams();
     std::lock_guard<std::mutex> h(g_host_mu);
     if (g_hA) cudaFree(g_hA);
     if (g_hB) cudaFree(g_hB);
@@ -493,7 +533,6 @@ void bf16x_split_acc(int on) { g_split_acc = on; }
 void bf16x_group_m(int g) { g_group_m = g; }
 void bf16x_max_ctas(int c) { g_max_ctas = c; }   // tile raster group height (0 = default)
 void bf16x_fused_a(int on) { g_fused_a = on; }   // 1 on, 0 off, -1 auto (fused-A warps)
-void bf16x_split_ahead(int on) { g_split_ahead = on; }   // split inside the GEMM (split-ahead warps)
 // Timeline of the last pipelined bf16x_gemm_host call, ms since its start: [0] start, [1] A
 // landed, [2] A split, [3] unused, then per chunk j: [4+3j] B_j landed, [5+3j] GEMM_j done,
 // [6+3j] C_j copied back (-1 = not recorded).  on: enable recording for later calls.
@@ -511,7 +550,6 @@ int bf16x_host_timeline(int on, float *ms, int cap) {
     return n;
 }
 void bf16x_host_chunks(int n) { g_host_chunks = n > 0 ? n : 12; }   // bf16x_gemm_host pipeline depth
-void bf16x_fused_split(int on) { g_fused = on; }   // 1: split inside the GEMM when eligible (default 0)
 void bf16x_multicast(int pairs) { g_multicast = pairs; }   // 0 = auto, 1 = off, 2 = on
 void bf16x_tune(int cta_group, int tile_n, int stages_per_interval) {
     g_force_cg = cta_group;

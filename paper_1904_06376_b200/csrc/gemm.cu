@@ -73,65 +73,6 @@ int make_f32_map(CUtensorMap *map, const float *base, int rows, int cols, int64_
     return r == CUDA_SUCCESS ? BF16X_SUCCESS : BF16X_ERR_CUDA;
 }
 
-// Stream-K fix-up workspace: partial accumulators + per-(tile, CTA) ready flags.  Flags are
-// zeroed when the buffer is (re)allocated and compared against a per-launch epoch, so no
-// per-launch reset is needed.  Launches on one stream are ordered; concurrent launches on
-// different streams would need their own workspace (documented in bf16x.h).
-static std::mutex g_sk_mu;
-static float *g_sk_ws = nullptr;
-static unsigned int *g_sk_flags = nullptr;
-static size_t g_sk_ws_n = 0, g_sk_flags_n = 0;
-static unsigned int g_sk_epoch = 0;
-
-int sk_workspace(size_t ws_floats, size_t nflags, float **ws, unsigned int **flags, unsigned int *epoch) {
-    std::lock_guard<std::mutex> g(g_sk_mu);
-    if (ws_floats > g_sk_ws_n) {
-        if (g_sk_ws) { cudaDeviceSynchronize(); cudaFree(g_sk_ws); }
-        g_sk_ws = nullptr;
-        g_sk_ws_n = 0;
-        if (cudaMalloc(&g_sk_ws, ws_floats * sizeof(float)) != cudaSuccess) {
-            cudaGetLastError();
-            set_error_msg("stream-K workspace: allocation failed");
-            return BF16X_ERR_ALLOC;
-        }
-        g_sk_ws_n = ws_floats;
-    }
-    if (nflags > g_sk_flags_n) {
-        if (g_sk_flags) { cudaDeviceSynchronize(); cudaFree(g_sk_flags); }
-        g_sk_flags = nullptr;
-        g_sk_flags_n = 0;
-        if (cudaMalloc(&g_sk_flags, nflags * sizeof(unsigned int)) != cudaSuccess ||
-            cudaMemset(g_sk_flags, 0, nflags * sizeof(unsigned int)) != cudaSuccess) {
-            cudaGetLastError();
-            set_error_msg("stream-K flags: allocation failed");
-            return BF16X_ERR_ALLOC;
-        }
-        g_sk_flags_n = nflags;
-    }
-    if (++g_sk_epoch == 0) ++g_sk_epoch;  // never 0 (the reset value)
-    *ws = g_sk_ws;
-    *flags = g_sk_flags;
-    *epoch = g_sk_epoch;
-    return BF16X_SUCCESS;
-}
-
-// Split-ahead slab counters: nslab ready counters + one completion counter, zero between
-// launches (the last CTA of each launch resets them).  Grown with a device sync.
-static unsigned int *g_sp_ctr = nullptr;
-static size_t g_sp_ctr_n = 0;
-
-void release_gemm_workspace() {
-    std::lock_guard<std::mutex> g(g_sk_mu);
-    if (g_sp_ctr) cudaFree(g_sp_ctr);
-    g_sp_ctr = nullptr;
-    g_sp_ctr_n = 0;
-    if (g_sk_ws) cudaFree(g_sk_ws);
-    if (g_sk_flags) cudaFree(g_sk_flags);
-    g_sk_ws = nullptr;
-    g_sk_flags = nullptr;
-    g_sk_ws_n = g_sk_flags_n = 0;
-}
-
 int num_sms() {
     static int n = 0;
     if (!n) {
@@ -147,34 +88,6 @@ int pieces_a(int variant) { return variant_pieces_a(variant); }
 int pieces_b(int variant) { return variant_pieces_b(variant); }
 int default_cta_group() { return kDefaultCtaGroup; }
 
-
-int sp_counters(int nslab, unsigned int **ctr) {
-    std::lock_guard<std::mutex> g(g_sk_mu);
-    const size_t need = (size_t)nslab + 1;
-    if (need > g_sp_ctr_n) {
-        const size_t cap = std::max<size_t>(need, 1024);
-        if (g_sp_ctr) { cudaDeviceSynchronize(); cudaFree(g_sp_ctr); }
-        g_sp_ctr = nullptr;
-        g_sp_ctr_n = 0;
-        if (cudaMalloc(&g_sp_ctr, cap * sizeof(unsigned int)) != cudaSuccess ||
-            cudaMemset(g_sp_ctr, 0, cap * sizeof(unsigned int)) != cudaSuccess) {
-            cudaGetLastError();
-            set_error_msg("split-ahead counters: allocation failed");
-            return BF16X_ERR_ALLOC;
-        }
-        g_sp_ctr_n = cap;
-    }
-    *ctr = g_sp_ctr;
-    return BF16X_SUCCESS;
-}
-
-bool split_ahead_ok(const GemmPlan &pl) {
-    const int cg = pl.cta_group ? pl.cta_group : kDefaultCtaGroup;
-    if (cg != 2 || pl.fp64 || pl.split_acc || pl.k <= 128 || pl.stages_per_interval == 1 || pl.tile_n == 192)
-        return false;
-    const bool mc2 = pl.multicast == 2 || (pl.multicast == 0 && (int64_t)pl.m * pl.n >= 12288LL * 12288LL);
-    return !mc2 && pl.Af && pl.Bf;
-}
 
 bool fused_a_ok(const GemmPlan &pl) {
     const int cg = pl.cta_group ? pl.cta_group : kDefaultCtaGroup;
@@ -195,21 +108,6 @@ static int dispatch(const GemmPlan &pl, cudaStream_t st, int kind) {
     case 9: return launch_variant_9(pl, st, kind);
     }
     return -12;
-}
-
-// Fused split: 2-CTA pairs, tile N 256, one 32-k stage per promotion interval, FP32 operands
-// read by TMA (16-byte aligned, leading dimensions multiples of 4 floats).  Not used where the
-// pre-split kernel is configured differently on purpose: forced CTA mode 1 / tile N / 2-stage
-// intervals, split accumulators, or the multicast schedule of large outputs.
-int launch_gemm_fused(const GemmPlan &pl, cudaStream_t st) {
-    const int cg = pl.cta_group ? pl.cta_group : kDefaultCtaGroup;
-    const bool aligned = pl.Af && pl.Bf && ((reinterpret_cast<uintptr_t>(pl.Af) | reinterpret_cast<uintptr_t>(pl.Bf)) & 15u) == 0 &&
-                         pl.lda % 4 == 0 && pl.ldb % 4 == 0;
-    const bool mc2 = pl.multicast == 2 || (pl.multicast == 0 && (int64_t)pl.m * pl.n >= 12288LL * 12288LL);
-    if (!aligned || cg != 2 || pl.split_acc || pl.scaled || pl.fp64 || mc2 || (pl.tile_n && pl.tile_n != 256) ||
-        pl.stages_per_interval == 2 || pl.k <= 0)
-        return -1;
-    return dispatch(pl, st, 3);
 }
 
 int launch_gemm_pieces(const GemmPlan &pl, cudaStream_t st) {

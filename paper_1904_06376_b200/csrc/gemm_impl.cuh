@@ -18,15 +18,8 @@ constexpr int kRowBytes = kBK * 2;    // 64 B rows -> SWIZZLE_64B
 constexpr int kSwizzleAtom = 8 * kRowBytes;  // 8 rows x 64 B: stride between row groups (SBO)
 constexpr int kNumEpiWarps = 8;       // 2 per TMEM lane quadrant, BN/2 columns each
 constexpr int kThreads = (4 + kNumEpiWarps) * 32;
-constexpr int kNumXfWarps = 8;        // fused split: warps 12..19 convert FP32 tiles to pieces
+constexpr int kNumXfWarps = 8;        // fused A: warps 12..19 convert FP32 A tiles to pieces
 constexpr int kThreadsFused = kThreads + kNumXfWarps * 32;
-// split-ahead (SP): warps 12..15 of every CTA split a static share of A and B into the global
-// piece workspace, slab by slab (kSlab values of k), while the TMA producers wait per slab on
-// a global counter -- the split hides behind the first wave's MMAs ("the splitting
-// can be hidden behind the computations") instead of running as a separate pre-pass.
-constexpr int kNumSpWarps = 4;
-constexpr int kThreadsSp = kThreads + kNumSpWarps * 32;
-constexpr int kSlab = 128;
 constexpr int kF32Tile = kBM * kBK * 4;   // one FP32 operand tile per CTA per stage (16 KB)
 constexpr int kTmemCols = 512;        // two accumulator buffers at column 0 and 256
 constexpr int kTmemBufStride = 256;
@@ -61,20 +54,6 @@ struct Cfg {
     static constexpr int SMEM = STAGES * STAGE + BAR_BYTES + 1024;
     static_assert(STAGES >= 2, "need at least two pipeline stages");
     static_assert(BN % (16 * CG) == 0 && BN <= 256 && EPI_COLS % 32 == 0, "invalid tile N");
-};
-
-// Fused-split configuration (2-CTA pairs, tile N 256, one stage per promotion interval): a ring
-// of FSTAGES FP32 stages (TMA destination: A rows x 32 k and B rows x 32 k per CTA) feeding a
-// ring of STAGES piece stages (MMA source), converted by the transform warps.
-template <int V>
-struct CfgF {
-    using Cf = Cfg<2, V, 256>;
-    static constexpr int FSTAGES = 2;
-    static constexpr int F32_STAGE = 2 * kF32Tile;
-    static constexpr int STAGES_RAW = (kSmemBudget - 256 - 1024 - FSTAGES * F32_STAGE) / Cf::STAGE;
-    static constexpr int STAGES = STAGES_RAW > 6 ? 6 : STAGES_RAW;
-    static constexpr int SMEM = STAGES * Cf::STAGE + FSTAGES * F32_STAGE + 256 + 1024;
-    static_assert(STAGES >= 2, "fused split needs two piece stages");
 };
 
 // Fused-A configuration (FA: A converted inside the GEMM from FP32 tiles, B pre-split): a ring of
@@ -112,14 +91,7 @@ struct KParams {
     int scaled;            // N2 scaled pieces (R29): scale the accumulator by 2^-8 per bin step
     int group_m;           // tile raster: m-tiles per group
     int lazy_full;         // issuer waits for each stage just before its first MMA (issue_interval)
-    // split-ahead (SP): FP32 operands in, piece workspace out (the layout the tensor maps read),
-    // per-slab ready counters (reset by the last CTA to finish)
-    const float *Af, *Bf;
-    int64_t lda, ldb;
-    uint16_t *Apw, *Bpw;
-    int64_t ldap, a_plane, ldbp, b_plane;
-    unsigned int *slab_ctr, *done_ctr;
-    int nslab;
+    int64_t pad[6];
 };
 
 struct Work {
@@ -249,162 +221,35 @@ __device__ __forceinline__ void issue_interval(uint32_t d_big, uint32_t d_small,
     for (int h = 0; h < H; ++h) if (h < nh) mma(0, 0, h);                                  // bin 0
 }
 
-// Split-ahead warps (SP): this CTA's contiguous share of every slab's work list (below)
-// converted into the piece workspace in the K-major layout of bf16x_split_t (A) / bf16x_split
-// (B), bit for bit the pre-pass's split (same split_pair arithmetic).  After a slab: proxy
-// fence, named barrier of the 4 warps, one release increment of the slab's counter.
-// Measured (r06, tools/sp_probe.py): correct and bit-identical, but not faster than the
-// pre-pass at 4096^3 / 8192^3 -- the transposed A pieces are written as 32-byte fragments per
-// lane (one row each), which the 4 warps cannot issue fast enough to stay ahead of the first
-// wave's MMAs (without the stores the kernel would be 3 % faster).  Opt-in (bf16x_split_ahead).
-template <int PA, int PB>
-__device__ __forceinline__ void store_piece16(uint16_t *dst, const uint32_t (&w)[8], int64_t kleft) {
-    // 16 values at dst (32-byte aligned); the piece row ends at a multiple of 8 (kp): write
-    // the second half only if it starts inside the row
-    if (kleft > 0) *reinterpret_cast<uint4 *>(dst) = make_uint4(w[0], w[1], w[2], w[3]);
-    if (kleft > 8) *reinterpret_cast<uint4 *>(dst + 8) = make_uint4(w[4], w[5], w[6], w[7]);
-}
-
-template <int NP>
-__device__ __forceinline__ void split16(const float (&x)[16], uint32_t (&q)[3][8], bool scaled) {
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-        uint32_t t[3];
-        if (scaled) split_pair<NP, true>(x[2 * j], x[2 * j + 1], t);
-        else split_pair<NP, false>(x[2 * j], x[2 * j + 1], t);
-#pragma unroll
-        for (int pc = 0; pc < 3; ++pc) q[pc][j] = t[pc];
-    }
-}
-
-
-template <int PA, int PB>
-__device__ __forceinline__ void split_ahead_warps(const KParams &p, int t) {
-    // Per slab the work is a list of items of 16 values of k: first A's (m * 8 items, ordered
-    // (block of 256 rows, 16-k part, row) so that a run of consecutive items reads 1 KB runs of
-    // one column of the column-major A), then B's (n * 8 items, (column, part): 8 consecutive
-    // items = one column's 512-byte slab).  Every CTA takes one contiguous share of the list.
-    constexpr int NPART = kSlab / 16;
-    constexpr int RB = 256;                 // rows per A block
-    constexpr int NT = kNumSpWarps * 32;
-    const int G = gridDim.x;
-    const int64_t IA = (int64_t)p.m * NPART, I = IA + (int64_t)p.n * NPART;
-    const int64_t i0 = I * blockIdx.x / G, i1 = I * (blockIdx.x + 1) / G;
-    const int64_t kp_a = p.ldap, kp_b = p.ldbp;
-    const bool scaled = p.scaled != 0;
-    const bool bvec = ((reinterpret_cast<uintptr_t>(p.Bf) & 15u) == 0) && (p.ldb % 4 == 0);
-    for (int slab = 0; slab < p.nslab; ++slab) {
-        const int k0 = slab * kSlab;
-        for (int64_t it0 = i0 + t; it0 < i1; it0 += 2 * NT) {
-            float x[2][16];
-            int64_t dst[2];      // element offset of the 16-value run in piece plane 0, or -1
-            int isb[2], kcv[2];
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const int64_t it = it0 + h * NT;
-                dst[h] = -1;
-                isb[h] = 0;
-                kcv[h] = 0;
-                if (it >= i1) {
-#pragma unroll
-                    for (int q = 0; q < 16; ++q) x[h][q] = 0.f;
-                    continue;
-                }
-                if (it < IA) {
-                    const int64_t blk = it / (RB * NPART);
-                    const int64_t rem = it - blk * (RB * NPART);
-                    const int rows_in = (int)min((int64_t)RB, (int64_t)p.m - blk * RB);   // last block may be short
-                    // within a block: part-major over its rows
-                    const int part = (int)(rem / rows_in), r = (int)(rem - (int64_t)part * rows_in);
-                    const int64_t row = blk * RB + r;
-                    const int kc = k0 + part * 16;
-                    kcv[h] = kc;
-                    if (kc < p.k) dst[h] = row * kp_a + kc;
-#pragma unroll
-                    for (int q = 0; q < 16; ++q)
-                        x[h][q] = (kc + q < p.k) ? __ldcs(p.Af + (int64_t)(kc + q) * p.lda + row) : 0.f;
-                } else {
-                    const int64_t j = it - IA;
-                    const int64_t col = j / NPART;
-                    const int part = (int)(j - col * NPART);
-                    const int kc = k0 + part * 16;
-                    kcv[h] = kc;
-                    isb[h] = 1;
-                    if (kc < p.k) dst[h] = col * kp_b + kc;
-                    const float *src = p.Bf + col * p.ldb + kc;
-                    if (bvec && kc + 16 <= p.k) {
-#pragma unroll
-                        for (int q = 0; q < 4; ++q) {
-                            const float4 v = __ldcs(reinterpret_cast<const float4 *>(src) + q);
-                            x[h][4 * q] = v.x; x[h][4 * q + 1] = v.y; x[h][4 * q + 2] = v.z; x[h][4 * q + 3] = v.w;
-                        }
-                    } else {
-#pragma unroll
-                        for (int q = 0; q < 16; ++q) x[h][q] = (kc + q < p.k) ? src[q] : 0.f;
-                    }
-                }
-            }
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                if (dst[h] < 0) continue;
-                uint32_t w[3][8];
-                if (isb[h]) {
-                    split16<PB>(x[h], w, scaled);
-#pragma unroll
-                    for (int pc = 0; pc < PB; ++pc)
-                        store_piece16<PA, PB>(p.Bpw + pc * p.b_plane + dst[h], w[pc], kp_b - kcv[h]);
-                } else {
-                    split16<PA>(x[h], w, scaled);
-#pragma unroll
-                    for (int pc = 0; pc < PA; ++pc)
-                        store_piece16<PA, PB>(p.Apw + pc * p.a_plane + dst[h], w[pc], kp_a - kcv[h]);
-                }
-            }
-        }
-        // publish the slab: stores -> async proxy (TMA readers), then one release increment
-        asm volatile("fence.proxy.async.global;" ::: "memory");
-        __threadfence();
-        asm volatile("bar.sync 2, %0;" ::"n"(NT));
-        if (t == 0) asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(p.slab_ctr + slab) : "memory");
-    }
-}
-
 // MC = number of CTA pairs per cluster sharing the B tile (1, or 2: two vertically adjacent
 // 256 x BN tiles; each pair loads half of every B slice and multicasts it to both pairs).
-// FU (fused split): tmA / tmB are FP32 maps of A and B; warp 0 loads FP32 tiles, warps
-// 12..15 convert them into the piece ring (the MMA reads exactly what the pre-pass + TMA path
-// would have placed there), and the piece-ring "full" barrier counts the converters' arrivals.
 // GD ("d" variants, R30; requires SA): the bins >= 1 and bin 0 are promoted into two separate
 // FP32 register accumulators (G[0, EC) = bin 0, G[EC, 2 EC) = bins >= 1: the paper's FP32
 // partial sums Z^(i,j), pooled per accumulator) and only their final collection is
 // FP64, rounded once to FP32 ("adding the final results together in FP64").
-// SP (split-ahead): see kNumSpWarps.
 // FA (fused A): A is read as FP32 tiles by TMA and converted by 4 extra warps (warps 12..15,
 // thread t = row t of the CTA's 128 A rows) into the A half of the piece ring; B's pieces come
 // from the pre-pass by TMA as usual.  The piece-ring "full" barrier counts the leader's
 // expect-tx arrival (B bytes) plus the converters' arrivals of both CTAs.
-template <int CG, int V, int BN, int S, int MC, bool SA, bool FU = false, bool GD = false, bool SP = false,
-          bool FA = false>
-__global__ void __launch_bounds__((FU || FA) ? kThreadsFused : (SP ? kThreadsSp : kThreads), 1)
+template <int CG, int V, int BN, int S, int MC, bool SA, bool GD = false, bool FA = false>
+__global__ void __launch_bounds__(FA ? kThreadsFused : kThreads, 1)
     gemm_split_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                       const KParams p) {
     using Cf = Cfg<CG, V, BN>;
-    constexpr int NST = FU ? CfgF<V>::STAGES : (FA ? CfgFA<V>::STAGES : Cf::STAGES);   // piece ring stages
-    constexpr int NF = FU ? CfgF<V>::FSTAGES : (FA ? CfgFA<V>::FSTAGES : 0);         // FP32 ring stages
-    constexpr int F32_STAGE = FA ? kF32Tile : 2 * kF32Tile;                          // FP32 ring stage bytes
-    static_assert(!FA || (CG == 2 && BN == 256 && MC == 1 && !SA && !FU && !SP && !GD), "fused A: 2-CTA, N 256");
-    static_assert(!FU || (CG == 2 && BN == 256 && S == 1 && MC == 1 && !SA), "fused split: 2-CTA, N 256, S 1");
+    constexpr int NST = FA ? CfgFA<V>::STAGES : Cf::STAGES;   // piece ring stages
+    constexpr int NF = FA ? CfgFA<V>::FSTAGES : 0;            // FP32 ring stages (fused A)
+    constexpr int F32_STAGE = kF32Tile;                       // FP32 ring stage bytes
+    static_assert(!FA || (CG == 2 && BN == 256 && MC == 1 && !SA && !GD), "fused A: 2-CTA, N 256");
     constexpr int CL = CG * MC;   // cluster size
     static_assert(MC == 1 || CG == 2, "multicast needs 2-CTA pairs");
     static_assert(!SA || 2 * BN <= kTmemBufStride, "split accumulators need 4 x BN TMEM columns");
-    static_assert(!GD || (SA && !FU), "FP64 collection needs split accumulators");
-    static_assert(!SP || (!FU && !GD && !SA && MC == 1), "split-ahead: plain pre-split layout");
+    static_assert(!GD || SA, "FP64 collection needs split accumulators");
     constexpr int NG = GD ? 2 : 1;     // promoted accumulators per output element
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t *sA = smem;
     uint8_t *sB = smem + NST * Cf::A_STAGE;
-    uint8_t *f32 = smem + NST * Cf::STAGE;                      // FU: [NF][A tile | B tile]
+    uint8_t *f32 = smem + NST * Cf::STAGE;                      // FA: [NF][A tile]
     uint64_t *full = reinterpret_cast<uint64_t *>(smem + NST * Cf::STAGE + NF * F32_STAGE);
     uint64_t *empty = full + NST;
     uint64_t *acc_full = empty + NST;
@@ -424,14 +269,14 @@ __global__ void __launch_bounds__((FU || FA) ? kThreadsFused : (SP ? kThreadsSp 
     }
     if (warp == 1 && lane == 0) {
         for (int s = 0; s < NST; ++s) {
-            mbar_init(&full[s], FU ? kNumXfWarps * CG : (FA ? 1 + kNumXfWarps * CG : 1));
+            mbar_init(&full[s], FA ? 1 + kNumXfWarps * CG : 1);
             mbar_init(&empty[s], MC);     // one commit per pair reading the (shared) stage
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(&acc_full[b], 1);
             mbar_init(&acc_empty[b], kNumEpiWarps * CG);
         }
-        if constexpr (FU || FA)
+        if constexpr (FA)
             for (int b = 0; b < NF; ++b) {
                 mbar_init(&f32_full[b], 1);
                 mbar_init(&f32_empty[b], kNumXfWarps);
@@ -446,22 +291,19 @@ __global__ void __launch_bounds__((FU || FA) ? kThreadsFused : (SP ? kThreadsSp 
     // Programmatic dependent launch: everything above overlapped the previous kernel's tail;
     // from here on we read its outputs (the pieces) and may overwrite what it read.
     asm volatile("griddepcontrol.wait;" ::: "memory");
-    // FU register split (per warpgroup, at the top of each role): the epilogue warpgroups hold
-    // G (160 registers), producer / MMA and the two transform warpgroups need few (48); the sum
+    // FA register split (per warpgroup, at the top of each role): the epilogue warpgroups hold
+    // G (160 registers), producer / MMA and the two converter warpgroups need few (48); the sum
     // must not exceed the launch allocation (96 x 640), or the increase waits forever
 
     const int cid = blockIdx.x / CL, ncl = gridDim.x / CL;
 
     if (warp < 4) {
-        if constexpr (FU) asm volatile("setmaxnreg.dec.sync.aligned.u32 48;" ::: "memory");
-        if constexpr (SP) asm volatile("setmaxnreg.dec.sync.aligned.u32 56;" ::: "memory");
         if constexpr (FA) asm volatile("setmaxnreg.dec.sync.aligned.u32 48;" ::: "memory");
         if (warp == 0) {
             // ------------------------------ TMA producer ------------------------------
             if (lane == 0) {
                 int stage = 0;
                 uint32_t phase = 0;
-                int slab_ready = -1;   // SP: highest slab known to be split by every CTA
                 int fstage = 0;        // FA: FP32 ring
                 uint32_t fphase = 0;
                 WorkIter it(p, cid, ncl);
@@ -488,28 +330,7 @@ __global__ void __launch_bounds__((FU || FA) ? kThreadsFused : (SP ? kThreadsSp 
                         }
                         continue;
                     }
-                    if constexpr (FU) {
-                        // FP32 tiles of this CTA's 128 A rows and 128 B rows, local completion
-                        for (int kb = w.i0 * S; kb < kb_end; ++kb) {
-                            mbar_wait(&f32_empty[stage], phase ^ 1u);
-                            mbar_arrive_expect_tx(&f32_full[stage], 2 * kF32Tile);
-                            uint8_t *dst = f32 + stage * 2 * kF32Tile;
-                            tma_load_2d(dst, &tmA, &f32_full[stage], a_row, kb * kBK);
-                            tma_load_2d(dst + kF32Tile, &tmB, &f32_full[stage], kb * kBK, b_row);
-                            if (++stage == NF) { stage = 0; phase ^= 1u; }
-                        }
-                        continue;
-                    }
                     for (int kb = w.i0 * S; kb < kb_end; ++kb) {
-                        if constexpr (SP) {
-                            const int slab = kb * kBK / kSlab;
-                            if (slab > slab_ready) {
-                                while (ld_acquire_u32(p.slab_ctr + slab) < gridDim.x) __nanosleep(32);
-                                // generic-proxy stores of other CTAs -> this CTA's TMA reads
-                                asm volatile("fence.proxy.async.global;" ::: "memory");
-                                slab_ready = slab;
-                            }
-                        }
                         mbar_wait(&empty[stage], phase ^ 1u);
                         uint8_t *a_dst = sA + stage * Cf::A_STAGE;
                         uint8_t *b_dst = sB + stage * Cf::B_STAGE;
@@ -588,8 +409,7 @@ __global__ void __launch_bounds__((FU || FA) ? kThreadsFused : (SP ? kThreadsSp 
             }
         }
     } else if (warp < 4 + kNumEpiWarps) {
-        if constexpr (FU || FA) asm volatile("setmaxnreg.inc.sync.aligned.u32 160;" ::: "memory");
-        if constexpr (SP) asm volatile("setmaxnreg.inc.sync.aligned.u32 168;" ::: "memory");
+        if constexpr (FA) asm volatile("setmaxnreg.inc.sync.aligned.u32 160;" ::: "memory");
         // ------------------------- promotion + epilogue ---------------------------
         constexpr int EC = Cf::EPI_COLS;
         const int ew = warp - 4;
@@ -737,9 +557,6 @@ __global__ void __launch_bounds__((FU || FA) ? kThreadsFused : (SP ? kThreadsSp 
                 }
             }
         }
-    } else if constexpr (SP) {
-        asm volatile("setmaxnreg.dec.sync.aligned.u32 112;" ::: "memory");
-        split_ahead_warps<Cf::PA, Cf::PB>(p, threadIdx.x - kThreads);
     } else if constexpr (FA) {
         asm volatile("setmaxnreg.dec.sync.aligned.u32 48;" ::: "memory");
         // ------------------- fused A: FP32 A tiles -> A pieces -------------------
@@ -797,93 +614,6 @@ __global__ void __launch_bounds__((FU || FA) ? kThreadsFused : (SP ? kThreadsSp 
                 if (++ps == NST) { ps = 0; pph ^= 1u; }
             }
         }
-    } else if constexpr (FU) {
-        asm volatile("setmaxnreg.dec.sync.aligned.u32 48;" ::: "memory");
-        // ----------------------- fused split: FP32 tiles -> pieces ----------------------
-        // Threads 0..127 of the transform warps convert row t of the A tile ([k][128 rows] FP32,
-        // no swizzle), threads 128..255 row t of the B tile ([128 rows][32 k] FP32, 128-byte
-        // swizzle), 8 values of k at a time, into the K-major piece planes with the 64-byte
-        // swizzle the MMA descriptors expect (16-byte chunk c of row r at chunk
-        // c ^ ((r >> 1) & 3)): exactly the bytes the pre-pass + TMA would have written.
-        const int tx = threadIdx.x - (4 + kNumEpiWarps) * 32;
-        const bool isA = tx < kBM;
-        const int t = isA ? tx : tx - kBM;
-        const uint32_t swz = (uint32_t)((t >> 1) & 3);
-        const uint32_t f32_s = smem_u32(f32), sA_s = smem_u32(sA), sB_s = smem_u32(sB);
-        int fs = 0, ps = 0;
-        uint32_t fph = 0, pph = 0;
-        WorkIter it(p, cid, ncl);
-        Work w;
-        while (it.next(p, w)) {
-            const int kb_end = min(p.nkb, w.i1 * S);
-            for (int kb = w.i0 * S; kb < kb_end; ++kb) {
-                mbar_wait(&f32_full[fs], fph);
-                mbar_wait(&empty[ps], pph ^ 1u);
-                const uint32_t fbase = f32_s + (uint32_t)(fs * 2 * kF32Tile);
-                if (isA) {
-                    const uint32_t fa = fbase + (uint32_t)t * 4u;           // element (t, k) at k*512 + 4t
-                    const uint32_t pa = sA_s + (uint32_t)(ps * Cf::A_STAGE) + (uint32_t)t * kRowBytes;
-#pragma unroll
-                    for (int hh = 0; hh < 4; ++hh) {
-                        float x[8];
-#pragma unroll
-                        for (int j = 0; j < 8; ++j) x[j] = lds_f32(fa + (uint32_t)((hh * 8 + j) * kBM * 4));
-                        uint32_t q[4][3];
-                        bool ok = true;                     // one branch per 8 values
-#pragma unroll
-                        for (int j = 0; j < 8; ++j) ok = ok && regular(x[j]);
-                        if (ok) {
-#pragma unroll
-                            for (int j = 0; j < 4; ++j) split_pair_fast<Cf::PA>(x[2 * j], x[2 * j + 1], q[j]);
-                        } else {
-#pragma unroll
-                            for (int j = 0; j < 4; ++j) split_pair<Cf::PA>(x[2 * j], x[2 * j + 1], q[j]);
-                        }
-#pragma unroll
-                        for (int pc = 0; pc < Cf::PA; ++pc)
-                            sts_u32x4(pa + (uint32_t)(pc * Cf::A_PIECE) + (((uint32_t)hh ^ swz) << 4), q[0][pc], q[1][pc],
-                                      q[2][pc], q[3][pc]);
-                    }
-                } else {
-                    const uint32_t fb = fbase + (uint32_t)kF32Tile + (uint32_t)t * (kBK * 4);
-                    const uint32_t pb = sB_s + (uint32_t)(ps * Cf::B_STAGE) + (uint32_t)t * kRowBytes;
-#pragma unroll
-                    for (int hh = 0; hh < 4; ++hh) {
-                        float x[8];
-#pragma unroll
-                        for (int c2 = 0; c2 < 2; ++c2) {
-                            const uint32_t c = (uint32_t)(hh * 2 + c2);
-                            const float4 v = lds_f32x4(fb + ((c ^ (uint32_t)(t & 7)) << 4));
-                            x[4 * c2] = v.x; x[4 * c2 + 1] = v.y; x[4 * c2 + 2] = v.z; x[4 * c2 + 3] = v.w;
-                        }
-                        uint32_t q[4][3];
-                        bool ok = true;
-#pragma unroll
-                        for (int j = 0; j < 8; ++j) ok = ok && regular(x[j]);
-                        if (ok) {
-#pragma unroll
-                            for (int j = 0; j < 4; ++j) split_pair_fast<Cf::PB>(x[2 * j], x[2 * j + 1], q[j]);
-                        } else {
-#pragma unroll
-                            for (int j = 0; j < 4; ++j) split_pair<Cf::PB>(x[2 * j], x[2 * j + 1], q[j]);
-                        }
-#pragma unroll
-                        for (int pc = 0; pc < Cf::PB; ++pc)
-                            sts_u32x4(pb + (uint32_t)(pc * Cf::B_PIECE) + (((uint32_t)hh ^ swz) << 4), q[0][pc], q[1][pc],
-                                      q[2][pc], q[3][pc]);
-                    }
-                }
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // visible to the tensor core
-                __syncwarp();
-                if (lane == 0) {
-                    mbar_arrive(&f32_empty[fs]);
-                    if (rank == 0) mbar_arrive(&full[ps]);
-                    else mbar_arrive_release_cluster(&full[ps], pair * CG);
-                }
-                if (++fs == NF) { fs = 0; fph ^= 1u; }
-                if (++ps == NST) { ps = 0; pph ^= 1u; }
-            }
-        }
     }
 
     tc_fence_before();
@@ -891,18 +621,6 @@ __global__ void __launch_bounds__((FU || FA) ? kThreadsFused : (SP ? kThreadsSp 
     if (warp == 2) {
         tc_fence_after();
         tmem_dealloc<CG>(tmem_base, kTmemCols);
-    }
-    if constexpr (SP) {
-        // the last CTA to get here resets the slab counters for the next launch (every CTA's
-        // producer has passed its last wait and every split warp its last increment)
-        if (threadIdx.x == 0) {
-            __threadfence();
-            if (atomicAdd(p.done_ctr, 1u) == gridDim.x - 1) {
-                for (int s2 = 0; s2 < p.nslab; ++s2) p.slab_ctr[s2] = 0u;
-                *p.done_ctr = 0u;
-                __threadfence();
-            }
-        }
     }
 }
 
@@ -913,28 +631,24 @@ int make_piece_map(CUtensorMap *map, const uint16_t *base, int k, int rows, int6
                    int box_rows, int box_p = 0);
 int make_f32_map(CUtensorMap *map, const float *base, int rows, int cols, int64_t ld, int box_rows, int box_cols,
                  CUtensorMapSwizzle swz);
-int sk_workspace(size_t ws_floats, size_t nflags, float **ws, unsigned int **flags, unsigned int *epoch);
-// split-ahead slab counters (nslab + 1 words, zero between launches; one stream at a time)
-int sp_counters(int nslab, unsigned int **ctr);
+// stream-K fix-up buffers of stream st (per-stream resources, capi.cu): ws_floats partial
+// accumulators and nflags ready flags compared against the returned per-launch epoch
+int sk_workspace(cudaStream_t st, size_t ws_floats, size_t nflags, float **ws, unsigned int **flags,
+                 unsigned int *epoch);
 
-template <int CG, int V, int BN, int S, int MC, bool SA = false, bool FU = false, bool GD = false, bool SP = false,
-          bool FA = false>
+template <int CG, int V, int BN, int S, int MC, bool SA = false, bool GD = false, bool FA = false>
 int launch_t(const GemmPlan &pl, cudaStream_t st) {
     using Cf = Cfg<CG, V, BN>;
     constexpr int CL = CG * MC;
-    constexpr int THREADS = (FU || FA) ? kThreadsFused : (SP ? kThreadsSp : kThreads);
-    constexpr int SMEM = FU ? CfgF<V>::SMEM : (FA ? CfgFA<V>::SMEM : Cf::SMEM);
-    auto kern = gemm_split_kernel<CG, V, BN, S, MC, SA, FU, GD, SP, FA>;
+    constexpr int THREADS = FA ? kThreadsFused : kThreads;
+    constexpr int SMEM = FA ? CfgFA<V>::SMEM : Cf::SMEM;
+    auto kern = gemm_split_kernel<CG, V, BN, S, MC, SA, GD, FA>;
     CUtensorMap tmA, tmB;
     int rc;
     if constexpr (FA) {
         rc = make_f32_map(&tmA, pl.Af, pl.m, pl.k, pl.lda, kBM, kBK, CU_TENSOR_MAP_SWIZZLE_NONE);
         if (rc) return rc;
         rc = make_piece_map(&tmB, pl.Bp, pl.k, pl.n, pl.ldbp, pl.b_plane, Cf::PB, Cf::BN_LOCAL);
-    } else if constexpr (FU) {
-        rc = make_f32_map(&tmA, pl.Af, pl.m, pl.k, pl.lda, kBM, kBK, CU_TENSOR_MAP_SWIZZLE_NONE);
-        if (rc) return rc;
-        rc = make_f32_map(&tmB, pl.Bf, pl.k, pl.n, pl.ldb, kBK, Cf::BN_LOCAL, CU_TENSOR_MAP_SWIZZLE_128B);
     } else {
         rc = make_piece_map(&tmA, pl.Ap, pl.k, pl.m, pl.ldap, pl.a_plane, Cf::PA, kBM);
         if (rc) return rc;
@@ -996,24 +710,12 @@ int launch_t(const GemmPlan &pl, cudaStream_t st) {
     // TFLOPS, DRAM reads ~50 vs ~85 GB per launch -- power-limited, so traffic costs clock)
     kp.lazy_full = g_lazy_full;
     kp.group_m = pl.group_m > 0 ? pl.group_m : (MC == 2 ? 2 : (kp.tiles_n <= 16 ? 1 : kGroupM));
-    kp.Af = pl.Af; kp.Bf = pl.Bf; kp.lda = pl.lda; kp.ldb = pl.ldb;
-    kp.Apw = const_cast<uint16_t *>(pl.Ap); kp.Bpw = const_cast<uint16_t *>(pl.Bp);
-    kp.ldap = pl.ldap; kp.a_plane = pl.a_plane; kp.ldbp = pl.ldbp; kp.b_plane = pl.b_plane;
-    kp.slab_ctr = nullptr; kp.done_ctr = nullptr;
-    kp.nslab = (pl.k + kSlab - 1) / kSlab;
-    if constexpr (SP) {
-        unsigned int *ctr = nullptr;
-        const int rc3 = sp_counters(kp.nslab, &ctr);
-        if (rc3) return rc3;
-        kp.slab_ctr = ctr;
-        kp.done_ctr = ctr + kp.nslab;
-    }
     const int ncl = grid / CL;
     if (pl.stream_k != 0 && !(pl.flags & (BF16X_ACC_IN | BF16X_ACC_OUT)) && tiles > ncl && tiles % ncl != 0) {
         const int full = tiles / ncl;
         kp.dp_tiles = (full - 1) * ncl;
         kp.sk_tiles = tiles - kp.dp_tiles;
-        int rc2 = sk_workspace((size_t)kp.sk_tiles * CL * BN * kBM * (GD ? 2 : 1), (size_t)kp.sk_tiles * CL, &kp.sk_ws, &kp.sk_flags,
+        int rc2 = sk_workspace(st, (size_t)kp.sk_tiles * CL * BN * kBM * (GD ? 2 : 1), (size_t)kp.sk_tiles * CL, &kp.sk_ws, &kp.sk_flags,
                                &kp.epoch);
         if (rc2) return rc2;
     }
@@ -1075,14 +777,12 @@ int launch_s(const GemmPlan &pl, cudaStream_t st) {
     // and split-ahead x3 kernels follow the hook, so they stay bit-identical to the pre-pass path.
     if constexpr (CG == 2 && V == 3)
         if (s == 4 && !pl.fp64 && !pl.split_acc) {
-            if (pl.fused_a) return launch_t<2, V, 256, 4, 1, false, false, false, false, true>(pl, st);
-            if (pl.split_ahead) return launch_t<2, V, 256, 4, 1, false, false, false, true>(pl, st);
             if (pl.multicast == 2 || (pl.multicast == 0 && (int64_t)pl.m * pl.n >= 12288LL * 12288LL))
                 return launch_t<2, V, 256, 4, 2>(pl, st);
             return launch_t<2, V, 256, 4, 1>(pl, st);
         }
     if constexpr (CG == 2 && V == 1)
-        if (s == 4 && !pl.fp64 && !pl.split_ahead && !pl.split_acc && !pl.fused_a) return launch_t<2, V, 256, 4, 1>(pl, st);
+        if (s == 4 && !pl.fp64 && !pl.split_acc && !pl.fused_a) return launch_t<2, V, 256, 4, 1>(pl, st);
     // Short k (<= 128): the whole product is one or two intervals, so the tensor core's
     // truncating accumulation dominates the error; 32-k intervals halve it (measured wide
     // exponents, k = 64: max ratio to the oracle 2.07 -> 1.66) at no cost that matters.
@@ -1096,21 +796,16 @@ int launch_s(const GemmPlan &pl, cudaStream_t st) {
             // r06 tools/gd_probe.py); the longer-product variants keep 64-k intervals (x6d -4 %,
             // x9d -15 % with 128-k ones: their 6-stage ring then stalls between intervals)
             if (pl.stages_per_interval == 4 || (V <= 3 && pl.stages_per_interval == 0))
-                return launch_t<2, V, 128, 4, 1, true, false, true>(pl, st);
-            return launch_t<2, V, 128, 2, 1, true, false, true>(pl, st);
+                return launch_t<2, V, 128, 4, 1, true, true>(pl, st);
+            return launch_t<2, V, 128, 2, 1, true, true>(pl, st);
         }
-    // fused A: the caller (gemm_core) chose it with fused_a_ok() and split only B
+    // fused A (bf16x9 only, where it measured faster): the caller (gemm_core) chose it with
+    // fused_a_ok() and split only B
     if (pl.fused_a) {
-        if (CG == 2) return s == 2 ? launch_t<2, V, 256, 2, 1, false, false, false, false, true>(pl, st)
-                                   : launch_t<2, V, 256, 1, 1, false, false, false, false, true>(pl, st);
+        if constexpr (CG == 2 && V == 9)
+            return s == 2 ? launch_t<2, V, 256, 2, 1, false, false, true>(pl, st)
+                          : launch_t<2, V, 256, 1, 1, false, false, true>(pl, st);
         set_error_msg("fused-A plan not launchable");
-        return BF16X_ERR_CUDA;
-    }
-    // split-ahead: the caller (gemm_core) chose it with split_ahead_ok(), which mirrors the
-    // conditions below; the pieces are written by this launch only
-    if (pl.split_ahead) {
-        if (CG == 2 && s == 2) return launch_t<2, V, 256, 2, 1, false, false, false, true>(pl, st);
-        set_error_msg("split-ahead plan not launchable");
         return BF16X_ERR_CUDA;
     }
     if constexpr (CG == 2) {
@@ -1131,13 +826,12 @@ int launch_s(const GemmPlan &pl, cudaStream_t st) {
 }
 
 // Per-variant entry points, one translation unit each (gemm_v<V>.cu):
-//   kind 1 / 2: pre-split pieces, CTA group 1 / 2;  kind 3: fused split (2-CTA, N 256, 32-k intervals)
+//   kind 1 / 2: pre-split pieces (or fused A), CTA group 1 / 2
 #define BF16X_DEFINE_VARIANT(V)                                                        \
     int launch_variant_##V(const GemmPlan &pl, cudaStream_t st, int kind) {            \
         switch (kind) {                                                                \
         case 1: return launch_s<1, V>(pl, st);                                         \
         case 2: return launch_s<2, V>(pl, st);                                         \
-        case 3: return launch_t<2, V, 256, 1, 1, false, true>(pl, st);                 \
         }                                                                              \
         return -12;                                                                    \
     }

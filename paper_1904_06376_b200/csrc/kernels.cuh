@@ -38,28 +38,20 @@ struct GemmPlan {
     int scaled;          // 1 = N2 scaled pieces (R29): band transitions scale the accumulator by 2^-8
     int fp64;            // 1 = FP64 collection of the bins ("d" variants, R30; implies split_acc)
     int group_m;         // tile raster group height in m-tiles (0 = default 8)
-    int split_ahead;     // 1 = the GEMM splits A and B itself (split-ahead warps), Ap/Bp = workspace
     int fused_a;         // 1 = A converted inside the GEMM from FP32 tiles (Af), B pre-split (Bp)
-    // fused split (Ap == Bp == nullptr): the FP32 operands, converted to pieces inside the GEMM
+    // fused A: the FP32 A operand, converted to pieces inside the GEMM (B is pre-split)
     const float *Af, *Bf;   // A (m x k, lda), B (k x n, ldb), column-major, 16-byte aligned
     int64_t lda, ldb;
 };
 
 int launch_gemm_pieces(const GemmPlan &p, cudaStream_t st);
-// Whether launch_gemm_pieces would take the split-ahead kernel for this plan (2-CTA pairs,
-// 64-k intervals, tile N 256, no multicast / split accumulators / FP64 collection).
-bool split_ahead_ok(const GemmPlan &p);
 // Whether the fused-A kernel can run this plan (2-CTA pairs, tile N 256, no multicast / split
 // accumulators / FP64 collection / scaled pieces, A 16-byte aligned with lda % 4 == 0).
 bool fused_a_ok(const GemmPlan &p);
-// The fused-split GEMM for this plan's FP32 operands: BF16X_SUCCESS, or -1 if the plan does not
-// qualify (then the caller splits in a pre-pass and calls launch_gemm_pieces).
-int launch_gemm_fused(const GemmPlan &p, cudaStream_t st);
 int launch_scale(int m, int n, float beta, float *C, int ldc, cudaStream_t st);
 int pieces_a(int variant);   // BF16 pieces of A / B for a variant (x5: 2 / 3)
 int pieces_b(int variant);
 int num_sms();
 int default_cta_group();
-void release_gemm_workspace();
 
 }  // namespace bf16x

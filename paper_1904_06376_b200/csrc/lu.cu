@@ -457,15 +457,20 @@ __global__ void __launch_bounds__(kSubThreads) subpanel_kernel(float *LU, int ld
 
 // After sub-panel [s0, s0+w) (rows already interchanged): remaining panel columns [c1, c2)
 // get U = L11^-1 A[s0:s0+w, c1:c2] (L11 unit lower w x w; every block recomputes it with one
-// column per thread held in registers, block 0 stores it) and rows [c1, n) get A -= L21 U,
-// 64 rows per block, 4 x 4 outputs per thread from shared-memory tiles.
+// column per thread held in registers) and rows [c1, n) get A -= L21 U, 64 rows per block,
+// 4 x 4 outputs per thread from shared-memory tiles.  U overwrites its source rows, which every
+// block reads first: the store is made by the LAST block to finish its reads (arrival counter
+// `ctr`, reset by that block for the next launch), so no block can read U instead of A whatever
+// the order or residency of the blocks.
 constexpr int kUpdRows = 64;
 static size_t panel_update_smem(int nc) {
     const int ncp = (nc + 3) & ~3;
     return ((size_t)kSubW * ncp + (size_t)kSubW * (kSubW + 1) + (size_t)kSubW * kUpdRows) * sizeof(float);
 }
-__global__ void __launch_bounds__(256) panel_update_kernel(float *LU, int ld, int n, int s0, int w, int c1, int c2) {
+__global__ void __launch_bounds__(256) panel_update_kernel(float *LU, int ld, int n, int s0, int w, int c1, int c2,
+                                                           unsigned int *ctr) {
     extern __shared__ __align__(16) float su[];
+    __shared__ int store_u;
     const int nc = c2 - c1, ncp = (nc + 3) & ~3;
     float *sU = su;                                   // [kSubW][ncp]      row r of the w x nc block
     float *sL11 = sU + (size_t)kSubW * ncp;           // [kSubW][kSubW+1]  L11[r][i]
@@ -504,6 +509,12 @@ __global__ void __launch_bounds__(256) panel_update_kernel(float *LU, int ld, in
     };
     load_old(4 * tx);
     async_wait_all();
+    __syncthreads();                                   // this block's reads of the U rows are done
+    if (tid == 0) {
+        const bool last = atomicAdd(ctr, 1u) == gridDim.x - 1;
+        if (last) *ctr = 0u;                           // every block has arrived: ready for the next launch
+        store_u = last;
+    }
     __syncthreads();
     for (int c = tid; c < nc; c += blockDim.x) {      // forward substitution, column in registers
         float x[kSubW];
@@ -515,7 +526,7 @@ __global__ void __launch_bounds__(256) panel_update_kernel(float *LU, int ld, in
             for (int r = i + 1; r < kSubW; ++r) x[r] = x[r] - sL11[r * (kSubW + 1) + i] * x[i];
 #pragma unroll
         for (int r = 0; r < kSubW; ++r) sU[r * ncp + c] = x[r];
-        if (blockIdx.x == 0)
+        if (store_u)
 #pragma unroll
             for (int r = 0; r < kSubW; ++r)
                 if (r < w) LU[(int64_t)(c1 + c) * ld + s0 + r] = x[r];
@@ -987,6 +998,7 @@ struct LuWork {
     int *perm = nullptr, *npairs = nullptr;
     int2 *pairs = nullptr;
     unsigned int *bar = nullptr;  // [grid] arrive flags + [1] release
+    unsigned int *pu_ctr = nullptr;   // panel_update_kernel arrival counter (zero between launches)
     GridBar gb;
     unsigned int epoch = 1;
     double *r = nullptr, *d = nullptr, *part = nullptr, *scal = nullptr;
@@ -1056,7 +1068,7 @@ static void lu_free(LuWork &w) {
     if (w.own_LU) cudaFree(w.LU);
     if (w.own_ipiv) cudaFree(w.ipiv);
     cudaFree(w.perm); cudaFree(w.info); cudaFree(w.npairs); cudaFree(w.pairs);
-    cudaFree(w.bar); cudaFree(w.r); cudaFree(w.d); cudaFree(w.part); cudaFree(w.scal);
+    cudaFree(w.bar); cudaFree(w.pu_ctr); cudaFree(w.r); cudaFree(w.d); cudaFree(w.part); cudaFree(w.scal);
     cudaFree(w.tinv); cudaFree(w.tflags);
     for (void *p : w.extra) cudaFree(p);
     w = LuWork{};
@@ -1119,6 +1131,7 @@ static int lu_prepare(LuWork &w, int n, int nb, float *LU, int ld, int *ipiv, bo
     alloc((void **)&w.npairs, sizeof(int) * (size_t)nmap);            // one gather map per sub-panel
     alloc((void **)&w.pairs, sizeof(int2) * (size_t)nmap * 64);
     alloc((void **)&w.bar, sizeof(unsigned int) * ((size_t)w.coop_grid + 1));
+    alloc((void **)&w.pu_ctr, sizeof(unsigned int));
     alloc((void **)&w.r, sizeof(double) * n);
     alloc((void **)&w.d, sizeof(double) * n);
     alloc((void **)&w.part, sizeof(double) * (size_t)n * nchunk);
@@ -1134,6 +1147,7 @@ static int lu_prepare(LuWork &w, int n, int nb, float *LU, int ld, int *ipiv, bo
     w.gb.release = w.bar + w.coop_grid;
     cudaMemsetAsync(w.bar, 0, sizeof(unsigned int) * ((size_t)w.coop_grid + 1), st);
     cudaMemsetAsync(w.info, 0, sizeof(int), st);
+    cudaMemsetAsync(w.pu_ctr, 0, sizeof(unsigned int), st);
     return BF16X_SUCCESS;
 }
 
@@ -1185,7 +1199,8 @@ static int lu_factor(LuWork &w, int variant, cudaStream_t st) {
             const int c1 = s0 + sw;
             if (c1 < j1) {
                 const size_t smem = panel_update_smem(j1 - c1);
-                panel_update_kernel<<<(n - c1 + kUpdRows - 1) / kUpdRows, 256, smem, st>>>(w.LU, ld, n, s0, sw, c1, j1);
+                panel_update_kernel<<<(n - c1 + kUpdRows - 1) / kUpdRows, 256, smem, st>>>(w.LU, ld, n, s0, sw, c1, j1,
+                                                                                          w.pu_ctr);
                 count_launch();
             }
             rc = check_launch("panel");
@@ -1313,9 +1328,30 @@ extern "C" int bf16x_getrf(int n, float *A, int lda, int *ipiv, int variant, int
     return rc;
 }
 
+// ||b||_inf of a device vector (the relative-residual test of a caller tolerance, R14)
+static double host_inf_norm(const double *b, int n, cudaStream_t st) {
+    std::vector<double> h((size_t)n);
+    if (cudaMemcpyAsync(h.data(), b, sizeof(double) * (size_t)n, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+        cudaStreamSynchronize(st) != cudaSuccess) {
+        cudaGetLastError();
+        return -1.0;
+    }
+    double m = 0.0;
+    for (double v : h) m = std::max(m, std::fabs(v));
+    return m;
+}
+
+// the stopping threshold on ||r||_inf: the caller's relative tolerance tol * ||b||_inf (tol > 0:
+// the paper's "residual tolerance of cond(A)*eps", with tol = cond(A) * 2^-53), else
+// LAPACK dsgesv's sqrt(n) ||x||_inf ||A||_inf 2^-53 (R14)
+static double ir_threshold(double tol, double bnrm, int n, double xn, double anrm) {
+    return tol > 0.0 ? tol * bnrm : std::sqrt((double)n) * xn * anrm * std::ldexp(1.0, -53);
+}
+
 extern "C" int bf16x_gesv_ir(int n, const float *A, int lda, const double *b, double *x, int variant, int nb,
-                             int max_iter, double *residual_history, bf16x_ir_report *report) {
-    if (!report) return -10;
+                             double tol, int max_iter, double *residual_history, bf16x_ir_report *report) {
+    if (!report) return -11;
+    if (tol != tol) return -8;
     *report = bf16x_ir_report{};
     int rc = check_common(n, lda, variant);
     if (rc) return rc;
@@ -1347,8 +1383,8 @@ extern "C" int bf16x_gesv_ir(int n, const float *A, int lda, const double *b, do
     // ---------------- refinement ----------------
     if (rc == BF16X_SUCCESS) {
         const double anrm = inf_norm_A(w, A, lda, n, st);
+        const double bnrm = tol > 0.0 ? host_inf_norm(b, n, st) : 0.0;
         rc = solve_with_factors(w, n, b, x, w.coop_grid, st);
-        const double eps = std::ldexp(1.0, -53);
         std::vector<double> hist;
         int it = 0;
         bool converged = false;
@@ -1357,7 +1393,7 @@ extern "C" int bf16x_gesv_ir(int n, const float *A, int lda, const double *b, do
             rc = residual_norms(w, A, lda, n, x, b, st, &rn, &xn);
             if (rc) break;
             hist.push_back(rn);
-            report->tol = std::sqrt((double)n) * xn * anrm * eps;
+            report->tol = ir_threshold(tol, bnrm, n, xn, anrm);
             if (rn <= report->tol) {
                 converged = true;
                 break;
@@ -1390,13 +1426,14 @@ extern "C" int bf16x_gesv_ir(int n, const float *A, int lda, const double *b, do
 }
 
 extern "C" int bf16x_gesv_gmres_ir(int n, const float *A, int lda, const double *b, double *x, int variant, int nb,
-                                   int restart, double inner_tol, int max_iter, double *residual_history,
+                                   int restart, double inner_tol, double tol, int max_iter, double *residual_history,
                                    bf16x_ir_report *report) {
-    if (!report) return -12;
+    if (!report) return -13;
     *report = bf16x_ir_report{};
     int rc = check_common(n, lda, variant);
     if (rc) return rc;
     if (inner_tol < 0.0 || inner_tol != inner_tol) return -9;
+    if (tol != tol) return -10;
     rc = arch_ok();
     if (rc) return rc;
     if (n == 0) {
@@ -1455,7 +1492,7 @@ extern "C" int bf16x_gesv_gmres_ir(int n, const float *A, int lda, const double 
     // ---------------- GMRES-IR (reading R25) ----------------
     if (rc == BF16X_SUCCESS) {
         const double anrm = inf_norm_A(w, A, lda, n, st);
-        const double eps = std::ldexp(1.0, -53);
+        const double bnrm = tol > 0.0 ? host_inf_norm(b, n, st) : 0.0;
         cudaMemsetAsync(x, 0, sizeof(double) * n, st);
         std::vector<double> hist, H((size_t)(m + 1) * m), cs(m), sn(m), g(m + 1), y(m), hc(m + 2);
         int it = 0, inner = 0;
@@ -1465,7 +1502,7 @@ extern "C" int bf16x_gesv_gmres_ir(int n, const float *A, int lda, const double 
             rc = residual_norms(w, A, lda, n, x, b, st, &rn, &xn);
             if (rc) break;
             hist.push_back(rn);
-            report->tol = std::sqrt((double)n) * xn * anrm * eps;
+            report->tol = ir_threshold(tol, bnrm, n, xn, anrm);
             if (rn <= report->tol) {
                 converged = true;
                 break;

@@ -36,7 +36,7 @@ def test_gemm_argument_errors():
     assert f(4, 4, 4, 1.0, None, 4, None, 4, 0.0, None, 3, 6) == -11
     assert f(4, 4, 4, 1.0, None, 4, None, 4, 0.0, None, 4, 4) == -12
     ex = L.bf16x_gemm_ex
-    assert ex(4, 4, 4, 1.0, None, 4, None, 4, 0.0, None, 4, 6, 32, None, 0, 0, None, 0, 0, None, None, 0, None) == -13
+    assert ex(4, 4, 4, 1.0, None, 4, None, 4, 0.0, None, 4, 6, 64, None, 0, 0, None, 0, 0, None, None, 0, None) == -13
     # FP64 combine (R30) excludes the accumulator carry and the one-product variant
     assert ex(4, 4, 4, 1.0, None, 4, None, 4, 0.0, None, 4, 6, 9, None, 0, 0, None, 0, 0, 16, None, 0, None) == -13
     assert ex(4, 4, 4, 1.0, None, 4, None, 4, 0.0, None, 4, 1, 8, None, 0, 0, None, 0, 0, None, None, 0, None) == -13
@@ -83,12 +83,16 @@ def test_solver_argument_errors():
     L = bx.lib()
     rep = bx.IRReport()
     g = L.bf16x_gesv_gmres_ir
-    assert g(-1, None, 1, None, None, 3, 0, 0, 0.0, 0, None, ctypes.byref(rep)) == -1
-    assert g(4, None, 3, None, None, 3, 0, 0, 0.0, 0, None, ctypes.byref(rep)) == -3
-    assert g(4, None, 4, None, None, 7, 0, 0, 0.0, 0, None, ctypes.byref(rep)) == -6
-    assert g(4, None, 4, None, None, 3, 0, 0, -1.0, 0, None, ctypes.byref(rep)) == -9
-    assert g(4, None, 4, None, None, 3, 0, 0, 0.0, 0, None, None) == -12
-    assert L.bf16x_gesv_ir(4, None, 3, None, None, 3, 0, 0, None, ctypes.byref(rep)) == -3
+    assert g(-1, None, 1, None, None, 3, 0, 0, 0.0, 0.0, 0, None, ctypes.byref(rep)) == -1
+    assert g(4, None, 3, None, None, 3, 0, 0, 0.0, 0.0, 0, None, ctypes.byref(rep)) == -3
+    assert g(4, None, 4, None, None, 7, 0, 0, 0.0, 0.0, 0, None, ctypes.byref(rep)) == -6
+    assert g(4, None, 4, None, None, 3, 0, 0, -1.0, 0.0, 0, None, ctypes.byref(rep)) == -9
+    assert g(4, None, 4, None, None, 3, 0, 0, 0.0, float("nan"), 0, None, ctypes.byref(rep)) == -10
+    assert g(4, None, 4, None, None, 3, 0, 0, 0.0, 0.0, 0, None, None) == -13
+    ir = L.bf16x_gesv_ir
+    assert ir(4, None, 3, None, None, 3, 0, 0.0, 0, None, ctypes.byref(rep)) == -3
+    assert ir(4, None, 4, None, None, 3, 0, float("nan"), 0, None, ctypes.byref(rep)) == -8
+    assert ir(4, None, 4, None, None, 3, 0, 0.0, 0, None, None) == -11
     info = ctypes.c_int(0)
     f = L.bf16x_getrf
     assert f(-1, None, 1, None, 3, 0, ctypes.byref(info)) == -1
@@ -99,4 +103,4 @@ def test_solver_argument_errors():
     import torch
     if not torch.cuda.is_available():
         assert f(4, 16, 4, 32, 3, 0, ctypes.byref(info)) == bx.ERR_ARCH
-        assert g(4, 16, 4, 32, 48, 3, 0, 0, 0.0, 0, None, ctypes.byref(rep)) == bx.ERR_ARCH
+        assert g(4, 16, 4, 32, 48, 3, 0, 0, 0.0, 0.0, 0, None, ctypes.byref(rep)) == bx.ERR_ARCH

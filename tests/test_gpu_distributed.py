@@ -1,8 +1,9 @@
 """The column-sharded GEMM (paper_1904_06376_b200.distributed) on the GPU with the
-NCCL backend in a world of one process: the k-chunked A path (FP32 promoted accumulator
-carried between chunks through bf16x_gemm_ex ACC_IN / ACC_OUT) and the sub-block loop run on
-the CUDA library exactly as on every rank of a multi-GPU run, and must reproduce the one-call
-GEMM bit for bit.  (The collectives themselves are exercised with gloo, world size 2, in
+NCCL backend in a world of one process: A split once into the piece buffer chunk by chunk, the
+k-chunked first sub-block (FP32 promoted accumulator carried between chunks through
+bf16x_gemm_ex ACC_IN / ACC_OUT) and the sub-block loop on the pre-split A run on the CUDA
+library exactly as on every rank of a multi-GPU run, and must reproduce the one-call GEMM
+(BF16X_NO_STREAM_K) bit for bit.  (The collectives themselves are exercised with gloo, world size 2, in
 tests/test_distributed.py; more GPUs are not available to the test runs.)"""
 import socket
 
@@ -37,13 +38,14 @@ def nccl_world1():
 
 @pytest.mark.parametrize("variant", [3, 6, 9])
 @pytest.mark.parametrize("m,n,k,sub_blocks,k_chunks", [(512, 768, 1024, 1, 4), (1000, 1300, 700, 3, 3),
-                                                        (2048, 2048, 2048, 4, 8)])
+                                                        (2048, 2048, 2048, 4, 8), (4096, 4608, 1000, 2, 4),
+                                                        (300, 400, 300, 2, 4)])
 def test_colsharded_world1_bit_identical(nccl_world1, orc, m, n, k, sub_blocks, k_chunks, variant):
     A = synthetic.uniform(m, k, seed=m + k)
     B = synthetic.uniform(k, n, seed=n + k)
     Ad = torch.from_numpy(np.asfortranarray(A)).cuda()
     Bd = torch.from_numpy(np.asfortranarray(B)).cuda()
-    want = bx.gemm(Ad, Bd, variant=variant).cpu().numpy()
+    want = bx.gemm(Ad, Bd, variant=variant, no_stream_k=True).cpu().numpy()
     cols = local_columns(n, 1, 0, sub_blocks)
     assert cols == list(range(n))
     C = torch.full((n, m), float("nan"), dtype=torch.float32, device="cuda").t()   # column-major
@@ -56,3 +58,32 @@ def test_colsharded_world1_bit_identical(nccl_world1, orc, m, n, k, sub_blocks, 
     C64 = orc.dgemm(A, B, cols=sc)
     eo = orc.normwise_error(orc.gemm(A, B, variant=variant, cols=sc), C64, A, B[:, sc])
     assert orc.normwise_error(got[:, sc], C64, A, B[:, sc]) <= 2.0 * eo
+
+
+@pytest.mark.parametrize("P,sub_blocks", [(2, 2), (4, 2), (8, 2)])
+def test_rank_shards_equal_one_gpu_columns(orc, P, sub_blocks):
+    """Each rank's share of a P-GPU run (its block-cyclic columns, A split once into pieces,
+    B_local's sub-blocks) computed here one rank after another on one GPU (no collectives):
+    every shard must equal the same columns of the one-GPU call bit for bit, so the gathered C
+    of a real P-GPU run is the one-GPU C.  4096 x 4608 x 1000 has 288 tiles: the one-GPU call
+    would use stream-K without BF16X_NO_STREAM_K."""
+    from paper_1904_06376_b200.distributed import _PieceGemm, block_owner_layout
+    m, n, k = 4096, 4608, 1000
+    A = synthetic.uniform(m, k, seed=3)
+    B = synthetic.uniform(k, n, seed=4)
+    Ad = torch.from_numpy(np.asfortranarray(A)).cuda()
+    Bd = torch.from_numpy(np.asfortranarray(B)).cuda()
+    want = bx.gemm(Ad, Bd, variant=6, no_stream_k=True).cpu().numpy()
+    pg = _PieceGemm(Ad, 6)
+    pg.split_chunk(Ad, 0, k)
+    for q in range(P):
+        cols = local_columns(n, P, q, sub_blocks)
+        Bq = torch.from_numpy(np.asfortranarray(B[:, cols])).cuda()
+        Cq = torch.empty_strided((m, len(cols)), (1, m), dtype=torch.float32, device="cuda")
+        off = 0
+        for owners in block_owner_layout(n, P, sub_blocks):
+            w = owners[q][1]
+            pg.gemm(0, k, Bq[:, off:off + w], Cq[:, off:off + w], 0)
+            off += w
+        torch.cuda.synchronize()
+        assert np.array_equal(Cq.cpu().numpy().view(np.uint32), want[:, cols].view(np.uint32)), q

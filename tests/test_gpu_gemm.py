@@ -354,89 +354,6 @@ def test_underflow_range(orc, e):
 
 
 @pytest.fixture
-def fused_on():
-    L = bx.lib()
-    L.bf16x_fused_split(1)
-    yield L
-    L.bf16x_fused_split(0)
-    L.bf16x_tune(0, 0, 0)
-
-
-@pytest.mark.parametrize("variant", [3, 5, 6, 7, 9])
-@pytest.mark.parametrize("shape", [(256, 256, 64), (300, 700, 333), (1024, 2048, 1000), (130, 260, 37)])
-def test_fused_split_matches_prepass(orc, fused_on, shape, variant):
-    """The opt-in fused split (FP32 tiles converted inside the GEMM by transform warps) places
-    exactly the pre-pass's pieces in shared memory: with the same 32-k promotion interval the
-    two paths are bit-identical, and both meet the oracle bar."""
-    m, n, k = shape
-    A = synthetic.uniform(m, k, seed=m + k)
-    B = synthetic.uniform(k, n, seed=n + 3 * k)
-    L = fused_on
-    L.bf16x_tune(2, 0, 1)
-    L.bf16x_fused_split(1)
-    Gf = _gpu(A, B, variant=variant)
-    L.bf16x_fused_split(0)
-    Gp = _gpu(A, B, variant=variant)
-    assert np.array_equal(Gf, Gp)
-    C64 = orc.dgemm(A, B)
-    eo = orc.normwise_error(orc.gemm(A, B, variant=variant), C64, A, B)
-    assert orc.normwise_error(Gf, C64, A, B) <= RATIO * eo
-
-
-def test_fused_split_nonfinite_and_ragged(orc, fused_on):
-    """Non-finite and overflow-band inputs take the transform's exact slow path (R3, R4); the
-    NaN / Inf masks match the oracle's."""
-    A = synthetic.wide(200, 96, seed=41)
-    B = synthetic.wide(96, 150, seed=42)
-    A[5, 3] = np.nan
-    A[7, 50] = np.inf
-    B[10, 20] = -np.inf
-    fused_on.bf16x_fused_split(1)
-    G = _gpu(A, B, variant=6)
-    O = orc.gemm(A, B, variant=6)
-    assert np.array_equal(np.isnan(G), np.isnan(O))
-    assert np.array_equal(np.isinf(G), np.isinf(O))
-    # overflow band (b0 saturates, R3) and the section II-F / subnormal values: A * I equals the
-    # oracle's (which reproduces A except where the split itself loses bits, P:340-350)
-    Aw = synthetic.uniform(64, 48, seed=43)
-    Aw[1, 2] = np.float32(3.4e38)
-    Aw[3, 4] = np.float32(-3.39e38)
-    Aw[5, 6] = np.float32(1.1938613e-38)
-    Aw[7, 8] = np.float32(2.0 ** -140)
-    I = np.eye(48, dtype=np.float32)
-    assert np.array_equal(_gpu(Aw, I, variant=6), orc.gemm(Aw, I, variant=6))
-
-
-@pytest.fixture
-def split_ahead_on():
-    L = bx.lib()
-    L.bf16x_split_ahead(1)
-    yield L
-    L.bf16x_split_ahead(0)
-
-
-@pytest.mark.parametrize("scaled", [False, True])
-@pytest.mark.parametrize("variant", [1, 3, 5, 6, 7, 8, 9])
-@pytest.mark.parametrize("shape", [(256, 256, 200), (300, 700, 333), (1024, 2048, 1000), (130, 260, 1037), (4096, 1024, 2048)])
-def test_split_ahead_matches_prepass(orc, split_ahead_on, shape, variant, scaled):
-    """The opt-in split-ahead GEMM (the split done by 4 extra warps per CTA, slab by slab,
-    producers waiting on per-slab global counters) writes the pre-pass's pieces and so returns
-    the pre-pass result bit for bit, ragged k and rows included; back-to-back launches reuse the
-    self-resetting counters."""
-    m, n, k = shape
-    A = synthetic.wide(m, k, seed=m + k, E=20)
-    B = synthetic.wide(k, n, seed=n + k, E=20)
-    Ad = torch.from_numpy(np.asfortranarray(A)).cuda()
-    Bd = torch.from_numpy(np.asfortranarray(B)).cuda()
-    outs = []
-    for on in (1, 0, 1, 1):
-        split_ahead_on.bf16x_split_ahead(on)
-        outs.append(bx.gemm(Ad, Bd, variant=variant, scaled=scaled).cpu().numpy())
-    for o in outs[1:]:
-        assert np.array_equal(o.view(np.uint32), outs[0].view(np.uint32))
-
-
-@pytest.fixture
 def fused_a_on():
     L = bx.lib()
     L.bf16x_fused_a(1)
@@ -444,13 +361,14 @@ def fused_a_on():
     L.bf16x_fused_a(-1)
 
 
-@pytest.mark.parametrize("variant", [1, 3, 5, 6, 7, 8, 9])
+@pytest.mark.parametrize("variant", [9])
 @pytest.mark.parametrize("shape", [(256, 256, 200), (300, 700, 333), (1024, 2048, 1000), (130, 260, 1037),
                                    (4096, 1024, 2048), (200, 300, 96)])
 def test_fused_a_matches_prepass(orc, fused_a_on, shape, variant):
-    """Fused A (A's FP32 tiles converted by 4 extra warps inside the GEMM, only B split in the
-    pre-pass) places exactly the pre-pass's A pieces in shared memory, so C is bit-identical,
-    ragged rows / k and both promotion intervals (k <= 128 uses 32-k intervals) included."""
+    """Fused A (bf16x9's default: A's FP32 tiles converted by 8 extra warps inside the GEMM,
+    only B split in the pre-pass) places exactly the pre-pass's A pieces in shared memory, so C
+    is bit-identical, ragged rows / k and both promotion intervals (k <= 128 uses 32-k
+    intervals) included."""
     m, n, k = shape
     A = synthetic.wide(m, k, seed=m + 3 * k, E=20)
     B = synthetic.wide(k, n, seed=n + 5 * k, E=20)
@@ -482,7 +400,7 @@ def test_fused_a_nonfinite_and_ld(orc, fused_a_on):
     for on in (1, 0):
         fused_a_on.bf16x_fused_a(on)
         Cd = torch.from_numpy(np.asfortranarray(C0)).cuda()
-        res.append(bx.gemm(Ad, Bd, C=Cd, alpha=0.5, beta=2.0, variant=6).cpu().numpy())
+        res.append(bx.gemm(Ad, Bd, C=Cd, alpha=0.5, beta=2.0, variant=9).cpu().numpy())
     assert np.array_equal(res[0].view(np.uint32), res[1].view(np.uint32))
 
 
@@ -515,9 +433,10 @@ def test_128k_interval_hook(orc, dist, variant, mc):
 @pytest.mark.parametrize("shape", [(333, 517, 256), (1100, 900, 96), (2304, 2304, 256)])
 def test_red_add_epilogue_bit_identical(shape, variant, alpha):
     """C += +-Z through red.global.add.f32 (the LU's trailing update) is bit-identical to the
-    fmaf(alpha, Z, beta * C) epilogue for alpha = +-1, beta = 1 -- including subnormal C values,
-    results that cancel to zero or land in the subnormal range, and stream-K tiles (2304^2 has
-    a partial last wave)."""
+    fmaf(alpha, Z, beta * C) epilogue for alpha = +-1, beta = 1 wherever C and the result are
+    normal FP32 numbers -- including exact cancellation to +0 and stream-K tiles (2304^2 has a
+    partial last wave) -- and flushes results in the subnormal range to zero (the hardware's
+    FP32 reduction is FTZ), which the test pins as the only difference."""
     m, n, k = shape
     A = synthetic.uniform(m, k, seed=m + 13 * k)
     B = synthetic.uniform(k, n, seed=n + 17 * k)
@@ -531,15 +450,76 @@ def test_red_add_epilogue_bit_identical(shape, variant, alpha):
             outs.append(_gpu(A, B, C, alpha=alpha, beta=1.0, variant=variant))
         finally:
             bx.lib().bf16x_red_add(-1)
-    # exact cancellation: C = -(+-Z) read back from the fmaf path, then C + (+-Z) must be +0 / the
-    # same bits in both modes
-    C2 = (-outs[0] + C).astype(np.float32)
-    outs2 = []
+    # exact cancellation and subnormal results: Z = A B from a beta = 0 run; C2 = -alpha Z makes
+    # every result C2 + alpha Z an exact zero (both must give +0).  With A, B scaled by 2^-70 and
+    # 2^-60, Zs ~ 2^-130 is subnormal; C3 = -alpha Zs + d, d = +-k 2^-149, makes the exact result
+    # the subnormal d: rounding must keep it (no flush to zero of inputs or results)
+    Z = _gpu(A, B, None, alpha=1.0, beta=0.0, variant=variant)
+    C2 = (-np.float32(alpha) * Z).astype(np.float32)
+    As = (A * np.float32(2.0 ** -70)).astype(np.float32, order="F")
+    Bs = (B * np.float32(2.0 ** -60)).astype(np.float32, order="F")
+    Zs = _gpu(As, Bs, None, alpha=1.0, beta=0.0, variant=variant)
+    d = (np.arange(m * n).reshape(m, n, order="F") % 7 - 3) * 2.0 ** -149
+    C3 = (-alpha * Zs.astype(np.float64) + d).astype(np.float32)
+    assert np.array_equal(C3.astype(np.float64), -alpha * Zs.astype(np.float64) + d)   # exact
+    outs2, outs3 = [], []
     for mode in (0, 1):
         bx.lib().bf16x_red_add(mode)
         try:
             outs2.append(_gpu(A, B, C2, alpha=alpha, beta=1.0, variant=variant))
+            outs3.append(_gpu(As, Bs, C3, alpha=alpha, beta=1.0, variant=variant))
         finally:
             bx.lib().bf16x_red_add(-1)
+    assert np.all(outs2[0].view(np.uint32) == 0)                        # +0 from the fmaf epilogue
+    assert np.array_equal(outs2[0].view(np.uint32), outs2[1].view(np.uint32))
+    assert np.array_equal(outs3[0].astype(np.float64), d)                 # fmaf keeps the subnormal d
+    # red.global.add.f32 flushes subnormal inputs and results to (sign-preserving) zero (measured
+    # r08; K2 "red.add epilogue"): the one way it differs from the fmaf epilogue
+    assert np.all(outs3[1][d != 0] == 0), int(np.sum(outs3[1][d != 0] != 0))
     assert np.array_equal(outs[0].view(np.uint32), outs[1].view(np.uint32))
     assert np.array_equal(outs2[0].view(np.uint32), outs2[1].view(np.uint32))
+
+
+def test_concurrent_streams_bit_identical():
+    """The library's workspace and stream-K buffers are per stream (bf16x.h): GEMMs issued
+    concurrently on two streams -- each with stream-K tiles (4096 x 4608 and 3000 x 5000 have
+    partial last waves) -- must equal the same calls run one after the other, bit for bit."""
+    shapes = [(4096, 4608, 1000, 6), (3000, 5000, 700, 3)]
+    ops = []
+    for i, (m, n, k, v) in enumerate(shapes):
+        A = torch.from_numpy(synthetic.uniform(m, k, seed=40 + i)).cuda()
+        B = torch.from_numpy(synthetic.uniform(k, n, seed=50 + i)).cuda()
+        ops.append((A, B, v))
+    serial = []
+    for A, B, v in ops:
+        serial.append(bx.gemm(A, B, variant=v))
+        torch.cuda.synchronize()
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    for rep in range(3):
+        outs = [None, None]
+        torch.cuda.synchronize()
+        for rnd in range(4):          # interleave launches so the two streams overlap on the GPU
+            for i, (A, B, v) in enumerate(ops):
+                with torch.cuda.stream(streams[i]):
+                    outs[i] = bx.gemm(A, B, variant=v, stream=streams[i])
+        torch.cuda.synchronize()
+        for i in range(2):
+            assert torch.equal(outs[i].view(torch.int32), serial[i].view(torch.int32)), (rep, i)
+
+
+def test_gesv_ir_caller_tolerance(orc):
+    """bf16x_gesv_ir's tol (the paper's "residual tolerance of cond(A)*eps", P:469): with
+    tol = cond * 2^-53 the stopping test is ||r||_inf <= tol ||b||_inf, as in the oracle's
+    gesv_ir(tol=...); verdict and iteration count agree, the final residual meets the test."""
+    n = 384
+    for kappa in (1e2, 1e4):
+        A, _ = synthetic.conditioned(n, kappa, seed=int(kappa))
+        xt = synthetic.rhs(n, seed=3)
+        b = A.astype(np.float64) @ xt
+        tol = kappa * 2.0 ** -53 * 64
+        x, rep, hist = bx.gesv_ir(torch.from_numpy(A).cuda(), torch.from_numpy(b).cuda(), variant=3, nb=64, tol=tol)
+        ro = orc.gesv_ir(A, b, variant=3, nb=64, tol=tol)
+        assert rep.converged == int(ro["converged"]) == 1
+        assert abs(rep.iterations - ro["iterations"]) <= 1
+        assert rep.tol == pytest.approx(tol * np.max(np.abs(b)), rel=1e-12)
+        assert rep.final_residual <= rep.tol
