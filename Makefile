@@ -15,7 +15,7 @@ NVFLAGS := -O3 -std=c++17 $(GENCODE) -lineinfo -Xcompiler -fPIC -Iinclude -I$(CS
            --expt-relaxed-constexpr -Xptxas -v
 MAKEFLAGS += -j8
 
-.PHONY: all oracle lib clean
+.PHONY: all oracle lib clean trace
 all: oracle lib
 
 oracle: oracle/liboracle.so
@@ -30,6 +30,16 @@ $(OBJDIR)/%.o: $(CSRC)/%.cu $(CU_HDRS)
 $(PKG)/libbf16x.so: $(CU_OBJS)
 	$(NVCC) $(GENCODE) -shared -cudart static -o $@ $(CU_OBJS)
 	cat $(OBJDIR)/*.ptxas.log > build_ptxas.log
+
+# diagnostic build with the per-CTA %globaltimer trace compiled in (tools/gemm_trace.py loads it
+# through BF16X_LIB=build/trace/libbf16x.so); never the product library
+TRACE_OBJS := $(patsubst $(CSRC)/%.cu,build/trace/%.o,$(CU_SRCS))
+build/trace/%.o: $(CSRC)/%.cu $(CU_HDRS)
+	@mkdir -p build/trace
+	$(NVCC) $(NVFLAGS) -DBF16X_TRACE -c -o $@ $< 2> $@.ptxas.log || (cat $@.ptxas.log; false)
+trace: build/trace/libbf16x.so
+build/trace/libbf16x.so: $(TRACE_OBJS)
+	$(NVCC) $(GENCODE) -shared -cudart static -o $@ $(TRACE_OBJS)
 
 clean:
 	rm -rf oracle/liboracle.so $(PKG)/libbf16x.so $(OBJDIR)

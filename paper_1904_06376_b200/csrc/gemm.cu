@@ -143,3 +143,7 @@ extern "C" void bf16x_lazy_full(int on) { bf16x::g_lazy_full = on ? 1 : 0; }
 // testing hook (not in the public header): red.global.add epilogue for C += +-Z (alpha = +-1,
 // beta = 1): -1 where the caller asks for it (the LU's trailing update), 0 never, 1 always
 extern "C" void bf16x_red_add(int mode) { bf16x::g_red_add = mode; }
+// testing hook (not in the public header): KParams::dbg bits (bit 0: skip beta = 0 C stores)
+extern "C" void bf16x_gemm_debug(int bits) { bf16x::g_gemm_debug = bits; }
+// testing hook: device buffer of >= 32 * grid uint64 for the dbg bit 1 timeline (tools/gemm_trace.py)
+extern "C" void bf16x_gemm_trace(unsigned long long *buf) { bf16x::g_gemm_trace = buf; }

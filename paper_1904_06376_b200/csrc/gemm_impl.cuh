@@ -3,6 +3,7 @@
 // method and the B200 mapping.
 #pragma once
 #include <algorithm>
+#include <cstring>
 #include <mutex>
 #include <type_traits>
 
@@ -25,8 +26,14 @@ constexpr int kTmemCols = 512;        // two accumulator buffers at column 0 and
 constexpr int kTmemBufStride = 256;
 constexpr int kGroupM = 8;            // tile raster: 8 m-tiles per group for L2 reuse (default)
 constexpr int kDefaultCtaGroup = 2;   // 2-CTA pairs, 64-k promotion interval
-constexpr int kSmemBudget = 232448 - 1024;   // 227 KB opt-in maximum (x3: 7 stages of 32 KB)
+constexpr int kSmemBudget = 232448 - 1024;   // 227 KB opt-in maximum
+// C epilogue staging (TMA store): per epilogue warp two buffers of 32 rows x 16 columns FP32
+constexpr int kEpiRows = 32, kEpiCols = 16;
+constexpr int kEpiBuf = kEpiRows * kEpiCols * 4;
+constexpr int kEpiBytes = kNumEpiWarps * 2 * kEpiBuf;   // 32 KB
 inline int g_lazy_full = 1;           // lazy stage waits in the MMA issuer (bf16x_lazy_full hook)
+inline int g_gemm_debug = 0;          // KParams::dbg (bf16x_gemm_debug hook; tests / probes only)
+inline unsigned long long *g_gemm_trace = nullptr;   // KParams::trace (bf16x_gemm_trace hook)
 // Internal flag (not in the public header): C += alpha * Z with alpha = +-1, beta = 1 written as
 // red.global.add.f32 -- RN(C + (+-Z)) is exactly fmaf(+-1, Z, C) -- so the epilogue never waits
 // for the old C (the LU's trailing update, csrc/lu.cu).  g_red_add: -1 as requested (default),
@@ -49,9 +56,9 @@ struct Cfg {
     static constexpr int B_STAGE = PB * B_PIECE;
     static constexpr int STAGE = A_STAGE + B_STAGE;
     static constexpr int BAR_BYTES = 256;
-    static constexpr int STAGES_RAW = (kSmemBudget - BAR_BYTES - 1024) / STAGE;
+    static constexpr int STAGES_RAW = (kSmemBudget - BAR_BYTES - 1024 - kEpiBytes) / STAGE;
     static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
-    static constexpr int SMEM = STAGES * STAGE + BAR_BYTES + 1024;
+    static constexpr int SMEM = STAGES * STAGE + kEpiBytes + BAR_BYTES + 1024;
     static_assert(STAGES >= 2, "need at least two pipeline stages");
     static_assert(BN % (16 * CG) == 0 && BN <= 256 && EPI_COLS % 32 == 0, "invalid tile N");
 };
@@ -65,9 +72,9 @@ template <int V>
 struct CfgFA {
     using Cf = Cfg<2, V, 256>;
     static constexpr int FSTAGES = FA_FST;
-    static constexpr int STAGES_RAW = (232448 - 1280 - FSTAGES * kF32Tile) / Cf::STAGE;
+    static constexpr int STAGES_RAW = (232448 - 1280 - FSTAGES * kF32Tile - kEpiBytes) / Cf::STAGE;
     static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
-    static constexpr int SMEM = STAGES * Cf::STAGE + FSTAGES * kF32Tile + 256 + 1024;
+    static constexpr int SMEM = STAGES * Cf::STAGE + FSTAGES * kF32Tile + kEpiBytes + 256 + 1024;
     static_assert(STAGES >= 3, "fused A needs three piece stages");
 };
 
@@ -91,7 +98,12 @@ struct KParams {
     int scaled;            // N2 scaled pieces (R29): scale the accumulator by 2^-8 per bin step
     int group_m;           // tile raster: m-tiles per group
     int lazy_full;         // issuer waits for each stage just before its first MMA (issue_interval)
-    int64_t pad[6];
+    int dbg;               // testing hook (bf16x_gemm_debug): bit 0 = skip the C stores of beta = 0 tiles
+    int tma_c;             // C stored (beta = 0) / added (red-add) by TMA from the staging buffers
+    unsigned long long *trace;   // dbg bit 1: %globaltimer per CTA (tools/gemm_trace.py), 32 slots each
+    // (measured, nvcc 12.9: with the parameter block ending at lazy_full ptxas spills 96 bytes
+    // in the 2-CTA kernels; with >= 32 more bytes it allocates 168 registers without spills)
+    int64_t reserved[4];
 };
 
 struct Work {
@@ -234,7 +246,7 @@ __device__ __forceinline__ void issue_interval(uint32_t d_big, uint32_t d_small,
 template <int CG, int V, int BN, int S, int MC, bool SA, bool GD = false, bool FA = false>
 __global__ void __launch_bounds__(FA ? kThreadsFused : kThreads, 1)
     gemm_split_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                      const KParams p) {
+                      const __grid_constant__ CUtensorMap tmC, const KParams p) {
     using Cf = Cfg<CG, V, BN>;
     constexpr int NST = FA ? CfgFA<V>::STAGES : Cf::STAGES;   // piece ring stages
     constexpr int NF = FA ? CfgFA<V>::FSTAGES : 0;            // FP32 ring stages (fused A)
@@ -250,7 +262,8 @@ __global__ void __launch_bounds__(FA ? kThreadsFused : kThreads, 1)
     uint8_t *sA = smem;
     uint8_t *sB = smem + NST * Cf::A_STAGE;
     uint8_t *f32 = smem + NST * Cf::STAGE;                      // FA: [NF][A tile]
-    uint64_t *full = reinterpret_cast<uint64_t *>(smem + NST * Cf::STAGE + NF * F32_STAGE);
+    uint8_t *epi = f32 + NF * F32_STAGE;                        // [epilogue warp][2][32 x 16 FP32]
+    uint64_t *full = reinterpret_cast<uint64_t *>(epi + kEpiBytes);
     uint64_t *empty = full + NST;
     uint64_t *acc_full = empty + NST;
     uint64_t *acc_empty = acc_full + 2;
@@ -263,6 +276,21 @@ __global__ void __launch_bounds__(FA ? kThreadsFused : kThreads, 1)
     const uint32_t rank = crank % CG;                            // rank in the CTA pair
     const uint32_t pair = crank / CG;                            // which pair of the cluster
 
+    // dbg bit 1: trace slot 0 = kernel start, 1 = prologue done, 2 + 3 t .. = tile t (first
+    // interval promoted, last interval promoted, C issued), 31 = all stores complete
+    // (compiled in only with -DBF16X_TRACE: `make trace` builds build/trace/libbf16x.so)
+    auto trace = [&](int slot) {
+#ifdef BF16X_TRACE
+        if ((p.dbg & 2) && slot < 32) {
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            p.trace[blockIdx.x * 32 + slot] = t;
+        }
+#else
+        (void)slot;
+#endif
+    };
+    if (threadIdx.x == 4 * 32) trace(0);
     if (warp == 0 && lane == 0) {
         prefetch_tmap(&tmA);
         prefetch_tmap(&tmB);
@@ -291,6 +319,7 @@ __global__ void __launch_bounds__(FA ? kThreadsFused : kThreads, 1)
     // Programmatic dependent launch: everything above overlapped the previous kernel's tail;
     // from here on we read its outputs (the pieces) and may overwrite what it read.
     asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (threadIdx.x == 4 * 32) trace(1);
     // FA register split (per warpgroup, at the top of each role): the epilogue warpgroups hold
     // G (160 registers), producer / MMA and the two converter warpgroups need few (48); the sum
     // must not exceed the launch allocation (96 x 640), or the increase waits forever
@@ -419,6 +448,8 @@ __global__ void __launch_bounds__(FA ? kThreadsFused : kThreads, 1)
         uint32_t acc_it = 0;
         WorkIter it(p, cid, ncl);
         Work w;
+        int tcount = 0;
+        const bool tr = ew == 0 && lane == 0;
         while (it.next(p, w)) {
             int tm, tn;
             tile_coords(w.tile, p.tiles_m, p.tiles_n, p.group_m, tm, tn);
@@ -497,7 +528,9 @@ __global__ void __launch_bounds__(FA ? kThreadsFused : kThreads, 1)
                     if (CG == 1 || rank == 0) mbar_arrive(&acc_empty[buf]);
                     else mbar_arrive_cluster(&acc_empty[buf], pair * CG);
                 }
+                if (tr && kb == w.i0 * S) trace(2 + 3 * tcount);
             }
+            if (tr) trace(3 + 3 * tcount);
             if (w.role != 0) {
                 // stream-K fix-up: slot layout [sk tile][cta rank][column 0..BN)[row 0..127]
                 float *slot = p.sk_ws + ((size_t)w.sk_slot * CL + crank) * (size_t)NG * BN * kBM;
@@ -509,6 +542,8 @@ __global__ void __launch_bounds__(FA ? kThreadsFused : kThreads, 1)
                     __threadfence();
                     asm volatile("bar.sync 1, %0;" ::"n"(kNumEpiWarps * 32));
                     if (ew == 0 && lane == 0) st_release_u32(flag, p.epoch);
+                    if (tr) trace(4 + 3 * tcount);
+                    ++tcount;
                     continue;
                 }
                 if (lane == 0)
@@ -523,17 +558,45 @@ __global__ void __launch_bounds__(FA ? kThreadsFused : kThreads, 1)
                 if constexpr (GD) return __double2float_rn(__dadd_rn((double)G[EC + j] * qd, (double)G[j]));
                 else return G[j];
             };
-            if (row < p.m) {
+            // beta = 0 stores and the red-add update go through shared memory and TMA: each warp
+            // stages 16 columns of its 32 rows (2 KB, double-buffered) and one lane issues a 2D
+            // tensor store (or element-wise add in L2) of the box; the warp continues with the next
+            // tile while the TMA engine drains (rows / columns outside C are clipped by the TMA)
+            const bool radd = CG == 2 && BN == 256 && !GD && red_add;
+            if (p.tma_c && !(p.flags & BF16X_ACC_OUT) && (p.beta == 0.f || radd)) {
+                if (!(p.dbg & 1)) {
+                    float *wbuf = reinterpret_cast<float *>(epi) + ew * (2 * kEpiRows * kEpiCols);
+                    const int wrow = tm * Cf::TILE_M + (int)rank * kBM + quad * 32;
+#pragma unroll
+                    for (int q = 0; q < EC / kEpiCols; ++q) {
+                        float *dst = wbuf + (q & 1) * (kEpiRows * kEpiCols);
+                        if (lane == 0) bulk_wait_read<1>();      // this buffer's store two chunks ago has read it
+                        __syncwarp();
+#pragma unroll
+                        for (int j = 0; j < kEpiCols; ++j)
+                            dst[j * kEpiRows + lane] = radd ? p.alpha * zval(q * kEpiCols + j)
+                                                            : fmaf(p.alpha, zval(q * kEpiCols + j), 0.f);
+                        fence_proxy_async_smem();
+                        __syncwarp();
+                        if (lane == 0) {
+                            if (radd) tma_reduce_add_2d(&tmC, dst, wrow, col0 + q * kEpiCols);
+                            else tma_store_2d(&tmC, dst, wrow, col0 + q * kEpiCols);
+                            bulk_commit();
+                        }
+                    }
+                }
+            } else if (row < p.m) {
                 float *crow = p.C + row;
                 if (p.flags & BF16X_ACC_OUT) {
 #pragma unroll
                     for (int j = 0; j < EC; ++j)
                         if (col0 + j < p.n) p.acc[(int64_t)(col0 + j) * p.ldc + row] = G[j];
                 } else if (p.beta == 0.f) {
+                    if (!(p.dbg & 1))
 #pragma unroll
                     for (int j = 0; j < EC; ++j)
                         if (col0 + j < p.n) __stcs(crow + (int64_t)(col0 + j) * p.ldc, fmaf(p.alpha, zval(j), 0.f));
-                } else if (CG == 2 && BN == 256 && !GD && red_add) {
+                } else if (radd) {
                     // alpha * Z is exact (alpha = +-1): the L2 adds it to C with one RN rounding
 #pragma unroll
                     for (int j = 0; j < EC; ++j)
@@ -556,7 +619,11 @@ __global__ void __launch_bounds__(FA ? kThreadsFused : kThreads, 1)
                     }
                 }
             }
+            if (tr) trace(4 + 3 * tcount);
+            ++tcount;
         }
+        if (lane == 0) bulk_wait<0>();          // every TMA store of this warp is complete
+        if (tr) trace(31);
     } else if constexpr (FA) {
         asm volatile("setmaxnreg.dec.sync.aligned.u32 48;" ::: "memory");
         // ------------------- fused A: FP32 A tiles -> A pieces -------------------
@@ -643,7 +710,7 @@ int launch_t(const GemmPlan &pl, cudaStream_t st) {
     constexpr int THREADS = FA ? kThreadsFused : kThreads;
     constexpr int SMEM = FA ? CfgFA<V>::SMEM : Cf::SMEM;
     auto kern = gemm_split_kernel<CG, V, BN, S, MC, SA, GD, FA>;
-    CUtensorMap tmA, tmB;
+    CUtensorMap tmA, tmB, tmC;
     int rc;
     if constexpr (FA) {
         rc = make_f32_map(&tmA, pl.Af, pl.m, pl.k, pl.lda, kBM, kBK, CU_TENSOR_MAP_SWIZZLE_NONE);
@@ -709,9 +776,21 @@ int launch_t(const GemmPlan &pl, cudaStream_t st) {
     // super-rows on the multicast schedule of the largest outputs (16384^3 x6: 228 vs 215
     // TFLOPS, DRAM reads ~50 vs ~85 GB per launch -- power-limited, so traffic costs clock)
     kp.lazy_full = g_lazy_full;
+    kp.dbg = g_gemm_debug;
+    kp.trace = g_gemm_trace;
+    // C through TMA when its base and columns are 16-byte aligned (else per-thread stores)
+    kp.tma_c = 0;
+    std::memset(&tmC, 0, sizeof(tmC));
+    if (!(pl.flags & BF16X_ACC_OUT) && (reinterpret_cast<uintptr_t>(pl.C) & 15u) == 0 && pl.ldc % 4 == 0 &&
+        make_f32_map(&tmC, pl.C, pl.m, pl.n, pl.ldc, kEpiRows, kEpiCols, CU_TENSOR_MAP_SWIZZLE_NONE) == BF16X_SUCCESS)
+        kp.tma_c = 1;
     kp.group_m = pl.group_m > 0 ? pl.group_m : (MC == 2 ? 2 : (kp.tiles_n <= 16 ? 1 : kGroupM));
     const int ncl = grid / CL;
-    if (pl.stream_k != 0 && !(pl.flags & (BF16X_ACC_IN | BF16X_ACC_OUT)) && tiles > ncl && tiles % ncl != 0) {
+    // (not for short k: a split tile's fix-up -- the contributor's FP32 partial written and read
+    // back -- costs more than the balanced tail wins below 12 promotion intervals; measured r08,
+    // tools/shortk_sched_probe.py: 4096^2 x k = 256 x3 37.9 -> 34.0 us, k = 1024 x6 133.4 vs 136.0)
+    if (pl.stream_k != 0 && !(pl.flags & (BF16X_ACC_IN | BF16X_ACC_OUT)) && tiles > ncl && tiles % ncl != 0 &&
+        kp.n_int >= 12) {
         const int full = tiles / ncl;
         kp.dp_tiles = (full - 1) * ncl;
         kp.sk_tiles = tiles - kp.dp_tiles;
@@ -740,7 +819,7 @@ int launch_t(const GemmPlan &pl, cudaStream_t st) {
     attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 2;
-    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, tmA, tmB, kp);
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, tmA, tmB, tmC, kp);
     if (e != cudaSuccess) {
         set_cuda_error(e, "gemm launch");
         return BF16X_ERR_CUDA;

@@ -149,3 +149,34 @@ def sequential(A, B, variant=6):
     for s in reversed(order[:-1]):
         tot = (bins[s] + tot).astype(f)
     return tot
+
+
+def interval_partials(A, B, variant=6, interval=64):
+    """The tensor core's FP32 result of each promotion interval (one accumulator, bands smallest
+    first), as a list of (m, n) float32 arrays in increasing k order."""
+    m, k = A.shape
+    n = B.shape[1]
+    pa, pb = PIECES[variant]
+    Ap = [x.astype(np.float64) for x in split(A, pa)]
+    Bp = [x.astype(np.float64) for x in split(B, pb)]
+    out = []
+    for i0 in range(0, k, interval):
+        i1 = min(k, i0 + interval)
+        acc = None
+        for band in BANDS[variant]:
+            for h0 in range(i0, i1, 16):
+                h1 = min(i1, h0 + 16)
+                for (i, j) in band:
+                    a = np.broadcast_to(Ap[i][:, None, h0:h1], (m, n, h1 - h0))
+                    b = np.broadcast_to(Bp[j].T[None, :, h0:h1], (m, n, h1 - h0))
+                    acc = mma_step(acc if acc is not None else np.zeros((m, n)), a, b)
+        out.append(acc.astype(np.float32))
+    return out
+
+
+def promote(parts):
+    """G = RN32 sum of interval partials in order (the promotion), starting from 0."""
+    G = np.zeros(parts[0].shape, dtype=np.float32)
+    for d in parts:
+        G = (G + d).astype(np.float32)
+    return G

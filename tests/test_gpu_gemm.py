@@ -269,7 +269,7 @@ def test_ragged_ld_and_offsets(orc):
     assert np.all(outside == 7.0)
 
 
-@pytest.mark.parametrize("m,n,k", [(2560, 2560, 1000), (4096, 1536, 333), (2304, 4608, 64)])
+@pytest.mark.parametrize("m,n,k", [(2560, 2560, 1000), (4096, 1536, 800), (2304, 4608, 777)])
 def test_stream_k_schedule(orc, m, n, k, mc):
     """Hybrid stream-K (tiles > clusters, partial last wave): split tiles are finished by the
     cluster holding their first promotion intervals, which adds the other part's raw FP32
@@ -430,13 +430,14 @@ def test_128k_interval_hook(orc, dist, variant, mc):
 
 @pytest.mark.parametrize("alpha", [1.0, -1.0])
 @pytest.mark.parametrize("variant", [3, 6])
-@pytest.mark.parametrize("shape", [(333, 517, 256), (1100, 900, 96), (2304, 2304, 256)])
+@pytest.mark.parametrize("shape", [(333, 517, 256), (1100, 900, 96), (2304, 2304, 768)])
 def test_red_add_epilogue_bit_identical(shape, variant, alpha):
-    """C += +-Z through red.global.add.f32 (the LU's trailing update) is bit-identical to the
-    fmaf(alpha, Z, beta * C) epilogue for alpha = +-1, beta = 1 wherever C and the result are
-    normal FP32 numbers -- including exact cancellation to +0 and stream-K tiles (2304^2 has a
-    partial last wave) -- and flushes results in the subnormal range to zero (the hardware's
-    FP32 reduction is FTZ), which the test pins as the only difference."""
+    """C += +-Z in L2 (the LU's trailing update: a TMA element-wise add of staged tiles when C's
+    columns are 16-byte aligned, else red.global.add.f32 per element) is bit-identical to the
+    fmaf(alpha, Z, beta * C) epilogue for alpha = +-1, beta = 1 -- including exact cancellation
+    to +0 and stream-K tiles (2304^2 has a partial last wave).  Subnormal results: the TMA add
+    keeps them (bit-identical); red.global.add.f32 flushes them to zero, which the test pins as
+    its only difference (333 rows: unaligned columns)."""
     m, n, k = shape
     A = synthetic.uniform(m, k, seed=m + 13 * k)
     B = synthetic.uniform(k, n, seed=n + 17 * k)
@@ -451,13 +452,13 @@ def test_red_add_epilogue_bit_identical(shape, variant, alpha):
         finally:
             bx.lib().bf16x_red_add(-1)
     # exact cancellation and subnormal results: Z = A B from a beta = 0 run; C2 = -alpha Z makes
-    # every result C2 + alpha Z an exact zero (both must give +0).  With A, B scaled by 2^-70 and
-    # 2^-60, Zs ~ 2^-130 is subnormal; C3 = -alpha Zs + d, d = +-k 2^-149, makes the exact result
+    # every result C2 + alpha Z an exact zero (both must give +0).  With A, B scaled by 2^-72 and
+    # 2^-64, |Zs| <= k 2^-136 < 2^-126 is subnormal; C3 = -alpha Zs + d, d = +-k 2^-149, makes the exact result
     # the subnormal d: rounding must keep it (no flush to zero of inputs or results)
     Z = _gpu(A, B, None, alpha=1.0, beta=0.0, variant=variant)
     C2 = (-np.float32(alpha) * Z).astype(np.float32)
-    As = (A * np.float32(2.0 ** -70)).astype(np.float32, order="F")
-    Bs = (B * np.float32(2.0 ** -60)).astype(np.float32, order="F")
+    As = (A * np.float32(2.0 ** -72)).astype(np.float32, order="F")
+    Bs = (B * np.float32(2.0 ** -64)).astype(np.float32, order="F")
     Zs = _gpu(As, Bs, None, alpha=1.0, beta=0.0, variant=variant)
     d = (np.arange(m * n).reshape(m, n, order="F") % 7 - 3) * 2.0 ** -149
     C3 = (-alpha * Zs.astype(np.float64) + d).astype(np.float32)
@@ -473,9 +474,14 @@ def test_red_add_epilogue_bit_identical(shape, variant, alpha):
     assert np.all(outs2[0].view(np.uint32) == 0)                        # +0 from the fmaf epilogue
     assert np.array_equal(outs2[0].view(np.uint32), outs2[1].view(np.uint32))
     assert np.array_equal(outs3[0].astype(np.float64), d)                 # fmaf keeps the subnormal d
-    # red.global.add.f32 flushes subnormal inputs and results to (sign-preserving) zero (measured
-    # r08; K2 "red.add epilogue"): the one way it differs from the fmaf epilogue
-    assert np.all(outs3[1][d != 0] == 0), int(np.sum(outs3[1][d != 0] != 0))
+    if m % 4 == 0:
+        # 16-byte aligned columns: the update is a TMA element-wise add (cp.reduce.async.bulk
+        # .add.f32), IEEE in the subnormal range too -> bit-identical to the fmaf epilogue
+        assert np.array_equal(outs3[0].view(np.uint32), outs3[1].view(np.uint32))
+    else:
+        # otherwise per-thread red.global.add.f32, which flushes subnormal inputs and results to
+        # (sign-preserving) zero (measured r08): the one way it differs from the fmaf epilogue
+        assert np.all(outs3[1][d != 0] == 0), int(np.sum(outs3[1][d != 0] != 0))
     assert np.array_equal(outs[0].view(np.uint32), outs[1].view(np.uint32))
     assert np.array_equal(outs2[0].view(np.uint32), outs2[1].view(np.uint32))
 
@@ -484,7 +490,7 @@ def test_concurrent_streams_bit_identical():
     """The library's workspace and stream-K buffers are per stream (bf16x.h): GEMMs issued
     concurrently on two streams -- each with stream-K tiles (4096 x 4608 and 3000 x 5000 have
     partial last waves) -- must equal the same calls run one after the other, bit for bit."""
-    shapes = [(4096, 4608, 1000, 6), (3000, 5000, 700, 3)]
+    shapes = [(4096, 4608, 1000, 6), (3000, 5000, 800, 3)]
     ops = []
     for i, (m, n, k, v) in enumerate(shapes):
         A = torch.from_numpy(synthetic.uniform(m, k, seed=40 + i)).cuda()

@@ -129,7 +129,7 @@ def _interval(variant, cg, spi, k):
         stage = pa * 128 * 64 + pb * 256 * 64
     else:
         stage = pa * 128 * 64 + pb * 128 * 64
-    stages = min(8, (232448 - 1024 - 256 - 1024) // stage)
+    stages = min(8, (232448 - 1024 - 256 - 1024 - 32768) // stage)   # 32 KB: the C staging buffers
     s = spi if spi in (1, 2) else (2 if (cg == 2 and k > 128) else 1)
     if s == 2 and stages < 4:
         s = 1
@@ -161,3 +161,38 @@ def test_kernel_equals_schedule_model_default(variant):
             G = _gpu(A, B, variant)
             M = tc_model.simulate(A, B, variant, interval=32 if k <= 128 else 64)
             assert np.array_equal(G.view(np.uint32), M.view(np.uint32)), (m, n, k, dist)
+
+
+def test_stream_k_equals_model():
+    """Hybrid stream-K, bit for bit: with the grid capped at 4 CTA pairs (bf16x_max_ctas), a
+    512 x 768 output (2 x 3 tiles of 256 x 256) and k = 768 (12 intervals of 64 k) runs every
+    tile in stream-K mode: the 72 intervals are dealt 18 per cluster, so tiles 1 and 4 are cut
+    in two.  An uncut tile is the RN promotion of its 12 interval partials; a cut tile is
+    RN(G_owner + G_contributor), each the promotion of its own intervals (csrc/gemm_impl.cuh
+    WorkIter and the fix-up)."""
+    m, n, k, v = 512, 768, 768, 6
+    A = synthetic.uniform(m, k, seed=21)
+    B = synthetic.uniform(k, n, seed=22)
+    L = bx.lib()
+    L.bf16x_max_ctas(8)
+    try:
+        G = _gpu(A, B, v)
+    finally:
+        L.bf16x_max_ctas(0)
+    parts = tc_model.interval_partials(A, B, v, interval=64)
+    n_int, ncl, tiles_n = 12, 4, 3
+    U = 6 * n_int
+    bounds = [U * c // ncl for c in range(ncl + 1)]
+    want = np.empty((m, n), dtype=np.float32)
+    for t in range(6):
+        tm, tn = t // tiles_n, t % tiles_n                 # raster: one tile row per group (tiles_n <= 16)
+        rs, cs = slice(256 * tm, 256 * tm + 256), slice(256 * tn, 256 * tn + 256)
+        lo, hi = t * n_int, (t + 1) * n_int
+        cut = [b - lo for b in bounds if lo < b < hi]
+        P = [p[rs, cs] for p in parts]
+        if not cut:
+            want[rs, cs] = tc_model.promote(P)
+        else:
+            assert len(cut) == 1
+            want[rs, cs] = (tc_model.promote(P[:cut[0]]) + tc_model.promote(P[cut[0]:])).astype(np.float32)
+    assert np.array_equal(G.view(np.uint32), want.view(np.uint32)), int(np.sum(G != want))
