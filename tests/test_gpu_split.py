@@ -34,7 +34,8 @@ def test_all_2_32_patterns_bit_exact(orc):
     assert first_bad is None, f"pattern/piece/gpu/oracle: {first_bad}"
 
 
-@pytest.mark.parametrize("rows,cols,ld", [(1, 1, 1), (7, 3, 9), (129, 65, 130), (256, 33, 256), (1000, 17, 1003)])
+@pytest.mark.parametrize("rows,cols,ld", [(1, 1, 1), (7, 3, 9), (129, 65, 130), (256, 33, 256), (1000, 17, 1003),
+                                          (64, 128, 64), (200, 300, 204), (130, 257, 131), (513, 1030, 520)])
 def test_layouts_same_and_transposed(orc, rows, cols, ld):
     """Column-major with ld > rows, and the transposed (K-major) output used for A."""
     X = synthetic.wide(ld, cols, seed=rows * 31 + cols)
