@@ -72,9 +72,11 @@ template <int V>
 struct CfgFA {
     using Cf = Cfg<2, V, 256>;
     static constexpr int FSTAGES = FA_FST;
-    static constexpr int STAGES_RAW = (232448 - 1280 - FSTAGES * kF32Tile - kEpiBytes) / Cf::STAGE;
+    // (no C staging: the fused-A kernel keeps per-thread C stores and its fourth piece stage --
+    // with the 32 KB staging it had 3, and bf16x9 lost 28 % at 4096^3 / 8192^3, r08 sweep)
+    static constexpr int STAGES_RAW = (232448 - 1280 - FSTAGES * kF32Tile) / Cf::STAGE;
     static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
-    static constexpr int SMEM = STAGES * Cf::STAGE + FSTAGES * kF32Tile + kEpiBytes + 256 + 1024;
+    static constexpr int SMEM = STAGES * Cf::STAGE + FSTAGES * kF32Tile + 256 + 1024;
     static_assert(STAGES >= 3, "fused A needs three piece stages");
 };
 
@@ -262,8 +264,9 @@ __global__ void __launch_bounds__(FA ? kThreadsFused : kThreads, 1)
     uint8_t *sA = smem;
     uint8_t *sB = smem + NST * Cf::A_STAGE;
     uint8_t *f32 = smem + NST * Cf::STAGE;                      // FA: [NF][A tile]
+    constexpr int EPI_BYTES = FA ? 0 : kEpiBytes;
     uint8_t *epi = f32 + NF * F32_STAGE;                        // [epilogue warp][2][32 x 16 FP32]
-    uint64_t *full = reinterpret_cast<uint64_t *>(epi + kEpiBytes);
+    uint64_t *full = reinterpret_cast<uint64_t *>(epi + EPI_BYTES);
     uint64_t *empty = full + NST;
     uint64_t *acc_full = empty + NST;
     uint64_t *acc_empty = acc_full + 2;
@@ -322,7 +325,8 @@ __global__ void __launch_bounds__(FA ? kThreadsFused : kThreads, 1)
     if (threadIdx.x == 4 * 32) trace(1);
     // FA register split (per warpgroup, at the top of each role): the epilogue warpgroups hold
     // G (160 registers), producer / MMA and the two converter warpgroups need few (48); the sum
-    // must not exceed the launch allocation (96 x 640), or the increase waits forever
+    // must not exceed the launch allocation (96 x 640 = 61440: 128 x 48 + 256 x 48 + 256 x 160 =
+    // 59392), or the increase waits forever (176 hung the kernel, r08)
 
     const int cid = blockIdx.x / CL, ncl = gridDim.x / CL;
 
@@ -472,7 +476,7 @@ __global__ void __launch_bounds__(FA ? kThreadsFused : kThreads, 1)
                     if (col0 + j < p.n) asm volatile("prefetch.global.L2 [%0];" ::"l"(pc + (int64_t)(col0 + j) * p.ldc));
             }
             float G[NG * EC];
-            if ((p.flags & BF16X_ACC_IN) && w.i0 == 0) {   // (never with GD)
+            if (!GD && (p.flags & BF16X_ACC_IN) && w.i0 == 0) {   // (never with GD)
 #pragma unroll
                 for (int j = 0; j < EC; ++j)
                     G[j] = (row < p.m && col0 + j < p.n) ? p.acc[(int64_t)(col0 + j) * p.ldc + row] : 0.f;
@@ -552,18 +556,19 @@ __global__ void __launch_bounds__(FA ? kThreadsFused : kThreads, 1)
 #pragma unroll
                 for (int j = 0; j < NG * EC; ++j) G[j] = __fadd_rn(G[j], __ldcg(slot + (size_t)(half * NG * EC + j) * kBM + lrow));
             }
-            // GD: final collection in FP64, rounded once (R30)
-            const double qd = p.scaled ? 0x1p-8 : 1.0;
-            auto zval = [&](int j) -> float {
-                if constexpr (GD) return __double2float_rn(__dadd_rn((double)G[EC + j] * qd, (double)G[j]));
-                else return G[j];
-            };
+            // GD: final collection in FP64, rounded once (R30), in place into G[0, EC)
+            if constexpr (GD) {
+                const double qd = p.scaled ? 0x1p-8 : 1.0;
+#pragma unroll
+                for (int j = 0; j < EC; ++j) G[j] = __double2float_rn(__dadd_rn((double)G[EC + j] * qd, (double)G[j]));
+            }
+            auto zval = [&](int j) -> float { return G[j]; };
             // beta = 0 stores and the red-add update go through shared memory and TMA: each warp
             // stages 16 columns of its 32 rows (2 KB, double-buffered) and one lane issues a 2D
             // tensor store (or element-wise add in L2) of the box; the warp continues with the next
             // tile while the TMA engine drains (rows / columns outside C are clipped by the TMA)
             const bool radd = CG == 2 && BN == 256 && !GD && red_add;
-            if (p.tma_c && !(p.flags & BF16X_ACC_OUT) && (p.beta == 0.f || radd)) {
+            if (!FA && p.tma_c && !(p.flags & BF16X_ACC_OUT) && (p.beta == 0.f || radd)) {
                 if (!(p.dbg & 1)) {
                     float *wbuf = reinterpret_cast<float *>(epi) + ew * (2 * kEpiRows * kEpiCols);
                     const int wrow = tm * Cf::TILE_M + (int)rank * kBM + quad * 32;
@@ -587,7 +592,7 @@ __global__ void __launch_bounds__(FA ? kThreadsFused : kThreads, 1)
                 }
             } else if (row < p.m) {
                 float *crow = p.C + row;
-                if (p.flags & BF16X_ACC_OUT) {
+                if (!GD && (p.flags & BF16X_ACC_OUT)) {   // (never with GD)
 #pragma unroll
                     for (int j = 0; j < EC; ++j)
                         if (col0 + j < p.n) p.acc[(int64_t)(col0 + j) * p.ldc + row] = G[j];
@@ -781,7 +786,7 @@ int launch_t(const GemmPlan &pl, cudaStream_t st) {
     // C through TMA when its base and columns are 16-byte aligned (else per-thread stores)
     kp.tma_c = 0;
     std::memset(&tmC, 0, sizeof(tmC));
-    if (!(pl.flags & BF16X_ACC_OUT) && (reinterpret_cast<uintptr_t>(pl.C) & 15u) == 0 && pl.ldc % 4 == 0 &&
+    if (!FA && !(pl.flags & BF16X_ACC_OUT) && (reinterpret_cast<uintptr_t>(pl.C) & 15u) == 0 && pl.ldc % 4 == 0 &&
         make_f32_map(&tmC, pl.C, pl.m, pl.n, pl.ldc, kEpiRows, kEpiCols, CU_TENSOR_MAP_SWIZZLE_NONE) == BF16X_SUCCESS)
         kp.tma_c = 1;
     kp.group_m = pl.group_m > 0 ? pl.group_m : (MC == 2 ? 2 : (kp.tiles_n <= 16 ? 1 : kGroupM));
