@@ -56,9 +56,14 @@ struct Cfg {
     static constexpr int B_STAGE = PB * B_PIECE;
     static constexpr int STAGE = A_STAGE + B_STAGE;
     static constexpr int BAR_BYTES = 256;
-    static constexpr int STAGES_RAW = (kSmemBudget - BAR_BYTES - 1024 - kEpiBytes) / STAGE;
+    // C staging for the TMA epilogue only where the ring keeps >= 4 stages with it (1-CTA x5-x9
+    // tiles would drop to 2-3 stages: they keep per-thread C stores)
+    static constexpr int STAGES_EPI = (kSmemBudget - BAR_BYTES - 1024 - kEpiBytes) / STAGE;
+    static constexpr bool EPI = STAGES_EPI >= 4;
+    static constexpr int EPI_BYTES = EPI ? kEpiBytes : 0;
+    static constexpr int STAGES_RAW = (kSmemBudget - BAR_BYTES - 1024 - EPI_BYTES) / STAGE;
     static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
-    static constexpr int SMEM = STAGES * STAGE + kEpiBytes + BAR_BYTES + 1024;
+    static constexpr int SMEM = STAGES * STAGE + EPI_BYTES + BAR_BYTES + 1024;
     static_assert(STAGES >= 2, "need at least two pipeline stages");
     static_assert(BN % (16 * CG) == 0 && BN <= 256 && EPI_COLS % 32 == 0, "invalid tile N");
 };
@@ -264,7 +269,8 @@ __global__ void __launch_bounds__(FA ? kThreadsFused : kThreads, 1)
     uint8_t *sA = smem;
     uint8_t *sB = smem + NST * Cf::A_STAGE;
     uint8_t *f32 = smem + NST * Cf::STAGE;                      // FA: [NF][A tile]
-    constexpr int EPI_BYTES = FA ? 0 : kEpiBytes;
+    constexpr int EPI_BYTES = FA ? 0 : Cf::EPI_BYTES;
+    constexpr bool TMA_EPI = !FA && Cf::EPI;
     uint8_t *epi = f32 + NF * F32_STAGE;                        // [epilogue warp][2][32 x 16 FP32]
     uint64_t *full = reinterpret_cast<uint64_t *>(epi + EPI_BYTES);
     uint64_t *empty = full + NST;
@@ -568,7 +574,7 @@ __global__ void __launch_bounds__(FA ? kThreadsFused : kThreads, 1)
             // tensor store (or element-wise add in L2) of the box; the warp continues with the next
             // tile while the TMA engine drains (rows / columns outside C are clipped by the TMA)
             const bool radd = CG == 2 && BN == 256 && !GD && red_add;
-            if (!FA && p.tma_c && !(p.flags & BF16X_ACC_OUT) && (p.beta == 0.f || radd)) {
+            if (TMA_EPI && p.tma_c && !(p.flags & BF16X_ACC_OUT) && (p.beta == 0.f || radd)) {
                 if (!(p.dbg & 1)) {
                     float *wbuf = reinterpret_cast<float *>(epi) + ew * (2 * kEpiRows * kEpiCols);
                     const int wrow = tm * Cf::TILE_M + (int)rank * kBM + quad * 32;
@@ -786,7 +792,7 @@ int launch_t(const GemmPlan &pl, cudaStream_t st) {
     // C through TMA when its base and columns are 16-byte aligned (else per-thread stores)
     kp.tma_c = 0;
     std::memset(&tmC, 0, sizeof(tmC));
-    if (!FA && !(pl.flags & BF16X_ACC_OUT) && (reinterpret_cast<uintptr_t>(pl.C) & 15u) == 0 && pl.ldc % 4 == 0 &&
+    if (!FA && Cf::EPI && !(pl.flags & BF16X_ACC_OUT) && (reinterpret_cast<uintptr_t>(pl.C) & 15u) == 0 && pl.ldc % 4 == 0 &&
         make_f32_map(&tmC, pl.C, pl.m, pl.n, pl.ldc, kEpiRows, kEpiCols, CU_TENSOR_MAP_SWIZZLE_NONE) == BF16X_SUCCESS)
         kp.tma_c = 1;
     kp.group_m = pl.group_m > 0 ? pl.group_m : (MC == 2 ? 2 : (kp.tiles_n <= 16 ? 1 : kGroupM));

@@ -129,7 +129,11 @@ def _interval(variant, cg, spi, k):
         stage = pa * 128 * 64 + pb * 256 * 64
     else:
         stage = pa * 128 * 64 + pb * 128 * 64
-    stages = min(8, (232448 - 1024 - 256 - 1024 - 32768) // stage)   # 32 KB: the C staging buffers
+    base = 232448 - 1024 - 256 - 1024
+    stages = (base - 32768) // stage                  # 32 KB: the C staging buffers ...
+    if stages < 4:
+        stages = base // stage                        # ... only where 4 stages remain with them
+    stages = min(8, stages)
     s = spi if spi in (1, 2) else (2 if (cg == 2 and k > 128) else 1)
     if s == 2 and stages < 4:
         s = 1
