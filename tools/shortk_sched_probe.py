@@ -45,6 +45,7 @@ for k in (256, 512, 1024):
         res = {}
         for rep in range(2):
             res.setdefault("default", []).append(tm(g))
+
             if v == 3:
                 L.bf16x_tune(0, 0, 4)
                 res.setdefault("128k", []).append(tm(g))
