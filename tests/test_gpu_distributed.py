@@ -87,3 +87,51 @@ def test_rank_shards_equal_one_gpu_columns(orc, P, sub_blocks):
             off += w
         torch.cuda.synchronize()
         assert np.array_equal(Cq.cpu().numpy().view(np.uint32), want[:, cols].view(np.uint32)), q
+
+
+def _gloo_cuda_worker(rank, world, port, m, n, k, S, R, q):
+    import os
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        A_np = synthetic.uniform(m, k, seed=1)
+        B_np = synthetic.uniform(k, n, seed=2)
+        A = torch.from_numpy(A_np).cuda() if rank == 0 else torch.zeros((k, m), device="cuda").t()
+        cols = local_columns(n, world, rank, S)
+        Bl = torch.from_numpy(np.asfortranarray(B_np[:, cols])).cuda()
+        C = torch.full((n, m), float("nan"), device="cuda").t()
+        gemm_colsharded(A, Bl, C, variant=6, sub_blocks=S, k_chunks=R)
+        torch.cuda.synchronize()
+        want = bx.gemm(torch.from_numpy(A_np).cuda(), torch.from_numpy(B_np).cuda(), variant=6, no_stream_k=True)
+        torch.cuda.synchronize()
+        q.put((rank, bool(torch.equal(C.contiguous().view(torch.int32), want.contiguous().view(torch.int32))),
+               bool(torch.equal(A.contiguous().view(torch.int32),
+                                torch.from_numpy(A_np).cuda().contiguous().view(torch.int32)))))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("m,n,k,S,R", [(1024, 2048, 1536, 2, 3), (700, 1300, 900, 3, 4)])
+def test_colsharded_world2_on_one_gpu(m, n, k, S, R):
+    """The whole N > 1 data plane with real CUDA kernels: two processes share cuda:0 under the
+    gloo backend (CUDA tensors), so the side-stream broadcast of A's chunks (contiguous transpose
+    views), the per-chunk events, the chunked carry, the per-rank piece buffer and both all-gather
+    branches (in place for equal block widths, padded for 1300 columns in 6 blocks) run exactly
+    as they would across GPUs.  Each rank's kernels are independent (no kernel waits on another
+    rank), so sharing one GPU only serialises them.  Both ranks' C must equal the one-GPU C."""
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gloo_cuda_worker, args=(r, 2, port, m, n, k, S, R, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in range(2)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, c_ok, a_ok in res:
+        assert a_ok, rank
+        assert c_ok, rank
