@@ -271,9 +271,17 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # BF16X_BENCH_BACKEND=gloo: a functional run of the N > 1 path with all ranks on the GPUs
+    # there are (e.g. two ranks on one GPU) -- a check of the code path, never a measurement
+    backend = os.environ.get("BF16X_BENCH_BACKEND", "nccl")
+    if backend != "nccl":
+        local %= torch.cuda.device_count()
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     bx.device_check()
     cfg = CONFIGS[args.config]
     v = args.variant
