@@ -38,6 +38,8 @@ CONFIGS = {
     "c2": dict(m=4096, n=4096, k=4096, label="configs[1]: 4096^3 bf16x{v} GEMM on 1 B200, uniform [-1,1] inputs"),
     "c4": dict(m=16384, n=16384, k=16384,
                label="configs[3]: 16384^3 bf16x{v} GEMM column-sharded over {p} B200 (P = {p}), uniform [-1,1] inputs"),
+    "c4b": dict(m=32768, n=32768, k=32768,
+                label="configs[3]: 32768^3 bf16x{v} GEMM column-sharded over {p} B200 (P = {p}), uniform [-1,1] inputs"),
 }
 
 
@@ -171,7 +173,7 @@ def run_reference(args):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "TFLOPS", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
-        "higher_is_better": True, "scaling": "strong" if args.config == "c4" else "weak", "vs_baseline": None,
+        "higher_is_better": True, "scaling": "strong" if args.config in ("c4", "c4b") else "weak", "vs_baseline": None,
         "dtype": "f32", "data": "synthetic",
         "config": {"workload": cfg["label"].format(v=v, p=world), "m": m, "n": n, "k": k, "variant": v,
                    "sample_per_step": f"{ncols} random output columns (all rows, full k; the oracle splits A "
@@ -381,13 +383,14 @@ def run_ours(args):
     line = {
         "metric": METRIC, "value": value, "unit": "TFLOPS", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-        "scaling": "strong" if args.config == "c4" else "weak",
+        "scaling": "strong" if args.config in ("c4", "c4b") else "weak",
         "vs_baseline": None, "dtype": "f32", "mma_dtype": "bf16 x bf16 -> f32 (tcgen05 kind::f16)",
         "data": "synthetic",
         "config": {"workload": workload, "m": m, "n": n, "k": k, "n_per_gpu": n_loc, "variant": v,
                    "inputs": "A, B ~ U[-1,1] (FP64 draws rounded to FP32), seeded, column-major",
-                   "l2": "inputs 2 x 1 GiB FP32 + 3 GiB of pieces per step >> 126 MB L2; no flush needed"
-                         if args.config == "c4" else "one input set (use --config c4 for the headline)",
+                   "l2": f"inputs {4 * (m * k + k * n_loc) / 2 ** 30:.0f} GiB FP32 + {2 * p * (m * k + k * n_loc) / 2 ** 30:.0f} GiB "
+                         f"of pieces per step >> 126 MB L2; no flush needed"
+                         if args.config in ("c4", "c4b") else "one input set (use --config c4 for the headline)",
                    "parallelism": (f"column blocks of C, dp{world} (gemm_colsharded: {S} sub-blocks per rank, "
                                    f"A broadcast in 4 k-chunks and split once per rank, all-gathers on a side "
                                    f"stream)") if world > 1 else "single GPU"},
