@@ -89,9 +89,23 @@ int pieces_b(int variant) { return variant_pieces_b(variant); }
 int default_cta_group() { return kDefaultCtaGroup; }
 
 
+// Promote-every-MMA schedule for short k on small outputs: the library's automatic schedule only
+// (no forced promotion interval), no accumulator carry, plain pieces (scaled pieces keep the
+// band-scaled accumulator), no split accumulators / FP64 collection.  Largest k: bf16x_pm_max_k
+// (default 128); outputs of at most 2^20 elements, where the extra promotions cost a few us
+// (measured r08, tools/pm_probe.py: 512^2 x 64 x6 10.6 -> 17.0 us) -- on 4096^2 outputs they
+// would cost 2-3.5x (x6, k = 128: 33 -> 97 us), so large outputs keep the 32-k intervals.
+static int g_pm_max_k = 128;
+bool use_pm(const GemmPlan &pl) {
+    return pl.k <= g_pm_max_k && (int64_t)pl.m * pl.n <= (1LL << 20) && pl.stages_per_interval == 0 &&
+           !(pl.flags & (BF16X_ACC_IN | BF16X_ACC_OUT)) && !pl.scaled && !pl.fp64 && !pl.split_acc && !pl.fused_a &&
+           pl.tile_n != 192;
+}
+
 bool fused_a_ok(const GemmPlan &pl) {
     const int cg = pl.cta_group ? pl.cta_group : kDefaultCtaGroup;
     if (cg != 2 || pl.fp64 || pl.split_acc || pl.scaled || pl.k <= 0 || pl.tile_n == 192 || !pl.Af) return false;
+    if (use_pm(pl)) return false;    // short k: the promote-every-MMA schedule instead
     if ((reinterpret_cast<uintptr_t>(pl.Af) & 15u) || pl.lda % 4) return false;
     const bool mc2 = pl.multicast == 2 || (pl.multicast == 0 && (int64_t)pl.m * pl.n >= 12288LL * 12288LL);
     return !mc2;
@@ -147,3 +161,5 @@ extern "C" void bf16x_red_add(int mode) { bf16x::g_red_add = mode; }
 extern "C" void bf16x_gemm_debug(int bits) { bf16x::g_gemm_debug = bits; }
 // testing hook: device buffer of >= 32 * grid uint64 for the dbg bit 1 timeline (tools/gemm_trace.py)
 extern "C" void bf16x_gemm_trace(unsigned long long *buf) { bf16x::g_gemm_trace = buf; }
+// testing / tuning hook: largest k for the promote-every-MMA schedule (0: never)
+extern "C" void bf16x_pm_max_k(int k) { bf16x::g_pm_max_k = k; }

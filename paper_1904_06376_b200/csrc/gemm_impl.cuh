@@ -240,6 +240,25 @@ __device__ __forceinline__ void issue_interval(uint32_t d_big, uint32_t d_small,
     for (int h = 0; h < H; ++h) if (h < nh) mma(0, 0, h);                                  // bin 0
 }
 
+// The variant's products over nh K=16 halves in the issue order of issue_interval (bands
+// smallest bin first; every band over all nh halves; the band's pairs in order).
+template <int V, typename F>
+__device__ __forceinline__ void for_each_product(int nh, F &&f) {
+    if constexpr (V == 9)
+        for (int h = 0; h < nh; ++h) f(2, 2, h);
+    if constexpr (V >= 8)
+        for (int h = 0; h < nh; ++h) { f(1, 2, h); f(2, 1, h); }
+    if constexpr (V == 7)
+        for (int h = 0; h < nh; ++h) f(1, 2, h);
+    if constexpr (V >= 6)
+        for (int h = 0; h < nh; ++h) { f(0, 2, h); f(1, 1, h); f(2, 0, h); }
+    if constexpr (V == 5)
+        for (int h = 0; h < nh; ++h) { f(0, 2, h); f(1, 1, h); }
+    if constexpr (V >= 3)
+        for (int h = 0; h < nh; ++h) { f(0, 1, h); f(1, 0, h); }
+    for (int h = 0; h < nh; ++h) f(0, 0, h);
+}
+
 // MC = number of CTA pairs per cluster sharing the B tile (1, or 2: two vertically adjacent
 // 256 x BN tiles; each pair loads half of every B slice and multicasts it to both pairs).
 // GD ("d" variants, R30; requires SA): the bins >= 1 and bin 0 are promoted into two separate
@@ -250,11 +269,18 @@ __device__ __forceinline__ void issue_interval(uint32_t d_big, uint32_t d_small,
 // thread t = row t of the CTA's 128 A rows) into the A half of the piece ring; B's pieces come
 // from the pre-pass by TMA as usual.  The piece-ring "full" barrier counts the leader's
 // expect-tx arrival (B bytes) plus the converters' arrivals of both CTAs.
-template <int CG, int V, int BN, int S, int MC, bool SA, bool GD = false, bool FA = false>
+// PM (promote every MMA, short k): every K=16 MMA of every product is its own promotion unit --
+// the MMA overwrites a TMEM buffer and the epilogue adds it into G with FP32 round-to-nearest --
+// so no tensor-core accumulation ever spans more than 16 products, and the units of a tile (all
+// its k, at most S stages) go bin by bin, smallest first: G collects the small bins before bin 0,
+// the paper's "bins added from smallest to largest" at the promotion level
+// (R24).
+template <int CG, int V, int BN, int S, int MC, bool SA, bool GD = false, bool FA = false, bool PM = false>
 __global__ void __launch_bounds__(FA ? kThreadsFused : kThreads, 1)
     gemm_split_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                       const __grid_constant__ CUtensorMap tmC, const KParams p) {
     using Cf = Cfg<CG, V, BN>;
+    static_assert(!PM || (MC == 1 && !SA && !GD && !FA && BN == 256), "PM: plain kernel");
     constexpr int NST = FA ? CfgFA<V>::STAGES : Cf::STAGES;   // piece ring stages
     constexpr int NF = FA ? CfgFA<V>::FSTAGES : 0;            // FP32 ring stages (fused A)
     constexpr int F32_STAGE = kF32Tile;                       // FP32 ring stage bytes
@@ -406,6 +432,47 @@ __global__ void __launch_bounds__(FA ? kThreadsFused : kThreads, 1)
                 Work w;
                 while (it.next(p, w)) {
                     const int kb_end = min(p.nkb, w.i1 * S);
+                    if constexpr (PM) {
+                        // the whole tile (k <= 32 S) at once: wait for its stages, issue every
+                        // product of every K=16 half as its own unit, bins smallest first
+                        const int ns = kb_end - w.i0 * S;
+                        uint64_t ad[S], bd[S];
+                        int stg[S];
+#pragma unroll
+                        for (int q = 0; q < S; ++q) {
+                            stg[q] = stage;
+                            if (q < ns) {
+                                mbar_wait(&full[stage], phase);
+                                ad[q] = smem_desc_kmajor(smem_u32(sA + stage * Cf::A_STAGE), kSwizzleAtom, 4);
+                                bd[q] = smem_desc_kmajor(smem_u32(sB + stage * Cf::B_STAGE), kSwizzleAtom, 4);
+                                if (++stage == NST) { stage = 0; phase ^= 1u; }
+                            } else {
+                                ad[q] = ad[0];
+                                bd[q] = bd[0];
+                            }
+                        }
+                        tc_fence_after();
+                        const int nh = (p.k - w.i0 * S * kBK + kUK - 1) / kUK;   // K=16 halves inside k
+                        for_each_product<V>(nh, [&](int i, int j, int h) {
+                            const uint32_t buf = acc_it & 1u, apar = (acc_it >> 1) & 1u;
+                            mbar_wait(&acc_empty[buf], apar ^ 1u);
+                            tc_fence_after();
+                            const int q = h >> 1, kk = h & 1;
+                            uint64_t a0 = ad[0], b0 = bd[0];
+#pragma unroll
+                            for (int r = 1; r < S; ++r)
+                                if (q == r) { a0 = ad[r]; b0 = bd[r]; }
+                            umma_bf16_elect<CG>(tmem_base + buf * kTmemBufStride,
+                                                a0 + (uint64_t)((i * Cf::A_PIECE + kk * (kUK * 2)) >> 4),
+                                                b0 + (uint64_t)((j * Cf::B_PIECE + kk * (kUK * 2)) >> 4), idesc, 0u);
+                            umma_commit_elect<CG>(&acc_full[buf]);
+                            ++acc_it;
+                        });
+#pragma unroll
+                        for (int q = 0; q < S; ++q)
+                            if (q < ns) umma_commit_elect<CG>(&empty[stg[q]]);
+                        continue;
+                    }
                     for (int kb = w.i0 * S; kb < kb_end; kb += S, ++acc_it) {
                         const int ns = min(S, kb_end - kb);
                         const uint32_t buf = acc_it & 1u, apar = (acc_it >> 1) & 1u;
@@ -491,6 +558,31 @@ __global__ void __launch_bounds__(FA ? kThreadsFused : kThreads, 1)
                 for (int j = 0; j < NG * EC; ++j) G[j] = 0.f;
             }
             const int kb_end = min(p.nkb, w.i1 * S);
+            if constexpr (PM) {
+                {
+                    const int units = V * ((p.k - w.i0 * S * kBK + kUK - 1) / kUK);   // products x halves
+                    for (int u = 0; u < units; ++u, ++acc_it) {
+                        const uint32_t buf = acc_it & 1u, apar = (acc_it >> 1) & 1u;
+                        mbar_wait(&acc_full[buf], apar);
+                        tc_fence_after();
+                        const uint32_t taddr = tm_lane + buf * kTmemBufStride;
+#pragma unroll
+                        for (int c = 0; c < EC / 16; ++c) {
+                            float v[16];
+                            tmem_ld16(taddr + c * 16, v);
+                            tmem_ld_wait();
+#pragma unroll
+                            for (int j = 0; j < 16; ++j) G[c * 16 + j] = __fadd_rn(G[c * 16 + j], v[j]);
+                        }
+                        tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) {
+                            if (CG == 1 || rank == 0) mbar_arrive(&acc_empty[buf]);
+                            else mbar_arrive_cluster(&acc_empty[buf], pair * CG);
+                        }
+                    }
+                }
+            } else
             for (int kb = w.i0 * S; kb < kb_end; kb += S, ++acc_it) {
                 const uint32_t buf = acc_it & 1u, apar = (acc_it >> 1) & 1u;
                 mbar_wait(&acc_full[buf], apar);
@@ -714,13 +806,13 @@ int make_f32_map(CUtensorMap *map, const float *base, int rows, int cols, int64_
 int sk_workspace(cudaStream_t st, size_t ws_floats, size_t nflags, float **ws, unsigned int **flags,
                  unsigned int *epoch);
 
-template <int CG, int V, int BN, int S, int MC, bool SA = false, bool GD = false, bool FA = false>
+template <int CG, int V, int BN, int S, int MC, bool SA = false, bool GD = false, bool FA = false, bool PM = false>
 int launch_t(const GemmPlan &pl, cudaStream_t st) {
     using Cf = Cfg<CG, V, BN>;
     constexpr int CL = CG * MC;
     constexpr int THREADS = FA ? kThreadsFused : kThreads;
     constexpr int SMEM = FA ? CfgFA<V>::SMEM : Cf::SMEM;
-    auto kern = gemm_split_kernel<CG, V, BN, S, MC, SA, GD, FA>;
+    auto kern = gemm_split_kernel<CG, V, BN, S, MC, SA, GD, FA, PM>;
     CUtensorMap tmA, tmB, tmC;
     int rc;
     if constexpr (FA) {
@@ -876,6 +968,11 @@ int launch_s(const GemmPlan &pl, cudaStream_t st) {
     // Short k (<= 128): the whole product is one or two intervals, so the tensor core's
     // truncating accumulation dominates the error; 32-k intervals halve it (measured wide
     // exponents, k = 64: max ratio to the oracle 2.07 -> 1.66) at no cost that matters.
+    // Short k (<= pm_max_k, library schedule): every MMA promoted on its own (PM above) -- the
+    // accuracy of configs[0]-sized products then no longer depends on the tensor core's
+    // truncating accumulation across products
+    if (s == 0 && use_pm(pl) && (pl.k + kBK - 1) / kBK <= std::min(4, Cfg<CG, V, 256>::STAGES))
+        return launch_t<CG, V, 256, 4, 1, false, false, false, true>(pl, st);
     if (s != 1 && s != 2) s = (CG == 2 && (pl.k > 128 || carry)) ? 2 : 1;
     if (s == 2 && Cfg<CG, V, 256>::STAGES < 4) s = 1;
     // "d" variants (R30): 2-CTA pairs, tile N 128, split accumulators, FP64 collection, 64-k

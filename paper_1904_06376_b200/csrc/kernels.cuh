@@ -48,6 +48,8 @@ int launch_gemm_pieces(const GemmPlan &p, cudaStream_t st);
 // Whether the fused-A kernel can run this plan (2-CTA pairs, tile N 256, no multicast / split
 // accumulators / FP64 collection / scaled pieces, A 16-byte aligned with lda % 4 == 0).
 bool fused_a_ok(const GemmPlan &p);
+// Whether the library schedule promotes every MMA on its own (short k; gemm_impl.cuh PM).
+bool use_pm(const GemmPlan &p);
 int launch_scale(int m, int n, float beta, float *C, int ldc, cudaStream_t st);
 int pieces_a(int variant);   // BF16 pieces of A / B for a variant (x5: 2 / 3)
 int pieces_b(int variant);

@@ -35,11 +35,13 @@ def _gpu(A, B, variant):
 
 
 def test_config0_64cubed(orc):
-    """Uniform arm (configs[0] proper): GPU <= 2x oracle on every seed.  Wide / Gaussian
-    exponent arms: the tensor core truncates every MMA step's addends to the largest one's
-    24-bit window (K3 probe) where the oracle rounds each FMA to nearest, so single seeds can
-    exceed 2x (DESIGN.md section 7 "accuracy envelope"); there the test requires the mean ratio
-    over the 20 seeds to be <= 2 and records the maximum."""
+    """Uniform and wide-exponent arms: GPU <= 2x oracle on every seed (the library promotes
+    every MMA on its own at this size, smallest bins first, so the tensor core's truncating
+    accumulation spans one K=16 step only).  Gaussian-exponent arm: one MMA step still
+    truncates its 16 addends where the oracle rounds each FMA to nearest, and a Gaussian C is
+    dominated by single products on which the oracle can be within 0.2 ulp by luck, so single
+    seeds exceed 2x (reading R24); there the mean ratio over the 20 seeds
+    must be <= 2 and the maximum is recorded."""
     seeds = {"uniform": range(0, 20), "wide": range(100, 120), "gauss": range(200, 220)}
     table = {}
     for dist, ss in seeds.items():
@@ -53,7 +55,7 @@ def test_config0_64cubed(orc):
             for v in (3, 6, 8, 9):
                 eg = orc.normwise_error(_gpu(A, B, v), C64, A, B)
                 eo = orc.normwise_error(orc.gemm(A, B, variant=v), C64, A, B)
-                if dist == "uniform":
+                if dist in ("uniform", "wide"):
                     assert eg <= RATIO * eo, (dist, s, v, eg, eo)
                 errs[f"gpu{v}"].append(eg)
                 errs[f"orc{v}"].append(eo)

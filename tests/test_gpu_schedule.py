@@ -120,10 +120,8 @@ def test_elementwise_error_bound_p321(dist, k, variant):
 
 # ---------------------------------------------------------------------------------------
 # 3. schedule conformance (bit for bit against tests/tc_model.py)
-def _interval(variant, cg, spi, k):
-    """Promotion interval the dispatcher picks (csrc/gemm_impl.cuh launch_s): a forced spi of
-    1 or 2 stages of 32 k, unless the 2-stage ring would have fewer than 4 stages (tile N 256
-    per CTA with cta_group 1 and 3 pieces of B: 3 stages) -> 1."""
+def _stages(variant, cg):
+    """Piece-ring stages of the kernel (csrc/gemm_impl.cuh Cfg)."""
     pa, pb = tc_model.PIECES[variant]
     if cg == 1:
         stage = pa * 128 * 64 + pb * 256 * 64
@@ -133,7 +131,20 @@ def _interval(variant, cg, spi, k):
     stages = (base - 32768) // stage                  # 32 KB: the C staging buffers ...
     if stages < 4:
         stages = base // stage                        # ... only where 4 stages remain with them
-    stages = min(8, stages)
+    return min(8, stages)
+
+
+def _uses_pm(variant, cg, k, m=0, n=0):
+    """The library's automatic schedule promotes every MMA at k <= 128 on outputs of at most
+    2^20 elements when the tile's k fits the ring (gemm.cu use_pm, launch_s)."""
+    return k <= 128 and m * n <= (1 << 20) and -(-k // 32) <= min(4, _stages(variant, cg))
+
+
+def _interval(variant, cg, spi, k):
+    """Promotion interval the dispatcher picks (csrc/gemm_impl.cuh launch_s): a forced spi of
+    1 or 2 stages of 32 k, unless the 2-stage ring would have fewer than 4 stages (tile N 256
+    per CTA with cta_group 1 and 3 pieces of B: 3 stages) -> 1."""
+    stages = _stages(variant, cg)
     s = spi if spi in (1, 2) else (2 if (cg == 2 and k > 128) else 1)
     if s == 2 and stages < 4:
         s = 1
@@ -157,14 +168,40 @@ def test_kernel_equals_schedule_model(shape, dist, variant, cg, spi):
 @pytest.mark.parametrize("variant", [3, 6, 9])
 def test_kernel_equals_schedule_model_default(variant):
     """The library's own choice of schedule (no tuning override) on configs[0]'s 64^3 arms and
-    a k = 1000 problem: 32-k intervals at k <= 128, 64-k intervals above (2-CTA pairs)."""
+    a k = 1000 problem: every MMA promoted on its own at k <= 128 (PM), 64-k intervals above
+    (2-CTA pairs)."""
     for (m, n, k) in ((64, 64, 64), (96, 160, 1000)):
         for dist in ("uniform", "wide", "gauss"):
             A = synthetic.by_name(dist, m, k, seed=3)
             B = synthetic.by_name(dist, k, n, seed=4)
             G = _gpu(A, B, variant)
-            M = tc_model.simulate(A, B, variant, interval=32 if k <= 128 else 64)
+            if k <= 128:
+                M = tc_model.simulate(A, B, variant, interval=128, promote_every_mma=True)
+            else:
+                M = tc_model.simulate(A, B, variant, interval=64)
             assert np.array_equal(G.view(np.uint32), M.view(np.uint32)), (m, n, k, dist)
+
+
+@pytest.mark.parametrize("cg", [1, 2])
+@pytest.mark.parametrize("variant", [1, 3, 5, 6, 7, 8, 9])
+@pytest.mark.parametrize("shape", [(129, 257, 33), (300, 200, 128), (64, 600, 17)])
+def test_promote_every_mma_equals_model(shape, variant, cg):
+    """Short k (library schedule, k <= 128): each K=16 MMA of each product overwrites a TMEM
+    buffer and is added into G with FP32 round-to-nearest in issue order -- bins smallest first
+    over the whole k of the tile, then the halves, then the band's pairs -- bit for bit the
+    model's promote_every_mma schedule with one group spanning k, ragged k included (a last
+    K=16 half cut short)."""
+    m, n, k = shape
+    for dist in ("uniform", "gauss"):
+        A = synthetic.by_name(dist, m, k, seed=m + k + variant)
+        B = synthetic.by_name(dist, k, n, seed=n + k)
+        G = _gpu(A, B, variant, cg=cg)
+        if _uses_pm(variant, cg, k, m, n):
+            M = tc_model.simulate(A, B, variant, interval=128, promote_every_mma=True)
+        else:                                         # the tile's k does not fit the ring
+            M = tc_model.simulate(A, B, variant, interval=_interval(variant, cg, 0, k))
+        bad = G.view(np.uint32) != M.view(np.uint32)
+        assert not bad.any(), (dist, int(bad.sum()))
 
 
 def test_stream_k_equals_model():
