@@ -4,12 +4,15 @@
 
 Columns: ratio of normwise errors ||C - C64||_F / (||A||_F ||B||_F), schedule / paper order
 (tc_model.sequential: Z^(i,j) summed in FP32 RN in increasing k, bins smallest first):
-  kernel     the library's schedule (32-k intervals at k <= 128, one accumulator, bands
-             smallest first, RN promotion)
+  kernel     the library's schedule at this size since r08 (= pem-tile below)
+  i32        r07's schedule (32-k intervals at k <= 128, one accumulator, bands smallest first,
+             RN promotion)
   i16 / i64  16-k / 64-k promotion intervals
   sa16/sa32  bin 0 in its own accumulator (split accumulators), 16 / 32-k intervals
-  pem        every MMA step promoted on its own (no accumulation inside the tensor core
-             beyond one K=16 step)
+  pem-32     every MMA step promoted on its own (no accumulation inside the tensor core beyond
+             one K=16 step), bins smallest first within each 32-k stage
+  pem-tile   the same, bins smallest first over the tile's whole k (the r08 kernel for k <= 128
+             on small outputs)
   rev-k      the paper's own algorithm with k summed in decreasing order (an equally valid
              sequential order): how far the per-case ratio moves with the order alone.
 Writes profiles/r08/accuracy_study.txt."""
@@ -25,9 +28,9 @@ import synthetic
 import tc_model as tm
 
 SEEDS = {"uniform": range(0, 20), "wide": range(100, 120), "gauss": range(200, 220)}
-SCHED = {"kernel": dict(interval=32), "i16": dict(interval=16), "i64": dict(interval=64),
-         "sa16": dict(interval=16, split_acc=True), "sa32": dict(interval=32, split_acc=True),
-         "pem": dict(promote_every_mma=True)}
+SCHED = {"kernel": dict(interval=128, promote_every_mma=True), "i32": dict(interval=32), "i16": dict(interval=16),
+         "i64": dict(interval=64), "sa16": dict(interval=16, split_acc=True), "sa32": dict(interval=32, split_acc=True),
+         "pem-32": dict(interval=32, promote_every_mma=True)}
 
 
 def nerr(C, C64, A, B):
