@@ -411,7 +411,7 @@ def run_ours(args):
         "e2e": {"value": e2e_value, "unit": "TFLOPS", "h2d_bytes_per_step": 4 * (m * k + k * n_loc),
                 "d2h_bytes_per_step": 4 * m * n_loc, "steps": e2e_steps,
                 "api": "bf16x_gemm_host (pinned host buffers; H2D A, B + split + GEMM + D2H C, pipelined over "
-                       "column chunks)" + ("; each rank its own column block" if world > 1 else "")},
+                       "row blocks of A x column blocks of B)" + ("; each rank its own column block" if world > 1 else "")},
         "gpu_launches": launches,
         "gpu_launches_per_step": launches / args.steps,
         "clocks": clocks,

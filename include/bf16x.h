@@ -163,6 +163,12 @@ int bf16x_gemm_ex(int m, int n, int k, float alpha, const float *A, int lda,
  * pipelined over column chunks of B/C (width n / min(8, n/512) rounded up to 256): A is
  * copied and split once, each chunk's B copy overlaps the previous chunk's GEMM and each
  * chunk's C copy-back overlaps the next; every chunk equals bf16x_gemm on that column block.
+ * With beta == 0, m, n >= 4096 and a GEMM not much shorter than the copy-in
+ * (m*n*variant/(m+n) >= 32400) the pipeline is two-dimensional instead: A in row blocks and
+ * B in column blocks (each min(8, dim/1024) blocks, multiples of 256), copied in alternately,
+ * each split once as it lands; block (i, j) of C is computed as soon as A_i and B_j are split
+ * and copied back as soon as it is done.  Every element of C then equals
+ * bf16x_gemm_ex(..., BF16X_NO_STREAM_K) (R32: shape-independent results).
  * Pinned host memory is needed for the copies to overlap (pageable memory still works). */
 int bf16x_gemm_host(int m, int n, int k, float alpha, const float *A_host, int lda,
                     const float *B_host, int ldb, float beta, float *C_host, int ldc, int variant);

@@ -315,6 +315,13 @@ static int tl_record(int slot, cudaStream_t s) {
     return cudaEventRecord(g_tl_ev[slot], s) != cudaSuccess;
 }
 static cudaEvent_t g_ev_a = nullptr, g_ev_b[kHostChunks], g_ev_c[kHostChunks], g_ev_done = nullptr;
+// 2D block pipeline (beta == 0, large m and n): row blocks of A x column blocks of B
+constexpr int kH2dMax = 8;
+static int g_host_2d = 1;                               // bf16x_host_2d hook: 0 = column chunks only
+static cudaStream_t g_s_split = nullptr;
+static cudaEvent_t g_ev_ar[kH2dMax], g_ev_bc[kH2dMax], g_ev_as[kH2dMax], g_ev_bs[kH2dMax];
+static cudaEvent_t g_ev_blk[kH2dMax * kH2dMax];
+static bool g_h2d_init = false;
 
 static int ensure(float **p, size_t *cap, size_t n) {
     if (n <= *cap) return BF16X_SUCCESS;
@@ -363,6 +370,122 @@ static int host_pipeline_init() {
 // Each chunk is an independent GEMM: its columns equal bf16x_gemm on that column block without
 // the stream-K schedule (chunk width: n / min(12, n / 256) rounded up to 256 columns when
 // m*k >= 2^20 and n >= 1024).
+// 2D block pipeline for beta == 0: A is cut into R row blocks and B into Cb column blocks
+// (<= 8 each, multiples of 256); the copy-in stream sends A_0, B_0, A_1, B_1, ... so block
+// (i, j) of C can start as soon as A_i and B_j have landed -- after 1/R + 1/Cb of the inputs
+// instead of all of A -- each block of A / B is split once (K-major pieces at its offset, on a
+// split stream), the block GEMMs run on 4 compute streams in order of readiness, and each C block
+// goes back as soon as its GEMM is done.  PCIe carries A and B once each; every block of C
+// equals bf16x_gemm_ex(..., BF16X_NO_STREAM_K) on the same rows and columns.
+static int host_gemm_2d(int m, int n, int k, float alpha, const float *A_host, int lda, const float *B_host, int ldb,
+                        float *C_host, int ldc, int variant, cudaStream_t st) {
+    cudaError_t e = cudaSuccess;
+    if (!g_h2d_init) {
+        e = cudaStreamCreateWithFlags(&g_s_split, cudaStreamNonBlocking);
+        for (int i = 0; i < kH2dMax && e == cudaSuccess; ++i) {
+            e = cudaEventCreateWithFlags(&g_ev_ar[i], cudaEventDisableTiming);
+            if (e == cudaSuccess) e = cudaEventCreateWithFlags(&g_ev_bc[i], cudaEventDisableTiming);
+            if (e == cudaSuccess) e = cudaEventCreateWithFlags(&g_ev_as[i], cudaEventDisableTiming);
+            if (e == cudaSuccess) e = cudaEventCreateWithFlags(&g_ev_bs[i], cudaEventDisableTiming);
+        }
+        for (int i = 0; i < kH2dMax * kH2dMax && e == cudaSuccess; ++i)
+            e = cudaEventCreateWithFlags(&g_ev_blk[i], cudaEventDisableTiming);
+        if (e != cudaSuccess) {
+            set_cuda_error(e, "gemm_host 2d init");
+            return BF16X_ERR_CUDA;
+        }
+        g_h2d_init = true;
+    }
+    const int pa = pieces_a(variant), pb = pieces_b(variant);
+    const int64_t kp = round_up8(k);
+    int R = std::max(1, std::min(kH2dMax, m / 1024)), Cb = std::max(1, std::min(kH2dMax, n / 1024));
+    if (g_host_2d > 1) {                                     // tuning hook: explicit (R << 4) | Cb
+        R = std::max(1, std::min(kH2dMax, g_host_2d >> 4));
+        Cb = std::max(1, std::min(kH2dMax, g_host_2d & 15));
+    }
+    const int mb = ((m + R - 1) / R + 255) / 256 * 256, nbk = ((n + Cb - 1) / Cb + 255) / 256 * 256;
+    R = (m + mb - 1) / mb;
+    Cb = (n + nbk - 1) / nbk;
+    int rc = ensure(&g_hAp, &g_hAp_n, ((size_t)pa * m * kp + 1) / 2);
+    if (!rc) rc = ensure(&g_hBp, &g_hBp_n, ((size_t)pb * n * kp + 1) / 2);
+    if (rc) return rc;
+    uint16_t *ap = reinterpret_cast<uint16_t *>(g_hAp), *bp = reinterpret_cast<uint16_t *>(g_hBp);
+    const int64_t a_plane = (int64_t)m * kp, b_plane = (int64_t)n * kp;
+    e = cudaEventRecord(g_ev_done, st);                      // the caller's earlier work first
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(g_s_in, g_ev_done, 0);
+    for (int t = 0; t < std::max(R, Cb) && e == cudaSuccess; ++t) {
+        if (t < R) {
+            const int r0 = t * mb, mi = std::min(mb, m - r0);
+            e = cudaMemcpy2DAsync(g_hA + r0, (size_t)m * 4, A_host + r0, (size_t)lda * 4, (size_t)mi * 4, k,
+                                  cudaMemcpyHostToDevice, g_s_in);
+            if (e == cudaSuccess) e = cudaEventRecord(g_ev_ar[t], g_s_in);
+        }
+        if (t < Cb && e == cudaSuccess) {
+            const int c0 = t * nbk, nj = std::min(nbk, n - c0);
+            e = cudaMemcpy2DAsync(g_hB + (size_t)c0 * k, (size_t)k * 4, B_host + (size_t)c0 * ldb, (size_t)ldb * 4,
+                                  (size_t)k * 4, nj, cudaMemcpyHostToDevice, g_s_in);
+            if (e == cudaSuccess) e = cudaEventRecord(g_ev_bc[t], g_s_in);
+        }
+    }
+    // splits, in arrival order
+    for (int t = 0; t < std::max(R, Cb) && e == cudaSuccess && !rc; ++t) {
+        if (t < R) {
+            const int r0 = t * mb, mi = std::min(mb, m - r0);
+            e = cudaStreamWaitEvent(g_s_split, g_ev_ar[t], 0);
+            uint16_t *a0 = ap + (int64_t)r0 * kp;
+            if (e == cudaSuccess)
+                rc = launch_split(mi, k, g_hA + r0, m, a0, pa > 1 ? a0 + a_plane : nullptr, pa > 2 ? a0 + 2 * a_plane : nullptr,
+                                  kp, true, g_s_split);
+            if (!rc && e == cudaSuccess) e = cudaEventRecord(g_ev_as[t], g_s_split);
+        }
+        if (t < Cb && e == cudaSuccess && !rc) {
+            const int c0 = t * nbk, nj = std::min(nbk, n - c0);
+            e = cudaStreamWaitEvent(g_s_split, g_ev_bc[t], 0);
+            uint16_t *b0 = bp + (int64_t)c0 * kp;
+            if (e == cudaSuccess)
+                rc = launch_split(k, nj, g_hB + (size_t)c0 * k, k, b0, pb > 1 ? b0 + b_plane : nullptr,
+                                  pb > 2 ? b0 + 2 * b_plane : nullptr, kp, false, g_s_split);
+            if (!rc && e == cudaSuccess) e = cudaEventRecord(g_ev_bs[t], g_s_split);
+        }
+    }
+    // block GEMMs in order of readiness (shell t: blocks (t, 0..t) then (0..t-1, t)), C blocks back
+    int blk = 0;
+    for (int t = 0; t < std::max(R, Cb) && e == cudaSuccess && !rc; ++t) {
+        for (int u = 0; u <= 2 * t && e == cudaSuccess && !rc; ++u) {
+            const int i = u <= t ? t : u - t - 1, j = u <= t ? u : t;
+            if (i >= R || j >= Cb) continue;
+            const int r0 = i * mb, mi = std::min(mb, m - r0), c0 = j * nbk, nj = std::min(nbk, n - c0);
+            cudaStream_t cs = g_s_comp[blk % kHostStreams];
+            e = cudaStreamWaitEvent(cs, g_ev_as[i], 0);
+            if (e == cudaSuccess) e = cudaStreamWaitEvent(cs, g_ev_bs[j], 0);
+            if (e != cudaSuccess) break;
+            rc = gemm_core(mi, nj, k, alpha, nullptr, m, nullptr, k, 0.f, g_hC + r0 + (size_t)c0 * m, m, variant, 0u,
+                           ap + (int64_t)r0 * kp, kp, a_plane, bp + (int64_t)c0 * kp, kp, b_plane, nullptr, nullptr, 0,
+                           cs, 0, false, 0);
+            if (rc) break;
+            cudaEvent_t ev = g_ev_blk[i * kH2dMax + j];
+            e = cudaEventRecord(ev, cs);
+            if (e == cudaSuccess) e = cudaStreamWaitEvent(g_s_out, ev, 0);
+            if (e == cudaSuccess)
+                e = cudaMemcpy2DAsync(C_host + r0 + (size_t)c0 * ldc, (size_t)ldc * 4, g_hC + r0 + (size_t)c0 * m,
+                                      (size_t)m * 4, (size_t)mi * 4, nj, cudaMemcpyDeviceToHost, g_s_out);
+            ++blk;
+        }
+    }
+    for (int q = 0; q < kHostStreams && e == cudaSuccess; ++q) {   // the library stream joins
+        e = cudaEventRecord(g_ev_end[q], g_s_comp[q]);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(st, g_ev_end[q], 0);
+    }
+    if (rc) return rc;
+    if (e == cudaSuccess) e = cudaStreamSynchronize(g_s_out);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) {
+        set_cuda_error(e, "gemm_host 2d pipeline");
+        return BF16X_ERR_CUDA;
+    }
+    return BF16X_SUCCESS;
+}
+
 int bf16x_gemm_host(int m, int n, int k, float alpha, const float *A_host, int lda, const float *B_host, int ldb,
                     float beta, float *C_host, int ldc, int variant) {
     int a = gemm_args(m, n, k, lda, ldb, ldc, variant);
@@ -383,6 +506,15 @@ int bf16x_gemm_host(int m, int n, int k, float alpha, const float *A_host, int l
         nchunk = std::max(1, std::min(std::min(g_host_chunks, kHostChunks), n / 256));
     if (nchunk > 1) {
         if ((rc = host_pipeline_init())) return rc;
+        // 2D blocks pay off once the GEMM is not much shorter than the copy-in (tools/e2e_2d_sweep.py:
+        // 16384^3 x6 49 vs 56 ms, x9 60 vs 68; 8192^3 x6 / 16384^3 x3 the column chunks by 1-4 %):
+        // t_gemm / t_in ~ (2mnk v / 1.35 PFLOP/s) / (4 (mk + kn) / 50 GB/s) >= 0.6, i.e.
+        // m n v / (m + n) >= 32400, v = the variant's number of products
+        const bool two_d = g_host_2d > 1 ||
+                           (g_host_2d == 1 && beta == 0.f && m >= 4096 && n >= 4096 &&
+                            (double)m * n * variant / ((double)m + n) >= 32400.0);
+        if (two_d && beta == 0.f)
+            return host_gemm_2d(m, n, k, alpha, A_host, lda, B_host, ldb, C_host, ldc, variant, st);
         if ((rc = ensure(&g_hAp, &g_hAp_n, ((size_t)p * m * kp + 1) / 2))) return rc;
     }
     cudaError_t e = cudaSuccess;
@@ -550,6 +682,7 @@ int bf16x_host_timeline(int on, float *ms, int cap) {
     return n;
 }
 void bf16x_host_chunks(int n) { g_host_chunks = n > 0 ? n : 12; }   // bf16x_gemm_host pipeline depth
+void bf16x_host_2d(int on) { g_host_2d = on; }   // 0 off, 1 auto (default), >1 forced for beta = 0 with (R<<4)|Cb blocks
 void bf16x_multicast(int pairs) { g_multicast = pairs; }   // 0 = auto, 1 = off, 2 = on
 void bf16x_tune(int cta_group, int tile_n, int stages_per_interval) {
     g_force_cg = cta_group;

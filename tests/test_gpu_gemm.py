@@ -187,6 +187,38 @@ def test_host_api_pipelined_chunks(orc, beta, depth):
     assert orc.normwise_error(Gh[:, cols], C64, A, B[:, cols]) <= RATIO * eo
 
 
+@pytest.mark.parametrize("variant", [3, 6, 9])
+def test_host_api_2d_blocks(orc, variant):
+    """bf16x_gemm_host's 2D block pipeline (forced by the hook bf16x_host_2d((3 << 4) | 3): 3 x 3
+    blocks of 1792 / 1536, ragged last row and column blocks): equals the device GEMM with
+    BF16X_NO_STREAM_K bit for bit, and so do the column-chunk pipeline (hook 0) and the library
+    default; sampled columns meet the oracle bar."""
+    m, k, n = 4700, 520, 4400
+    A = synthetic.uniform(m, k, seed=31)
+    B = synthetic.uniform(k, n, seed=32)
+    bx.lib().bf16x_host_2d((3 << 4) | 3)
+    try:
+        Gh = bx.gemm_host(A, B, alpha=0.75, variant=variant)
+    finally:
+        bx.lib().bf16x_host_2d(1)
+    Ad = torch.from_numpy(np.asfortranarray(A)).cuda()
+    Bd = torch.from_numpy(np.asfortranarray(B)).cuda()
+    Gd = bx.gemm(Ad, Bd, alpha=0.75, variant=variant, no_stream_k=True).cpu().numpy()
+    assert np.array_equal(Gh, Gd)
+    bx.lib().bf16x_host_2d(0)
+    try:
+        Gc = bx.gemm_host(A, B, alpha=0.75, variant=variant)
+    finally:
+        bx.lib().bf16x_host_2d(1)
+    assert np.array_equal(Gc, Gd)
+    assert np.array_equal(bx.gemm_host(A, B, alpha=0.75, variant=variant), Gd)
+    cols = np.array([0, 1535, 1536, 3071, 3072, 4399])
+    O = orc.gemm(A, B, alpha=0.75, variant=variant, cols=cols)
+    C64 = orc.dgemm(A, B, cols=cols) * 0.75
+    eo = orc.normwise_error(O, C64, A, B[:, cols])
+    assert orc.normwise_error(Gh[:, cols], C64, A, B[:, cols]) <= RATIO * eo
+
+
 def test_bench_launch_sequence_matches_gemm():
     """bench.py's timed step (bf16x_split_operands of both operands into caller buffers, then
     bf16x_gemm_ex on the pre-split pieces) is the same computation as bf16x_gemm: bit-identical
