@@ -877,7 +877,11 @@ int launch_t(const GemmPlan &pl, cudaStream_t st) {
     // tiles (measured r06, tools/raster_probe.py: 4096^3 x6 +1.5 %, GEMM DRAM reads 830 -> 630
     // MB), 8-tall groups for wider outputs (8192^3: 8 beats 1 and 2 by 3-5 %), and groups of 2
     // super-rows on the multicast schedule of the largest outputs (16384^3 x6: 228 vs 215
-    // TFLOPS, DRAM reads ~50 vs ~85 GB per launch -- power-limited, so traffic costs clock)
+    // TFLOPS, DRAM reads ~50 vs ~85 GB per launch -- power-limited, so traffic costs clock);
+    // from 48 tile columns the row-major raster beats those groups again (r08,
+    // tools/raster_probe.py, alternating repetitions: 16384^3 x6 212.1 vs 209.7, 32768^3 212.1 vs
+    // 207.7 TFLOPS; DRAM reads 65.6 vs 65.9 GB at 16384^3 under ncu, so not a traffic effect),
+    // and below it 8-tall groups (8192^3 x6: 214.5 vs 207 TFLOPS for 2 or 1)
     kp.lazy_full = g_lazy_full;
     kp.dbg = g_gemm_debug;
     kp.trace = g_gemm_trace;
@@ -887,7 +891,7 @@ int launch_t(const GemmPlan &pl, cudaStream_t st) {
     if (!FA && Cf::EPI && !(pl.flags & BF16X_ACC_OUT) && (reinterpret_cast<uintptr_t>(pl.C) & 15u) == 0 && pl.ldc % 4 == 0 &&
         make_f32_map(&tmC, pl.C, pl.m, pl.n, pl.ldc, kEpiRows, kEpiCols, CU_TENSOR_MAP_SWIZZLE_NONE) == BF16X_SUCCESS)
         kp.tma_c = 1;
-    kp.group_m = pl.group_m > 0 ? pl.group_m : (MC == 2 ? 2 : (kp.tiles_n <= 16 ? 1 : kGroupM));
+    kp.group_m = pl.group_m > 0 ? pl.group_m : (MC == 2 ? (kp.tiles_n >= 48 ? 1 : kGroupM) : (kp.tiles_n <= 16 ? 1 : kGroupM));
     const int ncl = grid / CL;
     // (not for short k: a split tile's fix-up -- the contributor's FP32 partial written and read
     // back -- costs more than the balanced tail wins below 12 promotion intervals; measured r08,
