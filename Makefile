@@ -15,7 +15,7 @@ NVFLAGS := -O3 -std=c++17 $(GENCODE) -lineinfo -Xcompiler -fPIC -Iinclude -I$(CS
            --expt-relaxed-constexpr -Xptxas -v
 MAKEFLAGS += -j8
 
-.PHONY: all oracle lib clean trace
+.PHONY: all oracle lib clean trace variant
 all: oracle lib
 
 oracle: oracle/liboracle.so
@@ -40,6 +40,18 @@ build/trace/%.o: $(CSRC)/%.cu $(CU_HDRS)
 trace: build/trace/libbf16x.so
 build/trace/libbf16x.so: $(TRACE_OBJS)
 	$(NVCC) $(GENCODE) -shared -cudart static -o $@ $(TRACE_OBJS)
+
+# A/B build of the library with extra compile flags (probes only):
+#   make variant VDIR=build/epi4 VFLAGS=-DBF16X_EPI_NBUF=4  ->  BF16X_LIB=build/epi4/libbf16x.so
+VDIR ?= build/variant
+VFLAGS ?=
+VAR_OBJS := $(patsubst $(CSRC)/%.cu,$(VDIR)/%.o,$(CU_SRCS))
+$(VDIR)/%.o: $(CSRC)/%.cu $(CU_HDRS)
+	@mkdir -p $(VDIR)
+	$(NVCC) $(NVFLAGS) $(VFLAGS) -c -o $@ $< 2> $@.ptxas.log || (cat $@.ptxas.log; false)
+variant: $(VDIR)/libbf16x.so
+$(VDIR)/libbf16x.so: $(VAR_OBJS)
+	$(NVCC) $(GENCODE) -shared -cudart static -o $@ $(VAR_OBJS)
 
 clean:
 	rm -rf oracle/liboracle.so $(PKG)/libbf16x.so $(OBJDIR)

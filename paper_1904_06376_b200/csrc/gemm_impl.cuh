@@ -28,9 +28,18 @@ constexpr int kGroupM = 8;            // tile raster: 8 m-tiles per group for L2
 constexpr int kDefaultCtaGroup = 2;   // 2-CTA pairs, 64-k promotion interval
 constexpr int kSmemBudget = 232448 - 1024;   // 227 KB opt-in maximum
 // C epilogue staging (TMA store): per epilogue warp two buffers of 32 rows x 16 columns FP32
-constexpr int kEpiRows = 32, kEpiCols = 16;
-constexpr int kEpiBuf = kEpiRows * kEpiCols * 4;
-constexpr int kEpiBytes = kNumEpiWarps * 2 * kEpiBuf;   // 32 KB
+#ifndef BF16X_EPI_NBUF
+#define BF16X_EPI_NBUF 2
+#endif
+#ifndef BF16X_EPI_GROUP
+#define BF16X_EPI_GROUP 1
+#endif
+// kEpiGroup: the 4 warps of a column half (TMEM lane quadrants 0..3) stage one 128-row box
+constexpr bool kEpiGroup = BF16X_EPI_GROUP != 0;
+constexpr int kEpiRows = kEpiGroup ? 128 : 32, kEpiCols = 16;
+constexpr int kEpiNBuf = BF16X_EPI_NBUF;                // staging buffers per epilogue warp (group)
+constexpr int kEpiBuf = 32 * kEpiCols * 4;
+constexpr int kEpiBytes = kNumEpiWarps * kEpiNBuf * kEpiBuf;   // 32 KB
 inline int g_lazy_full = 1;           // lazy stage waits in the MMA issuer (bf16x_lazy_full hook)
 inline int g_gemm_debug = 0;          // KParams::dbg (bf16x_gemm_debug hook; tests / probes only)
 inline unsigned long long *g_gemm_trace = nullptr;   // KParams::trace (bf16x_gemm_trace hook)
@@ -667,13 +676,36 @@ __global__ void __launch_bounds__(FA ? kThreadsFused : kThreads, 1)
             // tile while the TMA engine drains (rows / columns outside C are clipped by the TMA)
             const bool radd = CG == 2 && BN == 256 && !GD && red_add;
             if (TMA_EPI && p.tma_c && !(p.flags & BF16X_ACC_OUT) && (p.beta == 0.f || radd)) {
-                if (!(p.dbg & 1)) {
-                    float *wbuf = reinterpret_cast<float *>(epi) + ew * (2 * kEpiRows * kEpiCols);
+                if (kEpiGroup && !(p.dbg & 1)) {
+                    // one 128-row x 16-column box per column half: warps quad 0..3 fill their 32
+                    // rows, warp quad 0's lane 0 issues the store
+                    float *gbuf = reinterpret_cast<float *>(epi) + half * (kEpiNBuf * kEpiRows * kEpiCols);
+                    const int grow = tm * Cf::TILE_M + (int)rank * kBM;
+                    const bool issuer = quad == 0 && lane == 0;
+#pragma unroll
+                    for (int q = 0; q < EC / kEpiCols; ++q) {
+                        float *dst = gbuf + (q % kEpiNBuf) * (kEpiRows * kEpiCols);
+                        if (issuer) bulk_wait_read<kEpiNBuf - 1>();
+                        asm volatile("bar.sync %0, 128;" ::"r"(2 + half) : "memory");
+#pragma unroll
+                        for (int j = 0; j < kEpiCols; ++j)
+                            dst[j * kEpiRows + quad * 32 + lane] = radd ? p.alpha * zval(q * kEpiCols + j)
+                                                                        : fmaf(p.alpha, zval(q * kEpiCols + j), 0.f);
+                        fence_proxy_async_smem();
+                        asm volatile("bar.sync %0, 128;" ::"r"(2 + half) : "memory");
+                        if (issuer) {
+                            if (radd) tma_reduce_add_2d(&tmC, dst, grow, col0 + q * kEpiCols);
+                            else tma_store_2d(&tmC, dst, grow, col0 + q * kEpiCols);
+                            bulk_commit();
+                        }
+                    }
+                } else if (!(p.dbg & 1)) {
+                    float *wbuf = reinterpret_cast<float *>(epi) + ew * (kEpiNBuf * kEpiRows * kEpiCols);
                     const int wrow = tm * Cf::TILE_M + (int)rank * kBM + quad * 32;
 #pragma unroll
                     for (int q = 0; q < EC / kEpiCols; ++q) {
-                        float *dst = wbuf + (q & 1) * (kEpiRows * kEpiCols);
-                        if (lane == 0) bulk_wait_read<1>();      // this buffer's store two chunks ago has read it
+                        float *dst = wbuf + (q % kEpiNBuf) * (kEpiRows * kEpiCols);
+                        if (lane == 0) bulk_wait_read<kEpiNBuf - 1>();   // this buffer's last store has read it
                         __syncwarp();
 #pragma unroll
                         for (int j = 0; j < kEpiCols; ++j)

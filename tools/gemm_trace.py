@@ -21,7 +21,8 @@ kp = (k + 7) // 8 * 8
 p = bx.PIECES[v]
 A = (torch.rand(k, m, device="cuda") * 2 - 1).t()
 B = (torch.rand(n, k, device="cuda") * 2 - 1).t()
-C = torch.empty_strided((m, n), (1, m), dtype=torch.float32, device="cuda")
+ldc = m + int(os.environ.get("LDC_PAD", "0"))
+C = torch.empty_strided((m, n), (1, ldc), dtype=torch.float32, device="cuda")
 Ap = torch.empty(p * m * kp, dtype=torch.uint16, device="cuda")
 Bp = torch.empty(p * n * kp, dtype=torch.uint16, device="cuda")
 bx._check(L.bf16x_split_operands(m, n, k, A.data_ptr(), m, B.data_ptr(), k, p, Ap.data_ptr(), kp, m * kp, Bp.data_ptr(),
@@ -30,10 +31,12 @@ tr = torch.zeros(148 * 32, dtype=torch.int64, device="cuda")
 
 
 def g():
-    bx.gemm_raw(m, n, k, 1.0, 0, m, 0, k, 0.0, C.data_ptr(), m, variant=v, A_pieces=Ap.data_ptr(), ldap=kp,
+    bx.gemm_raw(m, n, k, 1.0, 0, m, 0, k, 0.0, C.data_ptr(), ldc, variant=v, A_pieces=Ap.data_ptr(), ldap=kp,
                 a_plane=m * kp, B_pieces=Bp.data_ptr(), ldbp=kp, b_plane=n * kp)
 
 
+stg = int(os.environ.get("STAGGER", "0"))
+L.bf16x_stagger(stg, 0)
 for _ in range(3):
     g()
 torch.cuda.synchronize()
@@ -52,9 +55,14 @@ t0 = T[:, 0].min()
 R = (T - t0) / 1e3          # us since the first CTA started
 print(f"{m}x{n}x{k} x{v} dbg {extra_dbg}: event time {e0.elapsed_time(e1) * 1e3:.1f} us, CTAs traced {used.sum()}")
 print(f"  CTA start spread: {np.ptp(R[:, 0]):.2f} us; prologue (start -> griddepcontrol done): median {np.median(R[:, 1] - R[:, 0]):.2f} us")
-for t in range(9):
+tiles = ((m + 255) // 256) * ((n + 255) // 256)
+cid = np.arange(148)[used] // 2
+late = cid >= (tiles % 74 if tiles % 74 else 37)
+for grp, sel in ((("all", np.ones_like(late)),) if not stg else (("early", ~late), ("late", late))):
+  print(f" CTAs: {grp} (stagger {stg} ns)")
+  for t in range(9):
     a, b, c = R[:, 2 + 3 * t], R[:, 3 + 3 * t], R[:, 4 + 3 * t]
-    ok = (T[:, 2 + 3 * t] > 0) & (T[:, 4 + 3 * t] > 0)
+    ok = (T[:, 2 + 3 * t] > 0) & (T[:, 4 + 3 * t] > 0) & sel
     if ok.sum() == 0:
         break
     print(f"  tile {t}: first promotion at {np.median(a[ok]):7.2f} us (max {a[ok].max():7.2f}), last at {np.median(b[ok]):7.2f}, "
