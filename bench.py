@@ -191,12 +191,15 @@ def _split_gemm_step(L, bx, m, n, k, v, p, A, B, C, Ap, Bp, sh, ev=None, st=None
     kp = (k + 7) // 8 * 8
     if ev is not None:
         ev[0].record(st)
-    bx._check(L.bf16x_split_operands(m, n, k, A.data_ptr(), A.stride(1), B.data_ptr(), B.stride(1), p, Ap.data_ptr(),
-                                     kp, m * kp, Bp.data_ptr(), kp, n * kp, sh), "split_operands")
+    mp = (m + 7) // 8 * 8    # A's pieces in A's own layout (MN-major), as bf16x_gemm splits it
+    bx._check(L.bf16x_split_operands_ex(m, n, k, A.data_ptr(), A.stride(1), B.data_ptr(), B.stride(1), p,
+                                        Ap.data_ptr(), mp, mp * k, Bp.data_ptr(), kp, n * kp, bx.A_PIECES_MN, sh),
+              "split_operands_ex")
     if ev is not None:
         ev[1].record(st)
-    bx._check(L.bf16x_gemm_ex(m, n, k, 1.0, None, m, None, k, 0.0, C.data_ptr(), C.stride(1), v, flags,
-                              Ap.data_ptr(), kp, m * kp, Bp.data_ptr(), kp, n * kp, None, None, 0, sh), "gemm_ex")
+    bx._check(L.bf16x_gemm_ex(m, n, k, 1.0, None, m, None, k, 0.0, C.data_ptr(), C.stride(1), v,
+                              flags | bx.A_PIECES_MN, Ap.data_ptr(), mp, mp * k, Bp.data_ptr(), kp, n * kp, None,
+                              None, 0, sh), "gemm_ex")
     if ev is not None:
         ev[2].record(st)
 

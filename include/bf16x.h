@@ -70,6 +70,13 @@ enum {
 #define BF16X_FP64_COMBINE     8u
 #define BF16X_SPLIT_TRANSPOSED 16u
 #define BF16X_NO_STREAM_K      32u
+/* BF16X_A_PIECES_MN (gemm_ex and split_operands_ex): A's pieces are in A's own column-major
+ *   layout, as bf16x_split writes them -- element (i,l) of piece q at A_pieces[q*a_plane + i +
+ *   l*ldap], ldap >= max(1, m), ldap % 8 == 0, a_plane >= ldap*k, a_plane % 8 == 0 -- and the
+ *   tensor cores read them MN-major (tcgen05 a_major = MN, 128-byte swizzle).  The products are
+ *   the same; only the layout differs (the split of A then needs no transpose; this is the
+ *   layout bf16x_gemm uses internally). */
+#define BF16X_A_PIECES_MN      64u
 
 /* ------------------------------------------------------------------------------------
  * bf16x_split -- the 3-way decomposition of P:180-184 (section II-A):
@@ -109,6 +116,14 @@ int bf16x_split_operands(int m, int n, int k, const float *A, int64_t lda, const
                          int pieces, uint16_t *Ap, int64_t ldap, int64_t a_plane, uint16_t *Bp, int64_t ldbp,
                          int64_t b_plane, bf16x_stream_t stream);
 
+/* bf16x_split_operands with flags: BF16X_A_PIECES_MN (A split in its own layout, element (i,l) of
+ * piece q at Ap[q*a_plane + i + l*ldap], ldap >= max(1, m), a_plane >= ldap*k: both operands are
+ * then same-layout splits; this is the pre-pass bf16x_gemm runs) and BF16X_SCALED_PIECES (R29).
+ * Errors as bf16x_split_operands, plus -13 for unknown flags. */
+int bf16x_split_operands_ex(int m, int n, int k, const float *A, int64_t lda, const float *B, int64_t ldb,
+                            int pieces, uint16_t *Ap, int64_t ldap, int64_t a_plane, uint16_t *Bp, int64_t ldbp,
+                            int64_t b_plane, unsigned flags, bf16x_stream_t stream);
+
 /* ------------------------------------------------------------------------------------
  * bf16x_gemm -- C = alpha*A*B + beta*C (BLAS sgemm, transa = transb = 'N') with the
  * FP32 product emulated by BF16 x BF16 -> FP32 tensor-core products (section IV-A):
@@ -130,8 +145,8 @@ int bf16x_split_operands(int m, int n, int k, const float *A, int64_t lda, const
 int bf16x_gemm(int m, int n, int k, float alpha, const float *A, int lda,
                const float *B, int ldb, float beta, float *C, int ldc, int variant);
 
-/* Bytes of caller workspace bf16x_gemm_ex needs: 2 * (pA * m + pB * n) * round_up(k, 8), with
- * (pA, pB) the variant's pieces per operand: x1 (1,1), x3 (2,2), x5 (2,3), others (3,3). */
+/* Bytes of caller workspace bf16x_gemm_ex needs: 2 * (pA * round_up(m, 8) + pB * n) * round_up(k, 8),
+ * with (pA, pB) the variant's pieces per operand: x1 (1,1), x3 (2,2), x5 (2,3), others (3,3). */
 size_t bf16x_gemm_workspace_size(int m, int n, int k, int variant);
 
 /* Extended GEMM: explicit stream, caller workspace (NULL = library cache), optional
@@ -139,13 +154,15 @@ size_t bf16x_gemm_workspace_size(int m, int n, int k, int variant);
  *   A_pieces : NULL, or the base of pA K-major piece planes of A as written by
  *              bf16x_split_t: element (i,l) of piece q at A_pieces[q*a_plane + l + i*ldap],
  *              ldap >= k, ldap % 8 == 0, a_plane % 8 == 0, 16-byte aligned base;
- *              then A may be NULL.
+ *              with BF16X_A_PIECES_MN, planes in A's own layout as written by bf16x_split
+ *              (element (i,l) at A_pieces[q*a_plane + i + l*ldap], ldap >= m, ldap % 8 == 0,
+ *              a_plane >= ldap*k, a_plane % 8 == 0); then A may be NULL.
  *   B_pieces : NULL, or the base of pB piece planes of B as written by bf16x_split:
  *              element (l,j) of piece q at B_pieces[q*b_plane + l + j*ldbp], ldbp >= k,
  *              ldbp % 8 == 0, b_plane % 8 == 0; then B may be NULL.
  *   acc_carry: m x n FP32 (ld = ldc) used by BF16X_ACC_IN / BF16X_ACC_OUT.
  *   flags    : BF16X_ACC_IN | BF16X_ACC_OUT | BF16X_SCALED_PIECES | BF16X_FP64_COMBINE |
- *              BF16X_NO_STREAM_K (above).
+ *              BF16X_NO_STREAM_K | BF16X_A_PIECES_MN (above).
  *   workspace: NULL (the library's cache for `stream`), or ws_bytes >= bf16x_gemm_workspace_size
  *              bytes of device memory owned by the caller, not used by other work meanwhile.
  * Errors: as bf16x_gemm, plus -13 flags (unknown bits, FP64_COMBINE with ACC_* or with

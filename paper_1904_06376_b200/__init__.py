@@ -19,7 +19,7 @@ HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "bf16x.h")
 
 SUCCESS, ERR_CUDA, ERR_ALLOC, ERR_ARCH, ERR_SINGULAR, NOT_CONVERGED = 0, 1, 2, 3, 4, 5
 ACC_IN, ACC_OUT = 1, 2
-SCALED_PIECES, FP64_COMBINE, SPLIT_TRANSPOSED, NO_STREAM_K = 4, 8, 16, 32   # bf16x.h flags (R29, R30)
+SCALED_PIECES, FP64_COMBINE, SPLIT_TRANSPOSED, NO_STREAM_K, A_PIECES_MN = 4, 8, 16, 32, 64   # bf16x.h flags
 VARIANTS = (1, 3, 5, 6, 7, 8, 9)
 PIECES = {1: 1, 3: 2, 6: 3, 8: 3, 9: 3}
 
@@ -52,6 +52,8 @@ def lib() -> ctypes.CDLL:
         L.bf16x_split_t.argtypes = [_i64, _i64, _vp, _i64, _vp, _vp, _vp, _i64, _vp]
         L.bf16x_split_ex.argtypes = [_i64, _i64, _vp, _i64, _vp, _vp, _vp, _i64, _u, _vp]
         L.bf16x_split_operands.argtypes = [_i, _i, _i, _vp, _i64, _vp, _i64, _i, _vp, _i64, _i64, _vp, _i64, _i64, _vp]
+        L.bf16x_split_operands_ex.argtypes = [_i, _i, _i, _vp, _i64, _vp, _i64, _i, _vp, _i64, _i64, _vp, _i64, _i64, _u,
+                                              _vp]
         L.bf16x_gemm.argtypes = [_i, _i, _i, _f, _vp, _i, _vp, _i, _f, _vp, _i, _i]
         L.bf16x_gemm_workspace_size.argtypes = [_i, _i, _i, _i]
         L.bf16x_gemm_workspace_size.restype = ctypes.c_size_t

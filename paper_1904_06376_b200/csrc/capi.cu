@@ -164,8 +164,8 @@ int gemm_core(int m, int n, int k, float alpha, const float *A, int lda, const f
     if ((alpha == 0.f || k == 0) && !(flags & (BF16X_ACC_IN | BF16X_ACC_OUT)))
         return launch_scale(m, n, beta, C, ldc, st);
     const int pa = pieces_a(variant), pb = pieces_b(variant);
-    const int64_t kp = round_up8(k);
-    const size_t need = 2ull * ((Ap ? 0 : (size_t)pa * m) + (Bp ? 0 : (size_t)pb * n)) * (size_t)kp;
+    const int64_t kp = round_up8(k), mp = round_up8(m);
+    const size_t need = 2ull * ((Ap ? 0 : (size_t)pa * mp) + (Bp ? 0 : (size_t)pb * n)) * (size_t)kp;
     uint8_t *w = nullptr;
     if (need) {
         if (ws) {
@@ -193,6 +193,7 @@ int gemm_core(int m, int n, int k, float alpha, const float *A, int lda, const f
     pl.fp64 = (flags & BF16X_FP64_COMBINE) ? 1 : 0;
     pl.group_m = g_group_m;
     pl.fused_a = 0;
+    pl.a_mn = (flags & BF16X_A_PIECES_MN) ? 1 : 0;
     const bool sc = pl.scaled != 0;
     pl.Af = A; pl.Bf = B; pl.lda = lda; pl.ldb = ldb;
     if (!Ap && !Bp && g_fused_a != 0 && variant == 9 && fused_a_ok(pl)) {
@@ -208,26 +209,29 @@ int gemm_core(int m, int n, int k, float alpha, const float *A, int lda, const f
         pl.fused_a = 1;
         return launch_gemm_pieces(pl, st);
     }
+    // A is split in its own layout (MN-major pieces, ld round_up(m, 8)): no transpose in the pre-pass
     if (!Ap && !Bp) {   // both operands: one pre-pass launch
         uint16_t *a = (uint16_t *)w;
-        a_plane = (int64_t)m * kp;
-        ldap = kp;
+        ldap = mp;
+        a_plane = mp * (int64_t)k;
         uint16_t *b = a + pa * a_plane;
         b_plane = (int64_t)n * kp;
         ldbp = kp;
-        rc = launch_split_ab(m, n, k, A, lda, a, ldap, a_plane, B, ldb, b, ldbp, b_plane, pa, pb, st, sc);
+        rc = launch_split_ab(m, n, k, A, lda, a, ldap, a_plane, B, ldb, b, ldbp, b_plane, pa, pb, st, sc, false);
         if (rc) return rc;
         Ap = a;
         Bp = b;
+        pl.a_mn = 1;
     }
     if (!Ap) {
         uint16_t *a = (uint16_t *)w;
-        a_plane = (int64_t)m * kp;
-        ldap = kp;
+        ldap = mp;
+        a_plane = mp * (int64_t)k;
         rc = launch_split(m, k, A, lda, a, pa > 1 ? a + a_plane : nullptr, pa > 2 ? a + 2 * a_plane : nullptr, ldap,
-                          true, st, sc);
+                          false, st, sc);
         if (rc) return rc;
         Ap = a;
+        pl.a_mn = 1;
         w += 2ull * pa * (size_t)a_plane;
     }
     if (!Bp) {
@@ -261,7 +265,7 @@ int bf16x_gemm(int m, int n, int k, float alpha, const float *A, int lda, const 
 size_t bf16x_gemm_workspace_size(int m, int n, int k, int variant) {
     if (m < 0 || n < 0 || k < 0) return 0;
     const int v = variant_ok(variant) ? variant : 9;
-    return 2ull * ((size_t)pieces_a(v) * m + (size_t)pieces_b(v) * n) * (size_t)round_up8(k);
+    return 2ull * ((size_t)pieces_a(v) * round_up8(m) + (size_t)pieces_b(v) * n) * (size_t)round_up8(k);
 }
 
 int bf16x_gemm_ex(int m, int n, int k, float alpha, const float *A, int lda, const float *B, int ldb, float beta,
@@ -270,11 +274,14 @@ int bf16x_gemm_ex(int m, int n, int k, float alpha, const float *A, int lda, con
                   void *workspace_ptr, size_t ws_bytes, bf16x_stream_t stream) {
     int a = gemm_args(m, n, k, A_pieces ? (m > 1 ? m : 1) : lda, B_pieces ? (k > 1 ? k : 1) : ldb, ldc, variant);
     if (a) return a;
-    if (flags & ~(BF16X_ACC_IN | BF16X_ACC_OUT | BF16X_SCALED_PIECES | BF16X_FP64_COMBINE | BF16X_NO_STREAM_K))
+    if (flags & ~(BF16X_ACC_IN | BF16X_ACC_OUT | BF16X_SCALED_PIECES | BF16X_FP64_COMBINE | BF16X_NO_STREAM_K |
+                  BF16X_A_PIECES_MN))
         return -13;
     if ((flags & BF16X_FP64_COMBINE) && ((flags & (BF16X_ACC_IN | BF16X_ACC_OUT)) || variant == 1)) return -13;
-    if (A_pieces && (ldap < k || ldap % 8 || a_plane % 8 || a_plane < ldap * (int64_t)m ||
-                     (reinterpret_cast<uintptr_t>(A_pieces) & 15u)))
+    const bool amn = (flags & BF16X_A_PIECES_MN) != 0;
+    if (A_pieces && ((amn ? (ldap < (m > 1 ? m : 1) || a_plane < ldap * (int64_t)k)
+                          : (ldap < k || a_plane < ldap * (int64_t)m)) ||
+                     ldap % 8 || a_plane % 8 || (reinterpret_cast<uintptr_t>(A_pieces) & 15u)))
         return -14;
     if (B_pieces && (ldbp < k || ldbp % 8 || b_plane % 8 || b_plane < ldbp * (int64_t)n ||
                      (reinterpret_cast<uintptr_t>(B_pieces) & 15u)))
@@ -406,11 +413,12 @@ static int host_gemm_2d(int m, int n, int k, float alpha, const float *A_host, i
     const int mb = ((m + R - 1) / R + 255) / 256 * 256, nbk = ((n + Cb - 1) / Cb + 255) / 256 * 256;
     R = (m + mb - 1) / mb;
     Cb = (n + nbk - 1) / nbk;
-    int rc = ensure(&g_hAp, &g_hAp_n, ((size_t)pa * m * kp + 1) / 2);
+    const int64_t mp = round_up8(m);      // A's pieces in A's own layout (MN-major), ld mp
+    int rc = ensure(&g_hAp, &g_hAp_n, ((size_t)pa * mp * kp + 1) / 2);
     if (!rc) rc = ensure(&g_hBp, &g_hBp_n, ((size_t)pb * n * kp + 1) / 2);
     if (rc) return rc;
     uint16_t *ap = reinterpret_cast<uint16_t *>(g_hAp), *bp = reinterpret_cast<uint16_t *>(g_hBp);
-    const int64_t a_plane = (int64_t)m * kp, b_plane = (int64_t)n * kp;
+    const int64_t a_plane = mp * (int64_t)k, b_plane = (int64_t)n * kp;
     e = cudaEventRecord(g_ev_done, st);                      // the caller's earlier work first
     if (e == cudaSuccess) e = cudaStreamWaitEvent(g_s_in, g_ev_done, 0);
     for (int t = 0; t < std::max(R, Cb) && e == cudaSuccess; ++t) {
@@ -432,10 +440,10 @@ static int host_gemm_2d(int m, int n, int k, float alpha, const float *A_host, i
         if (t < R) {
             const int r0 = t * mb, mi = std::min(mb, m - r0);
             e = cudaStreamWaitEvent(g_s_split, g_ev_ar[t], 0);
-            uint16_t *a0 = ap + (int64_t)r0 * kp;
+            uint16_t *a0 = ap + r0;
             if (e == cudaSuccess)
                 rc = launch_split(mi, k, g_hA + r0, m, a0, pa > 1 ? a0 + a_plane : nullptr, pa > 2 ? a0 + 2 * a_plane : nullptr,
-                                  kp, true, g_s_split);
+                                  mp, false, g_s_split);
             if (!rc && e == cudaSuccess) e = cudaEventRecord(g_ev_as[t], g_s_split);
         }
         if (t < Cb && e == cudaSuccess && !rc) {
@@ -459,8 +467,8 @@ static int host_gemm_2d(int m, int n, int k, float alpha, const float *A_host, i
             e = cudaStreamWaitEvent(cs, g_ev_as[i], 0);
             if (e == cudaSuccess) e = cudaStreamWaitEvent(cs, g_ev_bs[j], 0);
             if (e != cudaSuccess) break;
-            rc = gemm_core(mi, nj, k, alpha, nullptr, m, nullptr, k, 0.f, g_hC + r0 + (size_t)c0 * m, m, variant, 0u,
-                           ap + (int64_t)r0 * kp, kp, a_plane, bp + (int64_t)c0 * kp, kp, b_plane, nullptr, nullptr, 0,
+            rc = gemm_core(mi, nj, k, alpha, nullptr, m, nullptr, k, 0.f, g_hC + r0 + (size_t)c0 * m, m, variant,
+                           BF16X_A_PIECES_MN, ap + r0, mp, a_plane, bp + (int64_t)c0 * kp, kp, b_plane, nullptr, nullptr, 0,
                            cs, 0, false, 0);
             if (rc) break;
             cudaEvent_t ev = g_ev_blk[i * kH2dMax + j];
@@ -515,7 +523,7 @@ int bf16x_gemm_host(int m, int n, int k, float alpha, const float *A_host, int l
                             (double)m * n * variant / ((double)m + n) >= 32400.0);
         if (two_d && beta == 0.f)
             return host_gemm_2d(m, n, k, alpha, A_host, lda, B_host, ldb, C_host, ldc, variant, st);
-        if ((rc = ensure(&g_hAp, &g_hAp_n, ((size_t)p * m * kp + 1) / 2))) return rc;
+        if ((rc = ensure(&g_hAp, &g_hAp_n, ((size_t)p * round_up8(m) * kp + 1) / 2))) return rc;
     }
     cudaError_t e = cudaSuccess;
     if (nchunk == 1) {
@@ -548,7 +556,8 @@ int bf16x_gemm_host(int m, int n, int k, float alpha, const float *A_host, int l
     const int cw = ((n + nchunk - 1) / nchunk + 255) / 256 * 256;
     nchunk = (n + cw - 1) / cw;
     uint16_t *ap = reinterpret_cast<uint16_t *>(g_hAp);
-    const int64_t a_plane = (int64_t)m * kp;
+    const int64_t mp = round_up8(m);     // A's pieces in A's own layout (MN-major), ld mp
+    const int64_t a_plane = mp * (int64_t)k;
     // the caller's stream may still be using the device buffers / host arrays
     e = cudaEventRecord(g_ev_done, st);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(g_s_in, g_ev_done, 0);
@@ -574,7 +583,7 @@ int bf16x_gemm_host(int m, int n, int k, float alpha, const float *A_host, int l
         set_cuda_error(e, "gemm_host h2d");
         return BF16X_ERR_CUDA;
     }
-    rc = launch_split(m, k, g_hA, m, ap, p > 1 ? ap + a_plane : nullptr, p > 2 ? ap + 2 * a_plane : nullptr, kp, true,
+    rc = launch_split(m, k, g_hA, m, ap, p > 1 ? ap + a_plane : nullptr, p > 2 ? ap + 2 * a_plane : nullptr, mp, false,
                       st);
     if (rc == BF16X_SUCCESS) e = cudaEventRecord(g_ev_asplit, st);
     tl_record(2, st);                                         // A split
@@ -590,7 +599,7 @@ int bf16x_gemm_host(int m, int n, int k, float alpha, const float *A_host, int l
         e = cudaStreamWaitEvent(cs, g_ev_b[j], 0);
         if (e != cudaSuccess) break;
         rc = gemm_core(m, nj, k, alpha, nullptr, m, g_hB + (size_t)c0 * k, k, beta, g_hC + (size_t)c0 * m, m, variant,
-                       0u, ap, kp, a_plane, nullptr, 0, 0, nullptr,
+                       BF16X_A_PIECES_MN, ap, mp, a_plane, nullptr, 0, 0, nullptr,
                        reinterpret_cast<uint8_t *>(g_hBp) + (j % kHostStreams) * slice, slice, cs, 0, false, 0);
         if (rc) break;
         e = cudaEventRecord(g_ev_c[j], cs);

@@ -431,6 +431,18 @@ __device__ __forceinline__ uint64_t smem_desc_kmajor(uint32_t saddr, uint32_t sb
     return d;
 }
 
+// MN-major operand, 128-byte swizzle (canonical ((64 elements, n), (8 rows, k)) atoms of 1 KB):
+// lbo_bytes = stride between 64-element MN atoms, sbo_bytes = stride between 8-row K groups
+__device__ __forceinline__ uint64_t smem_desc_mn128(uint32_t saddr, uint32_t lbo_bytes, uint32_t sbo_bytes) {
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+    d |= (uint64_t)((lbo_bytes >> 4) & 0x3FFFu) << 16;    // LBO
+    d |= (uint64_t)((sbo_bytes >> 4) & 0x3FFFu) << 32;    // SBO
+    d |= (uint64_t)1u << 46;                              // version = 1
+    d |= (uint64_t)2u << 61;                              // SWIZZLE_128B
+    return d;
+}
+
 // Instruction descriptor for kind::f16: BF16 x BF16 -> FP32, both K-major, M x N.
 __host__ __device__ constexpr uint32_t idesc_bf16_f32(int M, int N) {
     return (1u << 4)                          // c_format = F32

@@ -57,6 +57,19 @@ int make_piece_map(CUtensorMap *map, const uint16_t *base, int k, int rows, int6
     return r == CUDA_SUCCESS ? BF16X_SUCCESS : BF16X_ERR_CUDA;
 }
 
+int make_piece_map_mn(CUtensorMap *map, const uint16_t *base, int m, int k, int64_t ld, int64_t plane, int p) {
+    EncodeTiledFn enc = encode_fn();
+    if (!enc) return BF16X_ERR_CUDA;
+    cuuint64_t dims[3] = {(cuuint64_t)m, (cuuint64_t)k, (cuuint64_t)p};
+    cuuint64_t strides[2] = {(cuuint64_t)ld * 2, (cuuint64_t)plane * 2};
+    cuuint32_t box[3] = {64u, (cuuint32_t)kBK, (cuuint32_t)p};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<uint16_t *>(base), dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? BF16X_SUCCESS : BF16X_ERR_CUDA;
+}
+
 // 2D map over a column-major FP32 matrix: dims (rows [inner], cols), box (box_rows, box_cols);
 // out-of-range elements read as zero (they become zero pieces).
 int make_f32_map(CUtensorMap *map, const float *base, int rows, int cols, int64_t ld, int box_rows,

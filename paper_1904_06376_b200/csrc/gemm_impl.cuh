@@ -22,6 +22,10 @@ constexpr int kThreads = (4 + kNumEpiWarps) * 32;
 constexpr int kNumXfWarps = 8;        // fused A: warps 12..19 convert FP32 A tiles to pieces
 constexpr int kThreadsFused = kThreads + kNumXfWarps * 32;
 constexpr int kF32Tile = kBM * kBK * 4;   // one FP32 operand tile per CTA per stage (16 KB)
+// MN-major A (KParams::a_mn): per stage and CTA two TMA boxes (m 64 x k 32 x pieces), smem
+// [m half][piece][k 32][m 64] with the 128-byte swizzle: 8-row k groups 1024 B apart (SBO), the two
+// 64-row m atoms PA * 4 KB apart (LBO); a K = 16 step starts 2 groups (2 KB) further
+constexpr int kMnBox = 64 * kBK * 2;      // one piece of one 64-row half: 4 KB
 constexpr int kTmemCols = 512;        // two accumulator buffers at column 0 and 256
 constexpr int kTmemBufStride = 256;
 constexpr int kGroupM = 8;            // tile raster: 8 m-tiles per group for L2 reuse (default)
@@ -119,7 +123,9 @@ struct KParams {
     unsigned long long *trace;   // dbg bit 1: %globaltimer per CTA (tools/gemm_trace.py), 32 slots each
     // (measured, nvcc 12.9: with the parameter block ending at lazy_full ptxas spills 96 bytes
     // in the 2-CTA kernels; with >= 32 more bytes it allocates 168 registers without spills)
-    int64_t reserved[4];
+    int a_mn;              // A pieces MN-major (A's own column-major layout; 128-byte swizzle)
+    int reserved_i;
+    int64_t reserved[3];
 };
 
 struct Work {
@@ -188,7 +194,8 @@ __device__ __forceinline__ void tile_coords(int tile, int tiles_m, int tiles_n, 
 template <int CG, int V, int BN, int S, bool SA, bool LZ>
 __device__ __forceinline__ void issue_interval(uint32_t d_big, uint32_t d_small, const uint64_t (&a_desc)[S],
                                                const uint64_t (&b_desc)[S], int ns, uint32_t idesc, bool scaled,
-                                               uint64_t *fullw, const int (&stg)[S], const uint32_t (&phs)[S]) {
+                                               uint64_t *fullw, const int (&stg)[S], const uint32_t (&phs)[S],
+                                               uint32_t a_ps, uint32_t a_ks) {
     using Cf = Cfg<CG, V, BN>;
     constexpr int H = S * (kBK / kUK);     // K=16 halves per interval (max)
     const int nh = ns * (kBK / kUK);
@@ -203,7 +210,7 @@ __device__ __forceinline__ void issue_interval(uint32_t d_big, uint32_t d_small,
             tc_fence_after();
             waited |= 1u << st;
         }
-        const uint64_t ad = a_desc[st] + (uint64_t)((i * Cf::A_PIECE + kk * (kUK * 2)) >> 4);
+        const uint64_t ad = a_desc[st] + (uint64_t)(i * a_ps + kk * a_ks);   // 16-byte units
         const uint64_t bd = b_desc[st] + (uint64_t)((j * Cf::B_PIECE + kk * (kUK * 2)) >> 4);
         const bool big = SA && (i + j == 0);
         bool &first = (SA && !big) ? first_small : first_big;
@@ -410,11 +417,21 @@ __global__ void __launch_bounds__(FA ? kThreadsFused : kThreads, 1)
                         uint8_t *b_dst = sB + stage * Cf::B_STAGE;
                         if constexpr (CG == 1) {
                             mbar_arrive_expect_tx(&full[stage], Cf::STAGE);
-                            tma_load_3d(a_dst, &tmA, &full[stage], kb * kBK, a_row, 0);
+                            if (p.a_mn) {
+                                tma_load_3d(a_dst, &tmA, &full[stage], a_row, kb * kBK, 0);
+                                tma_load_3d(a_dst + Cf::PA * kMnBox, &tmA, &full[stage], a_row + 64, kb * kBK, 0);
+                            } else {
+                                tma_load_3d(a_dst, &tmA, &full[stage], kb * kBK, a_row, 0);
+                            }
                             tma_load_3d(b_dst, &tmB, &full[stage], kb * kBK, b_row, 0);
                         } else {
                             if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * Cf::STAGE);
-                            tma_load_3d_2sm(a_dst, &tmA, &full[stage], kb * kBK, a_row, 0);
+                            if (p.a_mn) {
+                                tma_load_3d_2sm(a_dst, &tmA, &full[stage], a_row, kb * kBK, 0);
+                                tma_load_3d_2sm(a_dst + Cf::PA * kMnBox, &tmA, &full[stage], a_row + 64, kb * kBK, 0);
+                            } else {
+                                tma_load_3d_2sm(a_dst, &tmA, &full[stage], kb * kBK, a_row, 0);
+                            }
                             if constexpr (MC == 1) {
                                 tma_load_3d_2sm(b_dst, &tmB, &full[stage], kb * kBK, b_row, 0);
                             } else {
@@ -434,7 +451,15 @@ __global__ void __launch_bounds__(FA ? kThreadsFused : kThreads, 1)
         } else if (warp == 1) {
             // ------------------------------ MMA issuer --------------------------------
             if (rank == 0) {   // warp-uniform loop; one elected lane issues (umma_*_elect)
-                const uint32_t idesc = idesc_bf16_f32(kBM * CG, BN);
+                const uint32_t idesc = idesc_bf16_f32(kBM * CG, BN) | (p.a_mn ? (1u << 15) : 0u);   // a_major
+                // A descriptor of a stage, piece and K = 16 step strides (16-byte units)
+                const bool amn = p.a_mn != 0;
+                const uint32_t a_ps = amn ? (uint32_t)(kMnBox >> 4) : (uint32_t)(Cf::A_PIECE >> 4);
+                const uint32_t a_ks = amn ? (uint32_t)((2 * 8 * 128) >> 4) : (uint32_t)((kUK * 2) >> 4);
+                auto adesc = [&](int stg_) -> uint64_t {
+                    const uint32_t sa = smem_u32(sA + stg_ * Cf::A_STAGE);
+                    return amn ? smem_desc_mn128(sa, Cf::PA * kMnBox, 1024) : smem_desc_kmajor(sa, kSwizzleAtom, 4);
+                };
                 int stage = 0;
                 uint32_t phase = 0, acc_it = 0;
                 WorkIter it(p, cid, ncl);
@@ -452,7 +477,7 @@ __global__ void __launch_bounds__(FA ? kThreadsFused : kThreads, 1)
                             stg[q] = stage;
                             if (q < ns) {
                                 mbar_wait(&full[stage], phase);
-                                ad[q] = smem_desc_kmajor(smem_u32(sA + stage * Cf::A_STAGE), kSwizzleAtom, 4);
+                                ad[q] = adesc(stage);
                                 bd[q] = smem_desc_kmajor(smem_u32(sB + stage * Cf::B_STAGE), kSwizzleAtom, 4);
                                 if (++stage == NST) { stage = 0; phase ^= 1u; }
                             } else {
@@ -472,7 +497,7 @@ __global__ void __launch_bounds__(FA ? kThreadsFused : kThreads, 1)
                             for (int r = 1; r < S; ++r)
                                 if (q == r) { a0 = ad[r]; b0 = bd[r]; }
                             umma_bf16_elect<CG>(tmem_base + buf * kTmemBufStride,
-                                                a0 + (uint64_t)((i * Cf::A_PIECE + kk * (kUK * 2)) >> 4),
+                                                a0 + (uint64_t)(i * a_ps + kk * a_ks),
                                                 b0 + (uint64_t)((j * Cf::B_PIECE + kk * (kUK * 2)) >> 4), idesc, 0u);
                             umma_commit_elect<CG>(&acc_full[buf]);
                             ++acc_it;
@@ -497,7 +522,7 @@ __global__ void __launch_bounds__(FA ? kThreadsFused : kThreads, 1)
                             phs[q] = phase;
                             if (q < ns) {
                                 if (!lz) mbar_wait(&full[stage], phase);
-                                a_desc[q] = smem_desc_kmajor(smem_u32(sA + stage * Cf::A_STAGE), kSwizzleAtom, 4);
+                                a_desc[q] = adesc(stage);
                                 b_desc[q] = smem_desc_kmajor(smem_u32(sB + stage * Cf::B_STAGE), kSwizzleAtom, 4);
                                 if (++stage == NST) { stage = 0; phase ^= 1u; }
                             } else {
@@ -510,7 +535,7 @@ __global__ void __launch_bounds__(FA ? kThreadsFused : kThreads, 1)
                         const uint32_t d_big = SA ? tmem_base + kTmemBufStride + buf * BN : tmem_base + buf * kTmemBufStride;
                         const uint32_t d_small = SA ? tmem_base + buf * BN : d_big;
                         issue_interval<CG, V, BN, S, SA, kLazy>(d_big, d_small, a_desc, b_desc, ns, idesc, p.scaled != 0,
-                                                                lz ? full : nullptr, stages, phs);
+                                                                lz ? full : nullptr, stages, phs, a_ps, a_ks);
 #pragma unroll
                         for (int q = 0; q < S; ++q)
                             if (q < ns) {
@@ -833,6 +858,9 @@ int make_piece_map(CUtensorMap *map, const uint16_t *base, int k, int rows, int6
                    int box_rows, int box_p = 0);
 int make_f32_map(CUtensorMap *map, const float *base, int rows, int cols, int64_t ld, int box_rows, int box_cols,
                  CUtensorMapSwizzle swz);
+// 3D map over p MN-major piece planes (element (i, l) at i + l * ld): dims (m, k, p), box (64, BK, p),
+// 128-byte swizzle
+int make_piece_map_mn(CUtensorMap *map, const uint16_t *base, int m, int k, int64_t ld, int64_t plane, int p);
 // stream-K fix-up buffers of stream st (per-stream resources, capi.cu): ws_floats partial
 // accumulators and nflags ready flags compared against the returned per-launch epoch
 int sk_workspace(cudaStream_t st, size_t ws_floats, size_t nflags, float **ws, unsigned int **flags,
@@ -852,7 +880,8 @@ int launch_t(const GemmPlan &pl, cudaStream_t st) {
         if (rc) return rc;
         rc = make_piece_map(&tmB, pl.Bp, pl.k, pl.n, pl.ldbp, pl.b_plane, Cf::PB, Cf::BN_LOCAL);
     } else {
-        rc = make_piece_map(&tmA, pl.Ap, pl.k, pl.m, pl.ldap, pl.a_plane, Cf::PA, kBM);
+        rc = pl.a_mn ? make_piece_map_mn(&tmA, pl.Ap, pl.m, pl.k, pl.ldap, pl.a_plane, Cf::PA)
+                     : make_piece_map(&tmA, pl.Ap, pl.k, pl.m, pl.ldap, pl.a_plane, Cf::PA, kBM);
         if (rc) return rc;
         if (MC == 1) rc = make_piece_map(&tmB, pl.Bp, pl.k, pl.n, pl.ldbp, pl.b_plane, Cf::PB, Cf::BN_LOCAL);
         else rc = make_piece_map(&tmB, pl.Bp, pl.k, pl.n, pl.ldbp, pl.b_plane, Cf::PB, Cf::BN_LOCAL / MC, 1);
@@ -915,6 +944,8 @@ int launch_t(const GemmPlan &pl, cudaStream_t st) {
     // 207.7 TFLOPS; DRAM reads 65.6 vs 65.9 GB at 16384^3 under ncu, so not a traffic effect),
     // and below it 8-tall groups (8192^3 x6: 214.5 vs 207 TFLOPS for 2 or 1)
     kp.lazy_full = g_lazy_full;
+    kp.a_mn = (!FA && pl.a_mn) ? 1 : 0;
+    kp.reserved_i = 0;
     kp.dbg = g_gemm_debug;
     kp.trace = g_gemm_trace;
     // C through TMA when its base and columns are 16-byte aligned (else per-thread stores)

@@ -14,7 +14,7 @@ int launch_split(int64_t rows, int64_t cols, const float *X, int64_t ldx, uint16
 
 int launch_split_ab(int m, int n, int k, const float *A, int64_t lda, uint16_t *Ap, int64_t ldap, int64_t a_plane,
                     const float *B, int64_t ldb, uint16_t *Bp, int64_t ldbp, int64_t b_plane, int npa, int npb,
-                    cudaStream_t st, bool scaled = false);
+                    cudaStream_t st, bool scaled = false, bool a_trans = true);
 
 struct GemmPlan {
     int m, n, k;
@@ -23,7 +23,9 @@ struct GemmPlan {
     int ldc;
     int variant;
     unsigned flags;
-    const uint16_t *Ap;  // K-major A pieces: plane q at Ap + q*a_plane, element (i,l) at i*ldap + l
+    const uint16_t *Ap;  // A pieces: plane q at Ap + q*a_plane, element (i,l) at i*ldap + l (K-major)
+                         // or, with a_mn, at i + l*ldap (MN-major: A's own layout)
+    int a_mn;
     int64_t ldap, a_plane;
     const uint16_t *Bp;  // K-major B pieces: plane q at Bp + q*b_plane, element (j,l) at j*ldbp + l
     int64_t ldbp, b_plane;

@@ -168,14 +168,18 @@ struct SplitArgs {
     uint16_t *P0, *P1, *P2;
     int vec;
 };
-template <int NPA, int NPB, bool SC>
+// TA = false: A is split in its own (column-major = MN-major) layout too, like B.
+template <int NPA, int NPB, bool SC, bool TA = true>
 __global__ void __launch_bounds__(256) split_ab_kernel(SplitArgs a, SplitArgs b, int gA) {
     extern __shared__ uint32_t s_trans[];
     asm volatile("griddepcontrol.launch_dependents;");   // let the GEMM's prologue start early
-    if ((int)blockIdx.x < gA)
-        split_trans_body<NPA, SC, kTransTCab>(a.rows, a.cols, a.X, a.ldx, a.P0, a.P1, a.P2, a.ldp, a.vec, blockIdx.x, gA,
-                                              s_trans);
-    else
+    if ((int)blockIdx.x < gA) {
+        if constexpr (TA)
+            split_trans_body<NPA, SC, kTransTCab>(a.rows, a.cols, a.X, a.ldx, a.P0, a.P1, a.P2, a.ldp, a.vec, blockIdx.x,
+                                                  gA, s_trans);
+        else
+            split_same_body<NPA, SC>(a.rows, a.cols, a.X, a.ldx, a.P0, a.P1, a.P2, a.ldp, a.vec, blockIdx.x, gA);
+    } else
         split_same_body<NPB, SC>(b.rows, b.cols, b.X, b.ldx, b.P0, b.P1, b.P2, b.ldp, b.vec, blockIdx.x - gA,
                              gridDim.x - gA);
 }
@@ -190,7 +194,14 @@ static size_t trans_smem(K kern, int np) {
 
 template <bool SC>
 static void split_ab_launch(const SplitArgs &a, const SplitArgs &b, int gA, unsigned grid, int npa, int npb,
-                            cudaStream_t st) {
+                            cudaStream_t st, bool ta) {
+    if (!ta) {   // both operands in their own layout: no shared memory
+        if (npa == 1 && npb == 1) split_ab_kernel<1, 1, SC, false><<<grid, 256, 0, st>>>(a, b, gA);
+        else if (npa == 2 && npb == 2) split_ab_kernel<2, 2, SC, false><<<grid, 256, 0, st>>>(a, b, gA);
+        else if (npa == 2 && npb == 3) split_ab_kernel<2, 3, SC, false><<<grid, 256, 0, st>>>(a, b, gA);
+        else split_ab_kernel<3, 3, SC, false><<<grid, 256, 0, st>>>(a, b, gA);
+        return;
+    }
     if (npa == 1 && npb == 1) {
         static size_t sm = trans_smem<kTransTCab>(split_ab_kernel<1, 1, SC>, 1);
         split_ab_kernel<1, 1, SC><<<grid, 256, sm, st>>>(a, b, gA);
@@ -263,19 +274,21 @@ int launch_split(int64_t rows, int64_t cols, const float *X, int64_t ldx, uint16
 
 int launch_split_ab(int m, int n, int k, const float *A, int64_t lda, uint16_t *Ap, int64_t ldap, int64_t a_plane,
                     const float *B, int64_t ldb, uint16_t *Bp, int64_t ldbp, int64_t b_plane, int npa, int npb,
-                    cudaStream_t st, bool scaled) {
+                    cudaStream_t st, bool scaled, bool a_trans) {
     if (m == 0 || n == 0 || k == 0) return BF16X_SUCCESS;
     SplitArgs a{m, k, lda, ldap, A, Ap, npa > 1 ? Ap + a_plane : nullptr, npa > 2 ? Ap + 2 * a_plane : nullptr, 0};
     SplitArgs b{k, n, ldb, ldbp, B, Bp, npb > 1 ? Bp + b_plane : nullptr, npb > 2 ? Bp + 2 * b_plane : nullptr, 0};
     a.vec = ((reinterpret_cast<uintptr_t>(A) & 15u) == 0) && lda % 4 == 0;
+    if (!a_trans)   // same-layout vector stores need the pieces 16-byte aligned too
+        a.vec = a.vec && ((reinterpret_cast<uintptr_t>(Ap) & 15u) == 0) && ldap % 8 == 0 && a_plane % 8 == 0;
     b.vec = ((reinterpret_cast<uintptr_t>(B) & 15u) == 0) && ldb % 4 == 0 &&
             ((reinterpret_cast<uintptr_t>(Bp) & 15u) == 0) && ldbp % 8 == 0 && b_plane % 8 == 0;
     const int64_t grid = (int64_t)sm_count() * 8;
     const double wa = (double)m * k, wb = (double)k * n;
     int gA = (int)(grid * wa / (wa + wb));
     gA = gA < 1 ? 1 : (gA > grid - 1 ? (int)grid - 1 : gA);
-    if (scaled) split_ab_launch<true>(a, b, gA, (unsigned)grid, npa, npb, st);
-    else split_ab_launch<false>(a, b, gA, (unsigned)grid, npa, npb, st);
+    if (scaled) split_ab_launch<true>(a, b, gA, (unsigned)grid, npa, npb, st, a_trans);
+    else split_ab_launch<false>(a, b, gA, (unsigned)grid, npa, npb, st, a_trans);
     count_launch();
     return check_launch("split_ab");
 }
@@ -318,7 +331,31 @@ extern "C" int bf16x_split_operands(int m, int n, int k, const float *A, int64_t
     int ok = arch_ok();
     if (ok) return ok;
     return launch_split_ab(m, n, k, A, lda, Ap, ldap, a_plane, B, ldb, Bp, ldbp, b_plane, pieces, pieces,
-                           (cudaStream_t)stream, false);
+                           (cudaStream_t)stream, false, true);
+}
+
+// Both operands, options: BF16X_A_PIECES_MN (A's pieces in A's own layout: element (i,l) of piece q at
+// Ap[q*a_plane + i + l*ldap], ldap >= m -- what bf16x_gemm_ex takes with the same flag),
+// BF16X_SCALED_PIECES (R29).
+extern "C" int bf16x_split_operands_ex(int m, int n, int k, const float *A, int64_t lda, const float *B, int64_t ldb,
+                                       int pieces, uint16_t *Ap, int64_t ldap, int64_t a_plane, uint16_t *Bp,
+                                       int64_t ldbp, int64_t b_plane, unsigned flags, bf16x_stream_t stream) {
+    if (m < 0) return -1;
+    if (n < 0) return -2;
+    if (k < 0) return -3;
+    if (lda < (m > 1 ? m : 1)) return -5;
+    if (ldb < (k > 1 ? k : 1)) return -7;
+    if (pieces < 1 || pieces > 3) return -8;
+    if (flags & ~(BF16X_A_PIECES_MN | BF16X_SCALED_PIECES)) return -13;
+    const bool mn = (flags & BF16X_A_PIECES_MN) != 0;
+    if (!Ap || (mn ? (ldap < (m > 1 ? m : 1) || a_plane < ldap * (int64_t)k)
+                   : (ldap < (k > 1 ? k : 1) || a_plane < ldap * (int64_t)m)))
+        return -9;
+    if (!Bp || ldbp < (k > 1 ? k : 1) || b_plane < ldbp * (int64_t)n) return -12;
+    int ok = arch_ok();
+    if (ok) return ok;
+    return launch_split_ab(m, n, k, A, lda, Ap, ldap, a_plane, B, ldb, Bp, ldbp, b_plane, pieces, pieces,
+                           (cudaStream_t)stream, (flags & BF16X_SCALED_PIECES) != 0, !mn);
 }
 
 extern "C" int bf16x_split_t(int64_t rows, int64_t cols, const float *X, int64_t ldx, uint16_t *P0, uint16_t *P1,

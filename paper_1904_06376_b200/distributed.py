@@ -9,9 +9,9 @@ are independent, so the only exchanges are
     contiguous column chunks A[:, Kc] -- each sent as its transpose view A[:, Kc]^T, a
     row-major-contiguous (|Kc| x m) tensor over the same memory, as NCCL requires -- so the
     first sub-block's GEMM can start on chunk c while chunk c+1 is in flight.  Each rank splits
-    every chunk ONCE, as it lands, into one K-major piece buffer of the whole A
-    (bf16x_split_t at column offset k0); every GEMM of every sub-block then reads those pieces
-    (bf16x_gemm_ex A_pieces), so A is split exactly once per rank.  The first sub-block carries
+    every chunk ONCE, as it lands, into one piece buffer of the whole A in A's own layout
+    (bf16x_split at column offset k0, no transpose); every GEMM of every sub-block then reads those
+    pieces (bf16x_gemm_ex A_pieces with BF16X_A_PIECES_MN), so A is split exactly once per rank.  The first sub-block carries
     its FP32 promoted accumulator between chunks (bf16x_gemm_ex ACC_IN / ACC_OUT), which makes
     the chunked result bit-identical to a one-pass GEMM: chunk edges are multiples of 128 (the
     longest promotion interval), deduplicated;
@@ -71,7 +71,8 @@ def _ld(t, rows):
 
 
 class _PieceGemm:
-    """The CUDA library path: A split once into K-major pieces, GEMMs on those pieces."""
+    """The CUDA library path: A split once into pieces in A's own layout (MN-major, ld round_up(m, 8)),
+    GEMMs on those pieces (bf16x_gemm_ex with BF16X_A_PIECES_MN)."""
 
     def __init__(self, A, variant):
         import paper_1904_06376_b200 as bx
@@ -80,8 +81,8 @@ class _PieceGemm:
         self.m, self.k = m, k
         self.variant = variant
         self.pa = 2 if variant in (3, 5) else (1 if variant == 1 else 3)
-        self.kp = (k + 7) // 8 * 8
-        self.a_plane = m * self.kp
+        self.mp = (m + 7) // 8 * 8
+        self.a_plane = self.mp * k
         self.P = torch.empty(max(1, self.pa * self.a_plane), dtype=torch.uint16, device=A.device)
         self.base = self.P.data_ptr()
 
@@ -90,15 +91,16 @@ class _PieceGemm:
         if k1 <= k0 or self.m == 0:
             return
         es = 2   # bytes per piece element
-        p = [self.base + (q * self.a_plane + k0) * es if q < self.pa else 0 for q in range(3)]
+        p = [self.base + (q * self.a_plane + k0 * self.mp) * es if q < self.pa else 0 for q in range(3)]
         self.bx.split_raw(self.m, k1 - k0, A.data_ptr() + k0 * A.stride(1) * 4, _ld(A, self.m), p[0], p[1], p[2],
-                          self.kp, transpose=True)
+                          self.mp)
 
     def gemm(self, k0, k1, Bq, Cq, flags, acc=None):
         n = Cq.shape[1]
         self.bx.gemm_raw(self.m, n, k1 - k0, 1.0, 0, self.m, Bq.data_ptr() + k0 * 4, _ld(Bq, Bq.shape[0]), 0.0,
                          Cq.data_ptr(), _ld(Cq, self.m), variant=self.variant,
-                         flags=flags | self.bx.NO_STREAM_K, A_pieces=self.base + k0 * 2, ldap=self.kp,
+                         flags=flags | self.bx.NO_STREAM_K | self.bx.A_PIECES_MN, A_pieces=self.base + k0 * self.mp * 2,
+                         ldap=self.mp,
                          a_plane=self.a_plane, acc=None if acc is None else acc.data_ptr())
 
 

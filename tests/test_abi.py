@@ -36,13 +36,35 @@ def test_gemm_argument_errors():
     assert f(4, 4, 4, 1.0, None, 4, None, 4, 0.0, None, 3, 6) == -11
     assert f(4, 4, 4, 1.0, None, 4, None, 4, 0.0, None, 4, 4) == -12
     ex = L.bf16x_gemm_ex
-    assert ex(4, 4, 4, 1.0, None, 4, None, 4, 0.0, None, 4, 6, 64, None, 0, 0, None, 0, 0, None, None, 0, None) == -13
+    assert ex(4, 4, 4, 1.0, None, 4, None, 4, 0.0, None, 4, 6, 128, None, 0, 0, None, 0, 0, None, None, 0, None) == -13
     # FP64 combine (R30) excludes the accumulator carry and the one-product variant
     assert ex(4, 4, 4, 1.0, None, 4, None, 4, 0.0, None, 4, 6, 9, None, 0, 0, None, 0, 0, 16, None, 0, None) == -13
     assert ex(4, 4, 4, 1.0, None, 4, None, 4, 0.0, None, 4, 1, 8, None, 0, 0, None, 0, 0, None, None, 0, None) == -13
     assert ex(4, 4, 4, 1.0, None, 4, None, 4, 0.0, None, 4, 6, 0, 16, 3, 32, None, 0, 0, None, None, 0, None) == -14
     assert ex(4, 4, 4, 1.0, None, 4, None, 4, 0.0, None, 4, 6, 0, None, 0, 0, 16, 8, 4, None, None, 0, None) == -16
     assert ex(4, 4, 4, 1.0, None, 4, None, 4, 0.0, None, 4, 6, 1, None, 0, 0, None, 0, 0, None, None, 0, None) == -19
+    # BF16X_A_PIECES_MN (64): A's pieces in A's own layout, ldap >= m, a_plane >= ldap * k, both % 8
+    mn = bx.A_PIECES_MN
+    assert ex(12, 4, 4, 1.0, None, 12, None, 4, 0.0, None, 12, 6, mn, 16, 8, 64, None, 0, 0, None, None, 0, None) == -14
+    assert ex(4, 4, 12, 1.0, None, 4, None, 12, 0.0, None, 4, 6, mn, 16, 8, 88, None, 0, 0, None, None, 0, None) == -14
+    assert ex(4, 4, 12, 1.0, None, 4, None, 12, 0.0, None, 4, 6, mn, 16, 12, 144, None, 0, 0, None, None, 0, None) == -14
+    # (valid MN layout: the host checks pass and the call stops at the device check, not computing on the CPU)
+    assert ex(4, 4, 12, 1.0, None, 4, None, 12, 0.0, None, 4, 6, mn, 16, 8, 96, None, 0, 0, None, None, 0, None) in (
+        bx.ERR_ARCH, bx.ERR_CUDA)
+
+
+def test_split_operands_ex_argument_errors():
+    so = bx.lib().bf16x_split_operands_ex
+    mn = bx.A_PIECES_MN
+    # MN layout of A's pieces: ldap >= m, a_plane >= ldap * k (-9); B as bf16x_split_operands (-12)
+    assert so(12, 4, 4, None, 12, None, 4, 3, 16, 8, 64, 16, 8, 64, mn, None) == -9
+    assert so(4, 4, 12, None, 4, None, 12, 3, 16, 8, 88, 16, 16, 64, mn, None) == -9
+    assert so(4, 4, 12, None, 4, None, 12, 3, 16, 8, 96, 16, 8, 64, mn, None) == -12
+    assert so(4, 4, 12, None, 4, None, 12, 3, 16, 8, 96, 16, 16, 64, 128, None) == -13
+    assert so(4, 4, 12, None, 4, None, 12, 4, 16, 8, 96, 16, 16, 64, mn, None) == -8
+    # K-major A (no flag): ldap >= k, a_plane >= ldap * m
+    assert so(4, 4, 12, None, 4, None, 12, 3, 16, 8, 96, 16, 16, 64, 0, None) == -9
+    assert so(4, 4, 12, None, 4, None, 12, 3, 16, 16, 64, 16, 16, 64, 0, None) in (bx.ERR_ARCH, bx.ERR_CUDA)
 
 
 def test_split_argument_errors():
@@ -63,10 +85,11 @@ def test_split_argument_errors():
 
 
 def test_workspace_size_formula():
-    # 2 bytes * p pieces * (m + n) rows * round_up(k, 8)
-    assert bx.workspace_size(100, 50, 33, 6) == 2 * 3 * 150 * 40
-    assert bx.workspace_size(100, 50, 33, 3) == 2 * 2 * 150 * 40
-    assert bx.workspace_size(100, 50, 33, 5) == 2 * (2 * 100 + 3 * 50) * 40
+    # 2 bytes * p pieces * (round_up(m, 8) + n) rows * round_up(k, 8) (A's pieces keep A's layout, ld round_up(m, 8))
+    assert bx.workspace_size(100, 50, 33, 6) == 2 * 3 * 154 * 40
+    assert bx.workspace_size(100, 50, 33, 3) == 2 * 2 * 154 * 40
+    assert bx.workspace_size(100, 50, 33, 5) == 2 * (2 * 104 + 3 * 50) * 40
+    assert bx.workspace_size(96, 50, 33, 6) == 2 * 3 * 146 * 40
 
 
 def test_no_cpu_fallback_without_gpu():

@@ -220,9 +220,10 @@ def test_host_api_2d_blocks(orc, variant):
 
 
 def test_bench_launch_sequence_matches_gemm():
-    """bench.py's timed step (bf16x_split_operands of both operands into caller buffers, then
-    bf16x_gemm_ex on the pre-split pieces) is the same computation as bf16x_gemm: bit-identical
-    C at configs[1]'s size, so the parity tests of bx.gemm cover the benchmarked launches."""
+    """bench.py's timed step (bf16x_split_operands_ex of both operands into caller buffers, A in its
+    own layout, then bf16x_gemm_ex on the pre-split pieces with BF16X_A_PIECES_MN) is the same
+    computation as bf16x_gemm: bit-identical C at configs[1]'s size, so the parity tests of bx.gemm
+    cover the benchmarked launches.  So is the K-major sequence (bf16x_split_operands, A transposed)."""
     n = 4096
     A = torch.from_numpy(np.asfortranarray(synthetic.uniform(n, n, seed=1))).cuda()
     B = torch.from_numpy(np.asfortranarray(synthetic.uniform(n, n, seed=2))).cuda()
@@ -236,6 +237,14 @@ def test_bench_launch_sequence_matches_gemm():
     assert L.bf16x_split_operands(n, n, n, A.data_ptr(), n, B.data_ptr(), n, 3, Ap.data_ptr(), kp, n * kp,
                                   Bp.data_ptr(), kp, n * kp, st) == 0
     assert L.bf16x_gemm_ex(n, n, n, 1.0, None, n, None, n, 0.0, C.data_ptr(), n, 6, 0, Ap.data_ptr(), kp, n * kp,
+                           Bp.data_ptr(), kp, n * kp, None, None, 0, st) == 0
+    torch.cuda.synchronize()
+    assert torch.equal(C.view(torch.int32), want.view(torch.int32))
+    C.zero_()
+    mn = bx.A_PIECES_MN
+    assert L.bf16x_split_operands_ex(n, n, n, A.data_ptr(), n, B.data_ptr(), n, 3, Ap.data_ptr(), n, n * n,
+                                     Bp.data_ptr(), kp, n * kp, mn, st) == 0
+    assert L.bf16x_gemm_ex(n, n, n, 1.0, None, n, None, n, 0.0, C.data_ptr(), n, 6, mn, Ap.data_ptr(), n, n * n,
                            Bp.data_ptr(), kp, n * kp, None, None, 0, st) == 0
     torch.cuda.synchronize()
     assert torch.equal(C.view(torch.int32), want.view(torch.int32))
