@@ -389,7 +389,9 @@ __global__ void __launch_bounds__(FA ? kThreadsFused : kThreads, 1)
                 uint32_t fphase = 0;
                 WorkIter it(p, cid, ncl);
                 Work w;
+                int ptc = -1;          // trace: tile count
                 while (it.next(p, w)) {
+                    ++ptc;
                     int tm, tn;
                     tile_coords(w.tile, p.tiles_m, p.tiles_n, p.group_m, tm, tn);
                     tm = tm * MC + (int)pair;
@@ -413,6 +415,7 @@ __global__ void __launch_bounds__(FA ? kThreadsFused : kThreads, 1)
                     }
                     for (int kb = w.i0 * S; kb < kb_end; ++kb) {
                         mbar_wait(&empty[stage], phase ^ 1u);
+                        if (kb == w.i0 * S && ptc < 5) trace(17 + ptc);   // first load of the tile issued
                         uint8_t *a_dst = sA + stage * Cf::A_STAGE;
                         uint8_t *b_dst = sB + stage * Cf::B_STAGE;
                         if constexpr (CG == 1) {
@@ -464,7 +467,9 @@ __global__ void __launch_bounds__(FA ? kThreadsFused : kThreads, 1)
                 uint32_t phase = 0, acc_it = 0;
                 WorkIter it(p, cid, ncl);
                 Work w;
+                int mtc = -1;          // trace: tile count
                 while (it.next(p, w)) {
+                    ++mtc;
                     const int kb_end = min(p.nkb, w.i1 * S);
                     if constexpr (PM) {
                         // the whole tile (k <= 32 S) at once: wait for its stages, issue every
@@ -531,6 +536,7 @@ __global__ void __launch_bounds__(FA ? kThreadsFused : kThreads, 1)
                             }
                         }
                         tc_fence_after();
+                        if (kb == w.i0 * S && mtc < 5 && lane == 0) trace(22 + mtc);   // first MMAs of the tile
                         // buffer layout: SA -> small at buf*BN, big at 256 + buf*BN; else one at buf*256
                         const uint32_t d_big = SA ? tmem_base + kTmemBufStride + buf * BN : tmem_base + buf * kTmemBufStride;
                         const uint32_t d_small = SA ? tmem_base + buf * BN : d_big;

@@ -20,37 +20,59 @@ namespace bf16x {
 // same layout: each thread splits 8 consecutive rows of one column per iteration;
 // 16-byte vector loads/stores when the whole matrix is 16-byte aligned (vec != 0).
 // ---------------------------------------------------------------------------------
-template <int NP, bool SC>
+// U chunks per thread per loop trip: all U chunks' loads are issued before the first split, so each
+// thread keeps U x 32 bytes in flight.  U = 4 in the grid-stride launch of both operands in their
+// own layout (8 blocks per SM: 4096^2 x 2 5422 -> 5818 GB/s, 8192^2 5502 -> 6042; r09
+// tools/split_bw.py); U = 1 where the grid covers the matrix (the standalone split: U = 4 costs
+// registers and residency there, 5779 -> 4516 GB/s at 4096^2) and beside the transposed A half.
+template <int NP, bool SC, int U = 1>
 __device__ __forceinline__ void split_same_body(int64_t rows, int64_t cols, const float *__restrict__ X, int64_t ldx,
                                                 uint16_t *__restrict__ P0, uint16_t *__restrict__ P1,
                                                 uint16_t *__restrict__ P2, int64_t ldp, int vec, int64_t vblock,
                                                 int64_t vgrid) {
     const int64_t nchunk = (rows + 7) / 8;
     const int64_t total = nchunk * cols;
-    for (int64_t t = vblock * blockDim.x + threadIdx.x; t < total; t += vgrid * blockDim.x) {
-        const int64_t col = t / nchunk, ch = t - col * nchunk;
-        const float *x = X + col * ldx;
-        const int64_t o = col * ldp;
-        const int64_t r0 = ch * 8;
-        if (vec && r0 + 8 <= rows) {
-            const float4 u = __ldcs(reinterpret_cast<const float4 *>(x + r0));
-            const float4 w = __ldcs(reinterpret_cast<const float4 *>(x + r0 + 4));
-            uint32_t q[4][3];
-            split_pair<NP, SC>(u.x, u.y, q[0]);
-            split_pair<NP, SC>(u.z, u.w, q[1]);
-            split_pair<NP, SC>(w.x, w.y, q[2]);
-            split_pair<NP, SC>(w.z, w.w, q[3]);
-            __stcs(reinterpret_cast<uint4 *>(P0 + o + r0), make_uint4(q[0][0], q[1][0], q[2][0], q[3][0]));
-            if constexpr (NP >= 2)
-                __stcs(reinterpret_cast<uint4 *>(P1 + o + r0), make_uint4(q[0][1], q[1][1], q[2][1], q[3][1]));
-            if constexpr (NP >= 3)
-                __stcs(reinterpret_cast<uint4 *>(P2 + o + r0), make_uint4(q[0][2], q[1][2], q[2][2], q[3][2]));
-        } else {
-            for (int64_t r = r0; r < rows && r < r0 + 8; ++r) {
-                Split3 s = split3_t<SC>(x[r]);
-                P0[o + r] = (uint16_t)s.b0;
-                if constexpr (NP >= 2) P1[o + r] = (uint16_t)s.b1;
-                if constexpr (NP >= 3) P2[o + r] = (uint16_t)s.b2;
+    const int64_t stride = vgrid * blockDim.x;
+    for (int64_t t0 = vblock * blockDim.x + threadIdx.x; t0 < total; t0 += U * stride) {
+        float4 u[U], w[U];
+        bool full[U];
+        int64_t xo[U], o[U];
+#pragma unroll
+        for (int q = 0; q < U; ++q) {
+            const int64_t t = t0 + q * stride;
+            const int64_t col = t / nchunk, r0 = (t - col * nchunk) * 8;
+            xo[q] = col * ldx + r0;
+            o[q] = col * ldp + r0;
+            full[q] = t < total && vec && r0 + 8 <= rows;
+            if (full[q]) {
+                u[q] = __ldcs(reinterpret_cast<const float4 *>(X + xo[q]));
+                w[q] = __ldcs(reinterpret_cast<const float4 *>(X + xo[q] + 4));
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < U; ++q) {
+            const int64_t t = t0 + q * stride;
+            if (t >= total) break;
+            if (full[q]) {
+                uint32_t v[4][3];
+                split_pair<NP, SC>(u[q].x, u[q].y, v[0]);
+                split_pair<NP, SC>(u[q].z, u[q].w, v[1]);
+                split_pair<NP, SC>(w[q].x, w[q].y, v[2]);
+                split_pair<NP, SC>(w[q].z, w[q].w, v[3]);
+                __stcs(reinterpret_cast<uint4 *>(P0 + o[q]), make_uint4(v[0][0], v[1][0], v[2][0], v[3][0]));
+                if constexpr (NP >= 2)
+                    __stcs(reinterpret_cast<uint4 *>(P1 + o[q]), make_uint4(v[0][1], v[1][1], v[2][1], v[3][1]));
+                if constexpr (NP >= 3)
+                    __stcs(reinterpret_cast<uint4 *>(P2 + o[q]), make_uint4(v[0][2], v[1][2], v[2][2], v[3][2]));
+            } else {
+                const int64_t col = t / nchunk, r0 = (t - col * nchunk) * 8;
+                const float *x = X + col * ldx;
+                for (int64_t r = r0; r < rows && r < r0 + 8; ++r) {
+                    Split3 sp = split3_t<SC>(x[r]);
+                    P0[o[q] - r0 + r] = (uint16_t)sp.b0;
+                    if constexpr (NP >= 2) P1[o[q] - r0 + r] = (uint16_t)sp.b1;
+                    if constexpr (NP >= 3) P2[o[q] - r0 + r] = (uint16_t)sp.b2;
+                }
             }
         }
     }
@@ -178,9 +200,9 @@ __global__ void __launch_bounds__(256) split_ab_kernel(SplitArgs a, SplitArgs b,
             split_trans_body<NPA, SC, kTransTCab>(a.rows, a.cols, a.X, a.ldx, a.P0, a.P1, a.P2, a.ldp, a.vec, blockIdx.x,
                                                   gA, s_trans);
         else
-            split_same_body<NPA, SC>(a.rows, a.cols, a.X, a.ldx, a.P0, a.P1, a.P2, a.ldp, a.vec, blockIdx.x, gA);
+            split_same_body<NPA, SC, 4>(a.rows, a.cols, a.X, a.ldx, a.P0, a.P1, a.P2, a.ldp, a.vec, blockIdx.x, gA);
     } else
-        split_same_body<NPB, SC>(b.rows, b.cols, b.X, b.ldx, b.P0, b.P1, b.P2, b.ldp, b.vec, blockIdx.x - gA,
+        split_same_body<NPB, SC, TA ? 1 : 4>(b.rows, b.cols, b.X, b.ldx, b.P0, b.P1, b.P2, b.ldp, b.vec, blockIdx.x - gA,
                              gridDim.x - gA);
 }
 

@@ -35,8 +35,6 @@ def g():
                 a_plane=m * kp, B_pieces=Bp.data_ptr(), ldbp=kp, b_plane=n * kp)
 
 
-stg = int(os.environ.get("STAGGER", "0"))
-L.bf16x_stagger(stg, 0)
 for _ in range(3):
     g()
 torch.cuda.synchronize()
@@ -55,11 +53,7 @@ t0 = T[:, 0].min()
 R = (T - t0) / 1e3          # us since the first CTA started
 print(f"{m}x{n}x{k} x{v} dbg {extra_dbg}: event time {e0.elapsed_time(e1) * 1e3:.1f} us, CTAs traced {used.sum()}")
 print(f"  CTA start spread: {np.ptp(R[:, 0]):.2f} us; prologue (start -> griddepcontrol done): median {np.median(R[:, 1] - R[:, 0]):.2f} us")
-tiles = ((m + 255) // 256) * ((n + 255) // 256)
-cid = np.arange(148)[used] // 2
-late = cid >= (tiles % 74 if tiles % 74 else 37)
-for grp, sel in ((("all", np.ones_like(late)),) if not stg else (("early", ~late), ("late", late))):
-  print(f" CTAs: {grp} (stagger {stg} ns)")
+for sel in (np.ones(len(T), dtype=bool),):
   for t in range(9):
     a, b, c = R[:, 2 + 3 * t], R[:, 3 + 3 * t], R[:, 4 + 3 * t]
     ok = (T[:, 2 + 3 * t] > 0) & (T[:, 4 + 3 * t] > 0) & sel
@@ -67,5 +61,13 @@ for grp, sel in ((("all", np.ones_like(late)),) if not stg else (("early", ~late
         break
     print(f"  tile {t}: first promotion at {np.median(a[ok]):7.2f} us (max {a[ok].max():7.2f}), last at {np.median(b[ok]):7.2f}, "
           f"C issued at {np.median(c[ok]):7.2f} (max {c[ok].max():7.2f}), CTAs {ok.sum()}")
+  for t in range(5):
+    pl, ms = R[:, 17 + t], R[:, 22 + t]
+    okp = (T[:, 17 + t] > 0) & sel
+    okm = (T[:, 22 + t] > 0) & sel
+    if okp.sum() == 0:
+        break
+    print(f"  tile {t}: producer first load at {np.median(pl[okp]):7.2f} us (max {pl[okp].max():7.2f}), "
+          f"MMA first interval at {np.median(ms[okm]) if okm.any() else float('nan'):7.2f} us (leader CTAs {okm.sum()})")
 done = R[:, 31]
 print(f"  all stores complete: median {np.median(done[T[:, 31] > 0]):.2f} us, max {done[T[:, 31] > 0].max():.2f} us")

@@ -38,13 +38,25 @@ L = bx.lib()
 
 def fab(i):
     a = P[i].data_ptr()
-    b = P[(i + 1) % NB].data_ptr()
+    b = P[(i + 2) % NB].data_ptr()
     L.bf16x_split_operands(n, n, n, X[i].data_ptr(), n, X[(i + 1) % NB].data_ptr(), n, 3, a, n, n * n, b, n, n * n,
-                           None)
+                           None)   # (K-major A)
 
 
 ms = timeit(fab, NB)
 print(f"split_ab    n={n}: {ms * 1e3:.1f} us  {20 * n * n / ms / 1e6:.0f} GB/s algorithmic (both operands)", flush=True)
+
+
+def fmn(i):
+    a = P[i].data_ptr()
+    b = P[(i + 2) % NB].data_ptr()
+    L.bf16x_split_operands_ex(n, n, n, X[i].data_ptr(), n, X[(i + 1) % NB].data_ptr(), n, 3, a, n, n * n, b, n, n * n,
+                              bx.A_PIECES_MN, None)
+
+
+ms = timeit(fmn, NB)
+print(f"split_ab_mn n={n}: {ms * 1e3:.1f} us  {20 * n * n / ms / 1e6:.0f} GB/s algorithmic (both, A in its own layout)",
+      flush=True)
 ms = timeit(lambda i: Y[i].copy_(X[i]), NB)
 print(f"copy fp32   n={n}: {ms * 1e3:.1f} us  {8 * n * n / ms / 1e6:.0f} GB/s", flush=True)
 Z = [torch.empty(3 * n * n, dtype=torch.uint16, device="cuda") for _ in range(NB)]
