@@ -291,7 +291,9 @@ __device__ __forceinline__ void for_each_product(int nh, F &&f) {
 // its k, at most S stages) go bin by bin, smallest first: G collects the small bins before bin 0,
 // the paper's "bins added from smallest to largest" at the promotion level
 // (R24).
-template <int CG, int V, int BN, int S, int MC, bool SA, bool GD = false, bool FA = false, bool PM = false>
+// NB: TMEM accumulator buffers (2 of 256 columns; 4 of BN = 128 columns for the short-k tile, so the
+// tensor core can run a whole k = 256 tile ahead of the epilogue's C store).
+template <int CG, int V, int BN, int S, int MC, bool SA, bool GD = false, bool FA = false, bool PM = false, int NB = 2>
 __global__ void __launch_bounds__(FA ? kThreadsFused : kThreads, 1)
     gemm_split_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                       const __grid_constant__ CUtensorMap tmC, const KParams p) {
@@ -304,6 +306,8 @@ __global__ void __launch_bounds__(FA ? kThreadsFused : kThreads, 1)
     constexpr int CL = CG * MC;   // cluster size
     static_assert(MC == 1 || CG == 2, "multicast needs 2-CTA pairs");
     static_assert(!SA || 2 * BN <= kTmemBufStride, "split accumulators need 4 x BN TMEM columns");
+    constexpr int ACC_STRIDE = NB == 2 ? kTmemBufStride : BN;   // TMEM columns between accumulator buffers
+    static_assert(NB == 2 || (!SA && !PM && NB * BN <= kTmemCols && NB <= 4), "accumulator ring");
     static_assert(!GD || SA, "FP64 collection needs split accumulators");
     constexpr int NG = GD ? 2 : 1;     // promoted accumulators per output element
     extern __shared__ uint8_t smem_raw[];
@@ -317,8 +321,8 @@ __global__ void __launch_bounds__(FA ? kThreadsFused : kThreads, 1)
     uint64_t *full = reinterpret_cast<uint64_t *>(epi + EPI_BYTES);
     uint64_t *empty = full + NST;
     uint64_t *acc_full = empty + NST;
-    uint64_t *acc_empty = acc_full + 2;
-    uint64_t *f32_full = acc_empty + 2;
+    uint64_t *acc_empty = acc_full + NB;
+    uint64_t *f32_full = acc_empty + NB;
     uint64_t *f32_empty = f32_full + (NF > 2 ? NF : 2);
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(f32_empty + (NF > 2 ? NF : 2));
 
@@ -351,7 +355,7 @@ __global__ void __launch_bounds__(FA ? kThreadsFused : kThreads, 1)
             mbar_init(&full[s], FA ? 1 + kNumXfWarps * CG : 1);
             mbar_init(&empty[s], MC);     // one commit per pair reading the (shared) stage
         }
-        for (int b = 0; b < 2; ++b) {
+        for (int b = 0; b < NB; ++b) {
             mbar_init(&acc_full[b], 1);
             mbar_init(&acc_empty[b], kNumEpiWarps * CG);
         }
@@ -501,7 +505,7 @@ __global__ void __launch_bounds__(FA ? kThreadsFused : kThreads, 1)
 #pragma unroll
                             for (int r = 1; r < S; ++r)
                                 if (q == r) { a0 = ad[r]; b0 = bd[r]; }
-                            umma_bf16_elect<CG>(tmem_base + buf * kTmemBufStride,
+                            umma_bf16_elect<CG>(tmem_base + buf * ACC_STRIDE,
                                                 a0 + (uint64_t)(i * a_ps + kk * a_ks),
                                                 b0 + (uint64_t)((j * Cf::B_PIECE + kk * (kUK * 2)) >> 4), idesc, 0u);
                             umma_commit_elect<CG>(&acc_full[buf]);
@@ -514,7 +518,7 @@ __global__ void __launch_bounds__(FA ? kThreadsFused : kThreads, 1)
                     }
                     for (int kb = w.i0 * S; kb < kb_end; kb += S, ++acc_it) {
                         const int ns = min(S, kb_end - kb);
-                        const uint32_t buf = acc_it & 1u, apar = (acc_it >> 1) & 1u;
+                        const uint32_t buf = acc_it % NB, apar = (acc_it / NB) & 1u;
                         mbar_wait(&acc_empty[buf], apar ^ 1u);
                         uint64_t a_desc[S], b_desc[S];
                         int stages[S];
@@ -538,7 +542,7 @@ __global__ void __launch_bounds__(FA ? kThreadsFused : kThreads, 1)
                         tc_fence_after();
                         if (kb == w.i0 * S && mtc < 5 && lane == 0) trace(22 + mtc);   // first MMAs of the tile
                         // buffer layout: SA -> small at buf*BN, big at 256 + buf*BN; else one at buf*256
-                        const uint32_t d_big = SA ? tmem_base + kTmemBufStride + buf * BN : tmem_base + buf * kTmemBufStride;
+                        const uint32_t d_big = SA ? tmem_base + kTmemBufStride + buf * BN : tmem_base + buf * ACC_STRIDE;
                         const uint32_t d_small = SA ? tmem_base + buf * BN : d_big;
                         issue_interval<CG, V, BN, S, SA, kLazy>(d_big, d_small, a_desc, b_desc, ns, idesc, p.scaled != 0,
                                                                 lz ? full : nullptr, stages, phs, a_ps, a_ks);
@@ -624,11 +628,11 @@ __global__ void __launch_bounds__(FA ? kThreadsFused : kThreads, 1)
                 }
             } else
             for (int kb = w.i0 * S; kb < kb_end; kb += S, ++acc_it) {
-                const uint32_t buf = acc_it & 1u, apar = (acc_it >> 1) & 1u;
+                const uint32_t buf = acc_it % NB, apar = (acc_it / NB) & 1u;
                 mbar_wait(&acc_full[buf], apar);
                 tc_fence_after();
                 if constexpr (!SA) {
-                    const uint32_t taddr = tm_lane + buf * kTmemBufStride;
+                    const uint32_t taddr = tm_lane + buf * ACC_STRIDE;
 #pragma unroll
                     for (int c = 0; c < EC / 16; ++c) {
                         float v[16];
@@ -872,13 +876,14 @@ int make_piece_map_mn(CUtensorMap *map, const uint16_t *base, int m, int k, int6
 int sk_workspace(cudaStream_t st, size_t ws_floats, size_t nflags, float **ws, unsigned int **flags,
                  unsigned int *epoch);
 
-template <int CG, int V, int BN, int S, int MC, bool SA = false, bool GD = false, bool FA = false, bool PM = false>
+template <int CG, int V, int BN, int S, int MC, bool SA = false, bool GD = false, bool FA = false, bool PM = false,
+          int NB = 2>
 int launch_t(const GemmPlan &pl, cudaStream_t st) {
     using Cf = Cfg<CG, V, BN>;
     constexpr int CL = CG * MC;
     constexpr int THREADS = FA ? kThreadsFused : kThreads;
     constexpr int SMEM = FA ? CfgFA<V>::SMEM : Cf::SMEM;
-    auto kern = gemm_split_kernel<CG, V, BN, S, MC, SA, GD, FA, PM>;
+    auto kern = gemm_split_kernel<CG, V, BN, S, MC, SA, GD, FA, PM, NB>;
     CUtensorMap tmA, tmB, tmC;
     int rc;
     if constexpr (FA) {
@@ -1015,7 +1020,7 @@ int launch_t(const GemmPlan &pl, cudaStream_t st) {
 inline int choose_tile_n(int m, int n, int cg, int units, int forced) {
     (void)m; (void)n; (void)units;
     if (cg == 1) return 256;
-    if (forced == 192) return 192;
+    if (forced == 192 || forced == 128) return forced;
     return 256;
 }
 
@@ -1074,6 +1079,7 @@ int launch_s(const GemmPlan &pl, cudaStream_t st) {
             const int bn = choose_tile_n(pl.m, pl.n, CG, units, pl.tile_n);
             if (bn == 192) return launch_t<CG, V, 192, 2, 1>(pl, st);
             if (pl.split_acc && V >= 3) return launch_t<CG, V, 128, 2, 1, true>(pl, st);
+            if (bn == 128) return launch_t<CG, V, 128, 2, 1, false, false, false, false, 4>(pl, st);
             // Two pairs per cluster sharing B (TMA multicast) cut L2->SM and DRAM traffic by a
             // quarter but clusters of 4 leave 16 SMs idle; measured (r05) a win only for large
             // outputs, where the kernel runs long enough to be power-limited (16384^3: x3 +17 %,

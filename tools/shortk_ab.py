@@ -12,7 +12,14 @@ import paper_1904_06376_b200 as bx
 
 L = bx.lib()
 m = n = 4096
-tag = os.environ.get("BF16X_LIB", "default")
+tag = (os.environ.get("BF16X_LIB", "default") + " mc" + os.environ.get("MC", "0") + " spi" + os.environ.get("SPI", "0")
+       + " bn" + os.environ.get("BN", "0"))
+MC, SPI, BN = (int(os.environ.get(x, "0")) for x in ("MC", "SPI", "BN"))
+
+
+def hooks(on):
+    L.bf16x_multicast(MC if on else 0)
+    L.bf16x_tune(0, BN if on else 0, SPI if on else 0)
 
 
 def tm(fn, it=50):
@@ -45,7 +52,13 @@ for k in (256, 512, 1024, 4096):
         def g():
             bx.gemm_raw(m, n, k, 1.0, 0, m, 0, k, 0.0, C.data_ptr(), ldc, variant=v, A_pieces=Ap.data_ptr(), ldap=kp,
                         a_plane=m * kp, B_pieces=Bp.data_ptr(), ldbp=kp, b_plane=n * kp)
+        hooks(False)
+        g()
+        ref = C.clone()
+        hooks(True)
         t = min(tm(g, 50 if k < 4096 else 20) for _ in range(3))
+        same = torch.equal(C.view(torch.int32), ref.view(torch.int32))
+        hooks(False)
         roof = v * 2.0 * m * n * k / 1691.9e12 * 1e6
-        out.append(f"k{k} x{v} {t:.1f}us ({100 * roof / t:.0f}%)")
+        out.append(f"k{k} x{v} {t:.1f}us ({100 * roof / t:.0f}%){'' if same else ' DIFFERS'}")
 print(tag, " ".join(out), flush=True)
