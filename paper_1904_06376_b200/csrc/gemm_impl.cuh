@@ -291,9 +291,7 @@ __device__ __forceinline__ void for_each_product(int nh, F &&f) {
 // its k, at most S stages) go bin by bin, smallest first: G collects the small bins before bin 0,
 // the paper's "bins added from smallest to largest" at the promotion level
 // (R24).
-// NB: TMEM accumulator buffers (2 of 256 columns; 4 of BN = 128 columns for the short-k tile, so the
-// tensor core can run a whole k = 256 tile ahead of the epilogue's C store).
-template <int CG, int V, int BN, int S, int MC, bool SA, bool GD = false, bool FA = false, bool PM = false, int NB = 2>
+template <int CG, int V, int BN, int S, int MC, bool SA, bool GD = false, bool FA = false, bool PM = false>
 __global__ void __launch_bounds__(FA ? kThreadsFused : kThreads, 1)
     gemm_split_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                       const __grid_constant__ CUtensorMap tmC, const KParams p) {
@@ -306,8 +304,7 @@ __global__ void __launch_bounds__(FA ? kThreadsFused : kThreads, 1)
     constexpr int CL = CG * MC;   // cluster size
     static_assert(MC == 1 || CG == 2, "multicast needs 2-CTA pairs");
     static_assert(!SA || 2 * BN <= kTmemBufStride, "split accumulators need 4 x BN TMEM columns");
-    constexpr int ACC_STRIDE = NB == 2 ? kTmemBufStride : BN;   // TMEM columns between accumulator buffers
-    static_assert(NB == 2 || (!SA && !PM && NB * BN <= kTmemCols && NB <= 4), "accumulator ring");
+    constexpr int NB = 2, ACC_STRIDE = kTmemBufStride;   // TMEM accumulator buffers, columns apart
     static_assert(!GD || SA, "FP64 collection needs split accumulators");
     constexpr int NG = GD ? 2 : 1;     // promoted accumulators per output element
     extern __shared__ uint8_t smem_raw[];
@@ -876,14 +873,13 @@ int make_piece_map_mn(CUtensorMap *map, const uint16_t *base, int m, int k, int6
 int sk_workspace(cudaStream_t st, size_t ws_floats, size_t nflags, float **ws, unsigned int **flags,
                  unsigned int *epoch);
 
-template <int CG, int V, int BN, int S, int MC, bool SA = false, bool GD = false, bool FA = false, bool PM = false,
-          int NB = 2>
+template <int CG, int V, int BN, int S, int MC, bool SA = false, bool GD = false, bool FA = false, bool PM = false>
 int launch_t(const GemmPlan &pl, cudaStream_t st) {
     using Cf = Cfg<CG, V, BN>;
     constexpr int CL = CG * MC;
     constexpr int THREADS = FA ? kThreadsFused : kThreads;
     constexpr int SMEM = FA ? CfgFA<V>::SMEM : Cf::SMEM;
-    auto kern = gemm_split_kernel<CG, V, BN, S, MC, SA, GD, FA, PM, NB>;
+    auto kern = gemm_split_kernel<CG, V, BN, S, MC, SA, GD, FA, PM>;
     CUtensorMap tmA, tmB, tmC;
     int rc;
     if constexpr (FA) {
@@ -1020,7 +1016,7 @@ int launch_t(const GemmPlan &pl, cudaStream_t st) {
 inline int choose_tile_n(int m, int n, int cg, int units, int forced) {
     (void)m; (void)n; (void)units;
     if (cg == 1) return 256;
-    if (forced == 192 || forced == 128) return forced;
+    if (forced == 192) return 192;
     return 256;
 }
 
@@ -1079,7 +1075,6 @@ int launch_s(const GemmPlan &pl, cudaStream_t st) {
             const int bn = choose_tile_n(pl.m, pl.n, CG, units, pl.tile_n);
             if (bn == 192) return launch_t<CG, V, 192, 2, 1>(pl, st);
             if (pl.split_acc && V >= 3) return launch_t<CG, V, 128, 2, 1, true>(pl, st);
-            if (bn == 128) return launch_t<CG, V, 128, 2, 1, false, false, false, false, 4>(pl, st);
             // Two pairs per cluster sharing B (TMA multicast) cut L2->SM and DRAM traffic by a
             // quarter but clusters of 4 leave 16 SMs idle; measured (r05) a win only for large
             // outputs, where the kernel runs long enough to be power-limited (16384^3: x3 +17 %,
