@@ -13,13 +13,15 @@ import paper_1904_06376_b200 as bx
 L = bx.lib()
 m = n = 4096
 tag = (os.environ.get("BF16X_LIB", "default") + " mc" + os.environ.get("MC", "0") + " spi" + os.environ.get("SPI", "0")
-       + " bn" + os.environ.get("BN", "0"))
-MC, SPI, BN = (int(os.environ.get(x, "0")) for x in ("MC", "SPI", "BN"))
+       + " bn" + os.environ.get("BN", "0") + " ae" + os.environ.get("AE", "0"))
+MC, SPI, BN, AE = (int(os.environ.get(x, "0")) for x in ("MC", "SPI", "BN", "AE"))
 
 
 def hooks(on):
     L.bf16x_multicast(MC if on else 0)
     L.bf16x_tune(0, BN if on else 0, SPI if on else 0)
+    if AE:   # (r09 probe build with the alternating-epilogue kernel; not kept)
+        L.bf16x_ae_max_k(AE if on else 0)
 
 
 def tm(fn, it=50):
