@@ -1,5 +1,5 @@
 // Per-SM L2 -> SM load bandwidth probe: G CTAs (one per SM at most, 1024 threads, 8 independent
-// 16-byte loads in flight per thread) stream an L2-resident 16 MB buffer `reps` times; prints the
+// 16-byte loads in flight per thread) stream an L2-resident 48 MB buffer `reps` times; prints the
 // per-CTA and aggregate rate for G = 8 .. 148.  (Companion of store_bw.cu.)
 #include <cstdio>
 #include <cuda_runtime.h>
@@ -21,7 +21,7 @@ __global__ void __launch_bounds__(1024) load_l2(const float4 *__restrict__ X, si
 }
 
 int main() {
-    const size_t bytes = 16u << 20, n4 = bytes / 16;
+    const size_t bytes = 48u << 20, n4 = bytes / 16;
     float4 *X;
     float *out;
     cudaMalloc(&X, bytes);
@@ -44,7 +44,7 @@ int main() {
             const size_t per = n4 / G;
             const double done = (double)G * (per / (8 * 1024)) * (8 * 1024) * 16.0 * reps;
             if (rep == 2)
-                printf("G %3d CTAs: %.1f us, %.1f GB/s per CTA, %.0f GB/s total (L2-resident 16 MB)\n", G, ms * 1e3,
+                printf("G %3d CTAs: %.1f us, %.1f GB/s per CTA, %.0f GB/s total (L2-resident 48 MB)\n", G, ms * 1e3,
                        done / G / (ms * 1e-3) / 1e9, done / (ms * 1e-3) / 1e9);
         }
     }
