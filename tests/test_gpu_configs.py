@@ -104,26 +104,34 @@ def test_config2_k_sweep_wide(orc):
                                      "accuracy": "16 sampled output columns vs FP64", "rows": rows})
 
 
-@pytest.mark.parametrize("m,n,k", [(16384, 16384, 16384), (16384, 2048, 16384)])
-def test_config3_full_size_sampled(orc, m, n, k):
+@pytest.mark.parametrize("m,n,k,variant", [(16384, 16384, 16384, 6), (16384, 2048, 16384, 6),
+                                           (16384, 16384, 16384, 3), (16384, 16384, 16384, 9)])
+def test_config3_full_size_sampled(orc, m, n, k, variant):
     """configs[3] at full size on one GPU: 16384^3 bf16x6 (the launch configuration of
-    `bench.py --config c4`: two CTA pairs per cluster sharing B by TMA multicast) and one rank's
-    column shard of it at P = 8 (16384 x 2048 x 16384, the per-GPU GEMM of the 8-GPU run).
-    Sampled output columns against the oracle: normwise error <= 2x the oracle's."""
+    `bench.py --config c4`: two CTA pairs per cluster sharing B by TMA multicast), one rank's
+    column shard of it at P = 8 (16384 x 2048 x 16384, the per-GPU GEMM of the 8-GPU run), and the
+    x3 / x9 variants at the same size (configs[3] names x3 / x6 / x9).  Sampled output columns
+    against the oracle: normwise error <= 2x the oracle's."""
     A = synthetic.uniform(m, k, seed=7)
     B = synthetic.uniform(k, n, seed=8)
     Ad = torch.from_numpy(np.asfortranarray(A)).cuda()
     Bd = torch.from_numpy(np.asfortranarray(B)).cuda()
-    G = bx.gemm(Ad, Bd, variant=6)
+    G = bx.gemm(Ad, Bd, variant=variant)
     torch.cuda.synchronize()
-    cols = np.linspace(0, n - 1, 24).astype(np.int64)
+    cols = np.linspace(0, n - 1, 24 if variant == 6 else 8).astype(np.int64)
     Gs = G[:, torch.from_numpy(cols).cuda()].cpu().numpy()
     del G, Ad, Bd
     torch.cuda.empty_cache()
-    O = orc.gemm(A, B, variant=6, cols=cols)
+    O = orc.gemm(A, B, variant=variant, cols=cols)
     C64 = orc.dgemm(A, B, cols=cols)
     eg = orc.normwise_error(Gs, C64, A, B[:, cols])
     eo = orc.normwise_error(O, C64, A, B[:, cols])
-    _report(f"config3_{m}x{n}x{k}_sampled.json", {"m": m, "n": n, "k": k, "variant": 6, "cols": cols.tolist(),
+    tag = "" if variant == 6 else f"_x{variant}"
+    _report(f"config3_{m}x{n}x{k}{tag}_sampled.json", {"m": m, "n": n, "k": k, "variant": variant, "cols": cols.tolist(),
                                                    "gpu_error": eg, "oracle_error": eo, "ratio": eg / eo})
     assert eg <= RATIO * eo, (eg, eo)
+    if variant >= 6:   # and every sampled output inside the elementwise bound of section II-E (P:321, R11)
+        u = 2.0 ** -24
+        gam = (k + 2) * u / (1 - (k + 2) * u)
+        bound = 1.01 * (gam + 2.0 ** -24) * (np.abs(A.astype(np.float64)) @ np.abs(B[:, cols].astype(np.float64)))
+        assert (np.abs(Gs.astype(np.float64) - C64) <= bound).all()
