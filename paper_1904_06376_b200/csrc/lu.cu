@@ -1020,8 +1020,9 @@ static int sub_rpt(int n, int cl) {
 // 2 = keys by st.async + winning row read from its CTA (default), 0 = whole records by 9 st.async
 // per peer, 1 = whole records by one bulk copy per peer, 3 = keys by plain remote stores polled
 // locally.  All four are bit-identical; measured (r06, tools/lu_bulk_probe.py / lu_time.py) the
-// factorisation device time is the same within 1 % (26.4 ms at n = 8192): the exchange is not
-// what bounds the ~1.9 us per column.
+// factorisation device time is the same within 1 % (26.4 ms at n = 8192): how the keys travel does
+// not change the ~1.9 us per column, whose critical path is warp 0's exchange chain itself (r09 ncu:
+// the row warps wait at its closing barrier for ~half of all stall samples).
 static int g_sub_bulk = 2;
 extern "C" void bf16x_lu_subpanel_bulk(int mode) { g_sub_bulk = mode & 7; }   // bit 4: trace
 
