@@ -9,8 +9,11 @@
 // B200 mapping:
 //   * persistent grid, one CTA per SM (cta_group::1, 128 x 256 tile) or one CTA pair per
 //     two SMs (cta_group::2, 256 x 256 tile, B halves split across the pair);
-//   * warp 0: TMA producer.  One 3D TMA box per operand per stage brings BK = 32 values of
-//     k for all p pieces: smem [piece][rows][32 bf16] with the 64-byte swizzle;
+//   * warp 0: TMA producer.  Per stage (BK = 32 values of k, all p pieces): B by one 3D TMA box,
+//     smem [piece][rows][32 bf16] with the 64-byte swizzle (K-major); A either the same way
+//     (K-major pieces from bf16x_split_t) or, as bf16x_gemm splits it since r09, in A's own
+//     column-major layout by two boxes [piece][k 32][m 64] with the 128-byte swizzle, which the
+//     MMA reads MN-major (instruction descriptor a_major = MN);
 //   * warp 1: MMA issuer (one thread).  Per stage (= one promotion interval of 32 k) it
 //     issues the variant's products band by band, smallest bin first, both K=16 halves
 //     of a band before the next band, into one TMEM accumulator whose first MMA
