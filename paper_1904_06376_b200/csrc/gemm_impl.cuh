@@ -469,6 +469,9 @@ __global__ void __launch_bounds__(FA ? kThreadsFused : kThreads, 1)
                 WorkIter it(p, cid, ncl);
                 Work w;
                 int mtc = -1;          // trace: tile count
+#ifdef BF16X_TRACE
+                long long wait_acc = 0, wait_full = 0, t_issue0 = clock64();   // issuer wait cycles
+#endif
                 while (it.next(p, w)) {
                     ++mtc;
                     const int kb_end = min(p.nkb, w.i1 * S);
@@ -516,7 +519,14 @@ __global__ void __launch_bounds__(FA ? kThreadsFused : kThreads, 1)
                     for (int kb = w.i0 * S; kb < kb_end; kb += S, ++acc_it) {
                         const int ns = min(S, kb_end - kb);
                         const uint32_t buf = acc_it % NB, apar = (acc_it / NB) & 1u;
+#ifdef BF16X_TRACE
+                        const long long tw0 = clock64();
+#endif
                         mbar_wait(&acc_empty[buf], apar ^ 1u);
+#ifdef BF16X_TRACE
+                        const long long tw1 = clock64();
+                        wait_acc += tw1 - tw0;
+#endif
                         uint64_t a_desc[S], b_desc[S];
                         int stages[S];
                         uint32_t phs[S];
@@ -537,6 +547,10 @@ __global__ void __launch_bounds__(FA ? kThreadsFused : kThreads, 1)
                             }
                         }
                         tc_fence_after();
+#ifdef BF16X_TRACE
+                        const long long tw2 = clock64();
+                        wait_full += tw2 - tw1;
+#endif
                         if (kb == w.i0 * S && mtc < 5 && lane == 0) trace(22 + mtc);   // first MMAs of the tile
                         // buffer layout: SA -> small at buf*BN, big at 256 + buf*BN; else one at buf*256
                         const uint32_t d_big = SA ? tmem_base + kTmemBufStride + buf * BN : tmem_base + buf * ACC_STRIDE;
@@ -553,6 +567,13 @@ __global__ void __launch_bounds__(FA ? kThreadsFused : kThreads, 1)
                         else umma_commit2_mask_elect(&acc_full[buf], (uint16_t)(3u << (CG * pair)));
                     }
                 }
+#ifdef BF16X_TRACE
+                if ((p.dbg & 2) && lane == 0) {   // slots 27 / 28 / 29: cycles waiting acc_empty / full, total
+                    p.trace[blockIdx.x * 32 + 27] = (unsigned long long)wait_acc;
+                    p.trace[blockIdx.x * 32 + 28] = (unsigned long long)wait_full;
+                    p.trace[blockIdx.x * 32 + 29] = (unsigned long long)(clock64() - t_issue0);
+                }
+#endif
             }
         }
     } else if (warp < 4 + kNumEpiWarps) {

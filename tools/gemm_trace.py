@@ -69,5 +69,10 @@ for sel in (np.ones(len(T), dtype=bool),):
         break
     print(f"  tile {t}: producer first load at {np.median(pl[okp]):7.2f} us (max {pl[okp].max():7.2f}), "
           f"MMA first interval at {np.median(ms[okm]) if okm.any() else float('nan'):7.2f} us (leader CTAs {okm.sum()})")
+lead = T[:, 29] > 0
+if lead.any():
+    wa, wf, tot = (T[lead, q].astype(np.float64) for q in (27, 28, 29))
+    print(f"  MMA issuer (leader CTAs {lead.sum()}): waits acc_empty {np.median(wa / tot) * 100:.1f} % / full stages "
+          f"{np.median(wf / tot) * 100:.1f} % of its cycles (median), total {np.median(tot):.0f} cycles")
 done = R[:, 31]
 print(f"  all stores complete: median {np.median(done[T[:, 31] > 0]):.2f} us, max {done[T[:, 31] > 0].max():.2f} us")
