@@ -31,19 +31,11 @@ constexpr int kTmemBufStride = 256;
 constexpr int kGroupM = 8;            // tile raster: 8 m-tiles per group for L2 reuse (default)
 constexpr int kDefaultCtaGroup = 2;   // 2-CTA pairs, 64-k promotion interval
 constexpr int kSmemBudget = 232448 - 1024;   // 227 KB opt-in maximum
-// C epilogue staging (TMA store): per epilogue warp two buffers of 32 rows x 16 columns FP32
-#ifndef BF16X_EPI_NBUF
-#define BF16X_EPI_NBUF 2
-#endif
-#ifndef BF16X_EPI_GROUP
-#define BF16X_EPI_GROUP 1
-#endif
-// kEpiGroup: the 4 warps of a column half (TMEM lane quadrants 0..3) stage one 128-row box
-constexpr bool kEpiGroup = BF16X_EPI_GROUP != 0;
-constexpr int kEpiRows = kEpiGroup ? 128 : 32, kEpiCols = 16;
-constexpr int kEpiNBuf = BF16X_EPI_NBUF;                // staging buffers per epilogue warp (group)
-constexpr int kEpiBuf = 32 * kEpiCols * 4;
-constexpr int kEpiBytes = kNumEpiWarps * kEpiNBuf * kEpiBuf;   // 32 KB
+// C epilogue staging (TMA store): per column half (the 4 epilogue warps of TMEM lane quadrants
+// 0..3) two buffers of one 128-row x 16-column FP32 box (r09: 128-row boxes instead of one 32-row
+// box per warp, x6 short k -4 %; 1-4 buffers measured alike, profiles/r09/shortk_epi_*.txt)
+constexpr int kEpiRows = 128, kEpiCols = 16, kEpiNBuf = 2;
+constexpr int kEpiBytes = 2 * kEpiNBuf * kEpiRows * kEpiCols * 4;   // 32 KB
 inline int g_lazy_full = 1;           // lazy stage waits in the MMA issuer (bf16x_lazy_full hook)
 inline int g_gemm_debug = 0;          // KParams::dbg (bf16x_gemm_debug hook; tests / probes only)
 inline unsigned long long *g_gemm_trace = nullptr;   // KParams::trace (bf16x_gemm_trace hook)
@@ -723,22 +715,20 @@ __global__ void __launch_bounds__(FA ? kThreadsFused : kThreads, 1)
                 for (int j = 0; j < EC; ++j) G[j] = __double2float_rn(__dadd_rn((double)G[EC + j] * qd, (double)G[j]));
             }
             auto zval = [&](int j) -> float { return G[j]; };
-            // beta = 0 stores and the red-add update go through shared memory and TMA: each warp
-            // stages 16 columns of its 32 rows (2 KB, double-buffered) and one lane issues a 2D
-            // tensor store (or element-wise add in L2) of the box; the warp continues with the next
-            // tile while the TMA engine drains (rows / columns outside C are clipped by the TMA)
+            // beta = 0 stores and the red-add update go through shared memory and TMA: the four warps
+            // of a column half stage a 128-row x 16-column box (8 KB, double-buffered) and warp quad 0's
+            // lane 0 issues a 2D tensor store (or element-wise add in L2) of it; the warps continue with
+            // the next tile while the TMA engine drains (rows / columns outside C are clipped by the TMA)
             const bool radd = CG == 2 && BN == 256 && !GD && red_add;
             if (TMA_EPI && p.tma_c && !(p.flags & BF16X_ACC_OUT) && (p.beta == 0.f || radd)) {
-                if (kEpiGroup && !(p.dbg & 1)) {
-                    // one 128-row x 16-column box per column half: warps quad 0..3 fill their 32
-                    // rows, warp quad 0's lane 0 issues the store
+                if (!(p.dbg & 1)) {
                     float *gbuf = reinterpret_cast<float *>(epi) + half * (kEpiNBuf * kEpiRows * kEpiCols);
                     const int grow = tm * Cf::TILE_M + (int)rank * kBM;
                     const bool issuer = quad == 0 && lane == 0;
 #pragma unroll
                     for (int q = 0; q < EC / kEpiCols; ++q) {
                         float *dst = gbuf + (q % kEpiNBuf) * (kEpiRows * kEpiCols);
-                        if (issuer) bulk_wait_read<kEpiNBuf - 1>();
+                        if (issuer) bulk_wait_read<kEpiNBuf - 1>();   // this buffer's last store has read it
                         asm volatile("bar.sync %0, 128;" ::"r"(2 + half) : "memory");
 #pragma unroll
                         for (int j = 0; j < kEpiCols; ++j)
@@ -749,26 +739,6 @@ __global__ void __launch_bounds__(FA ? kThreadsFused : kThreads, 1)
                         if (issuer) {
                             if (radd) tma_reduce_add_2d(&tmC, dst, grow, col0 + q * kEpiCols);
                             else tma_store_2d(&tmC, dst, grow, col0 + q * kEpiCols);
-                            bulk_commit();
-                        }
-                    }
-                } else if (!(p.dbg & 1)) {
-                    float *wbuf = reinterpret_cast<float *>(epi) + ew * (kEpiNBuf * kEpiRows * kEpiCols);
-                    const int wrow = tm * Cf::TILE_M + (int)rank * kBM + quad * 32;
-#pragma unroll
-                    for (int q = 0; q < EC / kEpiCols; ++q) {
-                        float *dst = wbuf + (q % kEpiNBuf) * (kEpiRows * kEpiCols);
-                        if (lane == 0) bulk_wait_read<kEpiNBuf - 1>();   // this buffer's last store has read it
-                        __syncwarp();
-#pragma unroll
-                        for (int j = 0; j < kEpiCols; ++j)
-                            dst[j * kEpiRows + lane] = radd ? p.alpha * zval(q * kEpiCols + j)
-                                                            : fmaf(p.alpha, zval(q * kEpiCols + j), 0.f);
-                        fence_proxy_async_smem();
-                        __syncwarp();
-                        if (lane == 0) {
-                            if (radd) tma_reduce_add_2d(&tmC, dst, wrow, col0 + q * kEpiCols);
-                            else tma_store_2d(&tmC, dst, wrow, col0 + q * kEpiCols);
                             bulk_commit();
                         }
                     }
