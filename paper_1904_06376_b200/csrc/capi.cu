@@ -692,7 +692,7 @@ int bf16x_host_timeline(int on, float *ms, int cap) {
 }
 void bf16x_host_chunks(int n) { g_host_chunks = n > 0 ? n : 12; }   // bf16x_gemm_host pipeline depth
 void bf16x_host_2d(int on) { g_host_2d = on; }   // 0 off, 1 auto (default), >1 forced for beta = 0 with (R<<4)|Cb blocks
-void bf16x_multicast(int pairs) { g_multicast = pairs; }   // 0 = auto, 1 = off, 2 = on
+void bf16x_multicast(int pairs) { g_multicast = pairs; }   // 0 = auto, 1 = off, 2 = B across 2 pairs, 4 = 2 x 2 pairs (A and B)
 void bf16x_tune(int cta_group, int tile_n, int stages_per_interval) {
     g_force_cg = cta_group;
     g_force_bn = tile_n;

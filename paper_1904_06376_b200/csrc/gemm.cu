@@ -123,7 +123,7 @@ bool fused_a_ok(const GemmPlan &pl) {
     if (cg != 2 || pl.fp64 || pl.split_acc || pl.scaled || pl.k <= 0 || pl.tile_n == 192 || !pl.Af) return false;
     if (use_pm(pl)) return false;    // short k: the promote-every-MMA schedule instead
     if ((reinterpret_cast<uintptr_t>(pl.Af) & 15u) || pl.lda % 4) return false;
-    const bool mc2 = pl.multicast == 2 || (pl.multicast == 0 && (int64_t)pl.m * pl.n >= 12288LL * 12288LL);
+    const bool mc2 = pl.multicast >= 2 || (pl.multicast == 0 && (int64_t)pl.m * pl.n >= 12288LL * 12288LL);
     return !mc2;
 }
 

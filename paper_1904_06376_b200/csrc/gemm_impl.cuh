@@ -267,8 +267,12 @@ __device__ __forceinline__ void for_each_product(int nh, F &&f) {
     for (int h = 0; h < nh; ++h) f(0, 0, h);
 }
 
-// MC = number of CTA pairs per cluster sharing the B tile (1, or 2: two vertically adjacent
-// 256 x BN tiles; each pair loads half of every B slice and multicasts it to both pairs).
+// MC = number of CTA pairs per cluster (1; 2: two vertically adjacent 256 x BN tiles sharing
+// the B tile -- each pair loads half of every B slice and multicasts it to both pairs; 4: a 2 x 2
+// block of tiles, pairs (pm, pn) = (pair % 2, pair / 2): B shared down each column of the block as
+// for 2, and A (MN-major pieces only) shared along each row -- pair pn loads the 64-row box pn of
+// its CTA's A rows and multicasts it to the pair beside it, so every A and B byte a cluster
+// reads leaves L2 once for two pairs).
 // GD ("d" variants, R30; requires SA): the bins >= 1 and bin 0 are promoted into two separate
 // FP32 register accumulators (G[0, EC) = bin 0, G[EC, 2 EC) = bins >= 1: the paper's FP32
 // partial sums Z^(i,j), pooled per accumulator) and only their final collection is
@@ -295,6 +299,9 @@ __global__ void __launch_bounds__(FA ? kThreadsFused : kThreads, 1)
     static_assert(!FA || (CG == 2 && BN == 256 && MC == 1 && !SA && !GD), "fused A: 2-CTA, N 256");
     constexpr int CL = CG * MC;   // cluster size
     static_assert(MC == 1 || CG == 2, "multicast needs 2-CTA pairs");
+    static_assert(MC == 1 || MC == 2 || (MC == 4 && !SA && !GD && !FA && !PM), "multicast: 1, 2 or 2 x 2 pairs");
+    constexpr int MCB = MC == 4 ? 2 : MC;   // pairs sharing B (tile rows of the cluster block)
+    constexpr int MCA = MC == 4 ? 2 : 1;    // pairs sharing A (tile columns of the cluster block)
     static_assert(!SA || 2 * BN <= kTmemBufStride, "split accumulators need 4 x BN TMEM columns");
     constexpr int NB = 2, ACC_STRIDE = kTmemBufStride;   // TMEM accumulator buffers, columns apart
     static_assert(!GD || SA, "FP64 collection needs split accumulators");
@@ -319,6 +326,7 @@ __global__ void __launch_bounds__(FA ? kThreadsFused : kThreads, 1)
     const uint32_t crank = (CL > 1) ? cluster_ctarank() : 0u;   // rank in the cluster
     const uint32_t rank = crank % CG;                            // rank in the CTA pair
     const uint32_t pair = crank / CG;                            // which pair of the cluster
+    const uint32_t pm = pair % MCB, pn = pair / MCB;             // its place in the cluster block
 
     // dbg bit 1: trace slot 0 = kernel start, 1 = prologue done, 2 + 3 t .. = tile t (first
     // interval promoted, last interval promoted, C issued), 31 = all stores complete
@@ -387,7 +395,8 @@ __global__ void __launch_bounds__(FA ? kThreadsFused : kThreads, 1)
                     ++ptc;
                     int tm, tn;
                     tile_coords(w.tile, p.tiles_m, p.tiles_n, p.group_m, tm, tn);
-                    tm = tm * MC + (int)pair;
+                    tm = tm * MCB + (int)pm;
+                    tn = tn * MCA + (int)pn;
                     const int a_row = tm * Cf::TILE_M + (int)rank * kBM;
                     const int b_row = tn * BN + (int)rank * Cf::BN_LOCAL;
                     const int kb_end = min(p.nkb, w.i1 * S);
@@ -422,7 +431,12 @@ __global__ void __launch_bounds__(FA ? kThreadsFused : kThreads, 1)
                             tma_load_3d(b_dst, &tmB, &full[stage], kb * kBK, b_row, 0);
                         } else {
                             if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * Cf::STAGE);
-                            if (p.a_mn) {
+                            if constexpr (MCA == 2) {
+                                // this pair's 64-row box of the CTA's A rows, to both pairs of the row
+                                const uint16_t amask = (uint16_t)((1u << ((pm * CG) + rank)) | (1u << (((MCB + pm) * CG) + rank)));
+                                tma_load_3d_2sm_mc(a_dst + (int)pn * Cf::PA * kMnBox, &tmA, &full[stage], a_row + 64 * (int)pn,
+                                                   kb * kBK, 0, amask);
+                            } else if (p.a_mn) {
                                 tma_load_3d_2sm(a_dst, &tmA, &full[stage], a_row, kb * kBK, 0);
                                 tma_load_3d_2sm(a_dst + Cf::PA * kMnBox, &tmA, &full[stage], a_row + 64, kb * kBK, 0);
                             } else {
@@ -432,12 +446,12 @@ __global__ void __launch_bounds__(FA ? kThreadsFused : kThreads, 1)
                                 tma_load_3d_2sm(b_dst, &tmB, &full[stage], kb * kBK, b_row, 0);
                             } else {
                                 // this pair's half of the B slice, piece by piece, to both pairs
-                                constexpr int HB = Cf::BN_LOCAL / MC;
-                                const uint16_t mask = (uint16_t)((1u << rank) | (1u << (CG + rank)));
+                                constexpr int HB = Cf::BN_LOCAL / MCB;
+                                const uint16_t mask = (uint16_t)((1u << ((pn * MCB) * CG + rank)) | (1u << ((pn * MCB + 1) * CG + rank)));
 #pragma unroll
                                 for (int q = 0; q < Cf::PB; ++q)
-                                    tma_load_3d_2sm_mc(b_dst + q * Cf::B_PIECE + (int)pair * HB * kRowBytes, &tmB,
-                                                       &full[stage], kb * kBK, b_row + (int)pair * HB, q, mask);
+                                    tma_load_3d_2sm_mc(b_dst + q * Cf::B_PIECE + (int)pm * HB * kRowBytes, &tmB,
+                                                       &full[stage], kb * kBK, b_row + (int)pm * HB, q, mask);
                             }
                         }
                         if (++stage == NST) { stage = 0; phase ^= 1u; }
@@ -584,7 +598,8 @@ __global__ void __launch_bounds__(FA ? kThreadsFused : kThreads, 1)
         while (it.next(p, w)) {
             int tm, tn;
             tile_coords(w.tile, p.tiles_m, p.tiles_n, p.group_m, tm, tn);
-            tm = tm * MC + (int)pair;
+            tm = tm * MCB + (int)pm;
+            tn = tn * MCA + (int)pn;
             const int row = tm * Cf::TILE_M + (int)rank * kBM + quad * 32 + lane;
             const int col0 = tn * BN + half * EC;
             // beta != 0: the old C values this thread will read (its row, its EC columns; one
@@ -882,7 +897,7 @@ int launch_t(const GemmPlan &pl, cudaStream_t st) {
                      : make_piece_map(&tmA, pl.Ap, pl.k, pl.m, pl.ldap, pl.a_plane, Cf::PA, kBM);
         if (rc) return rc;
         if (MC == 1) rc = make_piece_map(&tmB, pl.Bp, pl.k, pl.n, pl.ldbp, pl.b_plane, Cf::PB, Cf::BN_LOCAL);
-        else rc = make_piece_map(&tmB, pl.Bp, pl.k, pl.n, pl.ldbp, pl.b_plane, Cf::PB, Cf::BN_LOCAL / MC, 1);
+        else rc = make_piece_map(&tmB, pl.Bp, pl.k, pl.n, pl.ldbp, pl.b_plane, Cf::PB, Cf::BN_LOCAL / (MC == 4 ? 2 : MC), 1);
     }
     if (rc) return rc;
     KParams kp;
@@ -890,8 +905,13 @@ int launch_t(const GemmPlan &pl, cudaStream_t st) {
     kp.alpha = pl.alpha; kp.beta = pl.beta;
     kp.C = pl.C; kp.ldc = pl.ldc; kp.acc = pl.acc;
     kp.flags = g_red_add == 0 ? (pl.flags & ~kFlagRedAdd) : (g_red_add == 1 ? (pl.flags | kFlagRedAdd) : pl.flags);
-    kp.tiles_m = ((pl.m + Cf::TILE_M - 1) / Cf::TILE_M + MC - 1) / MC;   // rows of (MC-tall) super-tiles
-    kp.tiles_n = (pl.n + BN - 1) / BN;
+    constexpr int MCB = MC == 4 ? 2 : MC, MCA = MC == 4 ? 2 : 1;
+    if (MCA > 1 && (!pl.a_mn || FA)) {
+        set_error_msg("2 x 2 multicast needs MN-major A pieces");
+        return BF16X_ERR_CUDA;
+    }
+    kp.tiles_m = ((pl.m + Cf::TILE_M - 1) / Cf::TILE_M + MCB - 1) / MCB;   // rows of (MCB-tall) super-tiles
+    kp.tiles_n = ((pl.n + BN - 1) / BN + MCA - 1) / MCA;                   // columns of MCA-wide super-tiles
     kp.nkb = (pl.k + kBK - 1) / kBK;
     const int tiles = kp.tiles_m * kp.tiles_n;
     int units = num_sms() / CL;
@@ -952,7 +972,7 @@ int launch_t(const GemmPlan &pl, cudaStream_t st) {
     if (!FA && Cf::EPI && !(pl.flags & BF16X_ACC_OUT) && (reinterpret_cast<uintptr_t>(pl.C) & 15u) == 0 && pl.ldc % 4 == 0 &&
         make_f32_map(&tmC, pl.C, pl.m, pl.n, pl.ldc, kEpiRows, kEpiCols, CU_TENSOR_MAP_SWIZZLE_NONE) == BF16X_SUCCESS)
         kp.tma_c = 1;
-    kp.group_m = pl.group_m > 0 ? pl.group_m : (MC == 2 ? (kp.tiles_n >= 48 ? 1 : kGroupM) : (kp.tiles_n <= 16 ? 1 : kGroupM));
+    kp.group_m = pl.group_m > 0 ? pl.group_m : (MC >= 2 ? (kp.tiles_n >= 48 ? 1 : kGroupM) : (kp.tiles_n <= 16 ? 1 : kGroupM));
     const int ncl = grid / CL;
     // (not for short k: a split tile's fix-up -- the contributor's FP32 partial written and read
     // back -- costs more than the balanced tail wins below 12 promotion intervals; measured r08,
@@ -1070,7 +1090,8 @@ int launch_s(const GemmPlan &pl, cudaStream_t st) {
             // quarter but clusters of 4 leave 16 SMs idle; measured (r05) a win only for large
             // outputs, where the kernel runs long enough to be power-limited (16384^3: x3 +17 %,
             // x6 +7 %), and a loss at 8192^3.  Auto: multicast for m*n >= 12288^2.
-            const bool mc2 = pl.multicast == 2 || (pl.multicast == 0 && (int64_t)pl.m * pl.n >= 12288LL * 12288LL);
+            const bool mc2 = pl.multicast >= 2 || (pl.multicast == 0 && (int64_t)pl.m * pl.n >= 12288LL * 12288LL);
+            if (pl.multicast == 4 && pl.a_mn && !pl.fused_a) return launch_t<CG, V, 256, 2, 4>(pl, st);
             if (mc2) return launch_t<CG, V, 256, 2, 2>(pl, st);
         }
     }

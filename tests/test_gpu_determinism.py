@@ -31,11 +31,12 @@ def test_stream_k_repeatable(m, n, k, variant):
     assert _same(runs)
 
 
-def test_multicast_repeatable():
+@pytest.mark.parametrize("mc", [2, 4])
+def test_multicast_repeatable(mc):
     L = bx.lib()
     A = torch.from_numpy(synthetic.uniform(2048, 768, seed=3)).cuda()
     B = torch.from_numpy(synthetic.uniform(768, 2560, seed=4)).cuda()
-    L.bf16x_multicast(2)
+    L.bf16x_multicast(mc)
     try:
         runs = [bx.gemm(A, B, variant=6).clone() for _ in range(20)]
         torch.cuda.synchronize()

@@ -53,6 +53,7 @@ CASES = [  # (m, n, k, variant, hooks)
     (777, 129, 300, 5, {}),
     (2304, 2560, 1024, 6, {"mc": 1}),            # stream-K tail (90 tiles, 16 intervals)
     (2304, 2560, 520, 3, {"mc": 2}),             # TMA multicast, ragged k
+    (1000, 1300, 520, 6, {"mc": 4}),             # 2 x 2 pairs sharing A and B, ragged super-tiles
 ]
 
 

@@ -111,6 +111,32 @@ def test_mn_multicast_and_stream_k(tune, variant):
     _same(_internal_gemm(A, B, variant), _kmajor_gemm(A, B, variant))
 
 
+MC4_SHAPES = [(2304, 2560, 1024), (1000, 1300, 520), (300, 700, 200), (513, 257, 160), (4096, 512, 256)]
+
+
+@pytest.mark.parametrize("variant", [1, 3, 5, 6, 7, 8, 9])
+@pytest.mark.parametrize("shape", MC4_SHAPES, ids=lambda s: "x".join(map(str, s)))
+def test_mn_multicast_2x2(tune, shape, variant):
+    """2 x 2 CTA pairs per cluster (bf16x_multicast(4)): A's 64-row boxes shared along each row of
+    the cluster block, B's halves down each column.  Each tile's MMAs are the same, so with
+    BF16X_NO_STREAM_K the output equals the one-pair schedule's bit for bit (ragged m, n, k:
+    partial super-tiles whose out-of-range pairs read zeros); the default schedule (a stream-K
+    tail where the super-tile count is not a multiple of the cluster count) is repeatable and
+    equals the K-major path, which falls back to B-only multicast."""
+    A, B = _operands(*shape, seed=7 * variant + shape[2], dist="wide")
+    bx.lib().bf16x_fused_a(0)
+    bx.lib().bf16x_multicast(1)
+    want = _internal_gemm(A, B, variant, flags=bx.NO_STREAM_K)
+    bx.lib().bf16x_multicast(4)
+    _same(_internal_gemm(A, B, variant, flags=bx.NO_STREAM_K), want)
+    _same(_kmajor_gemm(A, B, variant, flags=bx.NO_STREAM_K), want)
+    first = _internal_gemm(A, B, variant)
+    _same(_internal_gemm(A, B, variant), first)
+    if variant == 9:
+        bx.lib().bf16x_fused_a(-1)    # fused A is not taken with multicast: same bits
+        _same(_internal_gemm(A, B, variant, flags=bx.NO_STREAM_K), want)
+
+
 @pytest.mark.parametrize("variant", [3, 6, 9])
 def test_mn_short_k_promote_every_mma(tune, variant):
     bx.lib().bf16x_fused_a(0)
