@@ -1042,6 +1042,15 @@ int launch_s(const GemmPlan &pl, cudaStream_t st) {
     // r07 tools/lazy_probe.py, burst clocks, 64-k vs 128-k step time 353.6 vs 386.6 us at
     // 4096^3 and 2.60 vs 2.82 ms at 8192^3 (profiles/r07/old_vs_fix.txt).  The opt-in fused-A
     // and split-ahead x3 kernels follow the hook, so they stay bit-identical to the pre-pass path.
+    // Short k, bf16x3 (library schedule, 64 < k <= 256): 128-k intervals, so a 256-k tile is
+    // two promotions and the tensor core runs further ahead of the epilogue's C stores
+    // (r10 tools/shortk_spi_probe.py, 4096^2 K2 alone: k = 128 24.2 -> 23.5 us, 192 29.1 -> 27.6,
+    // 256 33.4 -> 31.3; k = 64 and 320 unchanged; profiles/r10/shortk_spi_probe*.txt).  x3's error
+    // is that of its dropped products (2^-16 relative), far above the tensor core's
+    // accumulation truncation, so the longer interval costs it no accuracy.
+    if constexpr (CG == 2 && V == 3)
+        if (s == 0 && !carry && pl.k > 64 && pl.k <= 256 && !use_pm(pl) && !pl.fp64 && !pl.split_acc && !pl.fused_a)
+            s = 4;
     if constexpr (CG == 2 && V == 3)
         if (s == 4 && !pl.fp64 && !pl.split_acc) {
             if (pl.multicast == 2 || (pl.multicast == 0 && (int64_t)pl.m * pl.n >= 12288LL * 12288LL))

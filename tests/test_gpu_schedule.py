@@ -145,6 +145,8 @@ def _interval(variant, cg, spi, k):
     1 or 2 stages of 32 k, unless the 2-stage ring would have fewer than 4 stages (tile N 256
     per CTA with cta_group 1 and 3 pieces of B: 3 stages) -> 1."""
     stages = _stages(variant, cg)
+    if spi == 0 and variant == 3 and cg == 2 and 64 < k <= 256:
+        return 128                                    # x3 short k: 128-k intervals (callers exclude PM)
     s = spi if spi in (1, 2) else (2 if (cg == 2 and k > 128) else 1)
     if s == 2 and stages < 4:
         s = 1
@@ -167,10 +169,10 @@ def test_kernel_equals_schedule_model(shape, dist, variant, cg, spi):
 
 @pytest.mark.parametrize("variant", [3, 6, 9])
 def test_kernel_equals_schedule_model_default(variant):
-    """The library's own choice of schedule (no tuning override) on configs[0]'s 64^3 arms and
-    a k = 1000 problem: every MMA promoted on its own at k <= 128 (PM), 64-k intervals above
-    (2-CTA pairs)."""
-    for (m, n, k) in ((64, 64, 64), (96, 160, 1000)):
+    """The library's own choice of schedule (no tuning override) on configs[0]'s 64^3 arms, a
+    k = 200 problem and a k = 1000 problem: every MMA promoted on its own at k <= 128 (PM),
+    128-k intervals for bf16x3 at 128 < k <= 256, 64-k intervals otherwise (2-CTA pairs)."""
+    for (m, n, k) in ((64, 64, 64), (96, 160, 1000), (300, 260, 200)):
         for dist in ("uniform", "wide", "gauss"):
             A = synthetic.by_name(dist, m, k, seed=3)
             B = synthetic.by_name(dist, k, n, seed=4)
@@ -178,7 +180,7 @@ def test_kernel_equals_schedule_model_default(variant):
             if k <= 128:
                 M = tc_model.simulate(A, B, variant, interval=128, promote_every_mma=True)
             else:
-                M = tc_model.simulate(A, B, variant, interval=64)
+                M = tc_model.simulate(A, B, variant, interval=_interval(variant, 2, 0, k))
             assert np.array_equal(G.view(np.uint32), M.view(np.uint32)), (m, n, k, dist)
 
 
