@@ -1,7 +1,8 @@
 """GEMM time and bits vs the multicast mode (bf16x_multicast: 1 off, 2 B across 2 pairs, 4 = 2 x 2
 pairs sharing A and B).  Usage: python tools/mc_probe.py [n] [variant] [modes] [iters] [reps]
 Bit identity is checked with BF16X_NO_STREAM_K (stream-K's split tiles depend on the cluster count);
-times are for the default schedule.  PAUSE=s sleeps between modes (power state)."""
+times are for the default schedule.  PAUSE=s sleeps between modes (power state); GROUP=g sets
+the raster group height (bf16x_group_m)."""
 import os
 import sys
 import time
@@ -19,6 +20,8 @@ reps = int(sys.argv[5]) if len(sys.argv) > 5 else 2
 m = int(os.environ.get("M", n))
 k = int(os.environ.get("K", n))
 L = bx.lib()
+if os.environ.get("GROUP"):
+    L.bf16x_group_m(int(os.environ["GROUP"]))      # tile raster group height (0 = default)
 g = torch.Generator(device="cuda").manual_seed(1)
 A = (torch.rand(k, m, device="cuda", generator=g) * 2 - 1).t()    # column-major m x k
 B = (torch.rand(n, k, device="cuda", generator=g) * 2 - 1).t()    # column-major k x n
