@@ -34,6 +34,9 @@ def _gpu(A, B, variant):
     return C.cpu().numpy()
 
 
+GAUSS_MAX = 3.0   # per-seed ceiling of the Gaussian arm (R24; uniform and wide: RATIO per seed)
+
+
 def test_config0_64cubed(orc):
     """Uniform and wide-exponent arms: GPU <= 2x oracle on every seed (the library promotes
     every MMA on its own at this size, smallest bins first, so the tensor core's truncating
@@ -41,7 +44,7 @@ def test_config0_64cubed(orc):
     truncates its 16 addends where the oracle rounds each FMA to nearest, and a Gaussian C is
     dominated by single products on which the oracle can be within 0.2 ulp by luck, so single
     seeds exceed 2x (reading R24); there the mean ratio over the 20 seeds
-    must be <= 2 and the maximum is recorded."""
+    must be <= 2 and every seed <= GAUSS_MAX (3x, above the recorded 2.86)."""
     seeds = {"uniform": range(0, 20), "wide": range(100, 120), "gauss": range(200, 220)}
     table = {}
     for dist, ss in seeds.items():
@@ -62,6 +65,9 @@ def test_config0_64cubed(orc):
                 ratios[v].append(eg / eo)
         for v in (3, 6, 8, 9):
             assert np.mean(ratios[v]) <= RATIO, (dist, v, np.mean(ratios[v]))
+            # Gaussian arm per seed: the recorded envelope (max 2.86 x6 / 2.50 x9, reproduced bit for
+            # bit by tests/tc_model.py) may not grow -- a regression of the schedule shows here
+            assert np.max(ratios[v]) <= GAUSS_MAX, (dist, v, np.max(ratios[v]))
         table[dist] = {k: float(np.mean(v)) for k, v in errs.items()}
         table[dist]["ratio_mean"] = {v: float(np.mean(r)) for v, r in ratios.items()}
         table[dist]["ratio_max"] = {v: float(np.max(r)) for v, r in ratios.items()}
