@@ -496,16 +496,27 @@ __global__ void __launch_bounds__(256) panel_update_kernel(float *LU, int ld, in
     // this thread's first 4 x 4 block of the update target, loaded now so its latency overlaps
     // the staging copies and the forward substitution (rows rb.. are disjoint from the U rows
     // s0..s0+w that block 0 writes below)
-    const int ty = tid >> 4, tx = tid & 15;
+    // rows 4ty.. (ty = tid % 16), columns 4tx.. (tx = tid / 16): a warp covers 2 columns x 64
+    // consecutive rows, so each load / store instruction touches 4 cache lines (r10: was 16 columns
+    // x 8 rows = 16 lines)
+    const int ty = tid & 15, tx = tid >> 4;
+    // 16-byte accesses of a thread's 4 rows when they are aligned and inside the matrix
+    const bool vec = ((reinterpret_cast<uintptr_t>(LU) & 15u) == 0) && (ld % 4 == 0) && (rb % 4 == 0) && (4 * ty + 4 <= nr);
     float old[4][4];
     auto load_old = [&](int cq) {
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
+        for (int j = 0; j < 4; ++j) {
+            if (vec && cq + j < nc) {
+                const float4 v = *reinterpret_cast<const float4 *>(LU + (int64_t)(c1 + cq + j) * ld + rb + 4 * ty);
+                old[j][0] = v.x; old[j][1] = v.y; old[j][2] = v.z; old[j][3] = v.w;
+                continue;
+            }
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
                 const int r = 4 * ty + i;
                 old[j][i] = (cq + j < nc && r < nr) ? LU[(int64_t)(c1 + cq + j) * ld + rb + r] : 0.f;
             }
+        }
     };
     load_old(4 * tx);
     async_wait_all();
@@ -547,12 +558,18 @@ __global__ void __launch_bounds__(256) panel_update_kernel(float *LU, int ld, in
                 for (int i = 0; i < 4; ++i) acc[j][i] = fmaf(lv[i], uv[j], acc[j][i]);
         }
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
+        for (int j = 0; j < 4; ++j) {
+            if (vec && cq + j < nc) {
+                *reinterpret_cast<float4 *>(LU + (int64_t)(c1 + cq + j) * ld + rb + 4 * ty) =
+                    make_float4(old[j][0] - acc[j][0], old[j][1] - acc[j][1], old[j][2] - acc[j][2], old[j][3] - acc[j][3]);
+                continue;
+            }
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
                 const int r = 4 * ty + i;
                 if (cq + j < nc && r < nr) LU[(int64_t)(c1 + cq + j) * ld + rb + r] = old[j][i] - acc[j][i];
             }
+        }
     }
 }
 
