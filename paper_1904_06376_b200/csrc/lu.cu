@@ -463,15 +463,22 @@ __global__ void __launch_bounds__(kSubThreads) subpanel_kernel(float *LU, int ld
 // `ctr`, reset by that block for the next launch), so no block can read U instead of A whatever
 // the order or residency of the blocks.
 constexpr int kUpdRows = 64;
-static size_t panel_update_smem(int nc) {
+// sU row stride: a multiple of 4 (16-byte rows for the float4 reads) with an odd number of 16-byte
+// chunks, so the column copies (lanes along a column's 32 rows) are 4-way instead of 32-way bank
+// conflicted (r10)
+__host__ __device__ inline int upd_ncp(int nc) {
     const int ncp = (nc + 3) & ~3;
+    return ((ncp >> 2) & 1) ? ncp : ncp + 4;
+}
+static size_t panel_update_smem(int nc) {
+    const int ncp = upd_ncp(nc);
     return ((size_t)kSubW * ncp + (size_t)kSubW * (kSubW + 1) + (size_t)kSubW * kUpdRows) * sizeof(float);
 }
 __global__ void __launch_bounds__(256) panel_update_kernel(float *LU, int ld, int n, int s0, int w, int c1, int c2,
                                                            unsigned int *ctr) {
     extern __shared__ __align__(16) float su[];
     __shared__ int store_u;
-    const int nc = c2 - c1, ncp = (nc + 3) & ~3;
+    const int nc = c2 - c1, ncp = upd_ncp(nc);
     float *sU = su;                                   // [kSubW][ncp]      row r of the w x nc block
     float *sL11 = sU + (size_t)kSubW * ncp;           // [kSubW][kSubW+1]  L11[r][i]
     float *sL21 = sL11 + kSubW * (kSubW + 1);         // [kSubW][kUpdRows] (col t, row r)
@@ -630,22 +637,24 @@ __global__ void __launch_bounds__(256) laswp_multi_kernel(float *LU, int ld, int
 // (warp w owns 4 columns, lanes are rows: no CTA barrier per row), then the rows below take
 // the chunk's contribution as a small product, 4 rows per thread from a transposed L tile.
 constexpr int kTrsmCols = 32;
+constexpr int kTrsmLd = kTrsmCols + 1;    // sB row stride: column reads of a row block are conflict-free
 static size_t trsm_smem(int jb) {
     const int jbp = (jb + 3) & ~3;
-    return ((size_t)jb * kTrsmCols + 32 * 33 + (size_t)32 * jbp) * sizeof(float);
+    return ((size_t)jbp * kTrsmLd + 32 * 33 + (size_t)32 * jbp) * sizeof(float);
 }
 __global__ void __launch_bounds__(256) trsm_kernel(float *LU, int ld, int j0, int jb, int c0, int ncols) {
     extern __shared__ __align__(16) float sm[];
     const int jbp = (jb + 3) & ~3;
-    float *sB = sm;                                   // [jb][32]   (row r, column c)
-    float *sLd = sB + (size_t)jb * kTrsmCols;         // [32][33]   L[i0+r][i0+i]
+    float *sB = sm;                                   // [jb][33]   (row r, column c)
+    float *sLd = sB + (size_t)jbp * kTrsmLd;          // [32][33]   L[i0+r][i0+i]
     float *sLt = sLd + 32 * 33;                       // [32][jbp]  L[i0+ib+r][i0+i] at i*jbp + r
     const int cb = c0 + blockIdx.x * kTrsmCols;
     const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5, lane = tx;
-    const bool valid = (cb + tx) < c0 + ncols;
-    for (int r = ty; r < jb; r += 8) {
-        if (valid) async_copy_f32(sB + r * kTrsmCols + tx, LU + (int64_t)(cb + tx) * ld + j0 + r);
-        else sB[r * kTrsmCols + tx] = 0.f;
+    // the 32 columns' rows j0.. with lanes along a column (coalesced; r10, was one column per lane)
+    for (int e = tid; e < jb * kTrsmCols; e += blockDim.x) {
+        const int r = e % jb, cc = e / jb;
+        if (cb + cc < c0 + ncols) async_copy_f32(sB + r * kTrsmLd + cc, LU + (int64_t)(cb + cc) * ld + j0 + r);
+        else sB[r * kTrsmLd + cc] = 0.f;
     }
     for (int i0 = 0; i0 < jb; i0 += 32) {
         const int ib = min(32, jb - i0), below = jb - i0 - ib;
@@ -663,7 +672,7 @@ __global__ void __launch_bounds__(256) trsm_kernel(float *LU, int ld, int j0, in
         {   // diagonal triangle: warp ty owns columns 4ty .. 4ty+3, lane = row
             float v[4];
 #pragma unroll
-            for (int q = 0; q < 4; ++q) v[q] = (lane < ib) ? sB[(i0 + lane) * kTrsmCols + 4 * ty + q] : 0.f;
+            for (int q = 0; q < 4; ++q) v[q] = (lane < ib) ? sB[(i0 + lane) * kTrsmLd + 4 * ty + q] : 0.f;
             for (int i = 0; i < ib - 1; ++i) {
                 const float l = sLd[lane * 33 + i];
 #pragma unroll
@@ -674,13 +683,13 @@ __global__ void __launch_bounds__(256) trsm_kernel(float *LU, int ld, int j0, in
             }
             if (lane < ib)
 #pragma unroll
-                for (int q = 0; q < 4; ++q) sB[(i0 + lane) * kTrsmCols + 4 * ty + q] = v[q];
+                for (int q = 0; q < 4; ++q) sB[(i0 + lane) * kTrsmLd + 4 * ty + q] = v[q];
         }
         __syncthreads();
         if (below > 0) {  // rows below the chunk: column tx, 4 rows per step
             float x[32];
 #pragma unroll
-            for (int i = 0; i < 32; ++i) x[i] = (i < ib) ? sB[(i0 + i) * kTrsmCols + tx] : 0.f;
+            for (int i = 0; i < 32; ++i) x[i] = (i < ib) ? sB[(i0 + i) * kTrsmLd + tx] : 0.f;
             for (int rq = 4 * ty; rq < below; rq += 32) {
                 float acc[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
@@ -694,13 +703,15 @@ __global__ void __launch_bounds__(256) trsm_kernel(float *LU, int ld, int j0, in
                 }
 #pragma unroll
                 for (int u = 0; u < 4; ++u)
-                    if (rq + u < below) sB[(i0 + ib + rq + u) * kTrsmCols + tx] -= acc[u];
+                    if (rq + u < below) sB[(i0 + ib + rq + u) * kTrsmLd + tx] -= acc[u];
             }
         }
     }
     __syncthreads();
-    if (valid)
-        for (int r = ty; r < jb; r += 8) LU[(int64_t)(cb + tx) * ld + j0 + r] = sB[r * kTrsmCols + tx];
+    for (int e = tid; e < jb * kTrsmCols; e += blockDim.x) {
+        const int r = e % jb, cc = e / jb;
+        if (cb + cc < c0 + ncols) LU[(int64_t)(cb + cc) * ld + j0 + r] = sB[r * kTrsmLd + cc];
+    }
 }
 
 // ------------------------------------------------------------------------------------
