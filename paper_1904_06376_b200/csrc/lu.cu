@@ -7,7 +7,8 @@
 //     K4 subpanel_kernel    32-column sub-panels on one thread-block cluster (8-16 CTAs, rows in
 //                           shared memory, pivot exchange through DSMEM + cluster barrier);
 //        panel_update_kernel   TRSM + rank-32 update of the rest of the 256-wide panel
-//     K5 laswp_kernel   applies the panel's interchanges to all n columns
+//        (tail of K4)   the sub-panel's interchanges on the panel's columns and the permutation
+//     K5 laswp_multi_kernel  the panel's interchanges on the columns outside it
 //        trsm_kernel    U12 = L11^-1 A12 (FP32, unit lower)
 //     K2 bf16x GEMM     A22 <- -1 * L21 U12 + 1 * A22 in bf16x<variant>   (the cubic work)
 //   refine (FP64, factors widened exactly):
@@ -107,8 +108,8 @@ __device__ __forceinline__ void async_wait_all() {
 //       GPU-scope fence per column), picks the same winner everywhere and reads the winning
 //       row from the winner CTA's record (DSMEM load) as p.
 // Rows are not moved inside the sub-panel: at the end CTA 0 turns the chosen rows into the
-// LAPACK interchange sequence (ipiv) and the equivalent gather pairs, which laswp_kernel
-// then applies to all n columns.  All panel arithmetic is FP32.
+// LAPACK interchange sequence (ipiv) and the equivalent gather pairs, which the cluster applies
+// to the panel's columns after its last barrier (r10; laswp_multi_kernel later to the others).  All panel arithmetic is FP32.
 // ------------------------------------------------------------------------------------
 constexpr int kSubW = 32;
 constexpr int kSubThreads = 512;
@@ -186,7 +187,8 @@ extern "C" int bf16x_lu_subpanel_trace(unsigned long long *host, int clear) {   
 
 template <int RPT, bool TRACE>
 __global__ void __launch_bounds__(kSubThreads) subpanel_kernel(float *LU, int ld, int n, int s0, int w, int *ipiv,
-                                                              int2 *pairs, int *npairs, int *info, int bulk) {
+                                                              int2 *pairs, int *npairs, int *info, int bulk, int pc0,
+                                                              int pc1, int *perm) {
     namespace cg = cooperative_groups;
     cg::cluster_group cl = cg::this_cluster();
     const int ncta = (int)cl.num_blocks(), rank = (int)cl.block_rank();
@@ -441,7 +443,38 @@ __global__ void __launch_bounds__(kSubThreads) subpanel_kernel(float *LU, int ld
         }
         if (lane == 0) *npairs = np;
     }
-    cl.sync();   // no CTA exits while a peer may still push into it
+    cl.sync();   // no CTA exits while a peer may still push into it; pairs / *npairs are published
+    // The sub-panel's interchanges on the panel's columns [pc0, pc1) and on the row permutation, as
+    // a gather (every source read before any destination is written; <= 2w pairs, two per lane),
+    // one warp per column over all warps of the cluster -- fused here in r10 instead of a separate
+    // laswp launch.  The pairs and the columns' rows were written by other CTAs of the cluster
+    // before the barrier: read through L2.
+    {
+        const int np = __ldcg(npairs);
+        const int gw = rank * kSubWarps + wid, nw = ncta * kSubWarps;
+        int2 q[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) q[h] = (h * 32 + lane < np) ? __ldcg(pairs + h * 32 + lane) : make_int2(0, 0);
+        for (int c = pc0 + gw; c < pc1 && np > 0; c += nw) {
+            float *col = LU + (int64_t)c * ld;
+            float v[2];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) v[h] = (h * 32 + lane < np) ? __ldcg(col + q[h].y) : 0.f;
+            __syncwarp();
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+                if (h * 32 + lane < np) col[q[h].x] = v[h];
+        }
+        if (perm && np > 0 && gw == nw - 1) {       // the last warp (CTA 0 warp 1 builds the pairs)
+            int pv[2];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) pv[h] = (h * 32 + lane < np) ? __ldcg(perm + q[h].y) : 0;
+            __syncwarp();
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+                if (h * 32 + lane < np) perm[q[h].x] = pv[h];
+        }
+    }
     if (trace && lane == 0) atomicAdd(g_sp_trace + rank * 32 + 8 + wid, (unsigned long long)wwork);
     if (trace && (tid == 0 || (book && lane == 0))) {
         unsigned long long *tr = g_sp_trace + rank * 32;
@@ -578,38 +611,6 @@ __global__ void __launch_bounds__(256) panel_update_kernel(float *LU, int ld, in
             }
         }
     }
-}
-
-// K5a: apply the panel's row interchanges to columns [c0, c1) as a gather through shared
-// memory: one warp per column, lanes over the (dst <- src) pairs.  Block 0 also applies them
-// to the row permutation perm (perm[i] = original row now at position i), so the solves'
-// P never has to be rebuilt from ipiv.
-__global__ void __launch_bounds__(256) laswp_kernel(float *LU, int ld, int c0, int c1, const int2 *pairs,
-                                                    const int *npairs, int *perm) {
-    extern __shared__ float sv[];          // [8 warps][np]
-    const int np = *npairs;
-    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int c = c0 + blockIdx.x * 8 + wid;
-    if (np > 0 && perm && blockIdx.x == 0 && wid == 0) {   // np <= 2 * kSubW = 64
-        int pv[2];
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            const int e = h * 32 + lane;
-            pv[h] = (e < np) ? perm[pairs[e].y] : 0;
-        }
-        __syncwarp();
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            const int e = h * 32 + lane;
-            if (e < np) perm[pairs[e].x] = pv[h];
-        }
-    }
-    if (np == 0 || c >= c1) return;
-    float *col = LU + (int64_t)c * ld;
-    float *buf = sv + wid * np;
-    for (int e = lane; e < np; e += 32) buf[e] = col[pairs[e].y];
-    __syncwarp();
-    for (int e = lane; e < np; e += 32) col[pairs[e].x] = buf[e];
 }
 
 // K5a': a whole panel's interchanges (nmaps sub-panel gather maps of <= 64 pairs each, applied
@@ -760,7 +761,7 @@ __global__ void axpy_kernel(int n, double *x, const double *d) {
     if (i < n) x[i] += d[i];
 }
 
-// perm[i] = original row now at position i (the interchanges composed by laswp_kernel)
+// perm[i] = original row now at position i (the interchanges composed by the sub-panel tails)
 __global__ void iota_kernel(int n, int *perm) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) perm[i] = i;
@@ -1054,7 +1055,8 @@ static int sub_rpt(int n, int cl) {
 static int g_sub_bulk = 2;
 extern "C" void bf16x_lu_subpanel_bulk(int mode) { g_sub_bulk = mode & 7; }   // bit 4: trace
 
-static cudaError_t launch_subpanel(const LuWork &w, int s0, int sw, cudaStream_t st, int2 *pairs, int *npairs) {
+static cudaError_t launch_subpanel(const LuWork &w, int s0, int sw, cudaStream_t st, int2 *pairs, int *npairs, int pc0,
+                                   int pc1) {
     const int rpt = sub_rpt(w.n, w.cl);
     if (rpt == 0) return cudaErrorInvalidValue;
     cudaLaunchConfig_t cfg = {};
@@ -1071,7 +1073,8 @@ static cudaError_t launch_subpanel(const LuWork &w, int s0, int sw, cudaStream_t
     cfg.numAttrs = 1;
     const int bulk = g_sub_bulk;
 #define SUBPANEL_LAUNCH(R_, T_) \
-    cudaLaunchKernelEx(&cfg, subpanel_kernel<R_, T_>, w.LU, w.ld, w.n, s0, sw, w.ipiv, pairs, npairs, w.info, bulk)
+    cudaLaunchKernelEx(&cfg, subpanel_kernel<R_, T_>, w.LU, w.ld, w.n, s0, sw, w.ipiv, pairs, npairs, w.info, bulk, pc0, \
+                       pc1, w.perm)
     if (bulk & 4) {
         if (rpt == 1) return SUBPANEL_LAUNCH(1, true);
         if (rpt == 2) return SUBPANEL_LAUNCH(2, true);
@@ -1207,22 +1210,19 @@ static int lu_factor(LuWork &w, int variant, cudaStream_t st) {
             const int sw = std::min(kSubW, j1 - s0);
             int2 *pr = w.pairs + 64 * nm;
             int *np = w.npairs + nm;
-            // (1) sub-panel factorisation on one cluster (rows in registers, RPT per thread)
-            cudaError_t e = launch_subpanel(w, s0, sw, st, pr, np);
+            // (1) sub-panel factorisation on one cluster (rows in registers, RPT per thread), then
+            //     (2) its interchanges inside the panel and on the row permutation (fused, r10)
+            cudaError_t e = launch_subpanel(w, s0, sw, st, pr, np, j0, j1);
             if (e != cudaSuccess && w.cl == 16) {    // 16-CTA clusters unavailable: use 8
                 cudaGetLastError();
                 w.cl = 8;
-                e = launch_subpanel(w, s0, sw, st, pr, np);
+                e = launch_subpanel(w, s0, sw, st, pr, np, j0, j1);
             }
             if (e != cudaSuccess) {
                 set_cuda_error(e, "subpanel launch");
                 rc = BF16X_ERR_CUDA;
                 break;
             }
-            count_launch();
-            // (2) its interchanges inside the panel (and on the row permutation)
-            laswp_kernel<<<(jb + 7) / 8, 256, 8 * (size_t)(2 * sw) * sizeof(float), st>>>(w.LU, ld, j0, j1, pr, np,
-                                                                                          w.perm);
             count_launch();
             // (3) TRSM + rank-sw update of the rest of the panel
             const int c1 = s0 + sw;
