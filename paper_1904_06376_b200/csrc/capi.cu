@@ -633,6 +633,7 @@ bf16x_stream_t bf16x_get_stream(void) { return (bf16x_stream_t)g_stream; }
 
 void bf16x_release(void) {
     release_all_streams();
+    lu_release_cache();
     std::lock_guard<std::mutex> h(g_host_mu);
     if (g_hA) cudaFree(g_hA);
     if (g_hB) cudaFree(g_hB);

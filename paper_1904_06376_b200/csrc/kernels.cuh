@@ -56,6 +56,7 @@ int launch_scale(int m, int n, float beta, float *C, int ldc, cudaStream_t st);
 int pieces_a(int variant);   // BF16 pieces of A / B for a variant (x5: 2 / 3)
 int pieces_b(int variant);
 int num_sms();
+void lu_release_cache();   // lu.cu: the LU / solve workspace kept between calls
 int default_cta_group();
 
 }  // namespace bf16x

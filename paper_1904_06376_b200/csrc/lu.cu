@@ -19,6 +19,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cmath>
+#include <mutex>
 #include <vector>
 
 #include <cooperative_groups.h>
@@ -1034,6 +1035,7 @@ struct LuWork {
     double *tinv = nullptr;       // FP64 inverses of the diagonal blocks (solves only)
     unsigned int *tflags = nullptr, tepoch = 0;
     int n = 0, nb = 0, cl = 16, coop_grid = 0;
+    bool cached = false;          // buffers from the LU cache (lu_free keeps them)
     std::vector<void *> extra;    // further device buffers owned by the solve
 };
 
@@ -1096,13 +1098,34 @@ static int coop_launch(const void *fn, int grid, int threads, void **args, size_
     return BF16X_SUCCESS;
 }
 
+// Device buffers of the factorisation state, kept between calls (r10): a getrf / gesv call
+// otherwise spent its first milliseconds in cudaMalloc (the n x n copy of A for the solves
+// alone is 256 MB at n = 8192) while the GPU idled.  One call at a time owns the cache (try_lock;
+// a concurrent call allocates its own buffers as before); every user synchronises before it
+// returns, so the buffers are idle between calls.  bf16x_release frees them.
+constexpr int kLuSlots = 14;
+static std::mutex g_lu_cache_mu;
+static void *g_lu_cache[kLuSlots] = {};
+static size_t g_lu_cache_cap[kLuSlots] = {};
+void lu_release_cache() {
+    std::lock_guard<std::mutex> g(g_lu_cache_mu);
+    for (int i = 0; i < kLuSlots; ++i) {
+        if (g_lu_cache[i]) cudaFree(g_lu_cache[i]);
+        g_lu_cache[i] = nullptr;
+        g_lu_cache_cap[i] = 0;
+    }
+}
+
 static void lu_free(LuWork &w) {
-    if (w.own_LU) cudaFree(w.LU);
-    if (w.own_ipiv) cudaFree(w.ipiv);
-    cudaFree(w.perm); cudaFree(w.info); cudaFree(w.npairs); cudaFree(w.pairs);
-    cudaFree(w.bar); cudaFree(w.pu_ctr); cudaFree(w.r); cudaFree(w.d); cudaFree(w.part); cudaFree(w.scal);
-    cudaFree(w.tinv); cudaFree(w.tflags);
+    if (!w.cached) {
+        if (w.own_LU) cudaFree(w.LU);
+        if (w.own_ipiv) cudaFree(w.ipiv);
+        cudaFree(w.perm); cudaFree(w.info); cudaFree(w.npairs); cudaFree(w.pairs);
+        cudaFree(w.bar); cudaFree(w.pu_ctr); cudaFree(w.r); cudaFree(w.d); cudaFree(w.part); cudaFree(w.scal);
+        cudaFree(w.tinv); cudaFree(w.tflags);
+    }
     for (void *p : w.extra) cudaFree(p);
+    if (w.cached) g_lu_cache_mu.unlock();
     w = LuWork{};
 }
 
@@ -1143,19 +1166,41 @@ static int lu_prepare(LuWork &w, int n, int nb, float *LU, int ld, int *ipiv, bo
         attr = true;
     }
     int rc = BF16X_SUCCESS;
+    w.cached = g_lu_cache_mu.try_lock();            // released by lu_free
+    int slot = 0;
     auto alloc = [&](void **p, size_t bytes) {
-        if (!rc) rc = dev_alloc(p, bytes);
+        const int i = slot++;
+        if (rc) return;
+        if (!w.cached) {
+            rc = dev_alloc(p, bytes);
+            return;
+        }
+        if (g_lu_cache_cap[i] < bytes) {           // grow this slot
+            if (g_lu_cache[i]) cudaFree(g_lu_cache[i]);
+            g_lu_cache[i] = nullptr;
+            g_lu_cache_cap[i] = 0;
+            rc = dev_alloc(&g_lu_cache[i], bytes);
+            if (rc) return;
+            g_lu_cache_cap[i] = bytes;
+        }
+        *p = g_lu_cache[i];
     };
     w.own_LU = (LU == nullptr);
     w.own_ipiv = (ipiv == nullptr);
     if (LU) {
         w.LU = LU;
         w.ld = ld;
+        ++slot;
     } else {
         w.ld = (n + 3) & ~3;
         alloc((void **)&w.LU, sizeof(float) * (size_t)w.ld * n);
     }
-    if (ipiv) w.ipiv = ipiv; else alloc((void **)&w.ipiv, sizeof(int) * n);
+    if (ipiv) {
+        w.ipiv = ipiv;
+        ++slot;
+    } else {
+        alloc((void **)&w.ipiv, sizeof(int) * n);
+    }
     const int nchunk = (n + kResChunk - 1) / kResChunk;
     alloc((void **)&w.perm, sizeof(int) * n);
     alloc((void **)&w.info, sizeof(int));
@@ -1173,6 +1218,7 @@ static int lu_prepare(LuWork &w, int n, int nb, float *LU, int ld, int *ipiv, bo
         alloc((void **)&w.tinv, sizeof(double) * 2 * kTinvBlock * nblk);
         alloc((void **)&w.tflags, sizeof(unsigned int) * nblk);
     }
+    static_assert(kLuSlots >= 14, "one cache slot per buffer above");
     if (rc) return rc;
     if (solves) cudaMemsetAsync(w.tflags, 0, sizeof(unsigned int) * nblk, st);
     w.gb.arrive = w.bar;
