@@ -187,7 +187,7 @@ extern "C" int bf16x_lu_subpanel_trace(unsigned long long *host, int clear) {   
 }
 
 template <int RPT, bool TRACE>
-__global__ void __launch_bounds__(kSubThreads) subpanel_kernel(float *LU, int ld, int n, int s0, int w, int *ipiv,
+__global__ void __launch_bounds__(kSubThreads, 1) subpanel_kernel(float *LU, int ld, int n, int s0, int w, int *ipiv,
                                                               int2 *pairs, int *npairs, int *info, int bulk, int pc0,
                                                               int pc1, int *perm) {
     namespace cg = cooperative_groups;
