@@ -508,7 +508,7 @@ static size_t panel_update_smem(int nc) {
     const int ncp = upd_ncp(nc);
     return ((size_t)kSubW * ncp + (size_t)kSubW * (kSubW + 1) + (size_t)kSubW * kUpdRows) * sizeof(float);
 }
-__global__ void __launch_bounds__(256) panel_update_kernel(float *LU, int ld, int n, int s0, int w, int c1, int c2,
+__global__ void __launch_bounds__(256, 1) panel_update_kernel(float *LU, int ld, int n, int s0, int w, int c1, int c2,
                                                            unsigned int *ctr) {
     extern __shared__ __align__(16) float su[];
     __shared__ int store_u;
