@@ -846,7 +846,7 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 // y <- T^-1 y in place (T = L unit lower if lower, else U), y FP64 of length n.  LU: ld % 4
 // == 0, 16-byte aligned.  flags[p] = epoch once block p's solution is in y.  Cooperative launch
 // (all CTAs co-resident: CTA g owns blocks p = g, g + G, ...).
-__global__ void __launch_bounds__(kTrsvThreads) trsv_kernel(const float *LU, int ld, int n, double *y, int lower,
+__global__ void __launch_bounds__(kTrsvThreads, 1) trsv_kernel(const float *LU, int ld, int n, double *y, int lower,
                                                             const double *Tinv, unsigned int *flags,
                                                             unsigned int epoch) {
     extern __shared__ double sm_tr[];
