@@ -15,7 +15,10 @@
  *  - The caller owns every buffer it passes.  The library owns a cached device
  *    workspace PER STREAM (pieces of A and B, stream-K fix-up buffers), released by
  *    bf16x_release(): calls on different streams never share library memory and may run
- *    concurrently; calls on one stream are ordered by the stream.
+ *    concurrently; calls on one stream are ordered by the stream.  The synchronous LU
+ *    entry points (bf16x_getrf, bf16x_gesv_ir, bf16x_gesv_gmres_ir) keep their device
+ *    workspace between calls (one call at a time uses it; a concurrent call allocates its
+ *    own), also released by bf16x_release().
  *  - Return value: BF16X_SUCCESS (0), a positive BF16X_* status, or -i when argument
  *    i (1-based) is invalid (LAPACK xerbla convention).  NaN/Inf inputs are never
  *    rejected; they propagate (reading R4).
@@ -290,7 +293,7 @@ int bf16x_getrf(int n, float *A, int lda, int *ipiv, int variant, int nb, int *i
  * ---------------------------------------------------------------------------------- */
 int bf16x_set_stream(bf16x_stream_t stream);   /* stream used by bf16x_gemm / _host */
 bf16x_stream_t bf16x_get_stream(void);
-void bf16x_release(void);                      /* free cached device/host workspace */
+void bf16x_release(void);                      /* free cached device/host workspace (GEMM and LU) */
 const char *bf16x_status_string(int status);   /* static string; includes the last CUDA error */
 int bf16x_device_check(void);                  /* BF16X_SUCCESS iff the current device is sm_100 */
 /* Number of library kernels launched by this process so far (all entry points). */
